@@ -1,0 +1,110 @@
+/* hgpu — B200 (sm_100a) engine for the reference's O(N^3) hot path: the
+ * square-root-free LDL^T determinant of the Hankel moment matrix M - xI.
+ *
+ * This is the thin C ABI the host C++ (the DetEvaluator seam) calls.  It
+ * replaces, bit for bit:
+ *   ldlt_det_serial    /root/reference/proj/src/ldlt.hpp:30-31  (ldlt.cpp:31-77)
+ *   ldlt_det_parallel  /root/reference/proj/src/ldlt.hpp:56-57  (ldlt.cpp:315-341)
+ *   LdltCapture        /root/reference/proj/src/ldlt.hpp:16-19
+ *   ZeroPivot          /root/reference/proj/src/errors.hpp:49-58
+ *
+ * Numbers cross the boundary as GMP-style signed limb vectors: a signed
+ * int32 size (sign of the value times the number of little-endian 32-bit
+ * limbs, 0 for zero) and the limbs.  A strip of 2n-1 mantissas is passed as
+ * `sizes[2n-1]` plus all limbs concatenated in order.  Every mantissa carries
+ * frac_bits fractional bits (FixedPoint, fixed_point.hpp:12-22).
+ *
+ * Ownership: inputs are copied; results are owned by the returned handle.
+ * Threading: one call at a time per matrix handle.  Status-returning
+ * functions never throw; the message of the last failure in the calling
+ * thread is available from hgpu_last_error().
+ */
+#ifndef HGPU_H
+#define HGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hgpu_status {
+  HGPU_OK = 0,
+  HGPU_ERR_INVALID_ARGUMENT = 1,
+  HGPU_ERR_ZERO_PIVOT = 2,         /* heig::ZeroPivot; see hgpu_last_zero_pivot */
+  HGPU_ERR_PRECISION_MISMATCH = 3, /* heig::PrecisionMismatch (ldlt.cpp:36) */
+  HGPU_ERR_CUDA = 4,               /* device unavailable or a CUDA failure */
+  HGPU_ERR_CAPACITY = 5,           /* a value outgrew every plan that fits */
+  HGPU_ERR_INTERNAL = 6,           /* an exactness self-check failed */
+  HGPU_ERR_COMM = 7                /* heig::ChannelFailure (errors.hpp:107-111) */
+} hgpu_status;
+
+/* factor flags */
+#define HGPU_CAPTURE 1u /* keep the ratio columns (LdltCapture) */
+#define HGPU_FOLD 2u    /* fold the pivots into det (ldlt.cpp:22-27) */
+#define HGPU_PROFILE 4u /* time every trailing-update launch with events */
+
+typedef struct hgpu_matrix hgpu_matrix;
+typedef struct hgpu_factor hgpu_factor;
+
+/* Uploads the anti-diagonal strip of an order-n Hankel matrix (the
+ * HankelMatrix of hankel_matrix.hpp:17-42) to `device` and sizes the
+ * transform plan.  Replaces the per-call workspace init of ldlt.cpp:38-44. */
+hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,
+                            const uint32_t* strip_limbs, int device,
+                            hgpu_matrix** out);
+void hgpu_matrix_free(hgpu_matrix* m);
+
+/* Multi-GPU: join a column-block-cyclic factorisation as `rank` of `world`
+ * (one process per GPU).  `nccl_id` is the 128-byte ncclUniqueId produced by
+ * hgpu_nccl_unique_id on rank 0 and shared by the caller.  Must be called
+ * before the first factorisation; world == 1 is the default. */
+hgpu_status hgpu_nccl_unique_id(unsigned char out[128]);
+hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
+                                 const unsigned char nccl_id[128]);
+
+/* det(M - xI) by square-root-free LDL^T (ldlt_det_serial / _parallel).
+ * x must carry the matrix's frac_bits.  On HGPU_ERR_ZERO_PIVOT the pivot
+ * index is available from hgpu_last_zero_pivot(). */
+hgpu_status hgpu_ldlt_factor(hgpu_matrix* m, int32_t x_size,
+                             const uint32_t* x_limbs, long x_frac_bits,
+                             unsigned flags, hgpu_factor** out);
+
+long hgpu_factor_order(const hgpu_factor* f);
+long hgpu_factor_frac_bits(const hgpu_factor* f);
+/* Pivot D_p at frac_bits (LdltCapture::pivots). */
+hgpu_status hgpu_factor_pivot(const hgpu_factor* f, long p, int32_t* size,
+                              const uint32_t** limbs);
+/* Ratio R_p[r] at frac_bits/2, r > p (LdltCapture::ratio_columns);
+ * requires HGPU_CAPTURE. */
+hgpu_status hgpu_factor_ratio(const hgpu_factor* f, long p, long r,
+                              int32_t* size, const uint32_t** limbs);
+/* fold_pivots (ldlt.cpp:22-27) at frac_bits; requires HGPU_FOLD. */
+hgpu_status hgpu_factor_det(const hgpu_factor* f, int32_t* size,
+                            const uint32_t** limbs);
+/* Device time of the factorisation (CUDA events), and with HGPU_PROFILE the
+ * trailing-update kernel statistics: launches, summed ms, modular products. */
+double hgpu_factor_device_ms(const hgpu_factor* f);
+hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
+                                     double* ms, double* products);
+void hgpu_factor_free(hgpu_factor* f);
+
+/* Plan introspection: primes, transform length, digit width, limb capacity,
+ * workspace bytes on this rank. */
+hgpu_status hgpu_matrix_plan(const hgpu_matrix* m, int* nprimes, int* length,
+                             int* digit_bits, int* cap_limbs,
+                             double* workspace_bytes);
+
+/* Column-block owner (reflected round-robin of assignment.hpp:15-23 applied
+ * to blocks of `block` columns). */
+int hgpu_block_owner(long block_index, int world);
+
+long hgpu_last_zero_pivot(void);
+const char* hgpu_last_error(void);
+const char* hgpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HGPU_H */

@@ -1,0 +1,184 @@
+// extern "C" boundary of libhgpu (include/hgpu.h).  Exceptions never cross
+// it: every status-returning entry point maps hgpu::Error (and anything else)
+// to a status and a thread-local message, like the reference's C ABI does
+// (/root/reference/proj/src/capi.cpp:24-35, :118-139).
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/hgpu.h"
+#include "engine.h"
+
+struct hgpu_matrix {
+  std::unique_ptr<hgpu::Matrix> impl;
+};
+struct hgpu_factor {
+  hgpu::FactorResult res;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local long g_last_pivot = -1;
+
+template <typename F>
+hgpu_status guarded(F&& f) {
+  try {
+    f();
+    return HGPU_OK;
+  } catch (const hgpu::Error& e) {
+    g_last_error = e.what();
+    if (e.status == HGPU_ERR_ZERO_PIVOT) g_last_pivot = e.pivot;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return HGPU_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HGPU_ERR_INTERNAL;
+  }
+}
+
+hgpu::HostInt make_int(int32_t size, const uint32_t* limbs) {
+  hgpu::HostInt h;
+  const int len = size < 0 ? -size : size;
+  if (len && !limbs) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null limbs");
+  h.limbs.assign(limbs, limbs + len);
+  while (!h.limbs.empty() && h.limbs.back() == 0) h.limbs.pop_back();
+  h.size = h.limbs.empty() ? 0 : (size < 0 ? -1 : 1) * (int)h.limbs.size();
+  return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hgpu_version(void) { return "hgpu 0.1 (sm_100a)"; }
+const char* hgpu_last_error(void) { return g_last_error.c_str(); }
+long hgpu_last_zero_pivot(void) { return g_last_pivot; }
+
+int hgpu_block_owner(long block_index, int world) {
+  return world < 1 ? 0 : hgpu::block_owner(block_index, world);
+}
+
+hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,
+                            const uint32_t* strip_limbs, int device,
+                            hgpu_matrix** out) {
+  return guarded([&] {
+    if (!out || !strip_sizes)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 1 || n > 100000)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "order out of range");
+    auto m = std::make_unique<hgpu_matrix>();
+    m->impl = std::make_unique<hgpu::Matrix>((int)n, (int)frac_bits,
+                                             strip_sizes, strip_limbs, device);
+    *out = m.release();
+  });
+}
+
+void hgpu_matrix_free(hgpu_matrix* m) { delete m; }
+
+hgpu_status hgpu_nccl_unique_id(unsigned char out[128]) {
+  return guarded([&] {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess)
+      throw hgpu::Error(HGPU_ERR_COMM, "ncclGetUniqueId failed");
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+  });
+}
+
+hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
+                                 const unsigned char nccl_id[128]) {
+  return guarded([&] {
+    if (!m) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null matrix");
+    m->impl->set_comm(rank, world, nccl_id);
+  });
+}
+
+hgpu_status hgpu_ldlt_factor(hgpu_matrix* m, int32_t x_size,
+                             const uint32_t* x_limbs, long x_frac_bits,
+                             unsigned flags, hgpu_factor** out) {
+  return guarded([&] {
+    if (!m || !out) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    auto f = std::make_unique<hgpu_factor>();
+    hgpu::HostInt x = make_int(x_size, x_limbs);
+    f->res = m->impl->factor_checked(x, x_frac_bits, flags);
+    *out = f.release();
+  });
+}
+
+long hgpu_factor_order(const hgpu_factor* f) { return f ? f->res.n : 0; }
+long hgpu_factor_frac_bits(const hgpu_factor* f) { return f ? f->res.K : 0; }
+
+hgpu_status hgpu_factor_pivot(const hgpu_factor* f, long p, int32_t* size,
+                              const uint32_t** limbs) {
+  return guarded([&] {
+    if (!f || !size || !limbs || p < 0 || p >= (long)f->res.pivots.size())
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad pivot index");
+    *size = f->res.pivots[p].size;
+    *limbs = f->res.pivots[p].limbs.data();
+  });
+}
+
+hgpu_status hgpu_factor_ratio(const hgpu_factor* f, long p, long r,
+                              int32_t* size, const uint32_t** limbs) {
+  return guarded([&] {
+    if (!f || !size || !limbs)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    if (!f->res.have_ratios)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "ratios not captured");
+    if (p < 0 || p >= (long)f->res.ratios.size() || r <= p || r >= f->res.n)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad ratio index");
+    const hgpu::HostInt& h = f->res.ratios[p][r - p - 1];
+    *size = h.size;
+    *limbs = h.limbs.data();
+  });
+}
+
+hgpu_status hgpu_factor_det(const hgpu_factor* f, int32_t* size,
+                            const uint32_t** limbs) {
+  return guarded([&] {
+    if (!f || !size || !limbs)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    if (!f->res.have_det)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "determinant not folded");
+    *size = f->res.det.size;
+    *limbs = f->res.det.limbs.data();
+  });
+}
+
+double hgpu_factor_device_ms(const hgpu_factor* f) {
+  return f ? f->res.device_ms : 0.0;
+}
+
+hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
+                                     double* ms, double* products) {
+  return guarded([&] {
+    if (!f) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null factor");
+    if (launches) *launches = f->res.update_launches;
+    if (ms) *ms = f->res.update_ms;
+    if (products) *products = f->res.update_products;
+  });
+}
+
+void hgpu_factor_free(hgpu_factor* f) { delete f; }
+
+hgpu_status hgpu_matrix_plan(const hgpu_matrix* m, int* nprimes, int* length,
+                             int* digit_bits, int* cap_limbs,
+                             double* workspace_bytes) {
+  return guarded([&] {
+    if (!m) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null matrix");
+    const hgpu::Plan& P = m->impl->plan_or_build();
+    if (nprimes) *nprimes = P.np;
+    if (length) *length = P.L;
+    if (digit_bits) *digit_bits = P.w;
+    if (cap_limbs) *cap_limbs = P.cap;
+    if (workspace_bytes) *workspace_bytes = P.workspace_bytes();
+  });
+}
+
+}  // extern "C"

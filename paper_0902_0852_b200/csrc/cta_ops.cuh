@@ -1,0 +1,262 @@
+// CTA-cooperative building blocks on shared-memory arrays:
+//   * length-L number-theoretic transforms (Harvey lazy butterflies, Shoup
+//     twiddles) in bit-reversed-output (forward) / bit-reversed-input
+//     (inverse) order, so a length-L/2^k transform is a prefix of the
+//     length-L one and one twiddle table serves every length;
+//   * carry resolution of redundant digit sums by a block-wide scan over
+//     carry *functions* (carry-in in {-1,0,1,2} -> carry-out), which makes
+//     every multi-limb add/sub/normalise a constant-depth parallel step;
+//   * schoolbook limb multiplication (product scanning, 96-bit column sums
+//     on PTX carry chains), shifts and bit-field reads.
+// All routines must be called by every thread of the block.
+#pragma once
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace hgpu {
+
+// ---------------------------------------------------------------- NTT ------
+
+// Forward transform, natural order in (values < 4q), bit-reversed order out
+// (values < q).  tw/twp: twiddle table T[m+i] = w^{(Lmax/2m) bitrev_m(i)}
+// and its Shoup companions (shared by all lengths L <= Lmax).
+__device__ inline void cta_ntt_fwd(uint32_t* x, int logL, const uint32_t* tw,
+                                   const uint32_t* twp, uint32_t q) {
+  const int L = 1 << logL;
+  const uint32_t q2 = 2 * q;
+  for (int lm = 0; lm < logL; ++lm) {
+    const int m = 1 << lm;
+    const int lt = logL - 1 - lm;  // t = L / (2m)
+    for (int b = threadIdx.x; b < L / 2; b += blockDim.x) {
+      const int i = b >> lt;
+      const int j1 = (i << (lt + 1)) + (b & ((1 << lt) - 1));
+      const int j2 = j1 + (1 << lt);
+      uint32_t X = x[j1];
+      X = X >= q2 ? X - q2 : X;
+      const uint32_t T = mul_shoup(x[j2], tw[m + i], twp[m + i], q);
+      x[j1] = X + T;
+      x[j2] = X - T + q2;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    uint32_t X = x[i];
+    X = X >= q2 ? X - q2 : X;
+    x[i] = X >= q ? X - q : X;
+  }
+  __syncthreads();
+}
+
+// Inverse transform without the 1/L scale: bit-reversed in (values < 2q),
+// natural order out (values < 2q).  itw/itwp: inverses of the forward table.
+__device__ inline void cta_ntt_inv(uint32_t* x, int logL, const uint32_t* itw,
+                                   const uint32_t* itwp, uint32_t q) {
+  const int L = 1 << logL;
+  const uint32_t q2 = 2 * q;
+  for (int lt = 0; lt < logL; ++lt) {
+    const int m = L >> (lt + 1);
+    for (int b = threadIdx.x; b < L / 2; b += blockDim.x) {
+      const int i = b >> lt;
+      const int j1 = (i << (lt + 1)) + (b & ((1 << lt) - 1));
+      const int j2 = j1 + (1 << lt);
+      const uint32_t U = x[j1], V = x[j2];
+      uint32_t S = U + V;
+      x[j1] = S >= q2 ? S - q2 : S;
+      x[j2] = mul_shoup(U - V + q2, itw[m + i], itwp[m + i], q);
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------- carry functions -----
+// A carry function maps carry-in c in {-1,0,1,2} to carry-out in the same
+// set; entry c is stored in bits [2(c+1), 2(c+1)+2) as (out+1).
+constexpr uint32_t kCfIdentity = 0xE4u;
+
+__device__ __forceinline__ int cf_apply(uint32_t f, int c) {
+  return (int)((f >> (2 * (c + 1))) & 3u) - 1;
+}
+// later o earlier
+__device__ __forceinline__ uint32_t cf_compose(uint32_t later,
+                                               uint32_t earlier) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t mid = (earlier >> (2 * i)) & 3u;
+    r |= ((later >> (2 * mid)) & 3u) << (2 * i);
+  }
+  return r;
+}
+
+// Exclusive block-wide scan under composition: returns f_{t-1} o ... o f_0.
+// `red` needs blockDim.x/32 words of shared memory.
+__device__ inline uint32_t cta_exclusive_compose(uint32_t f, uint32_t* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t x = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = cf_compose(x, y);
+  }
+  if (lane == 31) red[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < nw ? red[lane] : kCfIdentity;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w = cf_compose(w, y);
+    }
+    if (lane < nw) red[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t before_warp = wid > 0 ? red[wid - 1] : kCfIdentity;
+  uint32_t excl = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) excl = kCfIdentity;
+  __syncthreads();
+  return cf_compose(excl, before_warp);
+}
+
+__device__ __forceinline__ int64_t floor_shift(int64_t v, int bits) {
+  return v >> bits;  // arithmetic shift = floor division by 2^bits
+}
+
+// Resolves sum_{k<M} v_k 2^{bits k} into digits d_k in [0, 2^bits), where
+// getv(k) returns v_k in [-2^bits + 1, 3*2^bits - 2] (int64).  putd(k, d)
+// receives every digit.  Returns the final carry (in {-1,0,1,2}) to all
+// threads: the exact value is sum d_k 2^{bits k} + carry 2^{bits M}.
+// `red` needs blockDim.x/32 + 1 words.
+template <class GetV, class PutD>
+__device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
+                           uint32_t* red) {
+  const int nt = blockDim.x;
+  const int chunk = (M + nt - 1) / nt;
+  const int k0 = min(M, (int)threadIdx.x * chunk);
+  const int k1 = min(M, k0 + chunk);
+  uint32_t F = kCfIdentity;
+  for (int k = k0; k < k1; ++k) {
+    const int64_t v = getv(k);
+    uint32_t f = 0;
+#pragma unroll
+    for (int c = -1; c <= 2; ++c) {
+      const int64_t o = floor_shift(v + c, bits);
+      f |= (uint32_t)(o + 1) << (2 * (c + 1));
+    }
+    F = cf_compose(f, F);
+  }
+  const uint32_t P = cta_exclusive_compose(F, red);
+  int c = cf_apply(P, 0);
+  const int64_t mask = (int64_t(1) << bits) - 1;
+  for (int k = k0; k < k1; ++k) {
+    const int64_t v = getv(k) + c;
+    putd(k, (uint32_t)(v & mask));
+    c = (int)floor_shift(v, bits);
+  }
+  const int nw = nt >> 5;
+  if (k1 == M && k0 < k1) red[nw] = (uint32_t)(c + 1);
+  if (M == 0 && threadIdx.x == 0) red[nw] = 1u;
+  __syncthreads();
+  const int carry = (int)red[nw] - 1;
+  __syncthreads();
+  return carry;
+}
+
+// ------------------------------------------------------- limb helpers -----
+
+// Bits [off, off+32) of the non-negative integer a[0..n) (off may be < 0).
+__device__ __forceinline__ uint32_t field32(const uint32_t* a, int n,
+                                            long long off) {
+  const long long li = off >> 5;
+  const int sh = (int)(off & 31);
+  const uint32_t lo = (li >= 0 && li < n) ? a[li] : 0u;
+  if (sh == 0) return lo;
+  const uint32_t hi = (li + 1 >= 0 && li + 1 < n) ? a[li + 1] : 0u;
+  return (lo >> sh) | (hi << (32 - sh));
+}
+
+// Number of significant limbs (block-wide).  `red` needs 1 word.
+__device__ inline int cta_limb_len(const uint32_t* a, int n, uint32_t* red) {
+  if (threadIdx.x == 0) red[0] = 0;
+  __syncthreads();
+  int best = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (a[i]) best = i + 1;
+  if (best) atomicMax(red, (uint32_t)best);
+  __syncthreads();
+  const int len = (int)red[0];
+  __syncthreads();
+  return len;
+}
+
+__device__ __forceinline__ int limbs_bits(const uint32_t* a, int len) {
+  return len == 0 ? 0 : 32 * (len - 1) + (32 - __clz(a[len - 1]));
+}
+
+// out[0..M) = low M limbs of a*b (M <= na+nb gives the exact product when
+// M == na+nb).  a, b, out in shared memory; out must not alias a or b.
+// col: 3*M words of shared scratch; red: blockDim/32+1 words.
+__device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
+                               int nb, uint32_t* out, int M, uint32_t* col,
+                               uint32_t* red) {
+  constexpr int G = 8;
+  const int ngroups = (M + G - 1) / G;
+  uint32_t* c0p = col;
+  uint32_t* c1p = col + M;
+  uint32_t* c2p = col + 2 * M;
+  for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+    const int k0 = g * G;
+    uint32_t c0[G], c1[G], c2[G];
+#pragma unroll
+    for (int t = 0; t < G; ++t) c0[t] = c1[t] = c2[t] = 0u;
+    if (na > 0 && nb > 0) {
+      const int ilo = max(0, k0 - nb + 1);
+      const int ihi = min(k0 + G - 1, na - 1);
+      // window w[t] = b[k0 + t - i]
+      uint32_t w[G];
+#pragma unroll
+      for (int t = 0; t < G; ++t) {
+        const int j = k0 + t - ilo;
+        w[t] = (j >= 0 && j < nb) ? b[j] : 0u;
+      }
+      for (int i = ilo; i <= ihi; ++i) {
+        const uint32_t ai = a[i];
+#pragma unroll
+        for (int t = 0; t < G; ++t) {
+          asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+              "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+              "addc.u32 %2, %2, 0;"
+              : "+r"(c0[t]), "+r"(c1[t]), "+r"(c2[t])
+              : "r"(ai), "r"(w[t]));
+        }
+        // slide: next i needs b[k0 + t - i - 1]
+#pragma unroll
+        for (int t = G - 1; t > 0; --t) w[t] = w[t - 1];
+        const int j = k0 - i - 1;
+        w[0] = (j >= 0 && j < nb) ? b[j] : 0u;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int k = k0 + t;
+      if (k < M) {
+        c0p[k] = c0[t];
+        c1p[k] = c1[t];
+        c2p[k] = c2[t];
+      }
+    }
+  }
+  __syncthreads();
+  cta_resolve(
+      M, 32,
+      [&](int k) -> int64_t {
+        int64_t v = c0p[k];
+        if (k >= 1) v += c1p[k - 1];
+        if (k >= 2) v += c2p[k - 2];
+        return v;
+      },
+      [&](int k, uint32_t d) { out[k] = d; }, red);
+}
+
+}  // namespace hgpu

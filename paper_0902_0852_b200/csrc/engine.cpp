@@ -1,0 +1,571 @@
+// Host side of the B200 LDL^T engine (see engine.h).
+#include "engine.h"
+
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+namespace hgpu {
+
+namespace {
+
+#define CU(expr)                                                           \
+  do {                                                                     \
+    cudaError_t e_ = (expr);                                               \
+    if (e_ != cudaSuccess)                                                 \
+      throw Error(HGPU_ERR_CUDA, std::string(#expr) + ": " +               \
+                                     cudaGetErrorString(e_));              \
+  } while (0)
+
+#define NC(expr)                                                           \
+  do {                                                                     \
+    ncclResult_t r_ = (expr);                                              \
+    if (r_ != ncclSuccess)                                                 \
+      throw Error(HGPU_ERR_COMM, std::string(#expr) + ": " +               \
+                                     ncclGetErrorString(r_));              \
+  } while (0)
+
+using u64 = unsigned long long;
+using u128 = unsigned __int128;
+
+u64 powmod(u64 b, u64 e, u64 m) {
+  u64 r = 1 % m;
+  b %= m;
+  while (e) {
+    if (e & 1) r = (u128)r * b % m;
+    b = (u128)b * b % m;
+    e >>= 1;
+  }
+  return r;
+}
+u64 invmod(u64 a, u64 m) { return powmod(a % m, m - 2, m); }  // m prime
+
+int bitrev(int x, int bits) {
+  int r = 0;
+  for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
+  return r;
+}
+
+double log2_u128(u128 v) {
+  return std::log2((double)(u64)(v >> 64) * 18446744073709551616.0 +
+                   (double)(u64)v);
+}
+
+template <typename T>
+T* dalloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CU(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+}  // namespace
+
+int block_owner(long block, int world) {
+  // reflected round-robin, assignment.hpp:15-23, over column blocks
+  const long r = block % (2L * world);
+  return (int)(r < world ? r : 2L * world - 1 - r);
+}
+
+Plan choose_plan(int n, int K, int bits, int min_logL) {
+  Plan best;
+  long long best_cost = LLONG_MAX;
+  for (int np = 2; np <= 3; ++np) {
+    u128 Q = 1;
+    for (int j = 0; j < np; ++j) Q *= kPrimes[j];
+    const double log2_quarter = log2_u128(Q) - 2.0;
+    for (int logL = std::max(5, min_logL); logL <= 17; ++logL) {
+      const int L = 1 << logL;
+      // L digits of w bits must hold any product, with two digits spare
+      const int w = (bits + 1 + (L - 2) - 1) / (L - 2);
+      if (w > 26) continue;
+      if (w < 4) continue;
+      // n stages x (L/2 overlapping terms) x (2^w-1)^2 (+ slack) < Q/4
+      const double lb = std::log2((double)n + 1) + std::log2((double)L / 2 + 1) +
+                        2.0 * w + 0.1;
+      if (lb >= log2_quarter) continue;
+      const long long cost = (long long)np * L;
+      if (cost < best_cost) {
+        best_cost = cost;
+        best.np = np;
+        best.L = L;
+        best.logL = logL;
+        best.w = w;
+      }
+      break;  // larger L at this np only costs more
+    }
+  }
+  if (best_cost == LLONG_MAX)
+    throw Error(HGPU_ERR_CAPACITY, "no transform plan fits the value sizes");
+  best.n = n;
+  best.K = K;
+  best.T = (32 * best.np + best.w - 1) / best.w + 1;
+  best.cap = (best.w * (best.L + best.T) + 31) / 32 + 2;
+  best.ycap = best.cap + (K / 2) / 32 + 8;
+  return best;
+}
+
+Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
+               int device)
+    : n_(n), K_(K), device_(device) {
+  if (n < 1) throw Error(HGPU_ERR_INVALID_ARGUMENT, "order must be >= 1");
+  if (K < 2 || K % 2 != 0)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "frac_bits must be even and >= 2");
+  strip_.resize(2 * n - 1);
+  const uint32_t* src = limbs;
+  for (int s = 0; s < 2 * n - 1; ++s) {
+    HostInt& h = strip_[s];
+    h.size = sizes[s];
+    const int len = std::abs(sizes[s]);
+    h.limbs.assign(src, src + len);
+    src += len;
+    while (!h.limbs.empty() && h.limbs.back() == 0) h.limbs.pop_back();
+    h.size = h.limbs.empty() ? 0 : (sizes[s] < 0 ? -1 : 1) * (int)h.limbs.size();
+    const int b = h.limbs.empty()
+                      ? 0
+                      : 32 * ((int)h.limbs.size() - 1) +
+                            (32 - __builtin_clz(h.limbs.back()));
+    strip_bits_ = std::max(strip_bits_, b);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(HGPU_ERR_CUDA, "no CUDA device available");
+  if (device < 0 || device >= ndev)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad device index");
+  CU(cudaSetDevice(device_));
+  CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  CU(cudaEventCreate(&ev0_));
+  CU(cudaEventCreate(&ev1_));
+}
+
+Matrix::~Matrix() {
+  cudaSetDevice(device_);
+  release();
+  if (comm_) ncclCommDestroy((ncclComm_t)comm_);
+  for (cudaEvent_t e : uev_) cudaEventDestroy(e);
+  if (ev0_) cudaEventDestroy(ev0_);
+  if (ev1_) cudaEventDestroy(ev1_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Matrix::release() {
+  for (void* p : {(void*)tw_, (void*)W_, (void*)that_, (void*)xhat_,
+                  (void*)colbase_, (void*)strip_hdr_, (void*)strip_limbs_,
+                  (void*)x_hdr_, (void*)x_limbs_, (void*)vhdr_, (void*)vlimbs_,
+                  (void*)rhdr_, (void*)rlimbs_, (void*)vhat_, (void*)rhat_,
+                  (void*)phdr_, (void*)plimbs_, (void*)ybuf_, (void*)rscratch_,
+                  (void*)dscratch_, (void*)ys_, (void*)stats_, (void*)err_})
+    dfree(p);
+  tw_ = W_ = that_ = xhat_ = nullptr;
+  colbase_ = nullptr;
+  strip_hdr_ = x_hdr_ = vhdr_ = rhdr_ = phdr_ = ys_ = stats_ = err_ = nullptr;
+  strip_limbs_ = x_limbs_ = vlimbs_ = rlimbs_ = vhat_ = rhat_ = plimbs_ =
+      ybuf_ = rscratch_ = dscratch_ = nullptr;
+  plan_ = Plan{};
+}
+
+void Matrix::set_comm(int rank, int world, const unsigned char* id) {
+  if (world < 1 || rank < 0 || rank >= world)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad rank/world");
+  CU(cudaSetDevice(device_));
+  if (comm_) {
+    ncclCommDestroy((ncclComm_t)comm_);
+    comm_ = nullptr;
+  }
+  rank_ = rank;
+  world_ = world;
+  if (world > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c;
+    NC(ncclCommInitRank(&c, world, uid, rank));
+    comm_ = c;
+  }
+  release();  // ownership changes the workspace layout
+}
+
+void Matrix::build(int min_logL) {
+  release();
+  // PD bound: every workspace entry and every product V_p[c] R_p[r] is
+  // bounded by the largest diagonal moment (plus the shift); 64 bits margin.
+  plan_ = choose_plan(n_, K_, strip_bits_ + 64, min_logL);
+  Plan& P = plan_;
+  // ownership: column blocks of kb columns, reflected round-robin
+  const int nblocks = (n_ + P.kb - 1) / P.kb;
+  owned_blocks_.clear();
+  colbase_h_.assign(n_, -1);
+  long long entries = 0;
+  for (int b = 0; b < nblocks; ++b) {
+    if (block_owner(b, world_) != rank_) continue;
+    owned_blocks_.push_back(b);
+    for (int c = b * P.kb; c < std::min(n_, (b + 1) * P.kb); ++c) {
+      colbase_h_[c] = entries;
+      entries += n_ - c;
+    }
+  }
+  P.entries = entries;
+
+  DevPlan& D = dp_;
+  D = DevPlan{};
+  D.n = n_;
+  D.K = K_;
+  D.k2 = K_ / 2;
+  D.np = P.np;
+  D.logL = P.logL;
+  D.L = P.L;
+  D.w = P.w;
+  D.T = P.T;
+  D.cap = P.cap;
+  D.ycap = P.ycap;
+  D.NW = P.np * P.L;
+  D.Lmax = P.L;
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    PrimeConsts& c = D.pc[j];
+    c.q = (uint32_t)q;
+    // -q^-1 mod 2^32 by Newton
+    uint32_t inv = 1;
+    for (int i = 0; i < 6; ++i) inv *= 2u - (uint32_t)q * inv;
+    c.qneg = (uint32_t)(0u - inv);
+    c.r32 = (uint32_t)((1ULL << 32) % q);
+    c.r32s = shoup_companion(c.r32, (uint32_t)q);
+    c.r64 = (uint32_t)((u128)c.r32 * c.r32 % q);
+    const u64 il = invmod(P.L, q);
+    D.invL[j] = (uint32_t)il;
+    D.invLp[j] = shoup_companion((uint32_t)il, (uint32_t)q);
+  }
+  const u64 q0 = kPrimes[0], q1 = kPrimes[1], q2 = kPrimes[2];
+  D.g1 = (uint32_t)invmod(q0 % q1, q1);
+  D.g1p = shoup_companion(D.g1, (uint32_t)q1);
+  D.g2 = (uint32_t)invmod((u128)q0 * q1 % q2, q2);
+  D.g2p = shoup_companion(D.g2, (uint32_t)q2);
+  D.q0m2 = (uint32_t)(q0 % q2);
+  D.q0m2p = shoup_companion(D.q0m2, (uint32_t)q2);
+  D.q01 = q0 * q1;
+  u128 Q = 1;
+  for (int j = 0; j < P.np; ++j) Q *= kPrimes[j];
+  const u128 H = (Q + 1) / 2;
+  D.Qlo = (u64)Q;
+  D.Qhi = (u64)(Q >> 64);
+  D.Hlo = (u64)H;
+  D.Hhi = (u64)(H >> 64);
+
+  // twiddles: T[m+i] = w^{(L/2m) bitrev_m(i)}, w a primitive L-th root
+  std::vector<uint32_t> tab(4 * (size_t)P.np * P.L, 0);
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    const u64 wL = powmod(kPrimRoots[j], (q - 1) / P.L, q);
+    uint32_t* tw = &tab[(0 * P.np + j) * (size_t)P.L];
+    uint32_t* twp = &tab[(1 * P.np + j) * (size_t)P.L];
+    uint32_t* itw = &tab[(2 * P.np + j) * (size_t)P.L];
+    uint32_t* itwp = &tab[(3 * P.np + j) * (size_t)P.L];
+    for (int lm = 0; (1 << lm) < P.L; ++lm) {
+      const int m = 1 << lm;
+      for (int i = 0; i < m; ++i) {
+        const u64 e = (u64)(P.L / (2 * m)) * bitrev(i, lm);
+        const u64 v = powmod(wL, e, q);
+        const u64 iv = invmod(v, q);
+        tw[m + i] = (uint32_t)v;
+        twp[m + i] = shoup_companion((uint32_t)v, (uint32_t)q);
+        itw[m + i] = (uint32_t)iv;
+        itwp[m + i] = shoup_companion((uint32_t)iv, (uint32_t)q);
+      }
+    }
+  }
+  tw_ = dalloc<uint32_t>(tab.size());
+  CU(cudaMemcpy(tw_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  D.tw = tw_;
+  D.twp = tw_ + (size_t)P.np * P.L;
+  D.itw = tw_ + 2 * (size_t)P.np * P.L;
+  D.itwp = tw_ + 3 * (size_t)P.np * P.L;
+
+  CU(configure_kernels(D, &div_smem_, &div_global_));
+
+  const size_t NW = (size_t)D.NW;
+  const int kb = P.kb;
+  W_ = dalloc<uint32_t>((size_t)std::max<long long>(entries, 1) * NW);
+  colbase_ = dalloc<long long>(n_);
+  CU(cudaMemcpy(colbase_, colbase_h_.data(), n_ * sizeof(long long),
+                cudaMemcpyHostToDevice));
+  // strip + x as limb integers, and their transforms
+  const int ns = 2 * n_ - 1;
+  strip_hdr_ = dalloc<int>(ns);
+  strip_limbs_ = dalloc<uint32_t>((size_t)ns * P.cap);
+  {
+    std::vector<int> hdr(ns);
+    std::vector<uint32_t> lim((size_t)ns * P.cap, 0);
+    for (int s = 0; s < ns; ++s) {
+      if ((int)strip_[s].limbs.size() > P.cap)
+        throw Error(HGPU_ERR_CAPACITY, "strip entry exceeds limb capacity");
+      hdr[s] = strip_[s].size;
+      std::copy(strip_[s].limbs.begin(), strip_[s].limbs.end(),
+                lim.begin() + (size_t)s * P.cap);
+    }
+    CU(cudaMemcpy(strip_hdr_, hdr.data(), ns * sizeof(int),
+                  cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(strip_limbs_, lim.data(), lim.size() * 4,
+                  cudaMemcpyHostToDevice));
+  }
+  that_ = dalloc<uint32_t>((size_t)ns * NW);
+  xhat_ = dalloc<uint32_t>(NW);
+  x_hdr_ = dalloc<int>(1);
+  x_limbs_ = dalloc<uint32_t>(P.cap);
+  err_ = dalloc<int>(kErrWords);
+  {
+    const int init[kErrWords] = {INT_MAX, 0, 0, 0};
+    CU(cudaMemcpy(err_, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
+  CU(launch_fwd_ints(D, IntBuf{strip_hdr_, strip_limbs_}, 0, that_, 0, ns, 0,
+                     nullptr, err_, stream_));
+  int herr[kErrWords];
+  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, stream_));
+  CU(cudaStreamSynchronize(stream_));
+  if (herr[kErrCapacity])
+    throw Error(HGPU_ERR_CAPACITY, "strip does not fit the transform plan");
+
+  vhdr_ = dalloc<int>((size_t)kb * n_);
+  rhdr_ = dalloc<int>((size_t)kb * n_);
+  vlimbs_ = dalloc<uint32_t>((size_t)kb * n_ * P.cap);
+  rlimbs_ = dalloc<uint32_t>((size_t)kb * n_ * P.cap);
+  vhat_ = dalloc<uint32_t>((size_t)kb * n_ * NW);
+  rhat_ = dalloc<uint32_t>((size_t)kb * n_ * NW);
+  phdr_ = dalloc<int>(n_);
+  plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
+  ybuf_ = dalloc<uint32_t>(P.ycap);
+  ys_ = dalloc<int>(2);
+  rscratch_ = dalloc<uint32_t>(recip_scratch_words(D));
+  if (div_global_)
+    dscratch_ = dalloc<uint32_t>((size_t)n_ * divide_smem_words(D));
+  stats_ = dalloc<int>(3 * (size_t)n_);
+}
+
+void Matrix::panel_broadcast(int owner, int p0, int ns, cudaStream_t st) {
+  if (world_ == 1) return;
+  ncclComm_t c = (ncclComm_t)comm_;
+  const Plan& P = plan_;
+  const size_t slot_rows = (size_t)ns * n_;
+  NC(ncclGroupStart());
+  NC(ncclBroadcast(vhdr_, vhdr_, slot_rows, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(rhdr_, rhdr_, slot_rows, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(vlimbs_, vlimbs_, slot_rows * P.cap, ncclUint32, owner, c, st));
+  NC(ncclBroadcast(rlimbs_, rlimbs_, slot_rows * P.cap, ncclUint32, owner, c, st));
+  NC(ncclBroadcast(phdr_ + p0, phdr_ + p0, ns, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(plimbs_ + (size_t)p0 * P.cap, plimbs_ + (size_t)p0 * P.cap,
+                   (size_t)ns * P.cap, ncclUint32, owner, c, st));
+  for (int k = 0; k < 3; ++k)
+    NC(ncclBroadcast(stats_ + (size_t)k * n_ + p0, stats_ + (size_t)k * n_ + p0,
+                     ns, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(err_, err_, kErrWords, ncclInt32, owner, c, st));
+  NC(ncclGroupEnd());
+}
+
+void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
+  const Plan& P = plan_;
+  const DevPlan& D = dp_;
+  cudaStream_t st = stream_;
+  const int n = n_, kb = P.kb;
+  const size_t NW = (size_t)D.NW;
+  const long long slot_stride = (long long)n * NW;
+
+  // x -> transform
+  if ((int)x.limbs.size() > P.cap)
+    throw Error(HGPU_ERR_CAPACITY, "shift exceeds limb capacity");
+  {
+    std::vector<uint32_t> xl(P.cap, 0);
+    std::copy(x.limbs.begin(), x.limbs.end(), xl.begin());
+    CU(cudaMemcpyAsync(x_limbs_, xl.data(), P.cap * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(x_hdr_, &x.size, 4, cudaMemcpyHostToDevice, st));
+  }
+  int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
+  CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+  CU(cudaMemsetAsync(stats_, 0xff, 3 * (size_t)n * sizeof(int), st));  // -1
+  CU(cudaEventRecord(ev0_, st));
+  CU(launch_fwd_ints(D, IntBuf{x_hdr_, x_limbs_}, 0, xhat_, 0, 1, 0, nullptr,
+                     err_, st));
+  CU(launch_init_w(D, that_, xhat_, colbase_, W_, st));
+
+  int* maxbitsV = stats_;
+  int* maxdegV = stats_ + n;
+  int* maxdegR = stats_ + 2 * n;
+  IntBuf vint{vhdr_, vlimbs_}, rint{rhdr_, rlimbs_}, piv{phdr_, plimbs_};
+  const bool capture = flags & HGPU_CAPTURE;
+  const bool profile = flags & HGPU_PROFILE;
+  if (capture) {
+    res.ratios.assign(n > 0 ? n - 1 : 0, {});
+    res.have_ratios = true;
+  }
+  std::vector<int> hv_hdr, hr_hdr;
+  std::vector<uint32_t> hr_limbs;
+  size_t uev_used = 0;
+  auto timed_update = [&](int nslots, int c_begin, int c_end) {
+    if (c_begin >= c_end || nslots <= 0) return;
+    if (profile) {
+      while (uev_.size() < uev_used + 2) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        uev_.push_back(e);
+      }
+      CU(cudaEventRecord(uev_[uev_used], st));
+    }
+    CU(launch_update(D, P.tile, W_, colbase_, vhat_, rhat_, slot_stride,
+                     nslots, c_begin, c_end, err_, st));
+    if (profile) {
+      CU(cudaEventRecord(uev_[uev_used + 1], st));
+      uev_used += 2;
+      // modular products: pairs x stages x NW
+      double pairs = 0;
+      for (int c = c_begin; c < c_end; ++c) pairs += n - c;
+      res.update_products += pairs * nslots * (double)NW;
+      ++res.update_launches;
+    }
+  };
+
+  const int nblocks = (n + kb - 1) / kb;
+  for (int b = 0; b < nblocks; ++b) {
+    const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
+    const int owner = block_owner(b, world_);
+    if (owner == rank_) {
+      for (int p = p0; p < p1; ++p) {
+        const int s = p - p0;
+        const long long row0 = (long long)s * n;  // slot base in row units
+        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, err_, st));
+        if (p == n - 1) break;
+        CU(launch_recip(D, vint, row0 + p, maxbitsV, p, ybuf_, ys_, rscratch_,
+                        err_, st));
+        CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, dscratch_,
+                         div_global_ ? 1 : 0, err_, st));
+        // transforms of V_p[r], R_p[r] for r in (p, n)
+        CU(launch_fwd_ints(D, vint, row0 + p + 1, vhat_, row0 + p + 1,
+                           n - p - 1, 0, maxdegV + p, err_, st));
+        CU(launch_fwd_ints(D, rint, row0 + p + 1, rhat_, row0 + p + 1,
+                           n - p - 1, 1, maxdegR + p, err_, st));
+        // in-panel columns (p, p1)
+        CU(launch_update(D, P.tile, W_, colbase_, vhat_ + (size_t)s * slot_stride,
+                         rhat_ + (size_t)s * slot_stride, slot_stride, 1, p + 1,
+                         p1, err_, st));
+      }
+    }
+    panel_broadcast(owner, p0, ns, st);
+    if (owner != rank_ && p1 < n) {
+      for (int s = 0; s < ns; ++s) {
+        const long long row0 = (long long)s * n;
+        CU(launch_fwd_ints(D, vint, row0 + p1, vhat_, row0 + p1, n - p1, 0,
+                           nullptr, err_, st));
+        CU(launch_fwd_ints(D, rint, row0 + p1, rhat_, row0 + p1, n - p1, 1,
+                           nullptr, err_, st));
+      }
+    }
+    if (capture) {
+      const int nsr = std::min(ns, n - 1 - p0);
+      if (nsr > 0) {
+        hr_hdr.resize((size_t)nsr * n);
+        hr_limbs.resize((size_t)nsr * n * P.cap);
+        CU(cudaMemcpyAsync(hr_hdr.data(), rhdr_, hr_hdr.size() * 4,
+                           cudaMemcpyDeviceToHost, st));
+        CU(cudaMemcpyAsync(hr_limbs.data(), rlimbs_, hr_limbs.size() * 4,
+                           cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (int s = 0; s < nsr; ++s) {
+          const int p = p0 + s;
+          auto& col = res.ratios[p];
+          col.resize(n - p - 1);
+          for (int r = p + 1; r < n; ++r) {
+            const size_t idx = (size_t)s * n + r;
+            HostInt& h = col[r - p - 1];
+            h.size = hr_hdr[idx];
+            const int len = std::abs(h.size);
+            h.limbs.assign(hr_limbs.begin() + idx * P.cap,
+                           hr_limbs.begin() + idx * P.cap + len);
+          }
+        }
+      }
+    }
+    // trailing update of owned columns >= p1
+    if (p1 < n) {
+      for (int ob : owned_blocks_) {
+        const int c0 = std::max(p1, ob * kb), c1 = std::min(n, (ob + 1) * kb);
+        if (c0 < c1) timed_update(std::min(ns, n - 1 - p0), c0, c1);
+      }
+      // single rank: owned blocks are contiguous -> one launch would do; the
+      // per-block loop above keeps the multi-rank path identical.
+    }
+  }
+  CU(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));
+  CU(cudaEventRecord(ev1_, st));
+
+  int herr[kErrWords];
+  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  res.device_ms = ms;
+  if (profile) {
+    for (size_t i = 0; i < uev_used; i += 2) {
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, uev_[i], uev_[i + 1]));
+      res.update_ms += t;
+    }
+  }
+  if (herr[kErrCapacity]) {
+    Error e(HGPU_ERR_CAPACITY,
+            "transform capacity exceeded (flags " +
+                std::to_string(herr[kErrCapacity]) + ")");
+    throw e;
+  }
+  if (herr[kErrZeroPivot] != INT_MAX) {
+    Error e(HGPU_ERR_ZERO_PIVOT,
+            "zero pivot at column " + std::to_string(herr[kErrZeroPivot]) +
+                " with " + std::to_string(K_) + " fractional bits");
+    e.pivot = herr[kErrZeroPivot];
+    throw e;
+  }
+  if (herr[kErrInternal])
+    throw Error(HGPU_ERR_INTERNAL, "exactness self-check failed (flags " +
+                                       std::to_string(herr[kErrInternal]) + ")");
+  // pivots to host
+  std::vector<int> ph(n);
+  std::vector<uint32_t> pl((size_t)n * P.cap);
+  CU(cudaMemcpy(ph.data(), phdr_, n * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(pl.data(), plimbs_, pl.size() * 4, cudaMemcpyDeviceToHost));
+  res.pivots.resize(n);
+  for (int p = 0; p < n; ++p) {
+    res.pivots[p].size = ph[p];
+    const int len = std::abs(ph[p]);
+    res.pivots[p].limbs.assign(pl.begin() + (size_t)p * P.cap,
+                               pl.begin() + (size_t)p * P.cap + len);
+  }
+}
+
+FactorResult Matrix::factor(const HostInt& x, unsigned flags) {
+  CU(cudaSetDevice(device_));
+  FactorResult res;
+  res.n = n_;
+  res.K = K_;
+  // plans escalate only on a capacity failure (non-PD shifts can outgrow
+  // the PD bound); every rank sees the same flags, so all escalate together
+  int min_logL = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    if (!W_ || (min_logL && plan_.logL < min_logL)) build(min_logL);
+    try {
+      res = FactorResult{};
+      res.n = n_;
+      res.K = K_;
+      run(x, flags, res);
+      return res;
+    } catch (const Error& e) {
+      if (e.status != HGPU_ERR_CAPACITY) throw;
+      min_logL = plan_.logL + 1;
+      release();
+    }
+  }
+  throw Error(HGPU_ERR_CAPACITY, "values outgrew every transform plan");
+}
+
+}  // namespace hgpu

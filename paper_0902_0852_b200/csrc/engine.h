@@ -1,0 +1,118 @@
+// Host side of the B200 LDL^T engine: transform plan, HBM buffers, the
+// stage/panel schedule, and the column-block-cyclic multi-GPU protocol.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hgpu.h"
+#include "ldlt_kernels.cuh"
+
+namespace hgpu {
+
+struct Error : std::runtime_error {
+  hgpu_status status;
+  long pivot = -1;
+  Error(hgpu_status s, const std::string& what)
+      : std::runtime_error(what), status(s) {}
+};
+
+// Signed limb integer (GMP-style size) on the host.
+struct HostInt {
+  int32_t size = 0;
+  std::vector<uint32_t> limbs;
+};
+
+struct Plan {
+  int n = 0, K = 0, np = 0, L = 0, logL = 0, w = 0, T = 0, cap = 0, ycap = 0;
+  int kb = 32;         // panel width (columns per block)
+  int tile = 8;        // update register tile
+  long long entries = 0;  // workspace entries on this rank
+  double workspace_bytes() const { return double(entries) * np * L * 4.0; }
+};
+
+// Picks (primes, length, digit width) minimising np*L such that every
+// product V_p[c] R_p[r] fits the cyclic length and the accumulated digit
+// coefficients stay below Q/4.  `bits` bounds the
+// magnitude of any workspace entry and product (PD bound + margin).
+Plan choose_plan(int n, int K, int bits, int min_logL = 0);
+
+struct FactorResult {
+  int n = 0, K = 0;
+  std::vector<HostInt> pivots;
+  std::vector<std::vector<HostInt>> ratios;  // [p][r-p-1], if captured
+  HostInt det;
+  bool have_det = false, have_ratios = false;
+  double device_ms = 0;
+  long update_launches = 0;
+  double update_ms = 0, update_products = 0;
+};
+
+class Matrix {
+ public:
+  Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs, int device);
+  ~Matrix();
+  void set_comm(int rank, int world, const unsigned char* id);
+  FactorResult factor(const HostInt& x, unsigned flags);
+  // PrecisionMismatch as in ldlt.cpp:36 when x carries other frac bits.
+  FactorResult factor_checked(const HostInt& x, long x_frac_bits,
+                              unsigned flags) {
+    if (x_frac_bits != K_)
+      throw Error(HGPU_ERR_PRECISION_MISMATCH,
+                  "fractional precision mismatch: " +
+                      std::to_string(x_frac_bits) + " vs " +
+                      std::to_string(K_));
+    return factor(x, flags);
+  }
+  const Plan& plan_or_build() {
+    if (!W_) build(0);
+    return plan_;
+  }
+  int frac_bits() const { return K_; }
+
+ private:
+  void build(int min_logL);
+  void release();
+  void run(const HostInt& x, unsigned flags, FactorResult& res);
+  void panel_broadcast(int owner, int p0, int ns, cudaStream_t st);
+
+  int n_, K_, device_;
+  std::vector<HostInt> strip_;
+  int strip_bits_ = 0;
+  Plan plan_;
+  DevPlan dp_{};
+  int rank_ = 0, world_ = 1;
+  void* comm_ = nullptr;  // ncclComm_t
+  std::vector<long long> colbase_h_;
+  std::vector<int> owned_blocks_;
+  // device buffers
+  uint32_t *tw_ = nullptr, *W_ = nullptr, *that_ = nullptr, *xhat_ = nullptr;
+  long long* colbase_ = nullptr;
+  int* strip_hdr_ = nullptr;
+  uint32_t* strip_limbs_ = nullptr;
+  int* x_hdr_ = nullptr;
+  uint32_t* x_limbs_ = nullptr;
+  int* vhdr_ = nullptr;
+  uint32_t* vlimbs_ = nullptr;
+  int* rhdr_ = nullptr;
+  uint32_t* rlimbs_ = nullptr;
+  uint32_t *vhat_ = nullptr, *rhat_ = nullptr;
+  int* phdr_ = nullptr;
+  uint32_t* plimbs_ = nullptr;
+  uint32_t *ybuf_ = nullptr, *rscratch_ = nullptr, *dscratch_ = nullptr;
+  int* ys_ = nullptr;
+  int* stats_ = nullptr;  // maxbitsV | maxdegV | maxdegR, n each
+  int* err_ = nullptr;
+  size_t div_smem_ = 0;
+  bool div_global_ = false;
+  cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  std::vector<cudaEvent_t> uev_;
+};
+
+int block_owner(long block, int world);
+
+}  // namespace hgpu

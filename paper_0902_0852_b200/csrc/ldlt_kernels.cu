@@ -1,0 +1,664 @@
+// sm_100a kernels of the LDL^T engine.  Each kernel cites the reference step
+// it reproduces (/root/reference/proj/src/ldlt.cpp).  Arithmetic is exact:
+// the only roundings are the reference's own truncations (tdiv_q_2exp for the
+// column values, tdiv_q for the ratios), so results are bit-identical.
+#include <climits>
+#include <cstdint>
+
+#include "cta_ops.cuh"
+#include "ldlt_kernels.cuh"
+
+namespace hgpu {
+
+// ------------------------------------------------------------ helpers -----
+
+__device__ __forceinline__ bool stage_aborted(const int* err) {
+  return *(volatile const int*)&err[kErrZeroPivot] != INT_MAX ||
+         *(volatile const int*)&err[kErrCapacity] != 0;
+}
+
+// Loads a signed limb integer: returns sign, writes magnitude to dst (n limbs).
+__device__ inline int load_int(const IntBuf& b, long long idx, int cap,
+                               uint32_t* dst, int* len_out) {
+  const int h = b.hdr[idx];
+  const int len = h < 0 ? -h : h;
+  const uint32_t* src = b.limbs + idx * (long long)cap;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) dst[i] = src[i];
+  *len_out = len;
+  __syncthreads();
+  return h < 0 ? -1 : (h > 0 ? 1 : 0);
+}
+
+// Digit d_i (w bits) of |X| -> residues of the signed digit, forward NTT per
+// prime, optional Montgomery scaling (x 2^32), store NW words to out.
+__device__ void transform_int(const DevPlan& P, const uint32_t* mag, int len,
+                              int sign, uint32_t* sm, uint32_t* out, bool mont,
+                              int* err) {
+  const int bits = limbs_bits(mag, len);
+  if (bits > P.w * P.L) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapDigits);
+  }
+  const uint32_t dmask = (1u << P.w) - 1u;
+  for (int j = 0; j < P.np; ++j) {
+    const uint32_t q = P.pc[j].q;
+    uint32_t* x = sm + j * P.L;
+    for (int i = threadIdx.x; i < P.L; i += blockDim.x) {
+      const uint32_t d = field32(mag, len, (long long)P.w * i) & dmask;
+      x[i] = (sign < 0 && d) ? q - d : d;
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < P.np; ++j)
+    cta_ntt_fwd(sm + j * P.L, P.logL, P.tw + j * P.Lmax, P.twp + j * P.Lmax,
+                P.pc[j].q);
+  for (int j = 0; j < P.np; ++j) {
+    const PrimeConsts& c = P.pc[j];
+    for (int i = threadIdx.x; i < P.L; i += blockDim.x) {
+      uint32_t v = sm[j * P.L + i];
+      if (mont) v = reduce_2q(mul_shoup(v, c.r32, c.r32s, c.q), c.q);
+      out[j * P.L + i] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------ forward transform --
+// For items i in [0,count): integer (in_base + i) of `src` -> transform at
+// out + (out_base + i)*NW.  Records deg = floor((bits-1)/w) via atomicMax.
+// Used for the strip moments at setup and for V_p / R_p rows every stage.
+__global__ void k_fwd_ints(DevPlan P, IntBuf src, long long in_base,
+                           uint32_t* out, long long out_base, int count,
+                           int mont, int* maxdeg, int* err) {
+  extern __shared__ uint32_t sm[];
+  const int item = blockIdx.x;
+  if (item >= count) return;
+  if (err && stage_aborted(err)) return;
+  uint32_t* mag = sm + P.np * P.L;
+  int len;
+  const int sign = load_int(src, in_base + item, P.cap, mag, &len);
+  if (maxdeg && len > 0 && threadIdx.x == 0)
+    atomicMax(maxdeg, (limbs_bits(mag, len) - 1) / P.w);
+  transform_int(P, mag, len, sign, sm, out + (out_base + item) * (long long)P.NW,
+                mont != 0, err);
+}
+
+// ------------------------------------------------------- workspace init ----
+// ldlt.cpp:38-44: cols[c][r-c] = strip[r+c], cols[c][0] -= x.  By linearity
+// the transform of strip[2c]-x is that[2c] - xhat.  grid.x: word blocks,
+// grid.y: column c (all rows r >= c of an owned column).
+__global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
+                         const long long* colbase, uint32_t* W) {
+  const int c = blockIdx.y;
+  const long long base = colbase[c];
+  if (base < 0) return;
+  const int wd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wd >= P.NW) return;
+  const uint32_t q = P.pc[wd / P.L].q;
+  for (int r = c; r < P.n; ++r) {
+    uint32_t v = that[(long long)(r + c) * P.NW + wd];
+    if (r == c) {
+      const uint32_t xv = xhat[wd];
+      v = v >= xv ? v - xv : v + q - xv;
+    }
+    W[(base + (r - c)) * P.NW + wd] = v;
+  }
+}
+
+// ------------------------------------------------------------ extraction ---
+// Stage p, rows r in [p, n): W[r][p] back to an exact integer (inverse NTT,
+// CRT, carry resolution).  Then
+//   pivot = W[p][p], ZeroPivot if 0                    (ldlt.cpp:48-50)
+//   V_p[r] = tdiv_q_2exp(W[r][p], K/2)                 (ldlt.cpp:54-55)
+//   ZeroPivot if V_p[p] == 0 and p < n-1               (ldlt.cpp:56)
+// V goes to vint[slot][r]; the full pivot to piv[p].
+__global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
+                          int p, IntBuf vint, long long vrow0, IntBuf piv,
+                          int* maxbitsV, int* err) {
+  extern __shared__ uint32_t sm[];
+  if (stage_aborted(err)) return;
+  const int r = p + blockIdx.x;
+  if (r >= P.n) return;
+  const int L = P.L, np = P.np, T = P.T, w = P.w;
+  const int M = L + T;
+  uint32_t* A = sm;                       // np*L residues -> CRT words
+  int* S = (int*)(sm + np * L);           // M digit sums
+  uint32_t* Dg = sm + np * L + M;         // M digits
+  uint32_t* Lb = Dg + M;                  // cap limbs of |W|
+  uint32_t* red = Lb + P.cap;             // scan scratch
+
+  const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
+  for (int i = threadIdx.x; i < P.NW; i += blockDim.x) A[i] = src[i];
+  __syncthreads();
+  for (int j = 0; j < np; ++j)
+    cta_ntt_inv(A + j * L, P.logL, P.itw + j * P.Lmax, P.itwp + j * P.Lmax,
+                P.pc[j].q);
+
+  // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    uint32_t a[kMaxPrimes];
+    for (int j = 0; j < np; ++j) {
+      const uint32_t q = P.pc[j].q;
+      uint32_t v = reduce_2q(A[j * L + i], q);
+      a[j] = reduce_2q(mul_shoup(v, P.invL[j], P.invLp[j], q), q);
+    }
+    const uint32_t q0 = P.pc[0].q, q1 = P.pc[1].q;
+    const uint32_t x0 = a[0];
+    const uint32_t x0m1 = x0 >= q1 ? x0 - q1 : x0;
+    const uint32_t x1 =
+        reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
+    unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
+    if (np == 3) {
+      const uint32_t q2 = P.pc[2].q;
+      const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
+      uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
+      u = reduce_2q(u, q2);
+      const uint32_t x2 =
+          reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
+      v += (unsigned __int128)x2 * P.q01;
+    }
+    const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
+    const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
+    if (v >= H) v -= Q;  // wraps to the two's complement of a negative value
+    for (int t = 0; t < np; ++t) A[t * L + i] = (uint32_t)(v >> (32 * t));
+  }
+  __syncthreads();
+
+  // Digit sums: s_k = sum_t piece_t(c_{k-t}); pieces are w-bit fields of the
+  // two's complement coefficient, the top piece carries the sign.
+  const uint32_t dmask = (1u << w) - 1u;
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    int s = 0;
+    for (int t = 0; t < T; ++t) {
+      const int i = k - t;
+      if (i < 0 || i >= L) continue;
+      __int128 c = 0;
+      for (int u = np - 1; u >= 0; --u) c = (c << 32) | A[u * L + i];
+      c = (c << (128 - 32 * np)) >> (128 - 32 * np);  // sign-extend
+      const __int128 sh = c >> (w * t);
+      s += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
+    }
+    S[k] = s;
+  }
+  __syncthreads();
+
+  int sg = 1;
+  int carry = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    carry = cta_resolve(
+        M, w,
+        [&](int k) -> int64_t {
+          const int64_t cur = (int64_t)sg * S[k];
+          int64_t v = cur & (int64_t)dmask;
+          if (k > 0) v += ((int64_t)sg * S[k - 1]) >> w;
+          return v;
+        },
+        [&](int k, uint32_t d) { Dg[k] = d; }, red);
+    if (carry >= 0) break;
+    sg = -1;  // negative: resolve the magnitude instead
+  }
+  if (carry != 0) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapCrt);
+    return;
+  }
+  // Pack base-2^w digits into 32-bit limbs of |W|.
+  const int nl = min(P.cap, (w * M + 31) / 32);
+  for (int m = threadIdx.x; m < P.cap; m += blockDim.x) {
+    uint64_t acc = 0;
+    if (m < nl) {
+      const int first = (32 * m) / w;
+      for (int k = first; k < M && (long long)w * k < 32LL * m + 32; ++k) {
+        const int shl = w * k - 32 * m;
+        acc |= shl >= 0 ? ((uint64_t)Dg[k] << shl) : ((uint64_t)Dg[k] >> -shl);
+      }
+    }
+    Lb[m] = (uint32_t)acc;
+  }
+  __syncthreads();
+  const int len = cta_limb_len(Lb, P.cap, red);
+  // anything beyond cap limbs would have been dropped: verify
+  if (threadIdx.x == 0 && (long long)w * M > 32LL * P.cap) {
+    for (int k = (32 * P.cap) / w; k < M; ++k)
+      if (Dg[k] && (long long)w * (k + 1) > 32LL * P.cap)
+        atomicOr(&err[kErrCapacity], kCapLimbs);
+  }
+  const int wsign = len == 0 ? 0 : sg;
+
+  if (r == p) {  // pivot
+    if (threadIdx.x == 0) {
+      piv.hdr[p] = wsign * len;
+      if (len == 0) atomicMin(&err[kErrZeroPivot], p);
+    }
+    uint32_t* dst = piv.limbs + (long long)p * P.cap;
+    for (int m = threadIdx.x; m < P.cap; m += blockDim.x) dst[m] = Lb[m];
+  }
+  // V = |W| >> k2 with the sign kept (tdiv_q_2exp).
+  const long long vidx = vrow0 + r;
+  uint32_t* vdst = vint.limbs + vidx * P.cap;
+  for (int m = threadIdx.x; m < P.cap; m += blockDim.x)
+    vdst[m] = field32(Lb, len, 32LL * m + P.k2);
+  const int vbits = max(0, limbs_bits(Lb, len) - P.k2);
+  const int vlen = (vbits + 31) / 32;
+  if (threadIdx.x == 0) {
+    vint.hdr[vidx] = vlen == 0 ? 0 : wsign * vlen;
+    if (r == p && vlen == 0 && p < P.n - 1) atomicMin(&err[kErrZeroPivot], p);
+    if (r > p) atomicMax(&maxbitsV[p], vbits);
+  }
+}
+
+// ------------------------------------------------------------- reciprocal --
+// Per stage, one CTA: Y ~ 2^S / |V_p| with |Y - 2^S/|V_p|| <= 2, where
+// S = bits(V_p) + e + 32 and e bounds the bits of every ratio of this stage.
+// Newton iteration Y += Y(2^S - D Y)/2^S from a 64-bit seed.  Scratch lives
+// in global memory (single CTA, L2 resident).  ys[0] = S, ys[1] = nY.
+__global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
+                        const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
+                        uint32_t* scratch, int* err) {
+  __shared__ uint32_t red[64];
+  if (stage_aborted(err)) return;
+  const int cap = P.cap;
+  uint32_t* D = scratch;
+  int nD;
+  load_int(vint, prow, cap, D, &nD);
+  if (nD == 0) return;  // flagged as ZeroPivot by k_extract
+  const int n = limbs_bits(D, nD);
+  const int amax = maxbitsV[p] + P.k2;
+  const int e = max(amax - n + 2, 1);
+  const int g = 32;
+  const int S = n + e + g;
+  const int nY = (e + g + 2 + 31) / 32 + 1;
+  if (nY > P.ycap) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return;
+  }
+  uint32_t* Y = D + cap;
+  uint32_t* Pr = Y + P.ycap;                 // nD + nY + 1
+  uint32_t* E = Pr + cap + P.ycap + 2;       // nD + nY + 1
+  uint32_t* Tm = E + cap + P.ycap + 2;       // nY + nE
+  uint32_t* col = Tm + cap + 2 * P.ycap + 4; // 3 * max product
+  // seed from the top 64 bits of D
+  if (threadIdx.x == 0) {
+    const uint32_t hi = field32(D, nD, (long long)n - 32);
+    const uint32_t lo = field32(D, nD, (long long)n - 64);
+    const double d = ldexp((double)hi, 32) + (double)lo;  // [2^63, 2^64)
+    const unsigned long long y63 =
+        (unsigned long long)(ldexp(1.0, 126) / d);        // (2^62, 2^63]
+    const int sh = S - n - 62;                            // Y0 = y63 * 2^sh
+    for (int i = 0; i < nY; ++i) {
+      // limb i of y63 * 2^sh
+      const long long off = 32LL * i - sh;
+      uint32_t v = 0;
+      if (off > -64 && off < 64) {
+        const uint64_t hv = off >= 0 ? (y63 >> off) : (y63 << -off);
+        v = (uint32_t)hv;
+        if (off < 0 && off > -32) v = (uint32_t)(y63 << -off);
+      }
+      Y[i] = v;
+    }
+  }
+  __syncthreads();
+  int iters = 2;
+  while ((48 << (iters - 2)) < e + g + 2) ++iters;
+  ++iters;
+  const int nP = nD + nY;
+  for (int it = 0; it < iters; ++it) {
+    // Pr = D*Y
+    cta_mul(D, nD, Y, nY, Pr, nP, col, red);
+    // E = 2^S - D*Y (signed) over nP+1 limbs
+    const int nEw = nP + 1;
+    const int Sl = S / 32;
+    const uint32_t Sb = 1u << (S % 32);
+    int sgn = 1, carry = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      carry = cta_resolve(
+          nEw, 32,
+          [&](int k) -> int64_t {
+            const int64_t a = (k == Sl) ? (int64_t)Sb : 0;
+            const int64_t b = k < nP ? (int64_t)Pr[k] : 0;
+            return sgn > 0 ? a - b : b - a;
+          },
+          [&](int k, uint32_t dd) { E[k] = dd; }, red);
+      if (carry >= 0) break;
+      sgn = -1;
+    }
+    const int nE = cta_limb_len(E, nEw, red);
+    if (nE == 0) break;
+    // Tm = Y * |E| >> S
+    const int nT = nY + nE;
+    cta_mul(Y, nY, E, nE, Tm, nT, col, red);
+    // Y +-= Tm >> S
+    cta_resolve(
+        nY, 32,
+        [&](int k) -> int64_t {
+          const int64_t t = field32(Tm, nT, 32LL * k + S);
+          return sgn > 0 ? (int64_t)Y[k] + t : (int64_t)Y[k] - t;
+        },
+        [&](int k, uint32_t dd) { Pr[k] = dd; }, red);
+    for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Pr[i];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < P.ycap; i += blockDim.x)
+    Ybuf[i] = i < nY ? Y[i] : 0u;
+  if (threadIdx.x == 0) {
+    ys[0] = S;
+    ys[1] = nY;
+  }
+}
+
+// ---------------------------------------------------------------- ratios ---
+// Stage p, rows r in (p, n):  R_p[r] = tdiv_q(V_p[r] << K/2, V_p[p])
+// (ldlt.cpp:15-20, 57-58).  Barrett: q~ = (|V_r| Y) >> (S - K/2) is within
+// one of the true quotient; the remainder window |V_r|2^{K/2} - q~|V_p|
+// (nD+2 limbs) decides the correction exactly.
+__global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+                         const uint32_t* Ybuf, const int* ys, IntBuf rint,
+                         long long rrow0, uint32_t* gscratch, int use_gscratch,
+                         int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  if (stage_aborted(err)) return;
+  const int r = p + 1 + blockIdx.x;
+  if (r >= P.n) return;
+  const int cap = P.cap, ycap = P.ycap;
+  const long long span = div_span_words(cap, ycap);
+  uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * span : sm_dyn;
+  uint32_t* V = sm;
+  uint32_t* D = V + cap;
+  uint32_t* Y = D + cap;
+  uint32_t* Pr = Y + ycap;                 // cap + ycap
+  uint32_t* red = Pr + cap + ycap + 2;     // 64
+  uint32_t* col = red + 64;                // 3 * (cap + ycap + 2)
+  uint32_t* Qt = col + 3 * (cap + ycap + 2);  // cap + ycap
+  uint32_t* Wa = Qt + cap + ycap + 2;      // cap + 2
+  uint32_t* Wb = Wa + cap + 2;             // cap + 2
+
+  int na, nD;
+  const int sV = load_int(vint, vrow0 + r, cap, V, &na);
+  const int sD = load_int(vint, vrow0 + p, cap, D, &nD);
+  const long long ridx = rrow0 + r;
+  if (na == 0) {
+    if (threadIdx.x == 0) rint.hdr[ridx] = 0;
+    uint32_t* dst = rint.limbs + ridx * cap;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x) dst[i] = 0u;
+    return;
+  }
+  const int S = ys[0], nY = ys[1];
+  for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
+  __syncthreads();
+  // q~ = (|V| * Y) >> (S - k2)
+  const int nP = na + nY;
+  cta_mul(V, na, Y, nY, Pr, nP, col, red);
+  const int shift = S - P.k2;
+  const int nQ = max(0, (32 * nP - shift + 31) / 32);
+  for (int i = threadIdx.x; i < nQ; i += blockDim.x)
+    Qt[i] = field32(Pr, nP, 32LL * i + shift);
+  __syncthreads();
+  int nq = cta_limb_len(Qt, nQ, red);
+  // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
+  const int nw = nD + 2;
+  cta_mul(Qt, nq, D, nD, Wb, nw, col, red);
+  cta_resolve(
+      nw, 32,
+      [&](int k) -> int64_t {
+        return (int64_t)field32(V, na, 32LL * k - P.k2) - (int64_t)Wb[k];
+      },
+      [&](int k, uint32_t d) { Wa[k] = d; }, red);
+  int adj = 0;
+  if (Wa[nw - 1] & 0x80000000u) {
+    adj = -1;  // remainder negative: q~ was one too large
+  } else {
+    // r - D >= 0 ? then q~ was one too small
+    cta_resolve(
+        nw, 32,
+        [&](int k) -> int64_t {
+          return (int64_t)Wa[k] - (int64_t)(k < nD ? D[k] : 0u);
+        },
+        [&](int k, uint32_t d) { Wb[k] = d; }, red);
+    if (!(Wb[nw - 1] & 0x80000000u)) {
+      adj = 1;
+      // and r - 2D must be negative
+      cta_resolve(
+          nw, 32,
+          [&](int k) -> int64_t {
+            return (int64_t)Wb[k] - (int64_t)(k < nD ? D[k] : 0u);
+          },
+          [&](int k, uint32_t d) { Wa[k] = d; }, red);
+      if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
+        atomicOr(&err[kErrInternal], kIntDivision);
+    }
+  }
+  if (adj != 0) {
+    const int nn = nq + 1;
+    cta_resolve(
+        nn, 32,
+        [&](int k) -> int64_t {
+          return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
+        },
+        [&](int k, uint32_t d) { Pr[k] = d; }, red);
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = Pr[i];
+    __syncthreads();
+    nq = cta_limb_len(Qt, nn, red);
+  }
+  if (nq > cap) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return;
+  }
+  const int rs = sV * sD;
+  uint32_t* dst = rint.limbs + ridx * cap;
+  for (int i = threadIdx.x; i < cap; i += blockDim.x)
+    dst[i] = i < nq ? Qt[i] : 0u;
+  if (threadIdx.x == 0) rint.hdr[ridx] = nq == 0 ? 0 : rs * nq;
+}
+
+// --------------------------------------------------------- trailing update -
+// W[r][c] -= sum_{s} Vhat[s][c] * Rhat[s][r]   for c in [c_begin, c_end),
+// r in [c, n), pointwise in the transform domain (ldlt.cpp:65-71, summed over
+// the panel's stages: exact, so order-free).  One thread per transform word,
+// a TILE x TILE (r,c) register tile, one 64-bit accumulator per pair for the
+// whole panel (products < 2^56, <= 256 stages), one Montgomery reduction.
+template <int TILE>
+__global__ void __launch_bounds__(128)
+k_update(DevPlan P, uint32_t* W, const long long* colbase,
+         const uint32_t* Vhat, const uint32_t* Rhat, long long row_stride_slot,
+         int nslots, int c_begin, int c_end, int nct, int nrt, const int* err) {
+  if (stage_aborted(err)) return;
+  const int wd = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wd >= P.NW) return;
+  // tile index -> (ct, rt) with rt >= ct
+  int t = blockIdx.y, ct = 0;
+  while (t >= nrt - ct) {
+    t -= nrt - ct;
+    ++ct;
+  }
+  const int rt = ct + t;
+  const int c0 = c_begin + ct * TILE;
+  const int r0 = c_begin + rt * TILE;
+  const PrimeConsts pc = P.pc[wd / P.L];
+
+  uint64_t acc[TILE][TILE];
+#pragma unroll
+  for (int i = 0; i < TILE; ++i)
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) acc[i][j] = 0;
+
+  for (int s = 0; s < nslots; ++s) {
+    const uint32_t* vs = Vhat + s * row_stride_slot;
+    const uint32_t* rs = Rhat + s * row_stride_slot;
+    uint32_t a[TILE], b[TILE];
+#pragma unroll
+    for (int i = 0; i < TILE; ++i) {
+      const int r = r0 + i;
+      a[i] = r < P.n ? __ldg(rs + (long long)r * P.NW + wd) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) {
+      const int c = c0 + j;
+      b[j] = c < c_end ? __ldg(vs + (long long)c * P.NW + wd) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < TILE; ++i)
+#pragma unroll
+      for (int j = 0; j < TILE; ++j) acc[i][j] += (uint64_t)a[i] * b[j];
+  }
+#pragma unroll
+  for (int j = 0; j < TILE; ++j) {
+    const int c = c0 + j;
+    if (c >= c_end) continue;
+    const long long base = colbase[c];
+#pragma unroll
+    for (int i = 0; i < TILE; ++i) {
+      const int r = r0 + i;
+      if (r < c || r >= P.n) continue;
+      uint32_t* ptr = W + (base + (r - c)) * (long long)P.NW + wd;
+      const uint32_t t32 = reduce_sum64(acc[i][j], pc);
+      const uint32_t old = *ptr;
+      *ptr = old >= t32 ? old - t32 : old + pc.q - t32;
+    }
+  }
+}
+
+
+// -------------------------------------------------------------- validate ---
+// Checks the transform capacity after the factorisation: for every stage
+// deg V + deg R < L (no cyclic wrap) and the accumulated coefficient bound
+// sum_p (min(degV,degR)+1)(2^w-1)^2 + 2^(w+1) < Q/2 (exact CRT).
+__global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
+                           int nstages, int* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long double bound = 2.0L * (long double)(1u << P.w);
+  const long double dig2 = ((long double)((1u << P.w) - 1)) *
+                           ((long double)((1u << P.w) - 1));
+  for (int p = 0; p < nstages; ++p) {
+    const int dv = maxdegV[p], dr = maxdegR[p];
+    if (dv < 0 || dr < 0) continue;
+    if (dv + dr >= P.L) atomicOr(&err[kErrCapacity], kCapDegree);
+    bound += (long double)(min(dv, dr) + 1) * dig2;
+  }
+  const long double half =
+      (long double)P.Hhi * 18446744073709551616.0L + (long double)P.Hlo;
+  if (bound >= half * 0.5L) atomicOr(&err[kErrCapacity], kCapCoeff);
+}
+
+// ------------------------------------------------------ launch wrappers --
+
+cudaError_t launch_fwd_ints(const DevPlan& P, IntBuf src, long long in_base,
+                            uint32_t* out, long long out_base, int count,
+                            int mont, int* maxdeg, int* err,
+                            cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  const size_t smem = (size_t)(P.np * P.L + P.cap) * 4;
+  k_fwd_ints<<<count, 256, smem, st>>>(P, src, in_base, out, out_base, count,
+                                       mont, maxdeg, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
+                          const uint32_t* xhat, const long long* colbase,
+                          uint32_t* W, cudaStream_t st) {
+  dim3 grid((P.NW + 255) / 256, P.n);
+  k_init_w<<<grid, 256, 0, st>>>(P, that, xhat, colbase, W);
+  return cudaGetLastError();
+}
+
+size_t extract_smem_bytes(const DevPlan& P) {
+  const int M = P.L + P.T;
+  return (size_t)(P.np * P.L + 2 * M + P.cap + 64) * 4;
+}
+
+cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
+                           const long long* colbase, int p, IntBuf vint,
+                           long long vrow0, IntBuf piv, int* maxbitsV,
+                           int* err, cudaStream_t st) {
+  const int rows = P.n - p;
+  if (rows <= 0) return cudaSuccess;
+  k_extract<<<rows, 256, extract_smem_bytes(P), st>>>(
+      P, W, colbase, p, vint, vrow0, piv, maxbitsV, err);
+  return cudaGetLastError();
+}
+
+size_t recip_scratch_words(const DevPlan& P) {
+  const int cap = P.cap, ycap = P.ycap;
+  return (size_t)cap + ycap + 2 * (cap + ycap + 2) + (cap + 2 * ycap + 4) +
+         3 * (cap + 2 * ycap + 4) + 64;
+}
+
+cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
+                         const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
+                         uint32_t* scratch, int* err, cudaStream_t st) {
+  k_recip<<<1, 512, 0, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
+                             err);
+  return cudaGetLastError();
+}
+
+size_t divide_smem_words(const DevPlan& P) { return div_span_words(P.cap, P.ycap); }
+
+cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
+                          int p, const uint32_t* Ybuf, const int* ys,
+                          IntBuf rint, long long rrow0, uint32_t* gscratch,
+                          int use_gscratch, int* err, cudaStream_t st) {
+  const int rows = P.n - p - 1;
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = use_gscratch ? 0 : divide_smem_words(P) * 4;
+  k_divide<<<rows, 256, smem, st>>>(P, vint, vrow0, p, Ybuf, ys, rint, rrow0,
+                                    gscratch, use_gscratch, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
+                          const long long* colbase, const uint32_t* Vhat,
+                          const uint32_t* Rhat, long long row_stride_slot,
+                          int nslots, int c_begin, int c_end, const int* err,
+                          cudaStream_t st) {
+  if (c_begin >= c_end || nslots <= 0) return cudaSuccess;
+  const int nct = (c_end - c_begin + tile - 1) / tile;
+  const int nrt = (P.n - c_begin + tile - 1) / tile;
+  long long tiles = 0;
+  for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
+  dim3 grid((P.NW + 127) / 128, (unsigned)tiles);
+  if (tile == 8)
+    k_update<8><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
+                                      row_stride_slot, nslots, c_begin, c_end,
+                                      nct, nrt, err);
+  else
+    k_update<4><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
+                                      row_stride_slot, nslots, c_begin, c_end,
+                                      nct, nrt, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
+                            const int* maxdegR, int nstages, int* err,
+                            cudaStream_t st) {
+  k_validate<<<1, 32, 0, st>>>(P, maxdegV, maxdegR, nstages, err);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
+                              bool* div_global) {
+  int dev;
+  cudaGetDevice(&dev);
+  int maxopt = 0;
+  cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t ext = extract_smem_bytes(P);
+  const size_t fwd = (size_t)(P.np * P.L + P.cap) * 4;
+  if ((int)ext > maxopt || (int)fwd > maxopt) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_extract,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ext)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_fwd_ints,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fwd)) != cudaSuccess)
+    return e;
+  const size_t div = divide_smem_words(P) * 4;
+  *div_smem = div;
+  *div_global = (int)div > maxopt;
+  if (!*div_global) {
+    if ((e = cudaFuncSetAttribute(k_divide,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)div)) != cudaSuccess)
+      return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace hgpu

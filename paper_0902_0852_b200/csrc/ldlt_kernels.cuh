@@ -1,0 +1,108 @@
+// Device-side data layout and kernel declarations of the B200 LDL^T engine.
+//
+// HBM layout:
+//   W       workspace, lower triangle of the owned columns, column-major
+//           packed: entry (r,c) at colbase[c] + (r-c); every entry is NW =
+//           np*L residues (np primes x L NTT points, bit-reversed order),
+//           i.e. the number-theoretic transform of the entry's base-2^w digit
+//           polynomial.  The rank-kb trailing update is pointwise there.
+//   Vint/Rint  per panel slot s and row r: the truncated column value
+//           V_p[r] and ratio R_p[r] as signed limb integers (hdr = sign*len,
+//           cap 32-bit limbs).  This is what a panel owner broadcasts.
+//   Vhat/Rhat  their transforms (Rhat in Montgomery form), per slot and row.
+//   piv     the full pivots W_pp (for the determinant fold).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "modarith.cuh"
+
+namespace hgpu {
+
+// Error words (device int32[kErrWords]).
+enum : int {
+  kErrZeroPivot = 0,  // first stage with a zero pivot (atomicMin), INT_MAX if none
+  kErrCapacity = 1,   // bitmask: transform / limb capacity exceeded
+  kErrInternal = 2,   // bitmask: arithmetic self-check failed
+  kErrWords = 4
+};
+enum : int {
+  kCapDigits = 1,     // an integer needs more than L digits
+  kCapLimbs = 2,      // an integer needs more than cap limbs
+  kCapCrt = 4,        // residue reconstruction out of range
+  kCapDegree = 8,     // deg V + deg R >= L somewhere
+  kCapCoeff = 16,     // accumulated coefficient bound reaches Q/2
+  kIntDivision = 1,   // quotient correction out of range
+  kIntRecip = 2,      // reciprocal did not converge
+};
+
+struct DevPlan {
+  int n;        // matrix order
+  int K;        // fractional bits
+  int k2;       // K/2
+  int np;       // primes in use (2 or 3)
+  int logL, L;  // transform length
+  int w;        // digit width in bits
+  int T;        // w-bit pieces per reconstructed coefficient
+  int cap;      // limbs per stored integer
+  int ycap;     // limbs of the per-stage reciprocal
+  int NW;       // np*L words per transformed number
+  int Lmax;     // twiddle table stride
+  PrimeConsts pc[kMaxPrimes];
+  uint32_t invL[kMaxPrimes], invLp[kMaxPrimes];
+  // Garner constants (q0 > q1 > q2)
+  uint32_t g1, g1p;          // q0^-1 mod q1
+  uint32_t g2, g2p;          // (q0 q1)^-1 mod q2
+  uint32_t q0m2, q0m2p;      // q0 mod q2
+  unsigned long long q01;    // q0*q1
+  unsigned long long Qlo, Qhi, Hlo, Hhi;  // Q and Q/2 (128-bit)
+  const uint32_t* tw;   // [np][Lmax]
+  const uint32_t* twp;
+  const uint32_t* itw;
+  const uint32_t* itwp;
+};
+
+struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
+  int* hdr;
+  uint32_t* limbs;
+};
+
+// Shared-memory words of one k_divide CTA (layout in ldlt_kernels.cu).
+__host__ __device__ inline long long div_span_words(int cap, int ycap) {
+  return 2LL * cap + ycap + (cap + ycap + 2) + 64 + 3LL * (cap + ycap + 2) +
+         (cap + ycap + 2) + 2LL * (cap + 2);
+}
+
+// Host launch wrappers (ldlt_kernels.cu).
+cudaError_t launch_fwd_ints(const DevPlan& P, IntBuf src, long long in_base,
+                            uint32_t* out, long long out_base, int count,
+                            int mont, int* maxdeg, int* err, cudaStream_t st);
+cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
+                          const uint32_t* xhat, const long long* colbase,
+                          uint32_t* W, cudaStream_t st);
+cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
+                           const long long* colbase, int p, IntBuf vint,
+                           long long vrow0, IntBuf piv, int* maxbitsV,
+                           int* err, cudaStream_t st);
+size_t recip_scratch_words(const DevPlan& P);
+cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
+                         const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
+                         uint32_t* scratch, int* err, cudaStream_t st);
+size_t divide_smem_words(const DevPlan& P);
+cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
+                          int p, const uint32_t* Ybuf, const int* ys,
+                          IntBuf rint, long long rrow0, uint32_t* gscratch,
+                          int use_gscratch, int* err, cudaStream_t st);
+cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
+                          const long long* colbase, const uint32_t* Vhat,
+                          const uint32_t* Rhat, long long row_stride_slot,
+                          int nslots, int c_begin, int c_end, const int* err,
+                          cudaStream_t st);
+cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
+                            const int* maxdegR, int nstages, int* err,
+                            cudaStream_t st);
+cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
+                              bool* div_global);
+
+}  // namespace hgpu

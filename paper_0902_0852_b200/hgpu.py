@@ -1,0 +1,251 @@
+"""ctypes binding of libhgpu.so (include/hgpu.h), the B200 LDL^T engine.
+
+Mirrors the reference's C++ entry points for the hot path
+(/root/reference/proj/src/ldlt.hpp):
+
+* ``ldlt_det_serial(m, x, capture)``  -> :meth:`HankelMatrixGPU.ldlt`
+  (ldlt.hpp:30-31, ldlt.cpp:31-77)
+* ``ldlt_det_parallel(m, x, workers)`` -> the same call after
+  :meth:`HankelMatrixGPU.set_comm` (one process per GPU; ldlt.hpp:56-57)
+* ``LdltCapture`` (ldlt.hpp:16-19)     -> :class:`LdltResult` pivots/ratios
+* ``ZeroPivot(pivot_index, frac_bits)`` (errors.hpp:49-58) -> :class:`ZeroPivot`
+
+There is no CPU fallback: importing this module on a machine without the
+built library, or factoring without a CUDA device, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhgpu.so")
+
+HGPU_CAPTURE = 1
+HGPU_FOLD = 2
+HGPU_PROFILE = 4
+
+STATUS = {
+    0: "ok", 1: "invalid argument", 2: "zero pivot", 3: "precision mismatch",
+    4: "cuda", 5: "capacity", 6: "internal", 7: "communication",
+}
+
+# every symbol include/hgpu.h declares
+EXPORTS = (
+    "hgpu_matrix_new", "hgpu_matrix_free", "hgpu_nccl_unique_id",
+    "hgpu_matrix_set_comm", "hgpu_ldlt_factor", "hgpu_factor_order",
+    "hgpu_factor_frac_bits", "hgpu_factor_pivot", "hgpu_factor_ratio",
+    "hgpu_factor_det", "hgpu_factor_device_ms", "hgpu_factor_update_stats",
+    "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
+    "hgpu_last_zero_pivot", "hgpu_last_error", "hgpu_version",
+)
+
+
+class HgpuError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"hgpu {STATUS.get(status, status)}: {message}")
+        self.status = status
+
+
+class ZeroPivot(HgpuError):
+    """heig::ZeroPivot (errors.hpp:49-58): same pivot index and frac bits."""
+
+    def __init__(self, pivot_index: int, frac_bits: int, message: str):
+        super().__init__(2, message)
+        self.pivot_index = pivot_index
+        self.frac_bits = frac_bits
+
+
+class PrecisionMismatch(HgpuError):
+    pass
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Loads libhgpu.so (built by ``__graft_entry__.build()``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FileNotFoundError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, u32p, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint32), ctypes.c_long
+    lib.hgpu_matrix_new.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int32), u32p, ctypes.c_int,
+                                    ctypes.POINTER(vp)]
+    lib.hgpu_matrix_free.argtypes = [vp]
+    lib.hgpu_nccl_unique_id.argtypes = [ctypes.c_char_p]
+    lib.hgpu_matrix_set_comm.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+    lib.hgpu_ldlt_factor.argtypes = [vp, i32, u32p, i64, ctypes.c_uint, ctypes.POINTER(vp)]
+    lib.hgpu_factor_order.argtypes = [vp]
+    lib.hgpu_factor_order.restype = i64
+    lib.hgpu_factor_frac_bits.argtypes = [vp]
+    lib.hgpu_factor_frac_bits.restype = i64
+    for name in ("hgpu_factor_pivot",):
+        getattr(lib, name).argtypes = [vp, i64, ctypes.POINTER(i32), ctypes.POINTER(u32p)]
+    lib.hgpu_factor_ratio.argtypes = [vp, i64, i64, ctypes.POINTER(i32), ctypes.POINTER(u32p)]
+    lib.hgpu_factor_det.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u32p)]
+    lib.hgpu_factor_device_ms.argtypes = [vp]
+    lib.hgpu_factor_device_ms.restype = ctypes.c_double
+    lib.hgpu_factor_update_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_factor_free.argtypes = [vp]
+    lib.hgpu_matrix_plan.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 4 + [ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_block_owner.argtypes = [i64, ctypes.c_int]
+    lib.hgpu_block_owner.restype = ctypes.c_int
+    lib.hgpu_last_zero_pivot.restype = i64
+    lib.hgpu_last_error.restype = ctypes.c_char_p
+    lib.hgpu_version.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(status: int, frac_bits: int = 0) -> None:
+    if status == 0:
+        return
+    lib = load()
+    msg = lib.hgpu_last_error().decode()
+    if status == 2:
+        raise ZeroPivot(int(lib.hgpu_last_zero_pivot()), frac_bits, msg)
+    if status == 3:
+        raise PrecisionMismatch(status, msg)
+    raise HgpuError(status, msg)
+
+
+# ----------------------------------------------------------- int <-> limbs --
+
+def int_to_limbs(v: int) -> tuple[int, np.ndarray]:
+    """Python int -> (signed size, little-endian uint32 limbs)."""
+    mag = -v if v < 0 else v
+    nbytes = (mag.bit_length() + 31) // 32 * 4
+    limbs = np.frombuffer(mag.to_bytes(nbytes, "little"), dtype=np.uint32) if nbytes else \
+        np.zeros(0, dtype=np.uint32)
+    n = len(limbs)
+    return (-n if v < 0 else n), limbs
+
+
+def limbs_to_int(size: int, ptr) -> int:
+    n = abs(size)
+    if n == 0:
+        return 0
+    raw = ctypes.string_at(ptr, 4 * n)
+    mag = int.from_bytes(raw, "little")
+    return -mag if size < 0 else mag
+
+
+def pack_ints(values: list[int]) -> tuple[np.ndarray, np.ndarray]:
+    sizes, chunks = [], []
+    for v in values:
+        s, l = int_to_limbs(v)
+        sizes.append(s)
+        chunks.append(l)
+    limbs = np.concatenate(chunks) if chunks else np.zeros(0, dtype=np.uint32)
+    return np.asarray(sizes, dtype=np.int32), np.ascontiguousarray(limbs, dtype=np.uint32)
+
+
+def _u32p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+# ------------------------------------------------------------------ API ----
+
+@dataclass
+class LdltResult:
+    """LdltCapture (ldlt.hpp:16-19) plus the folded determinant."""
+    n: int
+    frac_bits: int
+    pivots: list[int]
+    ratios: dict = field(default_factory=dict)  # (p, r) -> R_p[r]
+    det: int | None = None
+    device_ms: float = 0.0
+    update_launches: int = 0
+    update_ms: float = 0.0
+    update_products: float = 0.0
+
+
+class HankelMatrixGPU:
+    """The anti-diagonal strip of M (HankelMatrix, hankel_matrix.hpp:17-42)
+    resident on one B200, ready for repeated det(M - xI) evaluations."""
+
+    def __init__(self, strip: list[int], frac_bits: int, device: int = 0):
+        lib = load()
+        if len(strip) % 2 == 0 or not strip:
+            raise ValueError("strip must hold 2n-1 anti-diagonals")
+        self.n = (len(strip) + 1) // 2
+        self.frac_bits = frac_bits
+        sizes, limbs = pack_ints(strip)
+        h = ctypes.c_void_p()
+        _check(lib.hgpu_matrix_new(self.n, frac_bits, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                   _u32p(limbs), device, ctypes.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load().hgpu_matrix_free(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_comm(self, rank: int, world: int, nccl_id: bytes) -> None:
+        _check(load().hgpu_matrix_set_comm(self._h, rank, world, nccl_id))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load().hgpu_nccl_unique_id(buf))
+        return buf.raw
+
+    def plan(self) -> dict:
+        lib = load()
+        a, b, c, d = (ctypes.c_int() for _ in range(4))
+        wb = ctypes.c_double()
+        _check(lib.hgpu_matrix_plan(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                    ctypes.byref(d), ctypes.byref(wb)))
+        return {"nprimes": a.value, "length": b.value, "digit_bits": c.value,
+                "cap_limbs": d.value, "workspace_bytes": wb.value}
+
+    def ldlt(self, x: int, capture: bool = False, fold: bool = False, profile: bool = False,
+             x_frac_bits: int | None = None) -> LdltResult:
+        """det(M - xI) via square-root-free LDL^T (ldlt_det_serial)."""
+        lib = load()
+        xs, xl = int_to_limbs(x)
+        flags = (HGPU_CAPTURE if capture else 0) | (HGPU_FOLD if fold else 0) | \
+                (HGPU_PROFILE if profile else 0)
+        f = ctypes.c_void_p()
+        kx = self.frac_bits if x_frac_bits is None else x_frac_bits
+        _check(lib.hgpu_ldlt_factor(self._h, xs, _u32p(xl), kx, flags, ctypes.byref(f)),
+               self.frac_bits)
+        try:
+            n = self.n
+            size = ctypes.c_int32()
+            ptr = ctypes.POINTER(ctypes.c_uint32)()
+            pivots = []
+            for p in range(n):
+                _check(lib.hgpu_factor_pivot(f, p, ctypes.byref(size), ctypes.byref(ptr)))
+                pivots.append(limbs_to_int(size.value, ptr))
+            res = LdltResult(n=n, frac_bits=self.frac_bits, pivots=pivots,
+                             device_ms=lib.hgpu_factor_device_ms(f))
+            if capture:
+                for p in range(n - 1):
+                    for r in range(p + 1, n):
+                        _check(lib.hgpu_factor_ratio(f, p, r, ctypes.byref(size), ctypes.byref(ptr)))
+                        res.ratios[(p, r)] = limbs_to_int(size.value, ptr)
+            if fold:
+                _check(lib.hgpu_factor_det(f, ctypes.byref(size), ctypes.byref(ptr)))
+                res.det = limbs_to_int(size.value, ptr)
+            if profile:
+                nl, ms, prod = ctypes.c_long(), ctypes.c_double(), ctypes.c_double()
+                _check(lib.hgpu_factor_update_stats(f, ctypes.byref(nl), ctypes.byref(ms), ctypes.byref(prod)))
+                res.update_launches, res.update_ms, res.update_products = nl.value, ms.value, prod.value
+            return res
+        finally:
+            lib.hgpu_factor_free(f)
+
+
+def block_owner(block: int, world: int) -> int:
+    return int(load().hgpu_block_owner(block, world))
