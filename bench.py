@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark: the LDL^T (square-root-free Cholesky) factorisation of the
+Hankel moment matrix at BASELINE config 3 (N=1000, beta=1, P=24576 bits).
+
+One step = one full factorisation of M - xI on the device (every stage:
+extraction, pivot reciprocal, ratios, transforms, rank-kb trailing update)
+with x = x1 = -2^-16 * min(1, M00), the secant's first probe
+(secant.cpp:7-16), so ratios are truncated (not the exact x=0 closed form).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §6 for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = {"workload": "LDL^T factorisation of M - x1*I, N=1000, beta=1, P=24576",
+          "n": 1000, "beta": "1", "precision_bits": 24576, "shift": "x1=-2^-16",
+          "l2": "workspace 12.3 GB >> 126 MB L2 (inputs larger than L2)"}
+METRIC = "Cholesky MP-MAC/s (N=1000, beta=1, P=24576)"
+UNIT = "MP-MAC/s"
+
+
+def mp_macs(n: int) -> float:
+    """(N^3 - N)/6 MP multiply-adds per factorisation (ldlt.cpp:65-71)."""
+    return (n ** 3 - n) / 6.0
+
+
+def schoolbook_limb_products(n: int, k: int) -> float:
+    """Sum over the trailing updates of ceil(bits(V)/32)*ceil(bits(R)/32) for
+    beta=1, x=0 (closed form): the schoolbook-equivalent work,
+    independent of the algorithm actually used."""
+    import numpy as np
+    k2 = k // 2
+    lf = np.zeros(n + 1)
+    for i in range(2, n + 1):
+        lf[i] = lf[i - 1] + math.log2(i)
+    total = 0.0
+    for p in range(n - 1):
+        c = np.arange(p + 1, n)
+        vbits = 2 * lf[c] - lf[c - p] + k2 + 1       # (c!)^2/(c-p)! 2^k2
+        rbits = 2 * lf[c] - 2 * lf[p] - lf[c - p] + k2 + 1  # C(r,p) r!/p! 2^k2
+        vl = np.ceil(vbits / 32.0)
+        rl = np.ceil(rbits / 32.0)
+        # sum_{c<=r} vl[c]*rl[r] = sum_c vl[c] * suffix(rl)[c]
+        suffix = np.cumsum(rl[::-1])[::-1]
+        total += float(np.dot(vl, suffix))
+    return total
+
+
+# --------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """Samples nvidia-smi SM clocks + throttle reasons while running."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    if out.returncode == 0 and out.stdout.strip():
+                        self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- inputs ---
+
+def config_strip(n: int, k: int) -> list[int]:
+    """beta=1 moments M_ij = Gamma(1+i+j) = (i+j)!, exact at K bits: the
+    reference's build_matrix is exact for integer Gamma arguments
+    (hankel_matrix.cpp:13-31, gamma.cpp:193-197)."""
+    strip, f = [], 1
+    for s in range(2 * n - 1):
+        if s > 0:
+            f *= s
+        strip.append(f << k)
+    return strip
+
+
+def x1_shift(strip: list[int], k: int) -> int:
+    """initial_points (secant.cpp:7-16): x1 = -trunc(min(1, M00) / 2^16)."""
+    one = 1 << k
+    smaller = strip[0] if strip[0] < one else one
+    mant = smaller >> 16
+    return -(mant if mant else 1)
+
+
+# ------------------------------------------------------------- GPU arm -----
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_gpu(args) -> None:
+    import torch
+    world, rank, local = _dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    from paper_0902_0852_b200 import hgpu
+    n, k = CONFIG["n"], CONFIG["precision_bits"]
+    strip = config_strip(n, k)
+    x = x1_shift(strip, k)
+
+    m = hgpu.HankelMatrixGPU(strip, k, device=local)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [hgpu.HankelMatrixGPU.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        m.set_comm(rank, world, obj[0])
+    plan = m.plan()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        m.ldlt(x)
+    barrier()
+    clocks = ClockSampler(local).start()
+    dev_ms, launches, upd_ms, upd_prod, upd_n = [], 0, 0.0, 0.0, 0
+    for _ in range(args.steps):
+        r = m.ldlt(x, profile=True)
+        dev_ms.append(r.device_ms)
+        launches += r.launches
+        upd_ms += r.update_ms
+        upd_prod += r.update_products
+        upd_n += r.update_launches
+    barrier()
+    clk = clocks.stop()
+    total_ms = sum(dev_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = mp_macs(n) / (ms_per_step * 1e-3)
+
+    # end to end through the public API with host buffers: strip upload,
+    # transform plan, factorisation, pivots back to the host -- every step
+    e2e_ms, h2d, d2h = [], 0, 0
+    import numpy as np
+    sizes, limbs = hgpu.pack_ints(strip)
+    h2d = sizes.nbytes + limbs.nbytes + 8
+    del m
+    for _ in range(max(1, min(args.steps, 3))):
+        barrier()
+        t0 = time.perf_counter()
+        mm = hgpu.HankelMatrixGPU(strip, k, device=local)
+        if world > 1:
+            import torch.distributed as dist
+            obj = [hgpu.HankelMatrixGPU.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            mm.set_comm(rank, world, obj[0])
+        rr = mm.ldlt(x)
+        barrier()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        d2h = sum((abs(v).bit_length() + 31) // 32 * 4 + 4 for v in rr.pivots)
+        del mm
+    e2e_step = statistics.median(e2e_ms)
+
+    # roofline of the dominant kernel (trailing update): modular products per
+    # launch / average launch time, against the measured IMAD.WIDE rate
+    probe = probe_imad()
+    upd_avg_ms = upd_ms / max(upd_n, 1)
+    prod_per_launch = upd_prod / max(upd_n, 1)
+    achieved = prod_per_launch / (upd_avg_ms * 1e-3) / 1e12 if upd_n else None
+    peak = probe.get("wide_ops_per_s", 0) / 1e12 or None
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 (exact mod-q residues, 32-bit limbs)",
+        "data": "synthetic: exact factorial moments (the reference's beta=1 strip)",
+        "config": dict(CONFIG, parallelism=f"column-block-cyclic x{world}",
+                       plan=plan),
+        "limb_products_per_s": schoolbook_limb_products(n, k) / (ms_per_step * 1e-3),
+        "e2e": {"value": mp_macs(n) / (e2e_step * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_step},
+        "gpu_launches": launches,
+        "roofline": {"bound": "imad", "kernel": "k_update (trailing rank-kb update)",
+                     "achieved": achieved, "peak": peak, "unit": "Tprod/s (IMAD.WIDE)",
+                     "frac": (achieved / peak) if achieved and peak else None,
+                     "traffic": None, "peak_source": "measured IMAD.WIDE probe (csrc/probe.cu)",
+                     "update_share_of_step": (upd_ms / args.steps) / ms_per_step},
+        "imad_probe": probe,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def probe_imad() -> dict:
+    import ctypes
+    path = os.path.join(ROOT, "paper_0902_0852_b200", "libhgpu_probe.so")
+    if not os.path.exists(path):
+        return {}
+    lib = ctypes.CDLL(path)
+    lib.hgpu_probe_imad.argtypes = [ctypes.c_int] + [ctypes.POINTER(ctypes.c_double)] * 3
+    res = {}
+    for kind, name in ((0, "imad"), (1, "wide")):
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        if lib.hgpu_probe_imad(kind, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)) == 0:
+            res[f"{name}_ops_per_s"] = a.value
+            res[f"{name}_sm_mhz"] = b.value
+            res[f"{name}_per_clk_sm"] = c.value
+    return res
+
+
+# ------------------------------------------------------------ CPU legs -----
+
+def cpu_sample(seconds_budget: float = 20.0):
+    """Times the reference's own ldlt_det_parallel (oracle/_ref, all host
+    threads) on the leading n' x n' block of the config-3 matrix at the same
+    P and shift.  Returns (seconds, n', workers, limb-products of the sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    k = CONFIG["precision_bits"]
+    workers = os.cpu_count() or 1
+    ref = po.RefLib()
+    nprime = 120
+    while True:
+        strip = config_strip(nprime, k)
+        x = x1_shift(strip, k)
+        _, secs = ref.ldlt_parallel(strip, x, k, workers)
+        if secs * 2.2 ** 3 > seconds_budget or nprime >= 400:
+            break
+        nprime = int(nprime * 1.5)
+    return secs, nprime, workers, schoolbook_limb_products(nprime, k)
+
+
+def cpu_baseline(args) -> dict:
+    secs, nprime, workers, lp = cpu_sample()
+    full_lp = schoolbook_limb_products(CONFIG["n"], CONFIG["precision_bits"])
+    est_full_s = secs * full_lp / lp
+    return {"value": mp_macs(CONFIG["n"]) / est_full_s, "unit": UNIT, "cores": workers,
+            "kind": "reference",
+            "sample": f"ldlt_det_parallel (oracle/_ref, {workers} threads) on the leading "
+                      f"{nprime}x{nprime} block at P=24576: {secs:.2f} s; scaled to N=1000 by "
+                      f"schoolbook limb-products ({lp:.3e} -> {full_lp:.3e}): est {est_full_s:.0f} s "
+                      f"per factorisation"}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        cpu_sample(seconds_budget=5.0)
+    for _ in range(args.steps):
+        secs, nprime, workers, lp = cpu_sample(seconds_budget=10.0)
+        full_lp = schoolbook_limb_products(CONFIG["n"], CONFIG["precision_bits"])
+        vals.append(mp_macs(CONFIG["n"]) / (secs * full_lp / lp))
+    v = statistics.median(vals)
+    sample = (f"ldlt_det_parallel (oracle/_ref, {workers} threads) on the leading {nprime}x{nprime} "
+              f"block at P=24576, scaled to N=1000 by schoolbook limb-products")
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": mp_macs(CONFIG["n"]) / v * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "mpz (GMP 6.3.0)", "data": "synthetic: exact factorial moments",
+           "config": dict(CONFIG, parallelism=f"{workers} host threads"), "impl": "reference",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -87,6 +87,8 @@ hgpu_status hgpu_factor_det(const hgpu_factor* f, int32_t* size,
 double hgpu_factor_device_ms(const hgpu_factor* f);
 hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
                                      double* ms, double* products);
+/* Number of device kernels the factorisation launched. */
+long long hgpu_factor_launches(const hgpu_factor* f);
 void hgpu_factor_free(hgpu_factor* f);
 
 /* Plan introspection: primes, transform length, digit width, limb capacity,

@@ -165,6 +165,10 @@ hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
   });
 }
 
+long long hgpu_factor_launches(const hgpu_factor* f) {
+  return f ? f->res.launches : 0;
+}
+
 void hgpu_factor_free(hgpu_factor* f) { delete f; }
 
 hgpu_status hgpu_matrix_plan(const hgpu_matrix* m, int* nprimes, int* length,

@@ -286,7 +286,7 @@ void Matrix::build(int min_logL) {
   D.itw = tw_ + 2 * (size_t)P.np * P.L;
   D.itwp = tw_ + 3 * (size_t)P.np * P.L;
 
-  CU(configure_kernels(D, &div_smem_, &div_global_));
+  CU(configure_kernels(D, &div_smem_, &div_global_, &recip_global_));
 
   const size_t NW = (size_t)D.NW;
   const int kb = P.kb;
@@ -386,6 +386,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
   CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(stats_, 0xff, 3 * (size_t)n * sizeof(int), st));  // -1
+  const long long launches0 = kernel_launch_count();
   CU(cudaEventRecord(ev0_, st));
   CU(launch_fwd_ints(D, IntBuf{x_hdr_, x_limbs_}, 0, xhat_, 0, 1, 0, nullptr,
                      err_, st));
@@ -435,10 +436,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
         const long long row0 = (long long)s * n;  // slot base in row units
+        // left-looking inside the panel: column p receives stages [p0, p)
+        CU(launch_update_col(D, W_, colbase_, vhat_, rhat_, slot_stride, s, p,
+                             err_, st));
         CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, err_, st));
         if (p == n - 1) break;
         CU(launch_recip(D, vint, row0 + p, maxbitsV, p, ybuf_, ys_, rscratch_,
-                        err_, st));
+                        recip_global_ ? 1 : 0, err_, st));
         CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, dscratch_,
                          div_global_ ? 1 : 0, err_, st));
         // transforms of V_p[r], R_p[r] for r in (p, n)
@@ -446,10 +450,6 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                            n - p - 1, 0, maxdegV + p, err_, st));
         CU(launch_fwd_ints(D, rint, row0 + p + 1, rhat_, row0 + p + 1,
                            n - p - 1, 1, maxdegR + p, err_, st));
-        // in-panel columns (p, p1)
-        CU(launch_update(D, P.tile, W_, colbase_, vhat_ + (size_t)s * slot_stride,
-                         rhat_ + (size_t)s * slot_stride, slot_stride, 1, p + 1,
-                         p1, err_, st));
       }
     }
     panel_broadcast(owner, p0, ns, st);
@@ -499,6 +499,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   }
   CU(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));
   CU(cudaEventRecord(ev1_, st));
+  res.launches = kernel_launch_count() - launches0;
 
   int herr[kErrWords];
   CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));

@@ -49,6 +49,7 @@ struct FactorResult {
   double device_ms = 0;
   long update_launches = 0;
   double update_ms = 0, update_products = 0;
+  long long launches = 0;  // our kernels launched by the factorisation
 };
 
 class Matrix {
@@ -108,6 +109,7 @@ class Matrix {
   int* err_ = nullptr;
   size_t div_smem_ = 0;
   bool div_global_ = false;
+  bool recip_global_ = false;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> uev_;

@@ -246,98 +246,115 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
 }
 
 // ------------------------------------------------------------- reciprocal --
-// Per stage, one CTA: Y ~ 2^S / |V_p| with |Y - 2^S/|V_p|| <= 2, where
-// S = bits(V_p) + e + 32 and e bounds the bits of every ratio of this stage.
-// Newton iteration Y += Y(2^S - D Y)/2^S from a 64-bit seed.  Scratch lives
-// in global memory (single CTA, L2 resident).  ys[0] = S, ys[1] = nY.
+// Per stage, one CTA: Y ~ 2^S / |V_p| within a few units, S = n + Pt with
+// n = bits(V_p) and Pt = e + 32, where e bounds the bits of every ratio of the
+// stage.  Newton with precision doubling: level i holds Y_i ~ 2^(n_i+p_i)/D_i
+// for D_i = D truncated to its top n_i = min(n, p_{i+1}+G) bits, and
+//   Y_{i+1} = Y_i 2^d + (Y_i (2^(n'+p_i) - D' Y_i)) / 2^(n'+p_i-d),
+// d = p_{i+1} - p_i.  Only the last level touches Pt-sized operands, so the
+// whole reciprocal costs ~3 Pt x Pt limb products.  ys[0] = S, ys[1] = nY.
+__device__ inline int recip_levels(int Pt, int* lv) {
+  // lv[0] <= 48 < ... < lv[k] = Pt, lv[i] = ceil(lv[i+1]/2) + 8
+  int tmp[40], k = 0;
+  tmp[k++] = Pt;
+  while (tmp[k - 1] > 48) tmp[k] = (tmp[k - 1] + 1) / 2 + 8, ++k;
+  for (int i = 0; i < k; ++i) lv[i] = tmp[k - 1 - i];
+  return k;
+}
+
 __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
                         const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                        uint32_t* scratch, int* err) {
+                        uint32_t* gscratch, int use_gscratch, int* err) {
+  extern __shared__ uint32_t sm_dyn[];
   __shared__ uint32_t red[64];
   if (stage_aborted(err)) return;
-  const int cap = P.cap;
-  uint32_t* D = scratch;
-  int nD;
-  load_int(vint, prow, cap, D, &nD);
+  const int h = vint.hdr[prow];
+  const int nD = h < 0 ? -h : h;
   if (nD == 0) return;  // flagged as ZeroPivot by k_extract
-  const int n = limbs_bits(D, nD);
+  const uint32_t* Dg = vint.limbs + prow * (long long)P.cap;  // global
+  const int n = limbs_bits(Dg, nD);
   const int amax = maxbitsV[p] + P.k2;
   const int e = max(amax - n + 2, 1);
-  const int g = 32;
-  const int S = n + e + g;
-  const int nY = (e + g + 2 + 31) / 32 + 1;
-  if (nY > P.ycap) {
+  const int G = 32;
+  const int Pt = e + G;
+  const int S = n + Pt;
+  const int Lm = (Pt + G + 31) / 32 + 2;  // limbs of any D' or Y
+  const int nYf = (Pt + 2 + 31) / 32 + 1;
+  if (nYf > P.ycap) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     return;
   }
-  uint32_t* Y = D + cap;
-  uint32_t* Pr = Y + P.ycap;                 // nD + nY + 1
-  uint32_t* E = Pr + cap + P.ycap + 2;       // nD + nY + 1
-  uint32_t* Tm = E + cap + P.ycap + 2;       // nY + nE
-  uint32_t* col = Tm + cap + 2 * P.ycap + 4; // 3 * max product
-  // seed from the top 64 bits of D
+  uint32_t* sm = use_gscratch ? gscratch : sm_dyn;
+  uint32_t* Dt = sm;                 // Lm
+  uint32_t* Y = Dt + Lm;             // Lm
+  uint32_t* Pr = Y + Lm;             // 2 Lm + 1
+  uint32_t* E = Pr + 2 * Lm + 1;     // 2 Lm + 2
+  uint32_t* Tm = E + 2 * Lm + 2;     // 3 Lm + 2
+  uint32_t* col = Tm + 3 * Lm + 2;   // 3 (3 Lm + 2)
+  int lv[40];
+  const int nl = recip_levels(Pt, lv);
+  // seed: Y_0 = floor(2^(n+p0)/D) ~ (2^126/top64(D)) >> (62 - p0)
+  const int p0 = lv[0];
   if (threadIdx.x == 0) {
-    const uint32_t hi = field32(D, nD, (long long)n - 32);
-    const uint32_t lo = field32(D, nD, (long long)n - 64);
+    const uint32_t hi = field32(Dg, nD, (long long)n - 32);
+    const uint32_t lo = field32(Dg, nD, (long long)n - 64);
     const double d = ldexp((double)hi, 32) + (double)lo;  // [2^63, 2^64)
     const unsigned long long y63 =
         (unsigned long long)(ldexp(1.0, 126) / d);        // (2^62, 2^63]
-    const int sh = S - n - 62;                            // Y0 = y63 * 2^sh
-    for (int i = 0; i < nY; ++i) {
-      // limb i of y63 * 2^sh
-      const long long off = 32LL * i - sh;
-      uint32_t v = 0;
-      if (off > -64 && off < 64) {
-        const uint64_t hv = off >= 0 ? (y63 >> off) : (y63 << -off);
-        v = (uint32_t)hv;
-        if (off < 0 && off > -32) v = (uint32_t)(y63 << -off);
-      }
-      Y[i] = v;
-    }
+    const unsigned long long y0 = y63 >> (62 - p0);
+    Y[0] = (uint32_t)y0;
+    Y[1] = (uint32_t)(y0 >> 32);
   }
   __syncthreads();
-  int iters = 2;
-  while ((48 << (iters - 2)) < e + g + 2) ++iters;
-  ++iters;
-  const int nP = nD + nY;
-  for (int it = 0; it < iters; ++it) {
-    // Pr = D*Y
-    cta_mul(D, nD, Y, nY, Pr, nP, col, red);
-    // E = 2^S - D*Y (signed) over nP+1 limbs
+  int nY = 2;
+  for (int i = 0; i + 1 < nl; ++i) {
+    const int pa = lv[i], pb = lv[i + 1], dlt = pb - pa;
+    const int mb = min(n, pb + G);   // bits of D'
+    const int t = n - mb;
+    const int nDt = (mb + 31) / 32;
+    for (int k = threadIdx.x; k < nDt; k += blockDim.x)
+      Dt[k] = field32(Dg, nD, 32LL * k + t);
+    __syncthreads();
+    // Pr = D' * Y
+    const int nP = nDt + nY;
+    cta_mul(Dt, nDt, Y, nY, Pr, nP, col, red);
+    // E = 2^(mb+pa) - Pr, signed, over nP+1 limbs
     const int nEw = nP + 1;
-    const int Sl = S / 32;
-    const uint32_t Sb = 1u << (S % 32);
-    int sgn = 1, carry = 0;
+    const int Sb = mb + pa;
+    int sgn = 1;
     for (int pass = 0; pass < 2; ++pass) {
-      carry = cta_resolve(
+      const int c = cta_resolve(
           nEw, 32,
           [&](int k) -> int64_t {
-            const int64_t a = (k == Sl) ? (int64_t)Sb : 0;
+            const int64_t a = (k == Sb / 32) ? (int64_t)(1u << (Sb % 32)) : 0;
             const int64_t b = k < nP ? (int64_t)Pr[k] : 0;
             return sgn > 0 ? a - b : b - a;
           },
           [&](int k, uint32_t dd) { E[k] = dd; }, red);
-      if (carry >= 0) break;
+      if (c >= 0) break;
       sgn = -1;
     }
     const int nE = cta_limb_len(E, nEw, red);
-    if (nE == 0) break;
-    // Tm = Y * |E| >> S
+    // Tm = Y * |E|
     const int nT = nY + nE;
-    cta_mul(Y, nY, E, nE, Tm, nT, col, red);
-    // Y +-= Tm >> S
+    if (nE > 0) cta_mul(Y, nY, E, nE, Tm, nT, col, red);
+    // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
+    const int nYn = min(Lm, (pb + 2 + 31) / 32 + 1);
+    const int sh = Sb - dlt;
     cta_resolve(
-        nY, 32,
+        nYn, 32,
         [&](int k) -> int64_t {
-          const int64_t t = field32(Tm, nT, 32LL * k + S);
-          return sgn > 0 ? (int64_t)Y[k] + t : (int64_t)Y[k] - t;
+          const int64_t yv = field32(Y, nY, 32LL * k - dlt);
+          const int64_t tv = nE > 0 ? (int64_t)field32(Tm, nT, 32LL * k + sh) : 0;
+          return sgn > 0 ? yv + tv : yv - tv;
         },
         [&](int k, uint32_t dd) { Pr[k] = dd; }, red);
-    for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Pr[i];
+    for (int k = threadIdx.x; k < nYn; k += blockDim.x) Y[k] = Pr[k];
     __syncthreads();
+    nY = nYn;
   }
-  for (int i = threadIdx.x; i < P.ycap; i += blockDim.x)
-    Ybuf[i] = i < nY ? Y[i] : 0u;
+  for (int k = threadIdx.x; k < P.ycap; k += blockDim.x)
+    Ybuf[k] = k < nY ? Y[k] : 0u;
   if (threadIdx.x == 0) {
     ys[0] = S;
     ys[1] = nY;
@@ -460,10 +477,12 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
          const uint32_t* Vhat, const uint32_t* Rhat, long long row_stride_slot,
          int nslots, int c_begin, int c_end, int nct, int nrt, const int* err) {
   if (stage_aborted(err)) return;
-  const int wd = blockIdx.x * blockDim.x + threadIdx.x;
+  // grid.x walks the (r,c) tiles, grid.y the word blocks: all tiles of one
+  // word block run together, so the panel's operand slice for those words
+  // (2 x kb x n x 128 words) stays L2-resident while every tile reuses it.
+  const int wd = blockIdx.y * blockDim.x + threadIdx.x;
   if (wd >= P.NW) return;
-  // tile index -> (ct, rt) with rt >= ct
-  int t = blockIdx.y, ct = 0;
+  int t = blockIdx.x, ct = 0;
   while (t >= nrt - ct) {
     t -= nrt - ct;
     ++ct;
@@ -472,6 +491,15 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
   const int c0 = c_begin + ct * TILE;
   const int r0 = c_begin + rt * TILE;
   const PrimeConsts pc = P.pc[wd / P.L];
+  const long long NW = P.NW;
+
+  // out-of-range rows/columns are clamped to a valid one and never stored
+  const uint32_t* rp[TILE];
+  const uint32_t* vp[TILE];
+#pragma unroll
+  for (int i = 0; i < TILE; ++i) rp[i] = Rhat + (long long)min(r0 + i, P.n - 1) * NW + wd;
+#pragma unroll
+  for (int j = 0; j < TILE; ++j) vp[j] = Vhat + (long long)min(c0 + j, c_end - 1) * NW + wd;
 
   uint64_t acc[TILE][TILE];
 #pragma unroll
@@ -479,24 +507,27 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
 #pragma unroll
     for (int j = 0; j < TILE; ++j) acc[i][j] = 0;
 
-  for (int s = 0; s < nslots; ++s) {
-    const uint32_t* vs = Vhat + s * row_stride_slot;
-    const uint32_t* rs = Rhat + s * row_stride_slot;
-    uint32_t a[TILE], b[TILE];
+  uint32_t a[TILE], b[TILE];
 #pragma unroll
-    for (int i = 0; i < TILE; ++i) {
-      const int r = r0 + i;
-      a[i] = r < P.n ? __ldg(rs + (long long)r * P.NW + wd) : 0u;
-    }
+  for (int i = 0; i < TILE; ++i) a[i] = __ldg(rp[i]);
 #pragma unroll
-    for (int j = 0; j < TILE; ++j) {
-      const int c = c0 + j;
-      b[j] = c < c_end ? __ldg(vs + (long long)c * P.NW + wd) : 0u;
-    }
+  for (int j = 0; j < TILE; ++j) b[j] = __ldg(vp[j]);
+  for (int s = 1; s <= nslots; ++s) {
+    // prefetch the next stage while this one multiplies
+    uint32_t an[TILE], bn[TILE];
+    const long long off = (s < nslots ? s : s - 1) * row_stride_slot;
+#pragma unroll
+    for (int i = 0; i < TILE; ++i) an[i] = __ldg(rp[i] + off);
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) bn[j] = __ldg(vp[j] + off);
 #pragma unroll
     for (int i = 0; i < TILE; ++i)
 #pragma unroll
       for (int j = 0; j < TILE; ++j) acc[i][j] += (uint64_t)a[i] * b[j];
+#pragma unroll
+    for (int i = 0; i < TILE; ++i) a[i] = an[i];
+#pragma unroll
+    for (int j = 0; j < TILE; ++j) b[j] = bn[j];
   }
 #pragma unroll
   for (int j = 0; j < TILE; ++j) {
@@ -507,7 +538,7 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
     for (int i = 0; i < TILE; ++i) {
       const int r = r0 + i;
       if (r < c || r >= P.n) continue;
-      uint32_t* ptr = W + (base + (r - c)) * (long long)P.NW + wd;
+      uint32_t* ptr = W + (base + (r - c)) * NW + wd;
       const uint32_t t32 = reduce_sum64(acc[i][j], pc);
       const uint32_t old = *ptr;
       *ptr = old >= t32 ? old - t32 : old + pc.q - t32;
@@ -515,6 +546,52 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
   }
 }
 
+// -------------------------------------------------------- column update ---
+// In-panel, left-looking: right before column c is extracted it receives
+// every earlier stage of its panel at once,
+//   W[r][c] -= sum_{s < ns} Vhat[s][c] * Rhat[s][r],   r in [c, n),
+// so each entry of the panel is read-modify-written once per column instead
+// of once per stage.  Thread: one word x TR rows.
+template <int TR>
+__global__ void __launch_bounds__(128)
+k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
+             const uint32_t* Vhat, const uint32_t* Rhat,
+             long long row_stride_slot, int nslots, int c, const int* err) {
+  if (stage_aborted(err)) return;
+  const int wd = blockIdx.y * blockDim.x + threadIdx.x;
+  if (wd >= P.NW) return;
+  const int r0 = c + blockIdx.x * TR;
+  const PrimeConsts pc = P.pc[wd / P.L];
+  const long long NW = P.NW;
+  const uint32_t* rp[TR];
+#pragma unroll
+  for (int i = 0; i < TR; ++i) rp[i] = Rhat + (long long)min(r0 + i, P.n - 1) * NW + wd;
+  const uint32_t* vp = Vhat + (long long)c * NW + wd;
+  uint64_t acc[TR];
+#pragma unroll
+  for (int i = 0; i < TR; ++i) acc[i] = 0;
+  for (int s = 0; s < nslots; ++s) {
+    const long long off = s * row_stride_slot;
+    const uint32_t b = __ldg(vp + off);
+    uint32_t a[TR];
+#pragma unroll
+    for (int i = 0; i < TR; ++i) a[i] = __ldg(rp[i] + off);
+#pragma unroll
+    for (int i = 0; i < TR; ++i) acc[i] += (uint64_t)a[i] * b;
+  }
+  const long long base = colbase[c];
+  uint32_t old[TR];
+#pragma unroll
+  for (int i = 0; i < TR; ++i)
+    old[i] = r0 + i < P.n ? W[(base + (r0 + i - c)) * NW + wd] : 0u;
+#pragma unroll
+  for (int i = 0; i < TR; ++i) {
+    if (r0 + i >= P.n) continue;
+    const uint32_t t32 = reduce_sum64(acc[i], pc);
+    W[(base + (r0 + i - c)) * NW + wd] =
+        old[i] >= t32 ? old[i] - t32 : old[i] + pc.q - t32;
+  }
+}
 
 // -------------------------------------------------------------- validate ---
 // Checks the transform capacity after the factorisation: for every stage
@@ -539,12 +616,16 @@ __global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
 
 // ------------------------------------------------------ launch wrappers --
 
+static thread_local long long g_launches = 0;
+long long kernel_launch_count() { return g_launches; }
+
 cudaError_t launch_fwd_ints(const DevPlan& P, IntBuf src, long long in_base,
                             uint32_t* out, long long out_base, int count,
                             int mont, int* maxdeg, int* err,
                             cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   const size_t smem = (size_t)(P.np * P.L + P.cap) * 4;
+  ++g_launches;
   k_fwd_ints<<<count, 256, smem, st>>>(P, src, in_base, out, out_base, count,
                                        mont, maxdeg, err);
   return cudaGetLastError();
@@ -554,6 +635,7 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
                           const uint32_t* xhat, const long long* colbase,
                           uint32_t* W, cudaStream_t st) {
   dim3 grid((P.NW + 255) / 256, P.n);
+  ++g_launches;
   k_init_w<<<grid, 256, 0, st>>>(P, that, xhat, colbase, W);
   return cudaGetLastError();
 }
@@ -569,22 +651,27 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            int* err, cudaStream_t st) {
   const int rows = P.n - p;
   if (rows <= 0) return cudaSuccess;
+  ++g_launches;
   k_extract<<<rows, 256, extract_smem_bytes(P), st>>>(
       P, W, colbase, p, vint, vrow0, piv, maxbitsV, err);
   return cudaGetLastError();
 }
 
 size_t recip_scratch_words(const DevPlan& P) {
-  const int cap = P.cap, ycap = P.ycap;
-  return (size_t)cap + ycap + 2 * (cap + ycap + 2) + (cap + 2 * ycap + 4) +
-         3 * (cap + 2 * ycap + 4) + 64;
+  // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
+  const size_t Lm = (size_t)P.ycap + 4;
+  return Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
+         3 * (3 * Lm + 2) + 64;
 }
 
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                         uint32_t* scratch, int* err, cudaStream_t st) {
-  k_recip<<<1, 512, 0, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
-                             err);
+                         uint32_t* scratch, int use_gscratch, int* err,
+                         cudaStream_t st) {
+  ++g_launches;
+  const size_t smem = use_gscratch ? 0 : recip_scratch_words(P) * 4;
+  k_recip<<<1, 512, smem, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
+                                use_gscratch, err);
   return cudaGetLastError();
 }
 
@@ -597,6 +684,7 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   const int rows = P.n - p - 1;
   if (rows <= 0) return cudaSuccess;
   const size_t smem = use_gscratch ? 0 : divide_smem_words(P) * 4;
+  ++g_launches;
   k_divide<<<rows, 256, smem, st>>>(P, vint, vrow0, p, Ybuf, ys, rint, rrow0,
                                     gscratch, use_gscratch, err);
   return cudaGetLastError();
@@ -612,7 +700,8 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
   const int nrt = (P.n - c_begin + tile - 1) / tile;
   long long tiles = 0;
   for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
-  dim3 grid((P.NW + 127) / 128, (unsigned)tiles);
+  dim3 grid((unsigned)tiles, (P.NW + 127) / 128);
+  ++g_launches;
   if (tile == 8)
     k_update<8><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
                                       row_stride_slot, nslots, c_begin, c_end,
@@ -624,15 +713,30 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
   return cudaGetLastError();
 }
 
+cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
+                              const long long* colbase, const uint32_t* Vhat,
+                              const uint32_t* Rhat, long long row_stride_slot,
+                              int nslots, int c, const int* err,
+                              cudaStream_t st) {
+  if (nslots <= 0 || c >= P.n) return cudaSuccess;
+  constexpr int TR = 16;
+  dim3 grid((P.n - c + TR - 1) / TR, (P.NW + 127) / 128);
+  ++g_launches;
+  k_update_col<TR><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
+                                         row_stride_slot, nslots, c, err);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st) {
+  ++g_launches;
   k_validate<<<1, 32, 0, st>>>(P, maxdegV, maxdegR, nstages, err);
   return cudaGetLastError();
 }
 
 cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
-                              bool* div_global) {
+                              bool* div_global, bool* recip_global) {
   int dev;
   cudaGetDevice(&dev);
   int maxopt = 0;
@@ -649,6 +753,14 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fwd)) != cudaSuccess)
     return e;
+  const size_t rec = recip_scratch_words(P) * 4;
+  *recip_global = (int)rec > maxopt;
+  if (!*recip_global) {
+    if ((e = cudaFuncSetAttribute(k_recip,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)rec)) != cudaSuccess)
+      return e;
+  }
   const size_t div = divide_smem_words(P) * 4;
   *div_smem = div;
   *div_global = (int)div > maxopt;

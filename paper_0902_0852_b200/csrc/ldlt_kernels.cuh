@@ -88,7 +88,8 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
 size_t recip_scratch_words(const DevPlan& P);
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                         uint32_t* scratch, int* err, cudaStream_t st);
+                         uint32_t* scratch, int use_gscratch, int* err,
+                         cudaStream_t st);
 size_t divide_smem_words(const DevPlan& P);
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, const uint32_t* Ybuf, const int* ys,
@@ -99,10 +100,16 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const uint32_t* Rhat, long long row_stride_slot,
                           int nslots, int c_begin, int c_end, const int* err,
                           cudaStream_t st);
+cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
+                              const long long* colbase, const uint32_t* Vhat,
+                              const uint32_t* Rhat, long long row_stride_slot,
+                              int nslots, int c, const int* err,
+                              cudaStream_t st);
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
+long long kernel_launch_count();  // kernels launched by this thread
 cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
-                              bool* div_global);
+                              bool* div_global, bool* recip_global);
 
 }  // namespace hgpu

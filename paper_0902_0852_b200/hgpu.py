@@ -39,7 +39,7 @@ EXPORTS = (
     "hgpu_matrix_set_comm", "hgpu_ldlt_factor", "hgpu_factor_order",
     "hgpu_factor_frac_bits", "hgpu_factor_pivot", "hgpu_factor_ratio",
     "hgpu_factor_det", "hgpu_factor_device_ms", "hgpu_factor_update_stats",
-    "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
+    "hgpu_factor_launches", "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
     "hgpu_last_zero_pivot", "hgpu_last_error", "hgpu_version",
 )
 
@@ -94,6 +94,8 @@ def load() -> ctypes.CDLL:
     lib.hgpu_factor_device_ms.restype = ctypes.c_double
     lib.hgpu_factor_update_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_factor_launches.argtypes = [vp]
+    lib.hgpu_factor_launches.restype = ctypes.c_longlong
     lib.hgpu_factor_free.argtypes = [vp]
     lib.hgpu_matrix_plan.argtypes = [vp] + [ctypes.POINTER(ctypes.c_int)] * 4 + [ctypes.POINTER(ctypes.c_double)]
     lib.hgpu_block_owner.argtypes = [i64, ctypes.c_int]
@@ -166,6 +168,7 @@ class LdltResult:
     update_launches: int = 0
     update_ms: float = 0.0
     update_products: float = 0.0
+    launches: int = 0
 
 
 class HankelMatrixGPU:
@@ -229,7 +232,8 @@ class HankelMatrixGPU:
                 _check(lib.hgpu_factor_pivot(f, p, ctypes.byref(size), ctypes.byref(ptr)))
                 pivots.append(limbs_to_int(size.value, ptr))
             res = LdltResult(n=n, frac_bits=self.frac_bits, pivots=pivots,
-                             device_ms=lib.hgpu_factor_device_ms(f))
+                             device_ms=lib.hgpu_factor_device_ms(f),
+                             launches=int(lib.hgpu_factor_launches(f)))
             if capture:
                 for p in range(n - 1):
                     for r in range(p + 1, n):
