@@ -36,7 +36,10 @@ typedef enum hgpu_status {
   HGPU_ERR_CUDA = 4,               /* device unavailable or a CUDA failure */
   HGPU_ERR_CAPACITY = 5,           /* a value outgrew every plan that fits */
   HGPU_ERR_INTERNAL = 6,           /* an exactness self-check failed */
-  HGPU_ERR_COMM = 7                /* heig::ChannelFailure (errors.hpp:107-111) */
+  HGPU_ERR_COMM = 7,               /* heig::ChannelFailure (errors.hpp:107-111) */
+  HGPU_ERR_PRECISION_EXHAUSTED = 8 /* NoProgress / SignViolation /
+                                      RootHitAtPrecision (errors.hpp:60-80):
+                                      raise frac_bits and retry */
 } hgpu_status;
 
 /* factor flags */
@@ -90,6 +93,20 @@ hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
 /* Number of device kernels the factorisation launched. */
 long long hgpu_factor_launches(const hgpu_factor* f);
 void hgpu_factor_free(hgpu_factor* f);
+
+/* Smallest eigenvalue of the resident matrix at its frac_bits: the
+ * reference's secant on P(x) = det(M - xI) (secant.cpp:27-117) with every
+ * probe a GPU factorisation + fold, stopping when the top `digits`
+ * significant decimals of successive iterates agree (the reference: 15).
+ * Outputs (malloc'd, free with hgpu_string_free; each may be NULL):
+ *   eigenvalue  `digits`-digit truncation, scientific notation
+ *   trace       one line per recorded iterate: "<x hex> <det hex>"
+ * On HGPU_ERR_PRECISION_EXHAUSTED the caller escalates frac_bits, as
+ * driver.cpp:100-130 does. */
+hgpu_status hgpu_smallest_eigenvalue(hgpu_matrix* m, int digits,
+                                     char** eigenvalue, char** trace,
+                                     long* iterations, double* det_seconds);
+void hgpu_string_free(char* s);
 
 /* Plan introspection: primes, transform length, digit width, limb capacity,
  * workspace bytes on this rank. */

@@ -54,6 +54,14 @@ hgpu::HostInt make_int(int32_t size, const uint32_t* limbs) {
 
 }  // namespace
 
+namespace hgpu {
+Matrix* matrix_impl(hgpu_matrix* m) { return m ? m->impl.get() : nullptr; }
+void set_last_error(const std::string& s, long pivot) {
+  g_last_error = s;
+  if (pivot >= 0) g_last_pivot = pivot;
+}
+}  // namespace hgpu
+
 extern "C" {
 
 const char* hgpu_version(void) { return "hgpu 0.1 (sm_100a)"; }

@@ -542,6 +542,54 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     res.pivots[p].limbs.assign(pl.begin() + (size_t)p * P.cap,
                                pl.begin() + (size_t)p * P.cap + len);
   }
+  if (flags & HGPU_FOLD) fold(res);
+}
+
+void Matrix::fold(FactorResult& res) {
+  const Plan& P = plan_;
+  const int n = n_;
+  std::vector<int> plen(n);
+  int neg = 0;
+  long long nx = K_ / 32 + 1, xcap = nx;
+  for (int p = 0; p < n; ++p) {
+    plen[p] = std::abs(res.pivots[p].size);
+    neg ^= res.pivots[p].size < 0;
+    nx = nx + plen[p] - K_ / 32;
+    xcap = std::max(xcap, nx);
+  }
+  xcap += 2;
+  uint32_t* X0 = dalloc<uint32_t>(xcap);
+  uint32_t* X1 = dalloc<uint32_t>(xcap);
+  uint32_t* col = dalloc<uint32_t>(3 * (size_t)(xcap + P.cap));
+  const size_t nch = (size_t)(xcap + P.cap) / 2048 + 4;
+  uint32_t* cf = dalloc<uint32_t>(nch);
+  int* cc = dalloc<int>(nch);
+  long long launches = 0;
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  CU(cudaEventRecord(a, stream_));
+  const long long nfin = fold_pivots_device(plimbs_, plen.data(), n, P.cap, K_,
+                                            X0, X1, xcap, col, cf, cc,
+                                            stream_, &launches);
+  CU(cudaEventRecord(b, stream_));
+  std::vector<uint32_t> hx(std::max<long long>(nfin, 0));
+  if (nfin > 0)
+    CU(cudaMemcpyAsync(hx.data(), X0, nfin * 4, cudaMemcpyDeviceToHost, stream_));
+  CU(cudaStreamSynchronize(stream_));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  for (void* p : {(void*)X0, (void*)X1, (void*)col, (void*)cf, (void*)cc}) dfree(p);
+  CU(cudaGetLastError());
+  if (nfin < 0) throw Error(HGPU_ERR_INTERNAL, "fold buffer too small");
+  while (!hx.empty() && hx.back() == 0) hx.pop_back();
+  res.det.limbs = std::move(hx);
+  res.det.size = res.det.limbs.empty() ? 0 : (neg ? -1 : 1) * (int)res.det.limbs.size();
+  res.have_det = true;
+  res.fold_ms = ms;
+  res.launches += launches;
 }
 
 FactorResult Matrix::factor(const HostInt& x, unsigned flags) {

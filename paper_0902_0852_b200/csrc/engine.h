@@ -50,6 +50,7 @@ struct FactorResult {
   long update_launches = 0;
   double update_ms = 0, update_products = 0;
   long long launches = 0;  // our kernels launched by the factorisation
+  double fold_ms = 0;
 };
 
 class Matrix {
@@ -73,12 +74,15 @@ class Matrix {
     return plan_;
   }
   int frac_bits() const { return K_; }
+  int order() const { return n_; }
+  const HostInt& strip_entry(int s) const { return strip_[s]; }
 
  private:
   void build(int min_logL);
   void release();
   void run(const HostInt& x, unsigned flags, FactorResult& res);
   void panel_broadcast(int owner, int p0, int ns, cudaStream_t st);
+  void fold(FactorResult& res);
 
   int n_, K_, device_;
   std::vector<HostInt> strip_;

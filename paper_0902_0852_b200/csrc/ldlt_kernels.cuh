@@ -108,7 +108,13 @@ cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
-long long kernel_launch_count();  // kernels launched by this thread
+long long kernel_launch_count();
+// fold_kernels.cu
+long long fold_pivots_device(const uint32_t* plimbs, const int* plen, int n,
+                             int pcap, int K, uint32_t* X0, uint32_t* X1,
+                             long long xcap, uint32_t* col, uint32_t* chunk_fn,
+                             int* chunk_carry, cudaStream_t st,
+                             long long* launches);  // kernels launched by this thread
 cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                               bool* div_global, bool* recip_global);
 

@@ -31,6 +31,7 @@ HGPU_PROFILE = 4
 STATUS = {
     0: "ok", 1: "invalid argument", 2: "zero pivot", 3: "precision mismatch",
     4: "cuda", 5: "capacity", 6: "internal", 7: "communication",
+    8: "precision exhausted",
 }
 
 # every symbol include/hgpu.h declares
@@ -41,6 +42,7 @@ EXPORTS = (
     "hgpu_factor_det", "hgpu_factor_device_ms", "hgpu_factor_update_stats",
     "hgpu_factor_launches", "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
     "hgpu_last_zero_pivot", "hgpu_last_error", "hgpu_version",
+    "hgpu_smallest_eigenvalue", "hgpu_string_free",
 )
 
 
@@ -61,6 +63,11 @@ class ZeroPivot(HgpuError):
 
 class PrecisionMismatch(HgpuError):
     pass
+
+
+class PrecisionExhausted(HgpuError):
+    """NoProgress / SignViolation / RootHitAtPrecision (errors.hpp:60-80):
+    the working precision is exhausted; the driver escalates frac_bits."""
 
 
 _lib = None
@@ -103,6 +110,11 @@ def load() -> ctypes.CDLL:
     lib.hgpu_last_zero_pivot.restype = i64
     lib.hgpu_last_error.restype = ctypes.c_char_p
     lib.hgpu_version.restype = ctypes.c_char_p
+    cpp = ctypes.POINTER(ctypes.c_char_p)
+    lib.hgpu_smallest_eigenvalue.argtypes = [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                             ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64),
+                                             ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_string_free.argtypes = [ctypes.c_void_p]
     _lib = lib
     return lib
 
@@ -116,6 +128,8 @@ def _check(status: int, frac_bits: int = 0) -> None:
         raise ZeroPivot(int(lib.hgpu_last_zero_pivot()), frac_bits, msg)
     if status == 3:
         raise PrecisionMismatch(status, msg)
+    if status == 8:
+        raise PrecisionExhausted(status, msg)
     raise HgpuError(status, msg)
 
 
@@ -249,6 +263,31 @@ class HankelMatrixGPU:
             return res
         finally:
             lib.hgpu_factor_free(f)
+
+
+def _take_string(ptr: ctypes.c_void_p) -> str:
+    if not ptr.value:
+        return ""
+    try:
+        return ctypes.string_at(ptr.value).decode()
+    finally:
+        load().hgpu_string_free(ptr)
+
+
+def smallest_eigenvalue(m: "HankelMatrixGPU", digits: int = 15) -> dict:
+    """secant_smallest_eigenvalue (secant.cpp:27-117) on the GPU determinant:
+    returns {"eigenvalue": str, "iterates": [(x, det)], "iterations": int,
+    "det_seconds": float}."""
+    lib = load()
+    ev, tr = ctypes.c_void_p(), ctypes.c_void_p()
+    it, secs = ctypes.c_long(), ctypes.c_double()
+    _check(lib.hgpu_smallest_eigenvalue(m._h, digits, ctypes.byref(ev), ctypes.byref(tr),
+                                        ctypes.byref(it), ctypes.byref(secs)), m.frac_bits)
+    eig = _take_string(ev)
+    lines = _take_string(tr).split("\n")
+    iterates = [tuple(int(v, 16) for v in l.split()) for l in lines if l.strip()]
+    return {"eigenvalue": eig, "iterates": iterates, "iterations": it.value,
+            "det_seconds": secs.value}
 
 
 def block_owner(block: int, world: int) -> int:
