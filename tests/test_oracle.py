@@ -1,0 +1,132 @@
+"""CPU: the oracle is pinned before it is trusted.
+
+The compiled reference (oracle/_ref) reproduces the reference's own
+known-answer tests; the C and Python restatements agree with it bit for bit;
+and all of them agree with the committed golden fixtures that the reference
+generated (tests/golden/make_golden.py)."""
+import hashlib
+import json
+import math
+import os
+
+import pytest
+
+from helpers import random_pd_hankel, strip_from_ints
+import pyoracle as po
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return po.RefLib()
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return po.OracleLib()
+
+
+def test_reference_two_by_two(ref):
+    # tests/test_ldlt.cpp:96-109
+    assert ref.ldlt_serial(strip_from_ints([2, 0, 3], 32), 0, 32).det == 6 << 32
+    r = ref.ldlt_serial(strip_from_ints([2, 1, 2], 32), 0, 32)
+    assert r.det == 3 << 32 and r.pivots == [2 << 32, 3 << 31] and r.ratios == {(0, 1): 1 << 15}
+
+
+def test_reference_factorial_det_144(ref):
+    # tests/test_ldlt.cpp:111-117
+    assert ref.ldlt_serial(ref.build_strip(4, 1, 1, 512), 0, 512).det == 144 << 512
+
+
+def test_reference_zero_pivot_index(ref):
+    # tests/test_ldlt.cpp:185-194
+    with pytest.raises(po.ZeroPivotError) as e:
+        ref.ldlt_serial(strip_from_ints([1, 1, 1], 64), 0, 64)
+    assert e.value.pivot_index == 1 and e.value.frac_bits == 64
+
+
+def test_reference_lambda_pins(ref):
+    assert ref.heig_run(4, "1/1")["eigenvalue"] == "5.29002939538683e-2"   # test_verify.cpp:78
+    assert ref.heig_run(6, "1/1")["eigenvalue"].startswith("1.0451")      # test_capi.cpp:53
+    r = ref.heig_run(100, "1/1")                                            # README.md:110-116
+    assert (r["eigenvalue"], r["k_bits"], r["iterations"]) == ("2.10788597588794e-15", 832, 8)
+
+
+def test_exact_strip_equals_reference_build_matrix(ref):
+    for n, b, k in [(10, (1, 1), 512), (12, (1, 2), 640), (64, (1, 1), 1024)]:
+        assert ref.build_strip(n, *b, k) == po.exact_strip(n, *b, k)
+
+
+def test_closed_form_beta1_config1(ref):
+    # SURVEY §7 known answer, BASELINE config 1 size
+    want = ref.ldlt_serial(ref.build_strip(64, 1, 1, 1024), 0, 1024)
+    cf = po.closed_form_beta1(64, 1024)
+    assert want.pivots == cf.pivots and want.ratios == cf.ratios and want.det == cf.det
+
+
+@pytest.mark.parametrize("seed,n,f", [(53, 6, 128), (59, 9, 160), (61, 14, 128), (67, 30, 256)])
+def test_restatements_match_reference(ref, orc, seed, n, f):
+    strip = random_pd_hankel(seed, n, f)
+    for x in (0, -(7 << (f - 4)), 1 << (f // 2)):
+        want = ref.ldlt_serial(strip, x, f, capture=True)
+        got_c = orc.ldlt(strip, x, f, capture=True)
+        assert (got_c.det, got_c.pivots, got_c.ratios) == (want.det, want.pivots, want.ratios)
+        if n <= 14:
+            got_py = po.ldlt_py(strip, x, f)
+            assert (got_py.det, got_py.pivots, got_py.ratios) == (want.det, want.pivots, want.ratios)
+
+
+def test_reference_parallel_bit_identical_across_workers(ref):
+    # tests/test_parallel.cpp:42-55
+    for n in (9, 24):
+        strip = random_pd_hankel(73 + n, n, 128)
+        x = 1 << 100
+        serial = ref.ldlt_serial(strip, x, 128, capture=False).det
+        for workers in (1, 2, 3, 4, 5, 8):
+            assert ref.ldlt_parallel(strip, x, 128, workers)[0] == serial
+
+
+def test_column_owners_reflected_round_robin(ref):
+    # tests/test_ldlt.cpp:73-92
+    assert ref.column_owners(8, 4) == [0, 1, 2, 3, 3, 2, 1, 0]
+    assert ref.column_owners(13, 3) == [0, 1, 2, 2, 1, 0, 0, 1, 2, 2, 1, 0, 0]
+    for n in (7, 40, 101):
+        for s in (1, 2, 3, 5, 8):
+            assert ref.column_owners(n, s) == po.column_owners(n, s)
+
+
+def test_golden_ldlt_fixtures(orc):
+    cases = json.load(open(os.path.join(GOLDEN, "ldlt_small.json")))
+    assert len(cases) >= 6
+    for c in cases:
+        strip = [int(v, 16) for v in c["strip"]]
+        k, x = c["frac_bits"], int(c["x"], 16)
+        r = orc.ldlt(strip, x, k, capture=True)
+        assert po.to_hex(r.det) == c["det"], c["name"]
+        assert [po.to_hex(v) for v in r.pivots] == c["pivots"], c["name"]
+        assert [[p, q, po.to_hex(v)] for (p, q), v in sorted(r.ratios.items())] == c["ratios"]
+
+
+def test_golden_config2_digest(orc):
+    g = json.load(open(os.path.join(GOLDEN, "config2_strip.json")))
+    strip = [int(v, 16) for v in g["strip"]]
+    r = orc.ldlt(strip, 0, g["frac_bits"], capture=True)
+    h = hashlib.sha256()
+    for v in r.pivots:
+        h.update(po.to_hex(v).encode() + b"\n")
+    assert h.hexdigest() == g["pivots_sha256"]
+
+
+def test_golden_lambda_fixture_pins():
+    lam = {(d["n"], d["beta"]): d for d in json.load(open(os.path.join(GOLDEN, "lambda_secant.json")))}
+    assert lam[(4, "1/1")]["eigenvalue"] == "5.29002939538683e-2"
+    assert lam[(100, "1/1")]["eigenvalue"] == "2.10788597588794e-15"
+    # mpmath value for config 1: 5.5000214686372010414e-12
+    assert lam[(64, "1/1")]["eigenvalue"] == "5.50002146863720e-12"
+
+
+def test_fold_restatement(orc):
+    piv = po.closed_form_beta1(30, 512).pivots
+    assert orc.fold(piv, 512) == po.fold_pivots(piv, 512)
+    assert po.fold_pivots(piv, 512) == math.prod(math.factorial(k) ** 2 for k in range(30)) << 512
