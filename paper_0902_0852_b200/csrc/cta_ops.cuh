@@ -18,52 +18,68 @@ namespace hgpu {
 
 // ---------------------------------------------------------------- NTT ------
 
-// Forward transform, natural order in (values < 4q), bit-reversed order out
-// (values < q).  tw/twp: twiddle table T[m+i] = w^{(Lmax/2m) bitrev_m(i)}
-// and its Shoup companions (shared by all lengths L <= Lmax).
-__device__ inline void cta_ntt_fwd(uint32_t* x, int logL, const uint32_t* tw,
-                                   const uint32_t* twp, uint32_t q) {
-  const int L = 1 << logL;
-  const uint32_t q2 = 2 * q;
+// Forward transforms of np residue planes x[j*L ...] (natural order in,
+// values < 4q; bit-reversed order out, values < q), all primes in the same
+// level loop so each radix-2 level costs one barrier.  tw/twp: per-prime
+// tables T[m+i] = w^{(Lmax/2m) bitrev_m(i)} with Shoup companions, stride
+// `ts` (shared by every L <= Lmax, which is what makes length-L/2^k
+// transforms prefixes of length-L ones).
+__device__ inline void cta_ntt_fwd_multi(uint32_t* x, int np, int logL,
+                                         const uint32_t* tw,
+                                         const uint32_t* twp, int ts,
+                                         const PrimeConsts* pc) {
+  const int L = 1 << logL, half = L >> 1;
+  const int total = np * half;
   for (int lm = 0; lm < logL; ++lm) {
     const int m = 1 << lm;
     const int lt = logL - 1 - lm;  // t = L / (2m)
-    for (int b = threadIdx.x; b < L / 2; b += blockDim.x) {
+    for (int gb = threadIdx.x; gb < total; gb += blockDim.x) {
+      const int j = gb >> (logL - 1);
+      const int b = gb & (half - 1);
+      const uint32_t q = pc[j].q, q2 = 2 * q;
+      uint32_t* xj = x + j * L;
       const int i = b >> lt;
       const int j1 = (i << (lt + 1)) + (b & ((1 << lt) - 1));
       const int j2 = j1 + (1 << lt);
-      uint32_t X = x[j1];
+      uint32_t X = xj[j1];
       X = X >= q2 ? X - q2 : X;
-      const uint32_t T = mul_shoup(x[j2], tw[m + i], twp[m + i], q);
-      x[j1] = X + T;
-      x[j2] = X - T + q2;
+      const uint32_t T = mul_shoup(xj[j2], tw[j * ts + m + i], twp[j * ts + m + i], q);
+      xj[j1] = X + T;
+      xj[j2] = X - T + q2;
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    uint32_t X = x[i];
+  for (int gi = threadIdx.x; gi < np * L; gi += blockDim.x) {
+    const uint32_t q = pc[gi >> logL].q, q2 = 2 * q;
+    uint32_t X = x[gi];
     X = X >= q2 ? X - q2 : X;
-    x[i] = X >= q ? X - q : X;
+    x[gi] = X >= q ? X - q : X;
   }
   __syncthreads();
 }
 
-// Inverse transform without the 1/L scale: bit-reversed in (values < 2q),
-// natural order out (values < 2q).  itw/itwp: inverses of the forward table.
-__device__ inline void cta_ntt_inv(uint32_t* x, int logL, const uint32_t* itw,
-                                   const uint32_t* itwp, uint32_t q) {
-  const int L = 1 << logL;
-  const uint32_t q2 = 2 * q;
+// Inverse transforms without the 1/L scale: bit-reversed in (values < 2q),
+// natural order out (values < 2q).
+__device__ inline void cta_ntt_inv_multi(uint32_t* x, int np, int logL,
+                                         const uint32_t* itw,
+                                         const uint32_t* itwp, int ts,
+                                         const PrimeConsts* pc) {
+  const int L = 1 << logL, half = L >> 1;
+  const int total = np * half;
   for (int lt = 0; lt < logL; ++lt) {
     const int m = L >> (lt + 1);
-    for (int b = threadIdx.x; b < L / 2; b += blockDim.x) {
+    for (int gb = threadIdx.x; gb < total; gb += blockDim.x) {
+      const int j = gb >> (logL - 1);
+      const int b = gb & (half - 1);
+      const uint32_t q = pc[j].q, q2 = 2 * q;
+      uint32_t* xj = x + j * L;
       const int i = b >> lt;
       const int j1 = (i << (lt + 1)) + (b & ((1 << lt) - 1));
       const int j2 = j1 + (1 << lt);
-      const uint32_t U = x[j1], V = x[j2];
-      uint32_t S = U + V;
-      x[j1] = S >= q2 ? S - q2 : S;
-      x[j2] = mul_shoup(U - V + q2, itw[m + i], itwp[m + i], q);
+      const uint32_t U = xj[j1], V = xj[j2];
+      const uint32_t S = U + V;
+      xj[j1] = S >= q2 ? S - q2 : S;
+      xj[j2] = mul_shoup(U - V + q2, itw[j * ts + m + i], itwp[j * ts + m + i], q);
     }
     __syncthreads();
   }

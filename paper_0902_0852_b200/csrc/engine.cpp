@@ -489,12 +489,26 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     }
     // trailing update of owned columns >= p1
     if (p1 < n) {
+      // one launch per maximal run of contiguous owned blocks (a single
+      // rank owns one run; with several ranks the runs interleave)
+      int run_begin = -1, run_end = -1;
+      auto flush = [&]() {
+        if (run_begin >= 0 && run_begin < run_end)
+          timed_update(std::min(ns, n - 1 - p0), run_begin, run_end);
+        run_begin = run_end = -1;
+      };
       for (int ob : owned_blocks_) {
         const int c0 = std::max(p1, ob * kb), c1 = std::min(n, (ob + 1) * kb);
-        if (c0 < c1) timed_update(std::min(ns, n - 1 - p0), c0, c1);
+        if (c0 >= c1) continue;
+        if (run_begin >= 0 && c0 == run_end) {
+          run_end = c1;
+        } else {
+          flush();
+          run_begin = c0;
+          run_end = c1;
+        }
       }
-      // single rank: owned blocks are contiguous -> one launch would do; the
-      // per-block loop above keeps the multi-rank path identical.
+      flush();
     }
   }
   CU(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));

@@ -29,7 +29,7 @@ struct HostInt {
 struct Plan {
   int n = 0, K = 0, np = 0, L = 0, logL = 0, w = 0, T = 0, cap = 0, ycap = 0;
   int kb = 32;         // panel width (columns per block)
-  int tile = 8;        // update register tile
+  int tile = 16;       // update CTA tile (16: SMEM-staged kernel)
   long long entries = 0;  // workspace entries on this rank
   double workspace_bytes() const { return double(entries) * np * L * 4.0; }
 };

@@ -48,9 +48,7 @@ __device__ void transform_int(const DevPlan& P, const uint32_t* mag, int len,
     }
   }
   __syncthreads();
-  for (int j = 0; j < P.np; ++j)
-    cta_ntt_fwd(sm + j * P.L, P.logL, P.tw + j * P.Lmax, P.twp + j * P.Lmax,
-                P.pc[j].q);
+  cta_ntt_fwd_multi(sm, P.np, P.logL, P.tw, P.twp, P.Lmax, P.pc);
   for (int j = 0; j < P.np; ++j) {
     const PrimeConsts& c = P.pc[j];
     for (int i = threadIdx.x; i < P.L; i += blockDim.x) {
@@ -129,9 +127,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
   const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
   for (int i = threadIdx.x; i < P.NW; i += blockDim.x) A[i] = src[i];
   __syncthreads();
-  for (int j = 0; j < np; ++j)
-    cta_ntt_inv(A + j * L, P.logL, P.itw + j * P.Lmax, P.itwp + j * P.Lmax,
-                P.pc[j].q);
+  cta_ntt_inv_multi(A, np, P.logL, P.itw, P.itwp, P.Lmax, P.pc);
 
   // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
@@ -363,9 +359,13 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
 
 // ---------------------------------------------------------------- ratios ---
 // Stage p, rows r in (p, n):  R_p[r] = tdiv_q(V_p[r] << K/2, V_p[p])
-// (ldlt.cpp:15-20, 57-58).  Barrett: q~ = (|V_r| Y) >> (S - K/2) is within
-// one of the true quotient; the remainder window |V_r|2^{K/2} - q~|V_p|
-// (nD+2 limbs) decides the correction exactly.
+// (ldlt.cpp:15-20, 57-58).  With A = |V_r| 2^{K/2}, D = |V_p|, n = bits(D):
+//   F = (|V_r| >> t) * Y / 2^{S-K/2-t},   t = max(0, n - K/2 - 40),
+// differs from A/D by < 2^-31.9 (|Y - 2^S/D| <= 3 from k_recip; the dropped
+// low bits of V cost < 2^-39).  So when the 32 fraction bits of F lie in
+// [2, 2^32-3], q = floor(F) exactly and no remainder is needed.  Otherwise
+// (e.g. exact quotients) floor(F) is within one of q and the remainder
+// window A - q~ D over nD+2 limbs decides the correction exactly.
 __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* gscratch, int use_gscratch,
@@ -377,92 +377,100 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   const int cap = P.cap, ycap = P.ycap;
   const long long span = div_span_words(cap, ycap);
   uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * span : sm_dyn;
-  uint32_t* V = sm;
-  uint32_t* D = V + cap;
-  uint32_t* Y = D + cap;
-  uint32_t* Pr = Y + ycap;                 // cap + ycap
-  uint32_t* red = Pr + cap + ycap + 2;     // 64
-  uint32_t* col = red + 64;                // 3 * (cap + ycap + 2)
-  uint32_t* Qt = col + 3 * (cap + ycap + 2);  // cap + ycap
-  uint32_t* Wa = Qt + cap + ycap + 2;      // cap + 2
-  uint32_t* Wb = Wa + cap + 2;             // cap + 2
+  const int CY = cap + ycap + 2;
+  uint32_t* Vt = sm;                 // cap      } later: Qt (cap + ycap)
+  uint32_t* Y = Vt + cap;            // ycap     }
+  uint32_t* Pr = Y + ycap + 2;       // CY       later: windows Wa | Wb
+  uint32_t* col = Pr + CY;           // 3 CY
+  uint32_t* red = col + 3 * CY;      // 64
+  uint32_t* Qt = Vt;
 
-  int na, nD;
-  const int sV = load_int(vint, vrow0 + r, cap, V, &na);
-  const int sD = load_int(vint, vrow0 + p, cap, D, &nD);
+  const long long vidx = vrow0 + r, pidx = vrow0 + p;
+  const int hv = vint.hdr[vidx], hd = vint.hdr[pidx];
+  const int na = hv < 0 ? -hv : hv, nD = hd < 0 ? -hd : hd;
+  const int sV = hv < 0 ? -1 : (hv > 0), sD = hd < 0 ? -1 : (hd > 0);
+  const uint32_t* Vg = vint.limbs + vidx * cap;   // global, read-only
+  const uint32_t* Dg = vint.limbs + pidx * cap;
   const long long ridx = rrow0 + r;
-  if (na == 0) {
+  uint32_t* dst = rint.limbs + ridx * cap;
+  if (na == 0 || nD == 0) {
     if (threadIdx.x == 0) rint.hdr[ridx] = 0;
-    uint32_t* dst = rint.limbs + ridx * cap;
     for (int i = threadIdx.x; i < cap; i += blockDim.x) dst[i] = 0u;
     return;
   }
+  const int n = limbs_bits(Dg, nD);
+  const int vbits = limbs_bits(Vg, na);
+  const int tv = max(0, n - P.k2 - 40);
+  const int nt = max(0, (vbits - tv + 31) / 32);
   const int S = ys[0], nY = ys[1];
+  for (int i = threadIdx.x; i < nt; i += blockDim.x)
+    Vt[i] = field32(Vg, na, 32LL * i + tv);
   for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
   __syncthreads();
-  // q~ = (|V| * Y) >> (S - k2)
-  const int nP = na + nY;
-  cta_mul(V, na, Y, nY, Pr, nP, col, red);
-  const int shift = S - P.k2;
-  const int nQ = max(0, (32 * nP - shift + 31) / 32);
+  const int nP = nt + nY;
+  cta_mul(Vt, nt, Y, nY, Pr, nP, col, red);
+  const int sh = S - P.k2 - tv;
+  const int nQ = max(0, (int)((32LL * nP - sh + 31) / 32));
   for (int i = threadIdx.x; i < nQ; i += blockDim.x)
-    Qt[i] = field32(Pr, nP, 32LL * i + shift);
+    Qt[i] = field32(Pr, nP, 32LL * i + sh);
+  const uint32_t frac = field32(Pr, nP, (long long)sh - 32);
   __syncthreads();
   int nq = cta_limb_len(Qt, nQ, red);
-  // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
-  const int nw = nD + 2;
-  cta_mul(Qt, nq, D, nD, Wb, nw, col, red);
-  cta_resolve(
-      nw, 32,
-      [&](int k) -> int64_t {
-        return (int64_t)field32(V, na, 32LL * k - P.k2) - (int64_t)Wb[k];
-      },
-      [&](int k, uint32_t d) { Wa[k] = d; }, red);
-  int adj = 0;
-  if (Wa[nw - 1] & 0x80000000u) {
-    adj = -1;  // remainder negative: q~ was one too large
-  } else {
-    // r - D >= 0 ? then q~ was one too small
+  const bool exact_needed = sh < 32 || frac < 2u || frac > 0xFFFFFFFDu;
+  if (exact_needed) {
+    // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
+    const int nw = nD + 2;
+    uint32_t* Wa = Pr;
+    uint32_t* Wb = Pr + nw;
+    cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red);
     cta_resolve(
         nw, 32,
         [&](int k) -> int64_t {
-          return (int64_t)Wa[k] - (int64_t)(k < nD ? D[k] : 0u);
+          return (int64_t)field32(Vg, na, 32LL * k - P.k2) - (int64_t)Wb[k];
         },
-        [&](int k, uint32_t d) { Wb[k] = d; }, red);
-    if (!(Wb[nw - 1] & 0x80000000u)) {
-      adj = 1;
-      // and r - 2D must be negative
+        [&](int k, uint32_t d) { Wa[k] = d; }, red);
+    int adj = 0;
+    if (Wa[nw - 1] & 0x80000000u) {
+      adj = -1;  // remainder negative: q~ was one too large
+    } else {
       cta_resolve(
           nw, 32,
           [&](int k) -> int64_t {
-            return (int64_t)Wb[k] - (int64_t)(k < nD ? D[k] : 0u);
+            return (int64_t)Wa[k] - (int64_t)(k < nD ? Dg[k] : 0u);
           },
-          [&](int k, uint32_t d) { Wa[k] = d; }, red);
-      if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
-        atomicOr(&err[kErrInternal], kIntDivision);
+          [&](int k, uint32_t d) { Wb[k] = d; }, red);
+      if (!(Wb[nw - 1] & 0x80000000u)) {
+        adj = 1;
+        cta_resolve(
+            nw, 32,
+            [&](int k) -> int64_t {
+              return (int64_t)Wb[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+            },
+            [&](int k, uint32_t d) { Wa[k] = d; }, red);
+        if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
+          atomicOr(&err[kErrInternal], kIntDivision);
+      }
     }
-  }
-  if (adj != 0) {
-    const int nn = nq + 1;
-    cta_resolve(
-        nn, 32,
-        [&](int k) -> int64_t {
-          return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
-        },
-        [&](int k, uint32_t d) { Pr[k] = d; }, red);
-    for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = Pr[i];
-    __syncthreads();
-    nq = cta_limb_len(Qt, nn, red);
+    if (adj != 0) {
+      const int nn = nq + 1;
+      cta_resolve(
+          nn, 32,
+          [&](int k) -> int64_t {
+            return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
+          },
+          [&](int k, uint32_t d) { col[k] = d; }, red);
+      for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
+      __syncthreads();
+      nq = cta_limb_len(Qt, nn, red);
+    }
   }
   if (nq > cap) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     return;
   }
-  const int rs = sV * sD;
-  uint32_t* dst = rint.limbs + ridx * cap;
   for (int i = threadIdx.x; i < cap; i += blockDim.x)
     dst[i] = i < nq ? Qt[i] : 0u;
-  if (threadIdx.x == 0) rint.hdr[ridx] = nq == 0 ? 0 : rs * nq;
+  if (threadIdx.x == 0) rint.hdr[ridx] = nq == 0 ? 0 : sV * sD * nq;
 }
 
 // --------------------------------------------------------- trailing update -
@@ -537,6 +545,123 @@ k_update(DevPlan P, uint32_t* W, const long long* colbase,
 #pragma unroll
     for (int i = 0; i < TILE; ++i) {
       const int r = r0 + i;
+      if (r < c || r >= P.n) continue;
+      uint32_t* ptr = W + (base + (r - c)) * NW + wd;
+      const uint32_t t32 = reduce_sum64(acc[i][j], pc);
+      const uint32_t old = *ptr;
+      *ptr = old >= t32 ? old - t32 : old + pc.q - t32;
+    }
+  }
+}
+
+// ------------------------------------------------ trailing update (SMEM) --
+// Same contract as k_update.  A CTA (4 warps) owns a 16 x 16 (r,c) tile and
+// 32 consecutive transform words; warp w computes the 8 x 8 sub-tile
+// (w>>1, w&1), lane = word.  Each stage's operands -- 16 rows of Rhat and 16
+// columns of Vhat, 32 words each (4 KB) -- are staged into shared memory by
+// cp.async through a kStages-deep pipeline, so the L2 latency hides behind
+// the 64 IMAD.WIDE of the stages in flight and every operand word fetched
+// from L2 feeds 16 products (0.5 B/product).
+namespace {
+constexpr int kUT = 16;        // CTA tile edge
+constexpr int kUStages = 4;    // cp.async pipeline depth
+constexpr int kUWords = 32;    // words per CTA
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128, 2)
+k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
+               const uint32_t* Vhat, const uint32_t* Rhat,
+               long long row_stride_slot, int nslots, int c_begin, int c_end,
+               int nct, int nrt, const int* err) {
+  __shared__ __align__(16) uint32_t sm[kUStages][2 * kUT][kUWords];
+  if (stage_aborted(err)) return;
+  const int w0 = blockIdx.y * kUWords;
+  int t = blockIdx.x, ct = 0;
+  while (t >= nrt - ct) {
+    t -= nrt - ct;
+    ++ct;
+  }
+  const int rt = ct + t;
+  const int c0 = c_begin + ct * kUT;
+  const int r0 = c_begin + rt * kUT;
+  const long long NW = P.NW;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // loader: 32 operand rows x 8 chunks of 16 B = 256 chunks, 2 per thread
+  const uint32_t* src[2];
+  int dst_k[2], dst_w[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int chunk = tid + 128 * h;
+    const int k = chunk >> 3, part = chunk & 7;
+    const uint32_t* base;
+    if (k < kUT) base = Rhat + (long long)min(r0 + k, P.n - 1) * NW;
+    else base = Vhat + (long long)min(c0 + k - kUT, c_end - 1) * NW;
+    src[h] = base + w0 + part * 4;
+    dst_k[h] = k;
+    dst_w[h] = part * 4;
+  }
+  auto issue = [&](int s) {
+    const int buf = s % kUStages;
+    const long long off = s * row_stride_slot;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) cp_async16(&sm[buf][dst_k[h]][dst_w[h]], src[h] + off);
+  };
+#pragma unroll
+  for (int s = 0; s < kUStages - 1; ++s) {
+    if (s < nslots) issue(s);
+    cp_async_commit();
+  }
+
+  const int rm = (warp >> 1) * 8, cm = (warp & 1) * 8;
+  uint64_t acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+
+  for (int s = 0; s < nslots; ++s) {
+    if (s + kUStages - 1 < nslots) issue(s + kUStages - 1);
+    cp_async_commit();
+    cp_async_wait<kUStages - 1>();
+    __syncthreads();
+    const int buf = s % kUStages;
+    uint32_t a[8], b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = sm[buf][rm + i][lane];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) b[j] = sm[buf][kUT + cm + j][lane];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] += (uint64_t)a[i] * b[j];
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  const int wd = w0 + lane;
+  if (wd >= P.NW) return;
+  const PrimeConsts pc = P.pc[wd / P.L];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + cm + j;
+    if (c >= c_end) continue;
+    const long long base = colbase[c];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = r0 + rm + i;
       if (r < c || r >= P.n) continue;
       uint32_t* ptr = W + (base + (r - c)) * NW + wd;
       const uint32_t t32 = reduce_sum64(acc[i][j], pc);
@@ -696,6 +821,19 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           int nslots, int c_begin, int c_end, const int* err,
                           cudaStream_t st) {
   if (c_begin >= c_end || nslots <= 0) return cudaSuccess;
+  if (tile == 16 && P.NW % kUWords == 0) {
+    const int nct = (c_end - c_begin + kUT - 1) / kUT;
+    const int nrt = (P.n - c_begin + kUT - 1) / kUT;
+    long long tiles = 0;
+    for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
+    dim3 grid((unsigned)tiles, P.NW / kUWords);
+    ++g_launches;
+    k_update_tiled<<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
+                                         row_stride_slot, nslots, c_begin,
+                                         c_end, nct, nrt, err);
+    return cudaGetLastError();
+  }
+  if (tile == 16) tile = 8;
   const int nct = (c_end - c_begin + tile - 1) / tile;
   const int nrt = (P.n - c_begin + tile - 1) / tile;
   long long tiles = 0;

@@ -70,8 +70,8 @@ struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
 
 // Shared-memory words of one k_divide CTA (layout in ldlt_kernels.cu).
 __host__ __device__ inline long long div_span_words(int cap, int ycap) {
-  return 2LL * cap + ycap + (cap + ycap + 2) + 64 + 3LL * (cap + ycap + 2) +
-         (cap + ycap + 2) + 2LL * (cap + 2);
+  const long long CY = (long long)cap + ycap + 2;
+  return (long long)cap + ycap + 2 + 4 * CY + 64;
 }
 
 // Host launch wrappers (ldlt_kernels.cu).
