@@ -211,65 +211,88 @@ __device__ __forceinline__ int limbs_bits(const uint32_t* a, int len) {
 }
 
 // out[0..M) = low M limbs of a*b (M <= na+nb gives the exact product when
-// M == na+nb).  a, b, out in shared memory; out must not alias a or b.
-// col: 3*M words of shared scratch; red: blockDim/32+1 words.
+// M == na+nb).  Product scanning: a work item is a group of 8 consecutive
+// output columns times one segment of its i-range, so long middle columns
+// are split across threads (load balance); each item keeps 96-bit column
+// sums on PTX carry chains and writes them to its segment's planes.
+// col: scratch of `col_words` >= 3*M words (more words allow more segments);
+// out must not alias a, b or col.  red: blockDim/32+1 words.
 __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
                                int nb, uint32_t* out, int M, uint32_t* col,
-                               uint32_t* red) {
+                               uint32_t* red, int col_words = 0) {
   constexpr int G = 8;
   const int ngroups = (M + G - 1) / G;
-  uint32_t* c0p = col;
-  uint32_t* c1p = col + M;
-  uint32_t* c2p = col + 2 * M;
-  for (int g = threadIdx.x; g < ngroups; g += blockDim.x) {
+  const int maxseg = max(1, (col_words > 0 ? col_words : 3 * M) / (3 * M));
+  const int want = (2 * (int)blockDim.x + ngroups - 1) / max(ngroups, 1);
+  const int nseg = max(1, min(min(maxseg, want), 8));
+  const int minlen = min(na, nb);
+  const int seglen = (minlen + G - 1 + nseg - 1) / nseg;  // group i-range <= minlen+G-1
+  const int items = ngroups * nseg;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int g = it / nseg, sgi = it - g * nseg;
     const int k0 = g * G;
     uint32_t c0[G], c1[G], c2[G];
 #pragma unroll
     for (int t = 0; t < G; ++t) c0[t] = c1[t] = c2[t] = 0u;
     if (na > 0 && nb > 0) {
-      const int ilo = max(0, k0 - nb + 1);
-      const int ihi = min(k0 + G - 1, na - 1);
-      // window w[t] = b[k0 + t - i]
-      uint32_t w[G];
-#pragma unroll
-      for (int t = 0; t < G; ++t) {
-        const int j = k0 + t - ilo;
-        w[t] = (j >= 0 && j < nb) ? b[j] : 0u;
-      }
-      for (int i = ilo; i <= ihi; ++i) {
-        const uint32_t ai = a[i];
+      const int glo = max(0, k0 - nb + 1);
+      const int ghi = min(k0 + G - 1, na - 1);
+      const int ilo = glo + sgi * seglen;
+      const int ihi = min(ghi, ilo + seglen - 1);
+      if (ilo <= ihi) {
+        // window w[t] = b[k0 + t - i]
+        uint32_t w[G];
 #pragma unroll
         for (int t = 0; t < G; ++t) {
-          asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
-              "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
-              "addc.u32 %2, %2, 0;"
-              : "+r"(c0[t]), "+r"(c1[t]), "+r"(c2[t])
-              : "r"(ai), "r"(w[t]));
+          const int j = k0 + t - ilo;
+          w[t] = (j >= 0 && j < nb) ? b[j] : 0u;
         }
-        // slide: next i needs b[k0 + t - i - 1]
+        for (int i = ilo; i <= ihi; ++i) {
+          const uint32_t ai = a[i];
 #pragma unroll
-        for (int t = G - 1; t > 0; --t) w[t] = w[t - 1];
-        const int j = k0 - i - 1;
-        w[0] = (j >= 0 && j < nb) ? b[j] : 0u;
+          for (int t = 0; t < G; ++t) {
+            asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+                "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+                "addc.u32 %2, %2, 0;"
+                : "+r"(c0[t]), "+r"(c1[t]), "+r"(c2[t])
+                : "r"(ai), "r"(w[t]));
+          }
+#pragma unroll
+          for (int t = G - 1; t > 0; --t) w[t] = w[t - 1];
+          const int j = k0 - i - 1;
+          w[0] = (j >= 0 && j < nb) ? b[j] : 0u;
+        }
       }
     }
+    uint32_t* pl = col + (size_t)sgi * 3 * M;
 #pragma unroll
     for (int t = 0; t < G; ++t) {
       const int k = k0 + t;
       if (k < M) {
-        c0p[k] = c0[t];
-        c1p[k] = c1[t];
-        c2p[k] = c2[t];
+        pl[k] = c0[t];
+        pl[M + k] = c1[t];
+        pl[2 * M + k] = c2[t];
       }
     }
   }
   __syncthreads();
+  // S_k = sum over segments of the column value at weight 2^(32k) (< 2^64);
+  // v_k = (S_k mod 2^32) + floor(S_{k-1} / 2^32) stays in the resolve domain
+  auto colsum = [&](int k) -> uint64_t {
+    uint64_t v = 0;
+    for (int sg = 0; sg < nseg; ++sg) {
+      const uint32_t* pl = col + (size_t)sg * 3 * M;
+      v += pl[k];
+      if (k >= 1) v += pl[M + k - 1];
+      if (k >= 2) v += pl[2 * M + k - 2];
+    }
+    return v;
+  };
   cta_resolve(
       M, 32,
       [&](int k) -> int64_t {
-        int64_t v = c0p[k];
-        if (k >= 1) v += c1p[k - 1];
-        if (k >= 2) v += c2p[k - 2];
+        int64_t v = (int64_t)(uint32_t)colsum(k);
+        if (k >= 1) v += (int64_t)(colsum(k - 1) >> 32);
         return v;
       },
       [&](int k, uint32_t d) { out[k] = d; }, red);

@@ -141,6 +141,11 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad device index");
   CU(cudaSetDevice(device_));
   CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
+  }
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
 }
@@ -152,6 +157,8 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : uev_) cudaEventDestroy(e);
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
+  for (cudaEvent_t e : pev_) cudaEventDestroy(e);
+  if (stream_panel_) cudaStreamDestroy(stream_panel_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -330,12 +337,14 @@ void Matrix::build(int min_logL) {
   if (herr[kErrCapacity])
     throw Error(HGPU_ERR_CAPACITY, "strip does not fit the transform plan");
 
-  vhdr_ = dalloc<int>((size_t)kb * n_);
-  rhdr_ = dalloc<int>((size_t)kb * n_);
-  vlimbs_ = dalloc<uint32_t>((size_t)kb * n_ * P.cap);
-  rlimbs_ = dalloc<uint32_t>((size_t)kb * n_ * P.cap);
-  vhat_ = dalloc<uint32_t>((size_t)kb * n_ * NW);
-  rhat_ = dalloc<uint32_t>((size_t)kb * n_ * NW);
+  // two slot sets: panel b uses set b%2 (lookahead needs b+1 while the
+  // trailing update of b still reads b)
+  vhdr_ = dalloc<int>(2 * (size_t)kb * n_);
+  rhdr_ = dalloc<int>(2 * (size_t)kb * n_);
+  vlimbs_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
+  rlimbs_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
+  vhat_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * NW);
+  rhat_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * NW);
   phdr_ = dalloc<int>(n_);
   plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
   ybuf_ = dalloc<uint32_t>(P.ycap);
@@ -346,16 +355,21 @@ void Matrix::build(int min_logL) {
   stats_ = dalloc<int>(3 * (size_t)n_);
 }
 
-void Matrix::panel_broadcast(int owner, int p0, int ns, cudaStream_t st) {
+void Matrix::panel_broadcast(int owner, int p0, int ns, long long row0,
+                             cudaStream_t st) {
   if (world_ == 1) return;
   ncclComm_t c = (ncclComm_t)comm_;
   const Plan& P = plan_;
   const size_t slot_rows = (size_t)ns * n_;
+  int* vh = vhdr_ + row0;
+  int* rh = rhdr_ + row0;
+  uint32_t* vl = vlimbs_ + row0 * P.cap;
+  uint32_t* rl = rlimbs_ + row0 * P.cap;
   NC(ncclGroupStart());
-  NC(ncclBroadcast(vhdr_, vhdr_, slot_rows, ncclInt32, owner, c, st));
-  NC(ncclBroadcast(rhdr_, rhdr_, slot_rows, ncclInt32, owner, c, st));
-  NC(ncclBroadcast(vlimbs_, vlimbs_, slot_rows * P.cap, ncclUint32, owner, c, st));
-  NC(ncclBroadcast(rlimbs_, rlimbs_, slot_rows * P.cap, ncclUint32, owner, c, st));
+  NC(ncclBroadcast(vh, vh, slot_rows, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(rh, rh, slot_rows, ncclInt32, owner, c, st));
+  NC(ncclBroadcast(vl, vl, slot_rows * P.cap, ncclUint32, owner, c, st));
+  NC(ncclBroadcast(rl, rl, slot_rows * P.cap, ncclUint32, owner, c, st));
   NC(ncclBroadcast(phdr_ + p0, phdr_ + p0, ns, ncclInt32, owner, c, st));
   NC(ncclBroadcast(plimbs_ + (size_t)p0 * P.cap, plimbs_ + (size_t)p0 * P.cap,
                    (size_t)ns * P.cap, ncclUint32, owner, c, st));
@@ -369,7 +383,8 @@ void Matrix::panel_broadcast(int owner, int p0, int ns, cudaStream_t st) {
 void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   const Plan& P = plan_;
   const DevPlan& D = dp_;
-  cudaStream_t st = stream_;
+  cudaStream_t st = stream_;       // trailing updates (bulk)
+  cudaStream_t sp = stream_panel_; // panel factorisation (critical path)
   const int n = n_, kb = P.kb;
   const size_t NW = (size_t)D.NW;
   const long long slot_stride = (long long)n * NW;
@@ -402,10 +417,24 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     res.ratios.assign(n > 0 ? n - 1 : 0, {});
     res.have_ratios = true;
   }
-  std::vector<int> hv_hdr, hr_hdr;
+  std::vector<int> hr_hdr;
   std::vector<uint32_t> hr_limbs;
   size_t uev_used = 0;
-  auto timed_update = [&](int nslots, int c_begin, int c_end) {
+  const int nblocks = (n + kb - 1) / kb;
+  while ((int)pev_.size() < 3 * nblocks + 3) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pev_.push_back(e);
+  }
+  // events: panel_done[b], next_ready[b] (panel b's columns fully updated),
+  // trail_done[b] (slot set of panel b released)
+  cudaEvent_t* panel_done = pev_.data();
+  cudaEvent_t* next_ready = pev_.data() + nblocks + 1;
+  cudaEvent_t* trail_done = pev_.data() + 2 * nblocks + 2;
+
+  // slot set of panel b: rows [set*kb*n, ...) of Vint/Rint/Vhat/Rhat
+  auto set_row0 = [&](int b) { return (long long)(b % 2) * kb * n; };
+  auto timed_update = [&](int b, int nslots, int c_begin, int c_end) {
     if (c_begin >= c_end || nslots <= 0) return;
     if (profile) {
       while (uev_.size() < uev_used + 2) {
@@ -415,70 +444,96 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       }
       CU(cudaEventRecord(uev_[uev_used], st));
     }
-    CU(launch_update(D, P.tile, W_, colbase_, vhat_, rhat_, slot_stride,
-                     nslots, c_begin, c_end, err_, st));
+    const long long r0 = set_row0(b);
+    CU(launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW, rhat_ + r0 * NW,
+                     slot_stride, nslots, c_begin, c_end, err_, st));
     if (profile) {
       CU(cudaEventRecord(uev_[uev_used + 1], st));
       uev_used += 2;
-      // modular products: pairs x stages x NW
       double pairs = 0;
       for (int c = c_begin; c < c_end; ++c) pairs += n - c;
       res.update_products += pairs * nslots * (double)NW;
       ++res.update_launches;
     }
   };
+  // trailing update of panel b restricted to owned columns in [lo, hi)
+  auto trailing = [&](int b, int lo, int hi) {
+    const int p0 = b * kb, nsl = std::min(kb, n - 1 - p0);
+    int run_begin = -1, run_end = -1;
+    auto flush = [&]() {
+      if (run_begin >= 0 && run_begin < run_end)
+        timed_update(b, nsl, run_begin, run_end);
+      run_begin = run_end = -1;
+    };
+    for (int ob : owned_blocks_) {
+      const int c0 = std::max(lo, ob * kb), c1 = std::min(hi, (ob + 1) * kb);
+      if (c0 >= c1) continue;
+      if (run_begin >= 0 && c0 == run_end) {
+        run_end = c1;
+      } else {
+        flush();
+        run_begin = c0;
+        run_end = c1;
+      }
+    }
+    flush();
+  };
 
-  const int nblocks = (n + kb - 1) / kb;
+  CU(cudaEventRecord(next_ready[0], st));  // init done
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
+    const long long row0set = set_row0(b);
+    // ---- panel b on the high-priority stream
+    CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
+    if (b >= 2) CU(cudaStreamWaitEvent(sp, trail_done[b - 2], 0));
     if (owner == rank_) {
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
-        const long long row0 = (long long)s * n;  // slot base in row units
+        const long long row0 = row0set + (long long)s * n;
         // left-looking inside the panel: column p receives stages [p0, p)
-        CU(launch_update_col(D, W_, colbase_, vhat_, rhat_, slot_stride, s, p,
-                             err_, st));
-        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, err_, st));
+        CU(launch_update_col(D, W_, colbase_, vhat_ + row0set * NW,
+                             rhat_ + row0set * NW, slot_stride, s, p, err_, sp));
+        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, err_, sp));
         if (p == n - 1) break;
         CU(launch_recip(D, vint, row0 + p, maxbitsV, p, ybuf_, ys_, rscratch_,
-                        recip_global_ ? 1 : 0, err_, st));
+                        recip_global_ ? 1 : 0, err_, sp));
         CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, dscratch_,
-                         div_global_ ? 1 : 0, err_, st));
-        // transforms of V_p[r], R_p[r] for r in (p, n)
+                         div_global_ ? 1 : 0, err_, sp));
         CU(launch_fwd_ints(D, vint, row0 + p + 1, vhat_, row0 + p + 1,
-                           n - p - 1, 0, maxdegV + p, err_, st));
+                           n - p - 1, 0, maxdegV + p, err_, sp));
         CU(launch_fwd_ints(D, rint, row0 + p + 1, rhat_, row0 + p + 1,
-                           n - p - 1, 1, maxdegR + p, err_, st));
+                           n - p - 1, 1, maxdegR + p, err_, sp));
       }
     }
-    panel_broadcast(owner, p0, ns, st);
+    panel_broadcast(owner, p0, ns, row0set, sp);
     if (owner != rank_ && p1 < n) {
       for (int s = 0; s < ns; ++s) {
-        const long long row0 = (long long)s * n;
+        const long long row0 = row0set + (long long)s * n;
         CU(launch_fwd_ints(D, vint, row0 + p1, vhat_, row0 + p1, n - p1, 0,
-                           nullptr, err_, st));
+                           nullptr, err_, sp));
         CU(launch_fwd_ints(D, rint, row0 + p1, rhat_, row0 + p1, n - p1, 1,
-                           nullptr, err_, st));
+                           nullptr, err_, sp));
       }
     }
+    CU(cudaEventRecord(panel_done[b], sp));
     if (capture) {
       const int nsr = std::min(ns, n - 1 - p0);
       if (nsr > 0) {
         hr_hdr.resize((size_t)nsr * n);
         hr_limbs.resize((size_t)nsr * n * P.cap);
-        CU(cudaMemcpyAsync(hr_hdr.data(), rhdr_, hr_hdr.size() * 4,
-                           cudaMemcpyDeviceToHost, st));
-        CU(cudaMemcpyAsync(hr_limbs.data(), rlimbs_, hr_limbs.size() * 4,
-                           cudaMemcpyDeviceToHost, st));
-        CU(cudaStreamSynchronize(st));
+        CU(cudaMemcpyAsync(hr_hdr.data(), rhdr_ + row0set, hr_hdr.size() * 4,
+                           cudaMemcpyDeviceToHost, sp));
+        CU(cudaMemcpyAsync(hr_limbs.data(), rlimbs_ + row0set * P.cap,
+                           hr_limbs.size() * 4, cudaMemcpyDeviceToHost, sp));
+        CU(cudaStreamSynchronize(sp));
         for (int s = 0; s < nsr; ++s) {
           const int p = p0 + s;
-          auto& col = res.ratios[p];
-          col.resize(n - p - 1);
+          auto& colv = res.ratios[p];
+          colv.resize(n - p - 1);
           for (int r = p + 1; r < n; ++r) {
             const size_t idx = (size_t)s * n + r;
-            HostInt& h = col[r - p - 1];
+            HostInt& h = colv[r - p - 1];
             h.size = hr_hdr[idx];
             const int len = std::abs(h.size);
             h.limbs.assign(hr_limbs.begin() + idx * P.cap,
@@ -487,30 +542,23 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         }
       }
     }
-    // trailing update of owned columns >= p1
+    // ---- trailing update of panel b on the bulk stream: the next panel's
+    // columns first (they gate panel b+1), then everything to their right,
+    // which overlaps panel b+1's factorisation
+    CU(cudaStreamWaitEvent(st, panel_done[b], 0));
     if (p1 < n) {
-      // one launch per maximal run of contiguous owned blocks (a single
-      // rank owns one run; with several ranks the runs interleave)
-      int run_begin = -1, run_end = -1;
-      auto flush = [&]() {
-        if (run_begin >= 0 && run_begin < run_end)
-          timed_update(std::min(ns, n - 1 - p0), run_begin, run_end);
-        run_begin = run_end = -1;
-      };
-      for (int ob : owned_blocks_) {
-        const int c0 = std::max(p1, ob * kb), c1 = std::min(n, (ob + 1) * kb);
-        if (c0 >= c1) continue;
-        if (run_begin >= 0 && c0 == run_end) {
-          run_end = c1;
-        } else {
-          flush();
-          run_begin = c0;
-          run_end = c1;
-        }
-      }
-      flush();
+      const int p2 = std::min(n, p1 + kb);
+      trailing(b, p1, p2);
+      CU(cudaEventRecord(next_ready[b + 1], st));
+      trailing(b, p2, n);
+    } else {
+      CU(cudaEventRecord(next_ready[b + 1], st));
     }
+    CU(cudaEventRecord(trail_done[b], st));
   }
+  // join the panel stream back into the bulk stream
+  CU(cudaEventRecord(panel_done[nblocks], sp));
+  CU(cudaStreamWaitEvent(st, panel_done[nblocks], 0));
   CU(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));
   CU(cudaEventRecord(ev1_, st));
   res.launches = kernel_launch_count() - launches0;

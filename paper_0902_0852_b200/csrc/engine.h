@@ -81,7 +81,8 @@ class Matrix {
   void build(int min_logL);
   void release();
   void run(const HostInt& x, unsigned flags, FactorResult& res);
-  void panel_broadcast(int owner, int p0, int ns, cudaStream_t st);
+  void panel_broadcast(int owner, int p0, int ns, long long row0,
+                       cudaStream_t st);
   void fold(FactorResult& res);
 
   int n_, K_, device_;
@@ -114,7 +115,9 @@ class Matrix {
   size_t div_smem_ = 0;
   bool div_global_ = false;
   bool recip_global_ = false;
-  cudaStream_t stream_ = nullptr;
+  cudaStream_t stream_ = nullptr;        // bulk (trailing updates)
+  cudaStream_t stream_panel_ = nullptr;  // panel factorisation, high priority
+  std::vector<cudaEvent_t> pev_;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> uev_;
 };

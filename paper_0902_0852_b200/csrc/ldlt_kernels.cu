@@ -286,7 +286,8 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
   uint32_t* Pr = Y + Lm;             // 2 Lm + 1
   uint32_t* E = Pr + 2 * Lm + 1;     // 2 Lm + 2
   uint32_t* Tm = E + 2 * Lm + 2;     // 3 Lm + 2
-  uint32_t* col = Tm + 3 * Lm + 2;   // 3 (3 Lm + 2)
+  uint32_t* col = Tm + 3 * Lm + 2;   // 2 * 3 (3 Lm + 2)
+  const int col_words = 6 * (3 * Lm + 2);
   int lv[40];
   const int nl = recip_levels(Pt, lv);
   // seed: Y_0 = floor(2^(n+p0)/D) ~ (2^126/top64(D)) >> (62 - p0)
@@ -313,7 +314,7 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
     __syncthreads();
     // Pr = D' * Y
     const int nP = nDt + nY;
-    cta_mul(Dt, nDt, Y, nY, Pr, nP, col, red);
+    cta_mul(Dt, nDt, Y, nY, Pr, nP, col, red, col_words);
     // E = 2^(mb+pa) - Pr, signed, over nP+1 limbs
     const int nEw = nP + 1;
     const int Sb = mb + pa;
@@ -333,7 +334,7 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
     const int nE = cta_limb_len(E, nEw, red);
     // Tm = Y * |E|
     const int nT = nY + nE;
-    if (nE > 0) cta_mul(Y, nY, E, nE, Tm, nT, col, red);
+    if (nE > 0) cta_mul(Y, nY, E, nE, Tm, nT, col, red, col_words);
     // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
     const int nYn = min(Lm, (pb + 2 + 31) / 32 + 1);
     const int sh = Sb - dlt;
@@ -786,7 +787,7 @@ size_t recip_scratch_words(const DevPlan& P) {
   // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
   const size_t Lm = (size_t)P.ycap + 4;
   return Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
-         3 * (3 * Lm + 2) + 64;
+         6 * (3 * Lm + 2) + 64;
 }
 
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
