@@ -85,6 +85,167 @@ __device__ inline void cta_ntt_inv_multi(uint32_t* x, int np, int logL,
   }
 }
 
+// ------------------------------------------------ radix-16 NTT (SMEM) ------
+// The same transforms as above, restructured for B200 SMEM: every pass does
+// up to four butterfly levels on 16 registers per unit, so a length-2048
+// transform is 3 passes (3 barriers) instead of 11, and the pass whose
+// elements are contiguous (the last forward / first inverse pass) moves them
+// with 16-byte vector loads.  Twiddles are in Montgomery form (one word):
+//   mont_mul(a, w 2^32 mod q) = a w mod q  in [0, 2q)  for a < 2^32.
+__device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t wm,
+                                             uint32_t q, uint32_t qneg) {
+  const uint64_t t = (uint64_t)a * wm;
+  const uint32_t m = (uint32_t)t * qneg;
+  return (uint32_t)((t + (uint64_t)m * q) >> 32);
+}
+
+template <int R>
+__device__ __forceinline__ void load_unit(const uint32_t* xj, int base, int s,
+                                          uint32_t* a) {
+  if (s == 1 && R >= 4) {
+#pragma unroll
+    for (int u = 0; u < R; u += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(xj + base + u);
+      a[u] = v.x; a[u + 1] = v.y; a[u + 2] = v.z; a[u + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < R; ++u) a[u] = xj[base + u * s];
+  }
+}
+template <int R>
+__device__ __forceinline__ void store_unit(uint32_t* xj, int base, int s,
+                                           const uint32_t* a) {
+  if (s == 1 && R >= 4) {
+#pragma unroll
+    for (int u = 0; u < R; u += 4)
+      *reinterpret_cast<uint4*>(xj + base + u) = make_uint4(a[u], a[u + 1], a[u + 2], a[u + 3]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < R; ++u) xj[base + u * s] = a[u];
+  }
+}
+
+// forward pass over levels [lm0, lm0 + log2 R)
+template <int R>
+__device__ inline void fwd_pass(uint32_t* x, int np, int logL, int lm0,
+                                const uint32_t* twm, const PrimeConsts* pc) {
+  constexpr int r = R == 2 ? 1 : (R == 4 ? 2 : (R == 8 ? 3 : 4));
+  const int L = 1 << logL;
+  const int ls = logL - lm0 - r;  // log2 s
+  const int s = 1 << ls;
+  const int lupp = logL - r;      // log2 units per prime
+  const int total = np << lupp;
+  for (int gu = threadIdx.x; gu < total; gu += blockDim.x) {
+    const int j = gu >> lupp, v = gu & ((1 << lupp) - 1);
+    const int i0 = v >> ls, jj = v & (s - 1);
+    const int base = (i0 << (ls + r)) + jj;
+    uint32_t* xj = x + j * L;
+    const uint32_t* tw = twm + j * L;
+    const uint32_t q = pc[j].q, q2 = 2 * q, qneg = pc[j].qneg;
+    const int mi = (1 << lm0) + i0;
+    uint32_t a[R];
+    load_unit<R>(xj, base, s, a);
+#pragma unroll
+    for (int l = 0; l < r; ++l) {
+      const int half = R >> (l + 1);
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        if (u & half) continue;
+        const uint32_t w = tw[(mi << l) + (u >> (r - l))];
+        uint32_t X = a[u];
+        X = X >= q2 ? X - q2 : X;
+        const uint32_t T = mont_mul(a[u + half], w, q, qneg);
+        a[u] = X + T;
+        a[u + half] = X - T + q2;
+      }
+    }
+    store_unit<R>(xj, base, s, a);
+  }
+  __syncthreads();
+}
+
+// inverse (GS) pass over levels with half-sizes 2^lt0 .. 2^(lt0+log2R-1)
+template <int R>
+__device__ inline void inv_pass(uint32_t* x, int np, int logL, int lt0,
+                                const uint32_t* itwm, const PrimeConsts* pc) {
+  constexpr int r = R == 2 ? 1 : (R == 4 ? 2 : (R == 8 ? 3 : 4));
+  const int L = 1 << logL;
+  const int S = 1 << lt0;
+  const int lupp = logL - r;
+  const int total = np << lupp;
+  for (int gu = threadIdx.x; gu < total; gu += blockDim.x) {
+    const int j = gu >> lupp, v = gu & ((1 << lupp) - 1);
+    const int bb = v >> lt0, jj = v & (S - 1);
+    const int base = (bb << (lt0 + r)) + jj;
+    uint32_t* xj = x + j * L;
+    const uint32_t* tw = itwm + j * L;
+    const uint32_t q = pc[j].q, q2 = 2 * q, qneg = pc[j].qneg;
+    uint32_t a[R];
+    load_unit<R>(xj, base, S, a);
+#pragma unroll
+    for (int l = 0; l < r; ++l) {
+      const int half = 1 << l;
+      const int ml = L >> (lt0 + l + 1);
+#pragma unroll
+      for (int u = 0; u < R; ++u) {
+        if (u & half) continue;
+        const uint32_t w = tw[ml + (bb << (r - l - 1)) + (u >> (l + 1))];
+        const uint32_t U = a[u], V = a[u + half];
+        const uint32_t Sm = U + V;
+        a[u] = Sm >= q2 ? Sm - q2 : Sm;
+        a[u + half] = mont_mul(U - V + q2, w, q, qneg);
+      }
+    }
+    store_unit<R>(xj, base, S, a);
+  }
+  __syncthreads();
+}
+
+// Forward: natural in (< 4q), bit-reversed out (< q).  twm: [np][L] table
+// T[m+i] in Montgomery form (any memory; shared memory when it fits).
+__device__ inline void cta_ntt_fwd16(uint32_t* x, int np, int logL,
+                                     const uint32_t* twm, const PrimeConsts* pc) {
+  // first pass takes logL mod 4 levels (large stride), then passes of 4;
+  // the last pass (s = 1) moves contiguous 16-word units
+  int lm = 0;
+  while (lm < logL) {
+    const int r = (lm == 0 && logL % 4) ? logL % 4 : 4;
+    switch (r) {
+      case 1: fwd_pass<2>(x, np, logL, lm, twm, pc); break;
+      case 2: fwd_pass<4>(x, np, logL, lm, twm, pc); break;
+      case 3: fwd_pass<8>(x, np, logL, lm, twm, pc); break;
+      default: fwd_pass<16>(x, np, logL, lm, twm, pc); break;
+    }
+    lm += r;
+  }
+  const int L = 1 << logL;
+  for (int gi = threadIdx.x; gi < np * L; gi += blockDim.x) {
+    const uint32_t q = pc[gi >> logL].q, q2 = 2 * q;
+    uint32_t X = x[gi];
+    X = X >= q2 ? X - q2 : X;
+    x[gi] = X >= q ? X - q : X;
+  }
+  __syncthreads();
+}
+
+// Inverse without 1/L: bit-reversed in (< 2q), natural out (< 2q).
+__device__ inline void cta_ntt_inv16(uint32_t* x, int np, int logL,
+                                     const uint32_t* itwm, const PrimeConsts* pc) {
+  // passes of 4 from the contiguous end (S = 1); the last takes the rest
+  int lt = 0;
+  while (lt < logL) {
+    const int r = logL - lt >= 4 ? 4 : logL - lt;
+    switch (r) {
+      case 1: inv_pass<2>(x, np, logL, lt, itwm, pc); break;
+      case 2: inv_pass<4>(x, np, logL, lt, itwm, pc); break;
+      case 3: inv_pass<8>(x, np, logL, lt, itwm, pc); break;
+      default: inv_pass<16>(x, np, logL, lt, itwm, pc); break;
+    }
+    lt += r;
+  }
+}
+
 // ----------------------------------------------------- carry functions -----
 // A carry function maps carry-in c in {-1,0,1,2} to carry-out in the same
 // set; entry c is stored in bits [2(c+1), 2(c+1)+2) as (out+1).

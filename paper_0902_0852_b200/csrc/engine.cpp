@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 namespace hgpu {
@@ -286,12 +287,36 @@ void Matrix::build(int min_logL) {
       }
     }
   }
+  // Montgomery-form copies (w 2^32 mod q) for the radix-16 transforms
+  const size_t npl = (size_t)P.np * P.L;
+  tab.resize(6 * npl, 0);
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    for (int k = 1; k < P.L; ++k) {
+      tab[4 * npl + j * (size_t)P.L + k] =
+          (uint32_t)(((u128)tab[0 * npl + j * (size_t)P.L + k] << 32) % q);
+      tab[5 * npl + j * (size_t)P.L + k] =
+          (uint32_t)(((u128)tab[2 * npl + j * (size_t)P.L + k] << 32) % q);
+    }
+  }
   tw_ = dalloc<uint32_t>(tab.size());
   CU(cudaMemcpy(tw_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
   D.tw = tw_;
-  D.twp = tw_ + (size_t)P.np * P.L;
-  D.itw = tw_ + 2 * (size_t)P.np * P.L;
-  D.itwp = tw_ + 3 * (size_t)P.np * P.L;
+  D.twp = tw_ + npl;
+  D.itw = tw_ + 2 * npl;
+  D.itwp = tw_ + 3 * npl;
+  D.twm = tw_ + 4 * npl;
+  D.itwm = tw_ + 5 * npl;
+  {
+    // stage the tables in SMEM when the extraction CTA still fits twice
+    const size_t words = 3 * npl + 2 * (size_t)(P.L + P.T) + P.cap + 64;
+    D.tw_smem = words * 4 <= 110 * 1024 ? 1 : 0;
+    int dev = 0, nsm = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    D.grid_cap = 2 * nsm;
+    if (const char* dbg = std::getenv("HGPU_DEBUG")) D.debug = std::atoi(dbg);
+  }
 
   CU(configure_kernels(D, &div_smem_, &div_global_, &recip_global_));
 
@@ -351,7 +376,7 @@ void Matrix::build(int min_logL) {
   ys_ = dalloc<int>(2);
   rscratch_ = dalloc<uint32_t>(recip_scratch_words(D));
   if (div_global_)
-    dscratch_ = dalloc<uint32_t>((size_t)n_ * divide_smem_words(D));
+    dscratch_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
   stats_ = dalloc<int>(3 * (size_t)n_);
 }
 
@@ -494,16 +519,15 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         // left-looking inside the panel: column p receives stages [p0, p)
         CU(launch_update_col(D, W_, colbase_, vhat_ + row0set * NW,
                              rhat_ + row0set * NW, slot_stride, s, p, err_, sp));
-        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, err_, sp));
+        // W[r][p] -> V_p[r] (+ its transform for rows r > p)
+        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, vhat_,
+                          maxdegV, err_, sp));
         if (p == n - 1) break;
         CU(launch_recip(D, vint, row0 + p, maxbitsV, p, ybuf_, ys_, rscratch_,
                         recip_global_ ? 1 : 0, err_, sp));
-        CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, dscratch_,
-                         div_global_ ? 1 : 0, err_, sp));
-        CU(launch_fwd_ints(D, vint, row0 + p + 1, vhat_, row0 + p + 1,
-                           n - p - 1, 0, maxdegV + p, err_, sp));
-        CU(launch_fwd_ints(D, rint, row0 + p + 1, rhat_, row0 + p + 1,
-                           n - p - 1, 1, maxdegR + p, err_, sp));
+        // R_p[r] (+ its Montgomery-form transform)
+        CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, rhat_,
+                         maxdegR + p, dscratch_, div_global_ ? 1 : 0, err_, sp));
       }
     }
     panel_broadcast(owner, p0, ns, row0set, sp);

@@ -3,6 +3,8 @@
 // the only roundings are the reference's own truncations (tdiv_q_2exp for the
 // column values, tdiv_q for the ratios), so results are bit-identical.
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 
 #include "cta_ops.cuh"
@@ -29,33 +31,52 @@ __device__ inline int load_int(const IntBuf& b, long long idx, int cap,
   return h < 0 ? -1 : (h > 0 ? 1 : 0);
 }
 
-// Digit d_i (w bits) of |X| -> residues of the signed digit, forward NTT per
-// prime, optional Montgomery scaling (x 2^32), store NW words to out.
+// Stages the Montgomery twiddle tables in shared memory (when the plan says
+// they fit) and returns the pointers the transforms should use.
+__device__ inline void stage_tables(const DevPlan& P, uint32_t* sm_fwd,
+                                    uint32_t* sm_inv, const uint32_t** fwd,
+                                    const uint32_t** inv) {
+  if (P.tw_smem) {
+    for (int i = threadIdx.x; i < P.NW; i += blockDim.x) {
+      if (sm_fwd) sm_fwd[i] = P.twm[i];
+      if (sm_inv) sm_inv[i] = P.itwm[i];
+    }
+    __syncthreads();
+    if (fwd) *fwd = sm_fwd;
+    if (inv) *inv = sm_inv;
+  } else {
+    if (fwd) *fwd = P.twm;
+    if (inv) *inv = P.itwm;
+  }
+}
+
+// Digit d_i (w bits) of |X| >> shift -> residues of the signed digit,
+// forward NTT per prime, optional Montgomery scaling (x 2^32), store NW words
+// to out.  sm: NW words of scratch, must not alias mag.
 __device__ void transform_int(const DevPlan& P, const uint32_t* mag, int len,
-                              int sign, uint32_t* sm, uint32_t* out, bool mont,
+                              long long shift, int sign, uint32_t* sm,
+                              uint32_t* out, bool mont, const uint32_t* twm,
                               int* err) {
-  const int bits = limbs_bits(mag, len);
-  if (bits > P.w * P.L) {
+  const long long bits = (long long)limbs_bits(mag, len) - shift;
+  if (bits > (long long)P.w * P.L) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapDigits);
   }
   const uint32_t dmask = (1u << P.w) - 1u;
-  for (int j = 0; j < P.np; ++j) {
+  for (int gi = threadIdx.x; gi < P.NW; gi += blockDim.x) {
+    const int j = gi >> P.logL, i = gi & (P.L - 1);
     const uint32_t q = P.pc[j].q;
-    uint32_t* x = sm + j * P.L;
-    for (int i = threadIdx.x; i < P.L; i += blockDim.x) {
-      const uint32_t d = field32(mag, len, (long long)P.w * i) & dmask;
-      x[i] = (sign < 0 && d) ? q - d : d;
-    }
+    const uint32_t d = field32(mag, len, (long long)P.w * i + shift) & dmask;
+    sm[gi] = (sign < 0 && d) ? q - d : d;
   }
   __syncthreads();
-  cta_ntt_fwd_multi(sm, P.np, P.logL, P.tw, P.twp, P.Lmax, P.pc);
-  for (int j = 0; j < P.np; ++j) {
-    const PrimeConsts& c = P.pc[j];
-    for (int i = threadIdx.x; i < P.L; i += blockDim.x) {
-      uint32_t v = sm[j * P.L + i];
-      if (mont) v = reduce_2q(mul_shoup(v, c.r32, c.r32s, c.q), c.q);
-      out[j * P.L + i] = v;
+  cta_ntt_fwd16(sm, P.np, P.logL, twm, P.pc);
+  for (int gi = threadIdx.x; gi < P.NW; gi += blockDim.x) {
+    uint32_t v = sm[gi];
+    if (mont) {
+      const PrimeConsts& c = P.pc[gi >> P.logL];
+      v = reduce_2q(mont_mul(v, c.r64, c.q, c.qneg), c.q);
     }
+    out[gi] = v;
   }
   __syncthreads();
 }
@@ -63,21 +84,26 @@ __device__ void transform_int(const DevPlan& P, const uint32_t* mag, int len,
 // ------------------------------------------------------ forward transform --
 // For items i in [0,count): integer (in_base + i) of `src` -> transform at
 // out + (out_base + i)*NW.  Records deg = floor((bits-1)/w) via atomicMax.
-// Used for the strip moments at setup and for V_p / R_p rows every stage.
+// Used for the strip moments and the shift at setup, and by ranks that
+// receive a panel over NCCL.  Grid-stride over items.
 __global__ void k_fwd_ints(DevPlan P, IntBuf src, long long in_base,
                            uint32_t* out, long long out_base, int count,
                            int mont, int* maxdeg, int* err) {
   extern __shared__ uint32_t sm[];
-  const int item = blockIdx.x;
-  if (item >= count) return;
   if (err && stage_aborted(err)) return;
-  uint32_t* mag = sm + P.np * P.L;
-  int len;
-  const int sign = load_int(src, in_base + item, P.cap, mag, &len);
-  if (maxdeg && len > 0 && threadIdx.x == 0)
-    atomicMax(maxdeg, (limbs_bits(mag, len) - 1) / P.w);
-  transform_int(P, mag, len, sign, sm, out + (out_base + item) * (long long)P.NW,
-                mont != 0, err);
+  uint32_t* tab = sm;
+  uint32_t* buf = sm + (P.tw_smem ? P.NW : 0);
+  uint32_t* mag = buf + P.NW;
+  const uint32_t* twm;
+  stage_tables(P, tab, nullptr, &twm, nullptr);
+  for (int item = blockIdx.x; item < count; item += gridDim.x) {
+    int len;
+    const int sign = load_int(src, in_base + item, P.cap, mag, &len);
+    if (maxdeg && len > 0 && threadIdx.x == 0)
+      atomicMax(maxdeg, (limbs_bits(mag, len) - 1) / P.w);
+    transform_int(P, mag, len, 0, sign, buf,
+                  out + (out_base + item) * (long long)P.NW, mont != 0, twm, err);
+  }
 }
 
 // ------------------------------------------------------- workspace init ----
@@ -111,133 +137,149 @@ __global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
 // V goes to vint[slot][r]; the full pivot to piv[p].
 __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, IntBuf vint, long long vrow0, IntBuf piv,
-                          int* maxbitsV, int* err) {
+                          int* maxbitsV, uint32_t* vhat, int* maxdegV,
+                          int* err) {
   extern __shared__ uint32_t sm[];
   if (stage_aborted(err)) return;
-  const int r = p + blockIdx.x;
-  if (r >= P.n) return;
   const int L = P.L, np = P.np, T = P.T, w = P.w;
   const int M = L + T;
-  uint32_t* A = sm;                       // np*L residues -> CRT words
-  int* S = (int*)(sm + np * L);           // M digit sums
-  uint32_t* Dg = sm + np * L + M;         // M digits
-  uint32_t* Lb = Dg + M;                  // cap limbs of |W|
-  uint32_t* red = Lb + P.cap;             // scan scratch
-
-  const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
-  for (int i = threadIdx.x; i < P.NW; i += blockDim.x) A[i] = src[i];
-  __syncthreads();
-  cta_ntt_inv_multi(A, np, P.logL, P.itw, P.itwp, P.Lmax, P.pc);
-
-  // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    uint32_t a[kMaxPrimes];
-    for (int j = 0; j < np; ++j) {
-      const uint32_t q = P.pc[j].q;
-      uint32_t v = reduce_2q(A[j * L + i], q);
-      a[j] = reduce_2q(mul_shoup(v, P.invL[j], P.invLp[j], q), q);
-    }
-    const uint32_t q0 = P.pc[0].q, q1 = P.pc[1].q;
-    const uint32_t x0 = a[0];
-    const uint32_t x0m1 = x0 >= q1 ? x0 - q1 : x0;
-    const uint32_t x1 =
-        reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
-    unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
-    if (np == 3) {
-      const uint32_t q2 = P.pc[2].q;
-      const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
-      uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
-      u = reduce_2q(u, q2);
-      const uint32_t x2 =
-          reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
-      v += (unsigned __int128)x2 * P.q01;
-    }
-    const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
-    const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
-    if (v >= H) v -= Q;  // wraps to the two's complement of a negative value
-    for (int t = 0; t < np; ++t) A[t * L + i] = (uint32_t)(v >> (32 * t));
-  }
-  __syncthreads();
-
-  // Digit sums: s_k = sum_t piece_t(c_{k-t}); pieces are w-bit fields of the
-  // two's complement coefficient, the top piece carries the sign.
+  uint32_t* tabf = sm;
+  uint32_t* tabi = sm + (P.tw_smem ? P.NW : 0);
+  uint32_t* A = tabi + (P.tw_smem ? P.NW : 0);  // np*L residues -> CRT words
+  int* S = (int*)(A + P.NW);                     // M digit sums
+  uint32_t* Dg = A + P.NW + M;                   // M digits
+  uint32_t* Lb = Dg + M;                         // cap limbs of |W|
+  uint32_t* red = Lb + P.cap;                    // scan scratch
+  const uint32_t* twm;
+  const uint32_t* itwm;
+  stage_tables(P, tabf, tabi, &twm, &itwm);
   const uint32_t dmask = (1u << w) - 1u;
-  for (int k = threadIdx.x; k < M; k += blockDim.x) {
-    int s = 0;
-    for (int t = 0; t < T; ++t) {
-      const int i = k - t;
-      if (i < 0 || i >= L) continue;
-      __int128 c = 0;
-      for (int u = np - 1; u >= 0; --u) c = (c << 32) | A[u * L + i];
-      c = (c << (128 - 32 * np)) >> (128 - 32 * np);  // sign-extend
-      const __int128 sh = c >> (w * t);
-      s += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
-    }
-    S[k] = s;
-  }
-  __syncthreads();
 
-  int sg = 1;
-  int carry = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    carry = cta_resolve(
-        M, w,
-        [&](int k) -> int64_t {
-          const int64_t cur = (int64_t)sg * S[k];
-          int64_t v = cur & (int64_t)dmask;
-          if (k > 0) v += ((int64_t)sg * S[k - 1]) >> w;
-          return v;
-        },
-        [&](int k, uint32_t d) { Dg[k] = d; }, red);
-    if (carry >= 0) break;
-    sg = -1;  // negative: resolve the magnitude instead
-  }
-  if (carry != 0) {
-    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapCrt);
-    return;
-  }
-  // Pack base-2^w digits into 32-bit limbs of |W|.
-  const int nl = min(P.cap, (w * M + 31) / 32);
-  for (int m = threadIdx.x; m < P.cap; m += blockDim.x) {
-    uint64_t acc = 0;
-    if (m < nl) {
-      const int first = (32 * m) / w;
-      for (int k = first; k < M && (long long)w * k < 32LL * m + 32; ++k) {
-        const int shl = w * k - 32 * m;
-        acc |= shl >= 0 ? ((uint64_t)Dg[k] << shl) : ((uint64_t)Dg[k] >> -shl);
+  for (int r = p + blockIdx.x; r < P.n; r += gridDim.x) {
+    const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
+    for (int i = threadIdx.x; i < P.NW / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(A)[i] = reinterpret_cast<const uint4*>(src)[i];
+    __syncthreads();
+    cta_ntt_inv16(A, np, P.logL, itwm, P.pc);
+
+    // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      uint32_t a[kMaxPrimes];
+      for (int j = 0; j < np; ++j) {
+        const uint32_t q = P.pc[j].q;
+        uint32_t v = reduce_2q(A[j * L + i], q);
+        a[j] = reduce_2q(mul_shoup(v, P.invL[j], P.invLp[j], q), q);
+      }
+      const uint32_t q0 = P.pc[0].q, q1 = P.pc[1].q;
+      const uint32_t x0 = a[0];
+      const uint32_t x0m1 = x0 >= q1 ? x0 - q1 : x0;
+      const uint32_t x1 =
+          reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
+      unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
+      if (np == 3) {
+        const uint32_t q2 = P.pc[2].q;
+        const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
+        uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
+        u = reduce_2q(u, q2);
+        const uint32_t x2 =
+            reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
+        v += (unsigned __int128)x2 * P.q01;
+      }
+      const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
+      const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
+      if (v >= H) v -= Q;  // wraps to the two's complement of a negative value
+      for (int t = 0; t < np; ++t) A[t * L + i] = (uint32_t)(v >> (32 * t));
+    }
+    __syncthreads();
+
+    // Digit sums: s_k = sum_t piece_t(c_{k-t}); pieces are w-bit fields of the
+    // two's complement coefficient, the top piece carries the sign.
+    for (int k = threadIdx.x; k < M; k += blockDim.x) {
+      int ssum = 0;
+      for (int t = 0; t < T; ++t) {
+        const int i = k - t;
+        if (i < 0 || i >= L) continue;
+        unsigned __int128 cu = 0;
+        for (int u = np - 1; u >= 0; --u) cu = (cu << 32) | A[u * L + i];
+        cu <<= (128 - 32 * np);
+        const __int128 c = ((__int128)cu) >> (128 - 32 * np);  // sign-extend
+        const __int128 sh = c >> (w * t);
+        ssum += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
+      }
+      S[k] = ssum;
+    }
+    __syncthreads();
+
+    int sg = 1;
+    int carry = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      carry = cta_resolve(
+          M, w,
+          [&](int k) -> int64_t {
+            const int64_t cur = (int64_t)sg * S[k];
+            int64_t vv = cur & (int64_t)dmask;
+            if (k > 0) vv += ((int64_t)sg * S[k - 1]) >> w;
+            return vv;
+          },
+          [&](int k, uint32_t d) { Dg[k] = d; }, red);
+      if (carry >= 0) break;
+      sg = -1;  // negative: resolve the magnitude instead
+    }
+    if (carry != 0) {
+      if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapCrt);
+      return;
+    }
+    // Pack base-2^w digits into 32-bit limbs of |W|.
+    const int nl = min(P.cap, (w * M + 31) / 32);
+    for (int m = threadIdx.x; m < P.cap; m += blockDim.x) {
+      uint64_t acc = 0;
+      if (m < nl) {
+        const int first = (32 * m) / w;
+        for (int k = first; k < M && (long long)w * k < 32LL * m + 32; ++k) {
+          const int shl = w * k - 32 * m;
+          acc |= shl >= 0 ? ((uint64_t)Dg[k] << shl) : ((uint64_t)Dg[k] >> -shl);
+        }
+      }
+      Lb[m] = (uint32_t)acc;
+    }
+    __syncthreads();
+    const int len = cta_limb_len(Lb, P.cap, red);
+    if (threadIdx.x == 0 && (long long)w * M > 32LL * P.cap) {
+      for (int k = (32 * P.cap) / w; k < M; ++k)
+        if (Dg[k] && (long long)w * (k + 1) > 32LL * P.cap)
+          atomicOr(&err[kErrCapacity], kCapLimbs);
+    }
+    const int wsign = len == 0 ? 0 : sg;
+
+    if (r == p) {  // pivot
+      if (threadIdx.x == 0) {
+        piv.hdr[p] = wsign * len;
+        if (len == 0) atomicMin(&err[kErrZeroPivot], p);
+      }
+      uint32_t* dst = piv.limbs + (long long)p * P.cap;
+      for (int m = threadIdx.x; m < P.cap; m += blockDim.x) dst[m] = Lb[m];
+    }
+    // V = |W| >> k2 with the sign kept (tdiv_q_2exp).
+    const long long vidx = vrow0 + r;
+    uint32_t* vdst = vint.limbs + vidx * P.cap;
+    for (int m = threadIdx.x; m < P.cap; m += blockDim.x)
+      vdst[m] = field32(Lb, len, 32LL * m + P.k2);
+    const int vbits = max(0, limbs_bits(Lb, len) - P.k2);
+    const int vlen = (vbits + 31) / 32;
+    const int vsign = vlen == 0 ? 0 : wsign;
+    if (threadIdx.x == 0) {
+      vint.hdr[vidx] = vsign * vlen;
+      if (r == p && vlen == 0 && p < P.n - 1) atomicMin(&err[kErrZeroPivot], p);
+      if (r > p) {
+        atomicMax(&maxbitsV[p], vbits);
+        if (vbits > 0) atomicMax(&maxdegV[p], (vbits - 1) / w);
       }
     }
-    Lb[m] = (uint32_t)acc;
-  }
-  __syncthreads();
-  const int len = cta_limb_len(Lb, P.cap, red);
-  // anything beyond cap limbs would have been dropped: verify
-  if (threadIdx.x == 0 && (long long)w * M > 32LL * P.cap) {
-    for (int k = (32 * P.cap) / w; k < M; ++k)
-      if (Dg[k] && (long long)w * (k + 1) > 32LL * P.cap)
-        atomicOr(&err[kErrCapacity], kCapLimbs);
-  }
-  const int wsign = len == 0 ? 0 : sg;
-
-  if (r == p) {  // pivot
-    if (threadIdx.x == 0) {
-      piv.hdr[p] = wsign * len;
-      if (len == 0) atomicMin(&err[kErrZeroPivot], p);
-    }
-    uint32_t* dst = piv.limbs + (long long)p * P.cap;
-    for (int m = threadIdx.x; m < P.cap; m += blockDim.x) dst[m] = Lb[m];
-  }
-  // V = |W| >> k2 with the sign kept (tdiv_q_2exp).
-  const long long vidx = vrow0 + r;
-  uint32_t* vdst = vint.limbs + vidx * P.cap;
-  for (int m = threadIdx.x; m < P.cap; m += blockDim.x)
-    vdst[m] = field32(Lb, len, 32LL * m + P.k2);
-  const int vbits = max(0, limbs_bits(Lb, len) - P.k2);
-  const int vlen = (vbits + 31) / 32;
-  if (threadIdx.x == 0) {
-    vint.hdr[vidx] = vlen == 0 ? 0 : wsign * vlen;
-    if (r == p && vlen == 0 && p < P.n - 1) atomicMin(&err[kErrZeroPivot], p);
-    if (r > p) atomicMax(&maxbitsV[p], vbits);
+    // transform of V_p[r] for the trailing update (rows r > p)
+    if (r > p)
+      transform_int(P, Lb, len, P.k2, vsign, A,
+                    vhat + vidx * (long long)P.NW, false, twm, err);
+    __syncthreads();
   }
 }
 
@@ -369,109 +411,127 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
 // window A - q~ D over nD+2 limbs decides the correction exactly.
 __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
-                         long long rrow0, uint32_t* gscratch, int use_gscratch,
-                         int* err) {
+                         long long rrow0, uint32_t* rhat, int* maxdegR,
+                         uint32_t* gscratch, int use_gscratch, int* err) {
   extern __shared__ uint32_t sm_dyn[];
   if (stage_aborted(err)) return;
-  const int r = p + 1 + blockIdx.x;
-  if (r >= P.n) return;
   const int cap = P.cap, ycap = P.ycap;
   const long long span = div_span_words(cap, ycap);
-  uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * span : sm_dyn;
-  const int CY = cap + ycap + 2;
+  const long long cta_words = span + div_extra_words(P);
+  uint32_t* tab = sm_dyn;
+  uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * cta_words
+                              : sm_dyn + (P.tw_smem ? P.NW : 0);
+  const uint32_t* twm;
+  stage_tables(P, tab, nullptr, &twm, nullptr);
+  const int CY = (cap + ycap + 2 + 3) & ~3;  // 16-byte aligned regions
   uint32_t* Vt = sm;                 // cap      } later: Qt (cap + ycap)
   uint32_t* Y = Vt + cap;            // ycap     }
-  uint32_t* Pr = Y + ycap + 2;       // CY       later: windows Wa | Wb
+  uint32_t* Pr = Vt + CY;            // CY       later: windows Wa | Wb, NTT
   uint32_t* col = Pr + CY;           // 3 CY
   uint32_t* red = col + 3 * CY;      // 64
   uint32_t* Qt = Vt;
-
-  const long long vidx = vrow0 + r, pidx = vrow0 + p;
-  const int hv = vint.hdr[vidx], hd = vint.hdr[pidx];
-  const int na = hv < 0 ? -hv : hv, nD = hd < 0 ? -hd : hd;
-  const int sV = hv < 0 ? -1 : (hv > 0), sD = hd < 0 ? -1 : (hd > 0);
-  const uint32_t* Vg = vint.limbs + vidx * cap;   // global, read-only
-  const uint32_t* Dg = vint.limbs + pidx * cap;
-  const long long ridx = rrow0 + r;
-  uint32_t* dst = rint.limbs + ridx * cap;
-  if (na == 0 || nD == 0) {
-    if (threadIdx.x == 0) rint.hdr[ridx] = 0;
-    for (int i = threadIdx.x; i < cap; i += blockDim.x) dst[i] = 0u;
-    return;
-  }
-  const int n = limbs_bits(Dg, nD);
-  const int vbits = limbs_bits(Vg, na);
-  const int tv = max(0, n - P.k2 - 40);
-  const int nt = max(0, (vbits - tv + 31) / 32);
   const int S = ys[0], nY = ys[1];
-  for (int i = threadIdx.x; i < nt; i += blockDim.x)
-    Vt[i] = field32(Vg, na, 32LL * i + tv);
-  for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
-  __syncthreads();
-  const int nP = nt + nY;
-  cta_mul(Vt, nt, Y, nY, Pr, nP, col, red);
-  const int sh = S - P.k2 - tv;
-  const int nQ = max(0, (int)((32LL * nP - sh + 31) / 32));
-  for (int i = threadIdx.x; i < nQ; i += blockDim.x)
-    Qt[i] = field32(Pr, nP, 32LL * i + sh);
-  const uint32_t frac = field32(Pr, nP, (long long)sh - 32);
-  __syncthreads();
-  int nq = cta_limb_len(Qt, nQ, red);
-  const bool exact_needed = sh < 32 || frac < 2u || frac > 0xFFFFFFFDu;
-  if (exact_needed) {
-    // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
-    const int nw = nD + 2;
-    uint32_t* Wa = Pr;
-    uint32_t* Wb = Pr + nw;
-    cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red);
-    cta_resolve(
-        nw, 32,
-        [&](int k) -> int64_t {
-          return (int64_t)field32(Vg, na, 32LL * k - P.k2) - (int64_t)Wb[k];
-        },
-        [&](int k, uint32_t d) { Wa[k] = d; }, red);
-    int adj = 0;
-    if (Wa[nw - 1] & 0x80000000u) {
-      adj = -1;  // remainder negative: q~ was one too large
-    } else {
-      cta_resolve(
-          nw, 32,
-          [&](int k) -> int64_t {
-            return (int64_t)Wa[k] - (int64_t)(k < nD ? Dg[k] : 0u);
-          },
-          [&](int k, uint32_t d) { Wb[k] = d; }, red);
-      if (!(Wb[nw - 1] & 0x80000000u)) {
-        adj = 1;
+  const long long pidx = vrow0 + p;
+  const int hd = vint.hdr[pidx];
+  const int nD = hd < 0 ? -hd : hd;
+  const int sD = hd < 0 ? -1 : (hd > 0);
+  const uint32_t* Dg = vint.limbs + pidx * cap;
+  const int n = nD ? limbs_bits(Dg, nD) : 0;
+
+  for (int r = p + 1 + blockIdx.x; r < P.n; r += gridDim.x) {
+    const long long vidx = vrow0 + r;
+    const int hv = vint.hdr[vidx];
+    const int na = hv < 0 ? -hv : hv;
+    const int sV = hv < 0 ? -1 : (hv > 0);
+    const uint32_t* Vg = vint.limbs + vidx * cap;   // global, read-only
+    const long long ridx = rrow0 + r;
+    uint32_t* dst = rint.limbs + ridx * cap;
+    int nq = 0;
+    if (na > 0 && nD > 0) {
+      const int vbits = limbs_bits(Vg, na);
+      const int tv = max(0, n - P.k2 - 40);
+      const int nt = max(0, (vbits - tv + 31) / 32);
+      for (int i = threadIdx.x; i < nt; i += blockDim.x)
+        Vt[i] = field32(Vg, na, 32LL * i + tv);
+      for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
+      __syncthreads();
+      const int nP = nt + nY;
+      cta_mul(Vt, nt, Y, nY, Pr, nP, col, red);
+      const int sh = S - P.k2 - tv;
+      const int nQ = max(0, (int)((32LL * nP - sh + 31) / 32));
+      for (int i = threadIdx.x; i < nQ; i += blockDim.x)
+        Qt[i] = field32(Pr, nP, 32LL * i + sh);
+      const uint32_t frac = field32(Pr, nP, (long long)sh - 32);
+      __syncthreads();
+      nq = cta_limb_len(Qt, nQ, red);
+      const bool exact_needed = sh < 32 || frac < 2u || frac > 0xFFFFFFFDu;
+      if (exact_needed) {
+        // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
+        const int nw = nD + 2;
+        uint32_t* Wa = Pr;
+        uint32_t* Wb = Pr + nw;
+        cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red);
         cta_resolve(
             nw, 32,
             [&](int k) -> int64_t {
-              return (int64_t)Wb[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+              return (int64_t)field32(Vg, na, 32LL * k - P.k2) - (int64_t)Wb[k];
             },
             [&](int k, uint32_t d) { Wa[k] = d; }, red);
-        if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
-          atomicOr(&err[kErrInternal], kIntDivision);
+        int adj = 0;
+        if (Wa[nw - 1] & 0x80000000u) {
+          adj = -1;  // remainder negative: q~ was one too large
+        } else {
+          cta_resolve(
+              nw, 32,
+              [&](int k) -> int64_t {
+                return (int64_t)Wa[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+              },
+              [&](int k, uint32_t d) { Wb[k] = d; }, red);
+          if (!(Wb[nw - 1] & 0x80000000u)) {
+            adj = 1;
+            cta_resolve(
+                nw, 32,
+                [&](int k) -> int64_t {
+                  return (int64_t)Wb[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+                },
+                [&](int k, uint32_t d) { Wa[k] = d; }, red);
+            if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
+              atomicOr(&err[kErrInternal], kIntDivision);
+          }
+        }
+        if (adj != 0) {
+          const int nn = nq + 1;
+          cta_resolve(
+              nn, 32,
+              [&](int k) -> int64_t {
+                return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
+              },
+              [&](int k, uint32_t d) { col[k] = d; }, red);
+          for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
+          __syncthreads();
+          nq = cta_limb_len(Qt, nn, red);
+        }
+        // every thread has read the window signs before Pr is reused below
+        __syncthreads();
+      }
+      if (nq > cap) {
+        if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+        return;
       }
     }
-    if (adj != 0) {
-      const int nn = nq + 1;
-      cta_resolve(
-          nn, 32,
-          [&](int k) -> int64_t {
-            return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
-          },
-          [&](int k, uint32_t d) { col[k] = d; }, red);
-      for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
-      __syncthreads();
-      nq = cta_limb_len(Qt, nn, red);
+    const int rsign = nq == 0 ? 0 : sV * sD;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x)
+      dst[i] = i < nq ? Qt[i] : 0u;
+    if (threadIdx.x == 0) {
+      rint.hdr[ridx] = rsign * nq;
+      if (nq > 0) atomicMax(maxdegR, (limbs_bits(Qt, nq) - 1) / P.w);
     }
+    // transform of R_p[r] (Montgomery form) for the trailing update; the
+    // NTT buffer reuses the Barrett scratch when it is large enough
+    uint32_t* X = P.NW <= 4 * CY ? Pr : sm + span;
+    transform_int(P, Qt, nq, 0, rsign, X, rhat + ridx * (long long)P.NW,
+                  true, twm, err);
   }
-  if (nq > cap) {
-    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
-    return;
-  }
-  for (int i = threadIdx.x; i < cap; i += blockDim.x)
-    dst[i] = i < nq ? Qt[i] : 0u;
-  if (threadIdx.x == 0) rint.hdr[ridx] = nq == 0 ? 0 : sV * sD * nq;
 }
 
 // --------------------------------------------------------- trailing update -
@@ -745,16 +805,28 @@ __global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
 static thread_local long long g_launches = 0;
 long long kernel_launch_count() { return g_launches; }
 
+// HGPU_SYNC_DEBUG=1: synchronise after every launch so a fault is reported
+// by the launch that caused it (debug aid; off by default).
+static cudaError_t post_launch(cudaStream_t st) {
+  static const bool sync_debug = [] {
+    const char* e = getenv("HGPU_SYNC_DEBUG");
+    return e && *e == '1';
+  }();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && sync_debug) e = cudaStreamSynchronize(st);
+  return e;
+}
+
 cudaError_t launch_fwd_ints(const DevPlan& P, IntBuf src, long long in_base,
                             uint32_t* out, long long out_base, int count,
                             int mont, int* maxdeg, int* err,
                             cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  const size_t smem = (size_t)(P.np * P.L + P.cap) * 4;
+  const size_t smem = (size_t)((P.tw_smem ? P.NW : 0) + P.NW + P.cap) * 4;
   ++g_launches;
-  k_fwd_ints<<<count, 256, smem, st>>>(P, src, in_base, out, out_base, count,
-                                       mont, maxdeg, err);
-  return cudaGetLastError();
+  k_fwd_ints<<<min(count, P.grid_cap), 256, smem, st>>>(
+      P, src, in_base, out, out_base, count, mont, maxdeg, err);
+  return post_launch(st);
 }
 
 cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
@@ -763,24 +835,25 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
   dim3 grid((P.NW + 255) / 256, P.n);
   ++g_launches;
   k_init_w<<<grid, 256, 0, st>>>(P, that, xhat, colbase, W);
-  return cudaGetLastError();
+  return post_launch(st);
 }
 
 size_t extract_smem_bytes(const DevPlan& P) {
   const int M = P.L + P.T;
-  return (size_t)(P.np * P.L + 2 * M + P.cap + 64) * 4;
+  return (size_t)((P.tw_smem ? 2 * P.NW : 0) + P.NW + 2 * M + P.cap + 64) * 4;
 }
 
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, IntBuf vint,
                            long long vrow0, IntBuf piv, int* maxbitsV,
-                           int* err, cudaStream_t st) {
+                           uint32_t* vhat, int* maxdegV, int* err,
+                           cudaStream_t st) {
   const int rows = P.n - p;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
-  k_extract<<<rows, 256, extract_smem_bytes(P), st>>>(
-      P, W, colbase, p, vint, vrow0, piv, maxbitsV, err);
-  return cudaGetLastError();
+  k_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
+      P, W, colbase, p, vint, vrow0, piv, maxbitsV, vhat, maxdegV, err);
+  return post_launch(st);
 }
 
 size_t recip_scratch_words(const DevPlan& P) {
@@ -798,22 +871,28 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
   const size_t smem = use_gscratch ? 0 : recip_scratch_words(P) * 4;
   k_recip<<<1, 512, smem, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
                                 use_gscratch, err);
-  return cudaGetLastError();
+  return post_launch(st);
 }
 
-size_t divide_smem_words(const DevPlan& P) { return div_span_words(P.cap, P.ycap); }
+size_t divide_smem_words(const DevPlan& P) {
+  return (size_t)(P.tw_smem ? P.NW : 0) + div_span_words(P.cap, P.ycap) +
+         div_extra_words(P);
+}
 
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, const uint32_t* Ybuf, const int* ys,
-                          IntBuf rint, long long rrow0, uint32_t* gscratch,
-                          int use_gscratch, int* err, cudaStream_t st) {
+                          IntBuf rint, long long rrow0, uint32_t* rhat,
+                          int* maxdegR, uint32_t* gscratch, int use_gscratch,
+                          int* err, cudaStream_t st) {
   const int rows = P.n - p - 1;
   if (rows <= 0) return cudaSuccess;
-  const size_t smem = use_gscratch ? 0 : divide_smem_words(P) * 4;
+  const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
+                                   : divide_smem_words(P) * 4;
   ++g_launches;
-  k_divide<<<rows, 256, smem, st>>>(P, vint, vrow0, p, Ybuf, ys, rint, rrow0,
-                                    gscratch, use_gscratch, err);
-  return cudaGetLastError();
+  k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
+      P, vint, vrow0, p, Ybuf, ys, rint, rrow0, rhat, maxdegR, gscratch,
+      use_gscratch, err);
+  return post_launch(st);
 }
 
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
@@ -849,7 +928,7 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
     k_update<4><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
                                       row_stride_slot, nslots, c_begin, c_end,
                                       nct, nrt, err);
-  return cudaGetLastError();
+  return post_launch(st);
 }
 
 cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
@@ -863,7 +942,7 @@ cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
   ++g_launches;
   k_update_col<TR><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
                                          row_stride_slot, nslots, c, err);
-  return cudaGetLastError();
+  return post_launch(st);
 }
 
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
@@ -871,7 +950,7 @@ cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             cudaStream_t st) {
   ++g_launches;
   k_validate<<<1, 32, 0, st>>>(P, maxdegV, maxdegR, nstages, err);
-  return cudaGetLastError();
+  return post_launch(st);
 }
 
 cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
@@ -881,7 +960,7 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
   int maxopt = 0;
   cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t ext = extract_smem_bytes(P);
-  const size_t fwd = (size_t)(P.np * P.L + P.cap) * 4;
+  const size_t fwd = (size_t)((P.tw_smem ? P.NW : 0) + P.NW + P.cap) * 4;
   if ((int)ext > maxopt || (int)fwd > maxopt) return cudaErrorInvalidValue;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k_extract,
@@ -903,7 +982,13 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
   const size_t div = divide_smem_words(P) * 4;
   *div_smem = div;
   *div_global = (int)div > maxopt;
-  if (!*div_global) {
+  if (*div_global) {
+    const int tab = (P.tw_smem ? P.NW : 0) * 4;
+    if ((e = cudaFuncSetAttribute(k_divide,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  tab)) != cudaSuccess)
+      return e;
+  } else {
     if ((e = cudaFuncSetAttribute(k_divide,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)div)) != cudaSuccess)

@@ -61,6 +61,11 @@ struct DevPlan {
   const uint32_t* twp;
   const uint32_t* itw;
   const uint32_t* itwp;
+  const uint32_t* twm;  // [np][L] forward twiddles, Montgomery form
+  const uint32_t* itwm; // [np][L] inverse twiddles, Montgomery form
+  int tw_smem;          // 1: kernels stage the Montgomery tables in SMEM
+  int grid_cap;         // CTAs for grid-stride row kernels
+  int debug;            // HGPU_DEBUG bits (bisection aid), 0 in production
 };
 
 struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
@@ -70,8 +75,14 @@ struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
 
 // Shared-memory words of one k_divide CTA (layout in ldlt_kernels.cu).
 __host__ __device__ inline long long div_span_words(int cap, int ycap) {
-  const long long CY = (long long)cap + ycap + 2;
-  return (long long)cap + ycap + 2 + 4 * CY + 64;
+  const long long CY = ((long long)cap + ycap + 2 + 3) & ~3LL;
+  return 5 * CY + 64;
+}
+
+// Extra words when the NTT buffer (NW) does not fit the Barrett scratch.
+__host__ __device__ inline long long div_extra_words(const DevPlan& P) {
+  const long long CY = ((long long)P.cap + P.ycap + 2 + 3) & ~3LL;
+  return (long long)P.NW <= 4 * CY ? 0 : (long long)P.NW;
 }
 
 // Host launch wrappers (ldlt_kernels.cu).
@@ -84,7 +95,8 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, IntBuf vint,
                            long long vrow0, IntBuf piv, int* maxbitsV,
-                           int* err, cudaStream_t st);
+                           uint32_t* vhat, int* maxdegV, int* err,
+                           cudaStream_t st);
 size_t recip_scratch_words(const DevPlan& P);
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
@@ -93,8 +105,9 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
 size_t divide_smem_words(const DevPlan& P);
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, const uint32_t* Ybuf, const int* ys,
-                          IntBuf rint, long long rrow0, uint32_t* gscratch,
-                          int use_gscratch, int* err, cudaStream_t st);
+                          IntBuf rint, long long rrow0, uint32_t* rhat,
+                          int* maxdegR, uint32_t* gscratch, int use_gscratch,
+                          int* err, cudaStream_t st);
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
