@@ -248,27 +248,28 @@ __device__ inline void cta_ntt_inv16(uint32_t* x, int np, int logL,
 
 // ----------------------------------------------------- carry functions -----
 // A carry function maps carry-in c in {-1,0,1,2} to carry-out in the same
-// set; entry c is stored in bits [2(c+1), 2(c+1)+2) as (out+1).
-constexpr uint32_t kCfIdentity = 0xE4u;
+// set.  It is stored as four bytes, byte (c+1) = out+1 in [0,3], so that
+// composition is one byte permute: (later o earlier) byte i =
+// later.byte[earlier.byte[i]].
+constexpr uint32_t kCfIdentity = 0x03020100u;
 
 __device__ __forceinline__ int cf_apply(uint32_t f, int c) {
-  return (int)((f >> (2 * (c + 1))) & 3u) - 1;
+  return (int)((f >> (8 * (c + 1))) & 0xFFu) - 1;
 }
 // later o earlier
 __device__ __forceinline__ uint32_t cf_compose(uint32_t later,
                                                uint32_t earlier) {
-  uint32_t r = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t mid = (earlier >> (2 * i)) & 3u;
-    r |= ((later >> (2 * mid)) & 3u) << (2 * i);
-  }
-  return r;
+  // selector nibble i = earlier byte i (each in [0,3])
+  const uint32_t t = earlier | (earlier >> 4);
+  const uint32_t sel = (t & 0xFFu) | ((t >> 8) & 0xFF00u);
+  return __byte_perm(later, 0u, sel);
 }
 
-// Exclusive block-wide scan under composition: returns f_{t-1} o ... o f_0.
+// Exclusive block-wide scan under composition: returns f_{t-1} o ... o f_0
+// and, in *total, the composition of all threads' functions.
 // `red` needs blockDim.x/32 words of shared memory.
-__device__ inline uint32_t cta_exclusive_compose(uint32_t f, uint32_t* red) {
+__device__ inline uint32_t cta_exclusive_compose(uint32_t f, uint32_t* red,
+                                                 uint32_t* total = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   uint32_t x = f;
@@ -290,6 +291,7 @@ __device__ inline uint32_t cta_exclusive_compose(uint32_t f, uint32_t* red) {
   }
   __syncthreads();
   const uint32_t before_warp = wid > 0 ? red[wid - 1] : kCfIdentity;
+  if (total) *total = red[nw - 1];
   uint32_t excl = __shfl_up_sync(0xffffffffu, x, 1);
   if (lane == 0) excl = kCfIdentity;
   __syncthreads();
@@ -300,11 +302,20 @@ __device__ __forceinline__ int64_t floor_shift(int64_t v, int bits) {
   return v >> bits;  // arithmetic shift = floor division by 2^bits
 }
 
+// carry function of one position holding v (carry-out = floor((v+c)/2^bits))
+__device__ __forceinline__ uint32_t cf_of(int64_t v, int bits) {
+  uint32_t f = 0;
+#pragma unroll
+  for (int c = -1; c <= 2; ++c)
+    f |= (uint32_t)(floor_shift(v + c, bits) + 1) << (8 * (c + 1));
+  return f;
+}
+
 // Resolves sum_{k<M} v_k 2^{bits k} into digits d_k in [0, 2^bits), where
 // getv(k) returns v_k in [-2^bits + 1, 3*2^bits - 2] (int64).  putd(k, d)
 // receives every digit.  Returns the final carry (in {-1,0,1,2}) to all
 // threads: the exact value is sum d_k 2^{bits k} + carry 2^{bits M}.
-// `red` needs blockDim.x/32 + 1 words.
+// `red` needs blockDim.x/32 words.  getv must not read what putd writes.
 template <class GetV, class PutD>
 __device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
                            uint32_t* red) {
@@ -313,17 +324,9 @@ __device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
   const int k0 = min(M, (int)threadIdx.x * chunk);
   const int k1 = min(M, k0 + chunk);
   uint32_t F = kCfIdentity;
-  for (int k = k0; k < k1; ++k) {
-    const int64_t v = getv(k);
-    uint32_t f = 0;
-#pragma unroll
-    for (int c = -1; c <= 2; ++c) {
-      const int64_t o = floor_shift(v + c, bits);
-      f |= (uint32_t)(o + 1) << (2 * (c + 1));
-    }
-    F = cf_compose(f, F);
-  }
-  const uint32_t P = cta_exclusive_compose(F, red);
+  for (int k = k0; k < k1; ++k) F = cf_compose(cf_of(getv(k), bits), F);
+  uint32_t total;
+  const uint32_t P = cta_exclusive_compose(F, red, &total);
   int c = cf_apply(P, 0);
   const int64_t mask = (int64_t(1) << bits) - 1;
   for (int k = k0; k < k1; ++k) {
@@ -331,13 +334,8 @@ __device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
     putd(k, (uint32_t)(v & mask));
     c = (int)floor_shift(v, bits);
   }
-  const int nw = nt >> 5;
-  if (k1 == M && k0 < k1) red[nw] = (uint32_t)(c + 1);
-  if (M == 0 && threadIdx.x == 0) red[nw] = 1u;
-  __syncthreads();
-  const int carry = (int)red[nw] - 1;
-  __syncthreads();
-  return carry;
+  __syncthreads();  // digits visible to every thread on return
+  return cf_apply(total, 0);
 }
 
 // ------------------------------------------------------- limb helpers -----
@@ -383,14 +381,18 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
                                uint32_t* red, int col_words = 0) {
   constexpr int G = 8;
   const int ngroups = (M + G - 1) / G;
-  const int maxseg = max(1, (col_words > 0 ? col_words : 3 * M) / (3 * M));
-  const int want = (2 * (int)blockDim.x + ngroups - 1) / max(ngroups, 1);
-  const int nseg = max(1, min(min(maxseg, want), 8));
   const int minlen = min(na, nb);
+  // split a group's i-range only when segments stay >= 64 iterations and
+  // there are idle threads to take them
+  // nseg > 1 needs 3*nseg*M words of planes plus 2*M for the reduced sums
+  const int maxseg = max(1, ((col_words > 0 ? col_words : 3 * M) - 2 * M) / (3 * M));
+  const int want = (2 * (int)blockDim.x + ngroups - 1) / max(ngroups, 1);
+  const int bylen = max(1, (minlen + G - 1) / 64);
+  const int nseg = max(1, min(min(min(maxseg, want), bylen), 8));
   const int seglen = (minlen + G - 1 + nseg - 1) / nseg;  // group i-range <= minlen+G-1
   const int items = ngroups * nseg;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int g = it / nseg, sgi = it - g * nseg;
+    const int g = nseg == 1 ? it : it / nseg, sgi = it - g * nseg;
     const int k0 = g * G;
     uint32_t c0[G], c1[G], c2[G];
 #pragma unroll
@@ -437,23 +439,43 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
     }
   }
   __syncthreads();
-  // S_k = sum over segments of the column value at weight 2^(32k) (< 2^64);
-  // v_k = (S_k mod 2^32) + floor(S_{k-1} / 2^32) stays in the resolve domain
-  auto colsum = [&](int k) -> uint64_t {
-    uint64_t v = 0;
-    for (int sg = 0; sg < nseg; ++sg) {
-      const uint32_t* pl = col + (size_t)sg * 3 * M;
-      v += pl[k];
-      if (k >= 1) v += pl[M + k - 1];
-      if (k >= 2) v += pl[2 * M + k - 2];
+  // S_k = sum over segments of the column value at weight 2^(32k) (< 2^64),
+  // reduced once into (lo, hi) planes 0 and 1 of segment 0's storage;
+  // v_k = lo_k + hi_{k-1} then stays in the resolve domain.
+  if (nseg > 1) {
+    for (int k = threadIdx.x; k < M; k += blockDim.x) {
+      uint64_t v = 0;
+      for (int sg = 0; sg < nseg; ++sg) {
+        const uint32_t* pl = col + (size_t)sg * 3 * M;
+        v += pl[k];
+        if (k >= 1) v += pl[M + k - 1];
+        if (k >= 2) v += pl[2 * M + k - 2];
+      }
+      col[3 * (size_t)nseg * M + k] = (uint32_t)v;
+      col[3 * (size_t)nseg * M + M + k] = (uint32_t)(v >> 32);
     }
-    return v;
-  };
+    __syncthreads();
+    const uint32_t* slo = col + 3 * (size_t)nseg * M;
+    const uint32_t* shi = slo + M;
+    cta_resolve(
+        M, 32,
+        [&](int k) -> int64_t {
+          int64_t v = slo[k];
+          if (k >= 1) v += shi[k - 1];
+          return v;
+        },
+        [&](int k, uint32_t d) { out[k] = d; }, red);
+    return;
+  }
+  const uint32_t* c0p = col;
+  const uint32_t* c1p = col + M;
+  const uint32_t* c2p = col + 2 * M;
   cta_resolve(
       M, 32,
       [&](int k) -> int64_t {
-        int64_t v = (int64_t)(uint32_t)colsum(k);
-        if (k >= 1) v += (int64_t)(colsum(k - 1) >> 32);
+        int64_t v = c0p[k];
+        if (k >= 1) v += c1p[k - 1];
+        if (k >= 2) v += c2p[k - 2];
         return v;
       },
       [&](int k, uint32_t d) { out[k] = d; }, red);

@@ -76,13 +76,7 @@ __device__ __forceinline__ int64_t fold_v(const uint32_t* c0p,
   return v;
 }
 
-__device__ __forceinline__ uint32_t carry_fn(int64_t v) {
-  uint32_t f = 0;
-#pragma unroll
-  for (int c = -1; c <= 2; ++c)
-    f |= (uint32_t)((floor_shift(v + c, 32)) + 1) << (2 * (c + 1));
-  return f;
-}
+__device__ __forceinline__ uint32_t carry_fn(int64_t v) { return cf_of(v, 32); }
 
 // F2: carry function of each chunk of kChunk positions.
 __global__ void __launch_bounds__(kFoldThreads)

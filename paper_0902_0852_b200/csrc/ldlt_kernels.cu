@@ -346,7 +346,10 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
   }
   __syncthreads();
   int nY = 2;
+  const bool prof = (P.debug & 256) && p == 50 && threadIdx.x == 0;
+  long long tph[6];
   for (int i = 0; i + 1 < nl; ++i) {
+    if (prof) tph[0] = clock64();
     const int pa = lv[i], pb = lv[i + 1], dlt = pb - pa;
     const int mb = min(n, pb + G);   // bits of D'
     const int t = n - mb;
@@ -356,7 +359,9 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
     __syncthreads();
     // Pr = D' * Y
     const int nP = nDt + nY;
+    if (prof) tph[1] = clock64();
     cta_mul(Dt, nDt, Y, nY, Pr, nP, col, red, col_words);
+    if (prof) tph[2] = clock64();
     // E = 2^(mb+pa) - Pr, signed, over nP+1 limbs
     const int nEw = nP + 1;
     const int Sb = mb + pa;
@@ -374,9 +379,11 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
       sgn = -1;
     }
     const int nE = cta_limb_len(E, nEw, red);
+    if (prof) tph[3] = clock64();
     // Tm = Y * |E|
     const int nT = nY + nE;
     if (nE > 0) cta_mul(Y, nY, E, nE, Tm, nT, col, red, col_words);
+    if (prof) tph[4] = clock64();
     // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
     const int nYn = min(Lm, (pb + 2 + 31) / 32 + 1);
     const int sh = Sb - dlt;
@@ -390,6 +397,12 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
         [&](int k, uint32_t dd) { Pr[k] = dd; }, red);
     for (int k = threadIdx.x; k < nYn; k += blockDim.x) Y[k] = Pr[k];
     __syncthreads();
+    if (prof) {
+      tph[5] = clock64();
+      printf("recip lvl %d pa=%d pb=%d nDt=%d nY=%d nE=%d: Dt %lld mul1 %lld E %lld mul2 %lld Yupd %lld\n",
+             i, pa, pb, nDt, nY, nE, tph[1] - tph[0], tph[2] - tph[1], tph[3] - tph[2],
+             tph[4] - tph[3], tph[5] - tph[4]);
+    }
     nY = nYn;
   }
   for (int k = threadIdx.x; k < P.ycap; k += blockDim.x)
@@ -856,6 +869,15 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
   return post_launch(st);
 }
 
+static int recip_threads() {
+  static const int t = [] {
+    const char* e = getenv("HGPU_RECIP_THREADS");
+    const int v = e ? atoi(e) : 256;
+    return (v >= 32 && v <= 1024 && v % 32 == 0) ? v : 256;
+  }();
+  return t;
+}
+
 size_t recip_scratch_words(const DevPlan& P) {
   // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
   const size_t Lm = (size_t)P.ycap + 4;
@@ -869,7 +891,7 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          cudaStream_t st) {
   ++g_launches;
   const size_t smem = use_gscratch ? 0 : recip_scratch_words(P) * 4;
-  k_recip<<<1, 512, smem, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
+  k_recip<<<1, recip_threads(), smem, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
                                 use_gscratch, err);
   return post_launch(st);
 }
