@@ -146,6 +146,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
+    CU(cudaStreamCreateWithPriority(&stream_helper_, cudaStreamNonBlocking, hi));
   }
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
@@ -159,6 +160,8 @@ Matrix::~Matrix() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   for (cudaEvent_t e : pev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : sev_) cudaEventDestroy(e);
+  if (stream_helper_) cudaStreamDestroy(stream_helper_);
   if (stream_panel_) cudaStreamDestroy(stream_panel_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -504,6 +507,26 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     flush();
   };
 
+  while ((int)sev_.size() < 2 * n) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sev_.push_back(e);
+  }
+  cudaStream_t sh = stream_helper_;
+  {
+    // bits bound of any diagonal Schur complement W_rr (PD: <= M_rr - x)
+    int db = 0;
+    for (int r = 0; r < n; ++r) {
+      const HostInt& d = strip_[2 * r];
+      if (!d.limbs.empty())
+        db = std::max(db, 32 * ((int)d.limbs.size() - 1) +
+                              (32 - __builtin_clz(d.limbs.back())));
+    }
+    if (!x.limbs.empty())
+      db = std::max(db, 32 * ((int)x.limbs.size() - 1) +
+                            (32 - __builtin_clz(x.limbs.back())));
+    dmax_bits_ = db + 1;
+  }
   CU(cudaEventRecord(next_ready[0], st));  // init done
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
@@ -516,15 +539,38 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
         const long long row0 = row0set + (long long)s * n;
-        // left-looking inside the panel: column p receives stages [p0, p)
-        CU(launch_update_col(D, W_, colbase_, vhat_ + row0set * NW,
-                             rhat_ + row0set * NW, slot_stride, s, p, err_, sp));
-        // W[r][p] -> V_p[r] (+ its transform for rows r > p)
-        CU(launch_extract(D, W_, colbase_, p, vint, row0, piv, maxbitsV, vhat_,
-                          maxdegV, err_, sp));
-        if (p == n - 1) break;
-        CU(launch_recip(D, vint, row0 + p, maxbitsV, p, ybuf_, ys_, rscratch_,
-                        recip_global_ ? 1 : 0, err_, sp));
+        const uint32_t* vh = vhat_ + row0set * NW;
+        const uint32_t* rh = rhat_ + row0set * NW;
+        if (recip_bound_ && p < n - 1) {
+          // critical chain on the helper stream: pivot entry -> D = V_p[p]
+          // -> reciprocal (precision from the PD bound), overlapping the
+          // update and extraction of the other rows on the panel stream
+          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p, p,
+                               p + 1, err_, sp));
+          CU(cudaEventRecord(sev_[2 * p], sp));
+          CU(cudaStreamWaitEvent(sh, sev_[2 * p], 0));
+          CU(launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0, piv,
+                            maxbitsV, vhat_, maxdegV, err_, sh));
+          CU(launch_recip(D, vint, row0 + p, maxbitsV, p, piv, dmax_bits_,
+                          ybuf_, ys_, rscratch_, recip_global_ ? 1 : 0, err_,
+                          sh));
+          CU(cudaEventRecord(sev_[2 * p + 1], sh));
+          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p,
+                               p + 1, n, err_, sp));
+          CU(launch_extract(D, W_, colbase_, p, p + 1, n, vint, row0, piv,
+                            maxbitsV, vhat_, maxdegV, err_, sp));
+          CU(cudaStreamWaitEvent(sp, sev_[2 * p + 1], 0));
+        } else {
+          // left-looking inside the panel: column p receives stages [p0, p)
+          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p, p,
+                               n, err_, sp));
+          // W[r][p] -> V_p[r] (+ its transform for rows r > p)
+          CU(launch_extract(D, W_, colbase_, p, p, n, vint, row0, piv,
+                            maxbitsV, vhat_, maxdegV, err_, sp));
+          if (p == n - 1) break;
+          CU(launch_recip(D, vint, row0 + p, maxbitsV, p, piv, 0, ybuf_, ys_,
+                          rscratch_, recip_global_ ? 1 : 0, err_, sp));
+        }
         // R_p[r] (+ its Montgomery-form transform)
         CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, rhat_,
                          maxdegR + p, dscratch_, div_global_ ? 1 : 0, err_, sp));
@@ -604,6 +650,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     Error e(HGPU_ERR_CAPACITY,
             "transform capacity exceeded (flags " +
                 std::to_string(herr[kErrCapacity]) + ")");
+    e.cap_flags = herr[kErrCapacity];
     throw e;
   }
   if (herr[kErrZeroPivot] != INT_MAX) {
@@ -696,6 +743,10 @@ FactorResult Matrix::factor(const HostInt& x, unsigned flags) {
       return res;
     } catch (const Error& e) {
       if (e.status != HGPU_ERR_CAPACITY) throw;
+      if (e.cap_flags == kCapAmax && recip_bound_) {
+        recip_bound_ = false;  // non-PD sizes: exact per-stage maxima
+        continue;
+      }
       min_logL = plan_.logL + 1;
       release();
     }

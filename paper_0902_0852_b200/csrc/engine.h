@@ -16,6 +16,7 @@ namespace hgpu {
 struct Error : std::runtime_error {
   hgpu_status status;
   long pivot = -1;
+  int cap_flags = 0;
   Error(hgpu_status s, const std::string& what)
       : std::runtime_error(what), status(s) {}
 };
@@ -117,7 +118,10 @@ class Matrix {
   bool recip_global_ = false;
   cudaStream_t stream_ = nullptr;        // bulk (trailing updates)
   cudaStream_t stream_panel_ = nullptr;  // panel factorisation, high priority
-  std::vector<cudaEvent_t> pev_;
+  cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
+  std::vector<cudaEvent_t> pev_, sev_;
+  bool recip_bound_ = true;  // reciprocal precision from the PD bound
+  int dmax_bits_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> uev_;
 };

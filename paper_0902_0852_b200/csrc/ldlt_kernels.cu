@@ -136,9 +136,9 @@ __global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
 //   ZeroPivot if V_p[p] == 0 and p < n-1               (ldlt.cpp:56)
 // V goes to vint[slot][r]; the full pivot to piv[p].
 __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
-                          int p, IntBuf vint, long long vrow0, IntBuf piv,
-                          int* maxbitsV, uint32_t* vhat, int* maxdegV,
-                          int* err) {
+                          int p, int r_begin, int r_end, IntBuf vint,
+                          long long vrow0, IntBuf piv, int* maxbitsV,
+                          uint32_t* vhat, int* maxdegV, int* err) {
   extern __shared__ uint32_t sm[];
   if (stage_aborted(err)) return;
   const int L = P.L, np = P.np, T = P.T, w = P.w;
@@ -155,7 +155,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
   stage_tables(P, tabf, tabi, &twm, &itwm);
   const uint32_t dmask = (1u << w) - 1u;
 
-  for (int r = p + blockIdx.x; r < P.n; r += gridDim.x) {
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
     const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
     for (int i = threadIdx.x; i < P.NW / 4; i += blockDim.x)
       reinterpret_cast<uint4*>(A)[i] = reinterpret_cast<const uint4*>(src)[i];
@@ -301,8 +301,9 @@ __device__ inline int recip_levels(int Pt, int* lv) {
 }
 
 __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
-                        const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                        uint32_t* gscratch, int use_gscratch, int* err) {
+                        const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
+                        uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+                        int use_gscratch, int* err) {
   extern __shared__ uint32_t sm_dyn[];
   __shared__ uint32_t red[64];
   if (stage_aborted(err)) return;
@@ -311,7 +312,19 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
   if (nD == 0) return;  // flagged as ZeroPivot by k_extract
   const uint32_t* Dg = vint.limbs + prow * (long long)P.cap;  // global
   const int n = limbs_bits(Dg, nD);
-  const int amax = maxbitsV[p] + P.k2;
+  // max over rows of bits(V_r 2^k2): exact (after the bulk extraction) or,
+  // when dmax_bits > 0, the PD bound |W_rp|^2 <= W_rr W_pp with
+  // bits(W_rr) <= dmax_bits, so the reciprocal can run concurrently with the
+  // extraction of the other rows; k_divide verifies the bound per row.
+  int amax;
+  if (dmax_bits > 0) {
+    const int hp = piv.hdr[p];
+    const int npl = hp < 0 ? -hp : hp;
+    const int wpp = limbs_bits(piv.limbs + (long long)p * P.cap, npl);
+    amax = (dmax_bits + 1 + wpp + 1) / 2 + 2;
+  } else {
+    amax = maxbitsV[p] + P.k2;
+  }
   const int e = max(amax - n + 2, 1);
   const int G = 32;
   const int Pt = e + G;
@@ -410,6 +423,7 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
   if (threadIdx.x == 0) {
     ys[0] = S;
     ys[1] = nY;
+    ys[2] = amax;
   }
 }
 
@@ -443,7 +457,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   uint32_t* col = Pr + CY;           // 3 CY
   uint32_t* red = col + 3 * CY;      // 64
   uint32_t* Qt = Vt;
-  const int S = ys[0], nY = ys[1];
+  const int S = ys[0], nY = ys[1], amax_used = ys[2];
   const long long pidx = vrow0 + p;
   const int hd = vint.hdr[pidx];
   const int nD = hd < 0 ? -hd : hd;
@@ -462,6 +476,10 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
     int nq = 0;
     if (na > 0 && nD > 0) {
       const int vbits = limbs_bits(Vg, na);
+      if (vbits + P.k2 > amax_used) {  // reciprocal too short for this row
+        if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapAmax);
+        return;
+      }
       const int tv = max(0, n - P.k2 - 40);
       const int nt = max(0, (vbits - tv + 31) / 32);
       for (int i = threadIdx.x; i < nt; i += blockDim.x)
@@ -755,16 +773,17 @@ template <int TR>
 __global__ void __launch_bounds__(128)
 k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
              const uint32_t* Vhat, const uint32_t* Rhat,
-             long long row_stride_slot, int nslots, int c, const int* err) {
+             long long row_stride_slot, int nslots, int c, int r_begin,
+             int r_end, const int* err) {
   if (stage_aborted(err)) return;
   const int wd = blockIdx.y * blockDim.x + threadIdx.x;
   if (wd >= P.NW) return;
-  const int r0 = c + blockIdx.x * TR;
+  const int r0 = r_begin + blockIdx.x * TR;
   const PrimeConsts pc = P.pc[wd / P.L];
   const long long NW = P.NW;
   const uint32_t* rp[TR];
 #pragma unroll
-  for (int i = 0; i < TR; ++i) rp[i] = Rhat + (long long)min(r0 + i, P.n - 1) * NW + wd;
+  for (int i = 0; i < TR; ++i) rp[i] = Rhat + (long long)min(r0 + i, r_end - 1) * NW + wd;
   const uint32_t* vp = Vhat + (long long)c * NW + wd;
   uint64_t acc[TR];
 #pragma unroll
@@ -782,10 +801,10 @@ k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
   uint32_t old[TR];
 #pragma unroll
   for (int i = 0; i < TR; ++i)
-    old[i] = r0 + i < P.n ? W[(base + (r0 + i - c)) * NW + wd] : 0u;
+    old[i] = r0 + i < r_end ? W[(base + (r0 + i - c)) * NW + wd] : 0u;
 #pragma unroll
   for (int i = 0; i < TR; ++i) {
-    if (r0 + i >= P.n) continue;
+    if (r0 + i >= r_end) continue;
     const uint32_t t32 = reduce_sum64(acc[i], pc);
     W[(base + (r0 + i - c)) * NW + wd] =
         old[i] >= t32 ? old[i] - t32 : old[i] + pc.q - t32;
@@ -857,15 +876,16 @@ size_t extract_smem_bytes(const DevPlan& P) {
 }
 
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
-                           const long long* colbase, int p, IntBuf vint,
-                           long long vrow0, IntBuf piv, int* maxbitsV,
-                           uint32_t* vhat, int* maxdegV, int* err,
-                           cudaStream_t st) {
-  const int rows = P.n - p;
+                           const long long* colbase, int p, int r_begin,
+                           int r_end, IntBuf vint, long long vrow0, IntBuf piv,
+                           int* maxbitsV, uint32_t* vhat, int* maxdegV,
+                           int* err, cudaStream_t st) {
+  const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
   k_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
-      P, W, colbase, p, vint, vrow0, piv, maxbitsV, vhat, maxdegV, err);
+      P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
+      maxdegV, err);
   return post_launch(st);
 }
 
@@ -886,13 +906,14 @@ size_t recip_scratch_words(const DevPlan& P) {
 }
 
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
-                         const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                         uint32_t* scratch, int use_gscratch, int* err,
-                         cudaStream_t st) {
+                         const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
+                         uint32_t* Ybuf, int* ys, uint32_t* scratch,
+                         int use_gscratch, int* err, cudaStream_t st) {
   ++g_launches;
   const size_t smem = use_gscratch ? 0 : recip_scratch_words(P) * 4;
-  k_recip<<<1, recip_threads(), smem, st>>>(P, vint, prow, maxbitsV, p, Ybuf, ys, scratch,
-                                use_gscratch, err);
+  k_recip<<<1, recip_threads(), smem, st>>>(P, vint, prow, maxbitsV, p, piv,
+                                            dmax_bits, Ybuf, ys, scratch,
+                                            use_gscratch, err);
   return post_launch(st);
 }
 
@@ -956,14 +977,15 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
 cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
                               const long long* colbase, const uint32_t* Vhat,
                               const uint32_t* Rhat, long long row_stride_slot,
-                              int nslots, int c, const int* err,
-                              cudaStream_t st) {
-  if (nslots <= 0 || c >= P.n) return cudaSuccess;
+                              int nslots, int c, int r_begin, int r_end,
+                              const int* err, cudaStream_t st) {
+  if (nslots <= 0 || r_begin >= r_end) return cudaSuccess;
   constexpr int TR = 16;
-  dim3 grid((P.n - c + TR - 1) / TR, (P.NW + 127) / 128);
+  dim3 grid((r_end - r_begin + TR - 1) / TR, (P.NW + 127) / 128);
   ++g_launches;
   k_update_col<TR><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
-                                         row_stride_slot, nslots, c, err);
+                                         row_stride_slot, nslots, c, r_begin,
+                                         r_end, err);
   return post_launch(st);
 }
 
@@ -994,7 +1016,11 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                 (int)fwd)) != cudaSuccess)
     return e;
   const size_t rec = recip_scratch_words(P) * 4;
-  *recip_global = (int)rec > maxopt;
+  // the reciprocal CTA runs beside the bulk kernels: keeping its scratch in
+  // global memory (L1/L2-resident) lets it start on any SM with free warp
+  // slots instead of waiting for one with ~200 KB of free shared memory
+  const char* rg = getenv("HGPU_RECIP_SMEM");
+  *recip_global = (int)rec > maxopt || !(rg && *rg == '1');
   if (!*recip_global) {
     if ((e = cudaFuncSetAttribute(k_recip,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -33,6 +33,7 @@ enum : int {
   kCapCrt = 4,        // residue reconstruction out of range
   kCapDegree = 8,     // deg V + deg R >= L somewhere
   kCapCoeff = 16,     // accumulated coefficient bound reaches Q/2
+  kCapAmax = 32,      // PD bound on the ratio sizes violated (non-PD shift)
   kIntDivision = 1,   // quotient correction out of range
   kIntRecip = 2,      // reciprocal did not converge
 };
@@ -93,15 +94,15 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
                           const uint32_t* xhat, const long long* colbase,
                           uint32_t* W, cudaStream_t st);
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
-                           const long long* colbase, int p, IntBuf vint,
-                           long long vrow0, IntBuf piv, int* maxbitsV,
-                           uint32_t* vhat, int* maxdegV, int* err,
-                           cudaStream_t st);
+                           const long long* colbase, int p, int r_begin,
+                           int r_end, IntBuf vint, long long vrow0, IntBuf piv,
+                           int* maxbitsV, uint32_t* vhat, int* maxdegV,
+                           int* err, cudaStream_t st);
 size_t recip_scratch_words(const DevPlan& P);
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
-                         const int* maxbitsV, int p, uint32_t* Ybuf, int* ys,
-                         uint32_t* scratch, int use_gscratch, int* err,
-                         cudaStream_t st);
+                         const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
+                         uint32_t* Ybuf, int* ys, uint32_t* scratch,
+                         int use_gscratch, int* err, cudaStream_t st);
 size_t divide_smem_words(const DevPlan& P);
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, const uint32_t* Ybuf, const int* ys,
@@ -116,8 +117,8 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
 cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
                               const long long* colbase, const uint32_t* Vhat,
                               const uint32_t* Rhat, long long row_stride_slot,
-                              int nslots, int c, const int* err,
-                              cudaStream_t st);
+                              int nslots, int c, int r_begin, int r_end,
+                              const int* err, cudaStream_t st);
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
