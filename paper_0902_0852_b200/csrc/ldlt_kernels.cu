@@ -678,6 +678,9 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
                long long row_stride_slot, int nslots, int c_begin, int c_end,
                int nct, int nrt, const int* err) {
   __shared__ __align__(16) uint32_t sm[kUStages][2 * kUT][kUWords];
+  // the tile's own workspace words, prefetched at entry so the epilogue's
+  // read-modify-write never waits on HBM
+  extern __shared__ __align__(16) uint32_t sW[];  // [kUT*kUT][kUWords]
   if (stage_aborted(err)) return;
   const int w0 = blockIdx.y * kUWords;
   int t = blockIdx.x, ct = 0;
@@ -711,6 +714,17 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
 #pragma unroll
     for (int h = 0; h < 2; ++h) cp_async16(&sm[buf][dst_k[h]][dst_w[h]], src[h] + off);
   };
+  // W tile prefetch: 256 pairs x 8 chunks of 16 B, 16 per thread, committed
+  // with the first operand stage
+#pragma unroll 4
+  for (int h = 0; h < (kUT * kUT * 8) / 128; ++h) {
+    const int chunk = tid + 128 * h;
+    const int pair = chunk >> 3, part = chunk & 7;
+    const int r = r0 + (pair >> 4), c = c0 + (pair & 15);
+    if (c < c_end && r >= c && r < P.n)
+      cp_async16(&sW[pair * kUWords + part * 4],
+                 W + (colbase[c] + (r - c)) * NW + w0 + part * 4);
+  }
 #pragma unroll
   for (int s = 0; s < kUStages - 1; ++s) {
     if (s < nslots) issue(s);
@@ -742,6 +756,7 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
     __syncthreads();
   }
   cp_async_wait<0>();
+  __syncthreads();
 
   const int wd = w0 + lane;
   if (wd >= P.NW) return;
@@ -755,10 +770,9 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
     for (int i = 0; i < 8; ++i) {
       const int r = r0 + rm + i;
       if (r < c || r >= P.n) continue;
-      uint32_t* ptr = W + (base + (r - c)) * NW + wd;
       const uint32_t t32 = reduce_sum64(acc[i][j], pc);
-      const uint32_t old = *ptr;
-      *ptr = old >= t32 ? old - t32 : old + pc.q - t32;
+      const uint32_t old = sW[((rm + i) * kUT + cm + j) * kUWords + lane];
+      W[(base + (r - c)) * NW + wd] = old >= t32 ? old - t32 : old + pc.q - t32;
     }
   }
 }
@@ -951,7 +965,7 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
     for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
     dim3 grid((unsigned)tiles, P.NW / kUWords);
     ++g_launches;
-    k_update_tiled<<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
+    k_update_tiled<<<grid, 128, kUT * kUT * kUWords * 4, st>>>(P, W, colbase, Vhat, Rhat,
                                          row_stride_slot, nslots, c_begin,
                                          c_end, nct, nrt, err);
     return cudaGetLastError();
