@@ -376,10 +376,16 @@ __device__ __forceinline__ int limbs_bits(const uint32_t* a, int len) {
 // sums on PTX carry chains and writes them to its segment's planes.
 // col: scratch of `col_words` >= 3*M words (more words allow more segments);
 // out must not alias a, b or col.  red: blockDim/32+1 words.
+// With k_begin > 0 only columns [k_begin, M) are formed (a "short product"):
+// out[k - k_begin] holds the digits of sum_{k >= k_begin} col_k 2^{32 k},
+// i.e. the top of the product without the carry from the dropped columns
+// (below the true value by < min(na,nb) 2^{32 k_begin + 33}).
 __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
-                               int nb, uint32_t* out, int M, uint32_t* col,
-                               uint32_t* red, int col_words = 0) {
+                               int nb, uint32_t* out, int M_end, uint32_t* col,
+                               uint32_t* red, int col_words = 0,
+                               int k_begin = 0) {
   constexpr int G = 8;
+  const int M = M_end - k_begin;  // columns formed
   const int ngroups = (M + G - 1) / G;
   const int minlen = min(na, nb);
   // split a group's i-range only when segments stay >= 64 iterations and
@@ -393,7 +399,7 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
   const int items = ngroups * nseg;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int g = nseg == 1 ? it : it / nseg, sgi = it - g * nseg;
-    const int k0 = g * G;
+    const int k0 = k_begin + g * G;
     uint32_t c0[G], c1[G], c2[G];
 #pragma unroll
     for (int t = 0; t < G; ++t) c0[t] = c1[t] = c2[t] = 0u;
@@ -430,7 +436,7 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
     uint32_t* pl = col + (size_t)sgi * 3 * M;
 #pragma unroll
     for (int t = 0; t < G; ++t) {
-      const int k = k0 + t;
+      const int k = k0 + t - k_begin;
       if (k < M) {
         pl[k] = c0[t];
         pl[M + k] = c1[t];

@@ -193,20 +193,30 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
     __syncthreads();
 
     // Digit sums: s_k = sum_t piece_t(c_{k-t}); pieces are w-bit fields of the
-    // two's complement coefficient, the top piece carries the sign.
-    for (int k = threadIdx.x; k < M; k += blockDim.x) {
-      int ssum = 0;
-      for (int t = 0; t < T; ++t) {
-        const int i = k - t;
-        if (i < 0 || i >= L) continue;
+    // two's complement coefficient, the top piece carries the sign.  Each
+    // thread owns 8 consecutive positions and decodes each coefficient that
+    // reaches them once (8+T-1 decodes instead of 8T).
+    for (int k0 = threadIdx.x * 8; k0 < M; k0 += blockDim.x * 8) {
+      int acc8[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc8[u] = 0;
+      const int ilo = max(0, k0 - T + 1), ihi = min(L - 1, k0 + 7);
+      for (int i = ilo; i <= ihi; ++i) {
         unsigned __int128 cu = 0;
         for (int u = np - 1; u >= 0; --u) cu = (cu << 32) | A[u * L + i];
         cu <<= (128 - 32 * np);
         const __int128 c = ((__int128)cu) >> (128 - 32 * np);  // sign-extend
-        const __int128 sh = c >> (w * t);
-        ssum += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = k0 + u - i;  // piece index landing on position k0+u
+          if (t < 0 || t >= T) continue;
+          const __int128 sh = c >> (w * t);
+          acc8[u] += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
+        }
       }
-      S[k] = ssum;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < M) S[k0 + u] = acc8[u];
     }
     __syncthreads();
 
@@ -432,8 +442,10 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
 // (ldlt.cpp:15-20, 57-58).  With A = |V_r| 2^{K/2}, D = |V_p|, n = bits(D):
 //   F = (|V_r| >> t) * Y / 2^{S-K/2-t},   t = max(0, n - K/2 - 40),
 // differs from A/D by < 2^-31.9 (|Y - 2^S/D| <= 3 from k_recip; the dropped
-// low bits of V cost < 2^-39).  So when the 32 fraction bits of F lie in
-// [2, 2^32-3], q = floor(F) exactly and no remainder is needed.  Otherwise
+// low bits of V cost < 2^-39), and the product is formed only from column
+// K0 = (sh-75)/32 up, which lowers F by < 2^-32 more.  So when the 32 fraction
+// bits of F lie in [4, 2^32-5], q = floor(F) exactly and no remainder is
+// needed.  Otherwise
 // (e.g. exact quotients) floor(F) is within one of q and the remainder
 // window A - q~ D over nD+2 limbs decides the correction exactly.
 __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
@@ -487,15 +499,19 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
       __syncthreads();
       const int nP = nt + nY;
-      cta_mul(Vt, nt, Y, nY, Pr, nP, col, red);
       const int sh = S - P.k2 - tv;
-      const int nQ = max(0, (int)((32LL * nP - sh + 31) / 32));
+      // short product: columns below K0 move F by < 2^-32 (see the header)
+      const int K0 = max(0, (sh - 75) / 32);
+      const int nPs = nP - K0;
+      const int shs = sh - 32 * K0;
+      cta_mul(Vt, nt, Y, nY, Pr, nP, col, red, 0, K0);
+      const int nQ = max(0, (int)((32LL * nPs - shs + 31) / 32));
       for (int i = threadIdx.x; i < nQ; i += blockDim.x)
-        Qt[i] = field32(Pr, nP, 32LL * i + sh);
-      const uint32_t frac = field32(Pr, nP, (long long)sh - 32);
+        Qt[i] = field32(Pr, nPs, 32LL * i + shs);
+      const uint32_t frac = field32(Pr, nPs, (long long)shs - 32);
       __syncthreads();
       nq = cta_limb_len(Qt, nQ, red);
-      const bool exact_needed = sh < 32 || frac < 2u || frac > 0xFFFFFFFDu;
+      const bool exact_needed = shs < 32 || frac < 4u || frac > 0xFFFFFFFAu;
       if (exact_needed) {
         // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
         const int nw = nD + 2;
