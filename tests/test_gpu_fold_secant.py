@@ -143,3 +143,38 @@ def test_heig_run_status_codes(hg):
         assert _heig_run(hg.LIB_PATH, 4, "1")[0] == 2
     finally:
         del os.environ["HANKEL_EIG_PRECISION_CAP"]
+
+
+@pytest.mark.parametrize("n,b,k", [(64, (1, 1), 1024), (40, (7, 4), 2048), (30, (1, 2), 2048)])
+def test_lambda_40_digits_certified_by_reference(hg, ref, n, b, k):
+    """north_star: lambda_min agrees in >= 40 significant decimals.  The GPU
+    secant runs to a 40-digit stopping rule; the reference's own interval
+    LDL^T (ldlt.cpp:79-152 via verify's probe construction, decimal.cpp)
+    at Kv = 2K certifies det(M - aI) > 0 > det(M - bI) for a = trunc40(l),
+    b = bump(a), i.e. every one of the 40 digits."""
+    strip = ref.build_strip(n, b[0], b[1], k)
+    got = hg.smallest_eigenvalue(hg.HankelMatrixGPU(strip, k), 40)
+    lam = got["eigenvalue"]
+    assert len(lam.split("e")[0].replace(".", "")) == 40
+    hi = ref.bump_last_digit(lam)
+    assert ref.interval_sign_decimal(n, b[0], b[1], 2 * k, lam) == 1
+    assert ref.interval_sign_decimal(n, b[0], b[1], 2 * k, hi) == -1
+    # and the 15-digit prefix is the reference's own secant answer
+    r15 = ref.secant(strip, k)["eigenvalue"]
+    assert lam.split("e")[0][:16] == r15.split("e")[0][:16]
+    assert lam.split("e")[1] == r15.split("e")[1]
+
+
+@pytest.mark.slow
+def test_config2_lambda_40_digits_certified(hg, ref):
+    """BASELINE config 2 at full size (N=300, beta=7/4, P=4096): 40 digits of
+    lambda_min from the GPU secant, certified by the reference's interval
+    LDL^T at Kv = 8192 (its own verification path, verify.cpp:8-42)."""
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "config2_strip.json")))
+    strip = [int(v, 16) for v in g["strip"]]
+    got = hg.smallest_eigenvalue(hg.HankelMatrixGPU(strip, g["frac_bits"]), 40)
+    lam = got["eigenvalue"]
+    assert lam.startswith("1.4844") and lam.endswith("e-102")  # PAPER.md:471
+    assert ref.interval_sign_decimal(300, 7, 4, 8192, lam) == 1
+    assert ref.interval_sign_decimal(300, 7, 4, 8192, ref.bump_last_digit(lam)) == -1
