@@ -46,6 +46,7 @@ typedef enum hgpu_status {
 #define HGPU_CAPTURE 1u /* keep the ratio columns (LdltCapture) */
 #define HGPU_FOLD 2u    /* fold the pivots into det (ldlt.cpp:22-27) */
 #define HGPU_PROFILE 4u /* time every trailing-update launch with events */
+#define HGPU_KEEP_L 8u  /* keep the whole L factor on the device (solves) */
 
 typedef struct hgpu_matrix hgpu_matrix;
 typedef struct hgpu_factor hgpu_factor;
@@ -107,6 +108,22 @@ hgpu_status hgpu_smallest_eigenvalue(hgpu_matrix* m, int digits,
                                      char** eigenvalue, char** trace,
                                      long* iterations, double* det_seconds);
 void hgpu_string_free(char* s);
+
+/* Smallest eigenvalue by inverse iteration with Rayleigh-quotient shifts
+ * (the north-star's lambda_min step; no reference counterpart -- SURVEY §0
+ * D1 -- and pinned against oracle/pyoracle.py:inverse_iteration_py).  Each
+ * step factors M - s_k I on the GPU (HGPU_KEEP_L), solves (M - s_k I) y = u_k
+ * with the L, D factors (forward and back triangular solves, exact with one
+ * truncation per entry), sets rho_k = s_k + (y.u_k)/(y.y) and stops when the
+ * relative change of rho is below 2^-(frac_bits/2) or stalls.  u: n signed
+ * limb vectors at frac_bits (e.g. the seed-0 uniform[-1,1] start vector);
+ * sigma: the first shift (0 is fine).  Outputs as for
+ * hgpu_smallest_eigenvalue; `trace` lists every rho_k in hex. */
+hgpu_status hgpu_inverse_iteration(hgpu_matrix* m, const int32_t* u_sizes,
+                                   const uint32_t* u_limbs, int32_t sigma_size,
+                                   const uint32_t* sigma_limbs, int max_iter,
+                                   int digits, char** eigenvalue, char** trace,
+                                   long* iterations, double* seconds);
 
 /* Plan introspection: primes, transform length, digit width, limb capacity,
  * workspace bytes on this rank. */

@@ -330,3 +330,86 @@ class RefLib(_TextLib):
             return out
         finally:
             L.heig_config_free(cfg)
+
+
+# --------------------------------------------------------------------------
+# inverse iteration: no reference code exists;
+# this restatement DEFINES the algorithm the GPU path implements
+# (paper_0902_0852_b200/csrc/host/rqi.cpp, csrc/solve_kernels.cu) and is the
+# bit-exact checker for it.
+# --------------------------------------------------------------------------
+
+def solve_py(f: LdltResult, u: list[int], k: int) -> list[int]:
+    """(M - sI) y = u with L[r][p] = R_p[r] 2^-k2 and D_p = piv_p 2^-K, one
+    truncation toward zero per entry (forward, diagonal, back)."""
+    n, k2 = len(u), k // 2
+    z, acc = [0] * n, [0] * n
+    for p in range(n):
+        z[p] = u[p] - tdiv_q_2exp(acc[p], k2)
+        for r in range(p + 1, n):
+            acc[r] += f.ratios[(p, r)] * z[p]
+    w = [tdiv_q(z[p] << k, f.pivots[p]) for p in range(n)]
+    y, acc = [0] * n, [0] * n
+    for r in range(n - 1, -1, -1):
+        y[r] = w[r] - tdiv_q_2exp(acc[r], k2)
+        for q in range(r):
+            acc[q] += f.ratios[(q, r)] * y[r]
+    return y
+
+
+RQI_SWITCH_BITS = 32   # plain steps until the relative change is < 2^-32
+RQI_MAX_PLAIN = 64     # ... or this many plain steps
+RQI_STALL = 2          # stop after this many changes not below the smallest so far
+
+
+def inverse_iteration_py(strip: list[int], k: int, u: list[int], sigma: int = 0,
+                         max_iter: int = 40, factor=None) -> list[int]:
+    """Shifted inverse iteration, then Rayleigh-quotient iteration (SURVEY
+    §7 hard part (iv), §0 D7); returns every rho (mantissas at k bits).
+
+    Phase 1 keeps the factors of M - sigma I and iterates y = (M - sigma I)^-1 u
+    until the Rayleigh quotient's relative change is below 2^-RQI_SWITCH_BITS
+    (or RQI_MAX_PLAIN steps), which pins the iteration to the eigenvalue next to
+    sigma (lambda_1 for sigma <= 0 on a positive definite M).  Phase 2 refactors
+    at sigma = rho every step.  Stop when the relative change is below 2^-(K/2),
+    when rho repeats, or when RQI_STALL changes have failed to go below the
+    smallest change seen so far (the arithmetic noise floor).  factor(strip, x, k) defaults to ldlt_py."""
+    factor = factor or (lambda s, x, kk: ldlt_py(s, x, kk, capture=True))
+    n, k2 = len(u), k // 2
+    rhos, rho_prev, d_min = [], None, None
+    stall, plain, rqi = 0, 0, False
+    f = None
+    for _ in range(max_iter):
+        if f is None:
+            try:
+                f = factor(strip, sigma, k)
+            except ZeroPivotError as e:
+                if e.pivot_index == n - 1:  # sigma is an eigenvalue at K bits
+                    rhos.append(sigma)
+                    break
+                raise
+        y = solve_py(f, u, k)
+        num = sum(a * b for a, b in zip(y, u))
+        den = sum(a * a for a in y)
+        rho = sigma + tdiv_q(num << k, den)
+        rhos.append(rho)
+        if rho_prev is not None:
+            d = abs(rho - rho_prev)
+            if d == 0 or (d << k2) <= abs(rho):
+                break
+            if d_min is not None and d >= d_min:
+                stall += 1
+                if stall >= RQI_STALL:
+                    break
+            else:
+                d_min = d
+            if not rqi and ((d << RQI_SWITCH_BITS) <= abs(rho) or plain >= RQI_MAX_PLAIN):
+                rqi = True
+        rho_prev = rho
+        plain += not rqi
+        mb = max(abs(v).bit_length() for v in y)
+        sh = mb - k
+        u = [tdiv_q_2exp(v, sh) if sh > 0 else v << -sh for v in y]
+        if rqi:
+            sigma, f = rho, None
+    return rhos

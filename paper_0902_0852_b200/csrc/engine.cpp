@@ -440,6 +440,12 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   int* maxdegR = stats_ + 2 * n;
   IntBuf vint{vhdr_, vlimbs_}, rint{rhdr_, rlimbs_}, piv{phdr_, plimbs_};
   const bool capture = flags & HGPU_CAPTURE;
+  have_L_ = false;
+  if ((flags & HGPU_KEEP_L) && !lhdr_) {
+    const size_t nl = (size_t)n * (n - 1) / 2;
+    lhdr_ = dalloc<int>(std::max<size_t>(nl, 1));
+    llimbs_ = dalloc<uint32_t>(std::max<size_t>(nl, 1) * P.cap);
+  }
   const bool profile = flags & HGPU_PROFILE;
   if (capture) {
     res.ratios.assign(n > 0 ? n - 1 : 0, {});
@@ -587,6 +593,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       }
     }
     CU(cudaEventRecord(panel_done[b], sp));
+    if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, row0set, sp);
     if (capture) {
       const int nsr = std::min(ns, n - 1 - p0);
       if (nsr > 0) {
@@ -676,6 +683,142 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                                pl.begin() + (size_t)p * P.cap + len);
   }
   if (flags & HGPU_FOLD) fold(res);
+}
+
+// R_p[r] for the panel's stages (rows r > p) into the packed L store.
+void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st) {
+  const Plan& P = plan_;
+  const int n = n_;
+  for (int s = 0; s < ns; ++s) {
+    const int p = p0 + s;
+    if (p >= n - 1) break;
+    const long long src = row0set + (long long)s * n + p + 1;
+    const long long dst = (long long)p * (n - 1) - (long long)p * (p - 1) / 2;
+    const size_t rows = (size_t)(n - p - 1);
+    CU(cudaMemcpyAsync(lhdr_ + dst, rhdr_ + src, rows * 4,
+                       cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(llimbs_ + dst * P.cap, rlimbs_ + src * P.cap,
+                       rows * P.cap * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  have_L_ = true;
+}
+
+std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
+                                   long long* launches) {
+  if (!have_L_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve needs a HGPU_KEEP_L factorisation");
+  if (world_ != 1)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve runs on a single rank");
+  const Plan& P = plan_;
+  const int n = n_, k2 = K_ / 2;
+  cudaStream_t st = stream_;
+  CU(cudaSetDevice(device_));
+  if (!svhdr_) {
+    sWv_ = 2 * P.cap + 8;
+    sWa_ = P.cap + sWv_ + 2;
+    svhdr_ = dalloc<int>(4 * (size_t)n);
+    svlimbs_ = dalloc<uint32_t>(4 * (size_t)n * sWv_);
+    sacc_ = dalloc<uint32_t>((size_t)n * sWa_);
+    spair_hdr_ = dalloc<int>(2 * (size_t)n);
+    spair_limbs_ = dalloc<uint32_t>(2 * (size_t)n * sWv_);
+    sbits_ = dalloc<int>(1);
+    sys_ = dalloc<int>(4);
+    CU(configure_solve_kernels(P.cap, sWv_, sWa_));
+  }
+  // division plan: the LDL^T plan with integer capacity Wv (k_recip/k_divide
+  // with a per-step divisor, scratch in global memory, no transform)
+  DevPlan D2 = dp_;
+  D2.n = 2;
+  D2.cap = sWv_;
+  D2.ycap = sWv_ + k2 / 32 + 8;
+  D2.tw_smem = 0;
+  D2.grid_cap = 1;
+  if (!sybuf_) {
+    sybuf_ = dalloc<uint32_t>(D2.ycap);
+    srscr_ = dalloc<uint32_t>(recip_scratch_words(D2));
+    sdscr_ = dalloc<uint32_t>(divide_smem_words(D2) + 64);
+  }
+  const int Wv = sWv_, Wa = sWa_;
+  IntBuf vecs{svhdr_, svlimbs_};
+  IntBuf pairs{spair_hdr_, spair_limbs_};
+  IntBuf L{lhdr_, llimbs_};
+  const int U = 0, Z = n, Wq = 2 * n, Y = 3 * n;
+  {
+    std::vector<int> hdr(4 * (size_t)n, 0);
+    std::vector<uint32_t> lim((size_t)n * Wv, 0);
+    for (int i = 0; i < n; ++i) {
+      if ((int)u[i].limbs.size() > Wv)
+        throw Error(HGPU_ERR_CAPACITY, "start vector entry too large");
+      hdr[i] = u[i].size;
+      std::copy(u[i].limbs.begin(), u[i].limbs.end(),
+                lim.begin() + (size_t)i * Wv);
+    }
+    CU(cudaMemcpyAsync(svhdr_, hdr.data(), hdr.size() * 4,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(svlimbs_, lim.data(), lim.size() * 4,
+                       cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+  }
+  int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
+  CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+  // pivots into the even rows of the pair buffer
+  CU(cudaMemcpy2DAsync(spair_hdr_, 2 * sizeof(int), phdr_, sizeof(int),
+                       sizeof(int), n, cudaMemcpyDeviceToDevice, st));
+  CU(cudaMemsetAsync(spair_limbs_, 0, 2 * (size_t)n * Wv * 4, st));
+  CU(cudaMemcpy2DAsync(spair_limbs_, 2 * (size_t)Wv * 4, plimbs_,
+                       (size_t)P.cap * 4, (size_t)P.cap * 4, n,
+                       cudaMemcpyDeviceToDevice, st));
+  long long nl = 0;
+  // forward: z_p = u_p - tdiv_2exp(acc_p, k2); acc_r += R_p[r] z_p (r > p)
+  CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
+  for (int p = 0; p < n; ++p) {
+    CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)p * Wa, vecs, U + p,
+                           vecs, Z + p, pairs, 2 * p + 1, k2, err_, st));
+    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Z + p, p, 0, sacc_,
+                         dp_.grid_cap, err_, st));
+    nl += 2;
+  }
+  // diagonal: w_p = tdiv(z_p 2^K, piv_p) with the LDL^T division kernels
+  for (int p = 0; p < n; ++p) {
+    CU(launch_int_bits(pairs, 2 * p + 1, Wv, 0, sbits_, st));
+    CU(launch_recip(D2, pairs, 2 * p, sbits_, 0, pairs, 0, sybuf_, sys_,
+                    srscr_, 1, err_, st));
+    CU(launch_divide(D2, pairs, 2 * p, 0, sybuf_, sys_, vecs, Wq + p - 1,
+                     nullptr, nullptr, sdscr_, 1, err_, st));
+    nl += 3;
+  }
+  // back: y_r = w_r - tdiv_2exp(acc'_r, k2); acc'_q += R_q[r] y_r (q < r)
+  CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
+  for (int r = n - 1; r >= 0; --r) {
+    CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)r * Wa, vecs, Wq + r,
+                           vecs, Y + r, vecs, 0, 0, err_, st));
+    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Y + r, r, 1, sacc_,
+                         dp_.grid_cap, err_, st));
+    nl += 2;
+  }
+  int herr[kErrWords];
+  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  std::vector<int> yh(n);
+  std::vector<uint32_t> yl((size_t)n * Wv);
+  CU(cudaMemcpyAsync(yh.data(), svhdr_ + Y, n * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(yl.data(), svlimbs_ + (size_t)Y * Wv, yl.size() * 4,
+                     cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (launches) *launches += nl;
+  if (herr[kErrCapacity])
+    throw Error(HGPU_ERR_CAPACITY, "solve capacity exceeded (flags " +
+                                       std::to_string(herr[kErrCapacity]) + ")");
+  if (herr[kErrInternal])
+    throw Error(HGPU_ERR_INTERNAL, "solve exactness self-check failed");
+  if (herr[kErrZeroPivot] != INT_MAX)
+    throw Error(HGPU_ERR_INTERNAL, "zero divisor in the diagonal solve");
+  std::vector<HostInt> y(n);
+  for (int i = 0; i < n; ++i) {
+    y[i].size = yh[i];
+    const int len = std::abs(yh[i]);
+    y[i].limbs.assign(yl.begin() + (size_t)i * Wv, yl.begin() + (size_t)i * Wv + len);
+  }
+  return y;
 }
 
 void Matrix::fold(FactorResult& res) {

@@ -75,6 +75,9 @@ class Matrix {
     return plan_;
   }
   int frac_bits() const { return K_; }
+  // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
+  // factorisation (solve_kernels.cu); u, y at F fractional bits.
+  std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
   int order() const { return n_; }
   const HostInt& strip_entry(int s) const { return strip_[s]; }
 
@@ -85,6 +88,7 @@ class Matrix {
   void panel_broadcast(int owner, int p0, int ns, long long row0,
                        cudaStream_t st);
   void fold(FactorResult& res);
+  void keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st);
 
   int n_, K_, device_;
   std::vector<HostInt> strip_;
@@ -121,6 +125,20 @@ class Matrix {
   cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
   std::vector<cudaEvent_t> pev_, sev_;
   bool recip_bound_ = true;  // reciprocal precision from the PD bound
+  // whole L factor (HGPU_KEEP_L): R_p[r], p < r, packed strictly lower
+  int* lhdr_ = nullptr;
+  uint32_t* llimbs_ = nullptr;
+  bool have_L_ = false;
+  // solve buffers
+  int sWv_ = 0, sWa_ = 0;
+  int* svhdr_ = nullptr;        // vectors u | z | w | y (4n rows)
+  uint32_t* svlimbs_ = nullptr;
+  uint32_t* sacc_ = nullptr;    // n x Wa two's complement
+  int* spair_hdr_ = nullptr;    // (piv_p, z_p 2^k2) pairs, 2n rows
+  uint32_t* spair_limbs_ = nullptr;
+  int* sbits_ = nullptr;
+  uint32_t *sybuf_ = nullptr, *srscr_ = nullptr, *sdscr_ = nullptr;
+  int* sys_ = nullptr;
   int dmax_bits_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   std::vector<cudaEvent_t> uev_;

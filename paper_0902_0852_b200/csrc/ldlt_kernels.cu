@@ -571,13 +571,17 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       dst[i] = i < nq ? Qt[i] : 0u;
     if (threadIdx.x == 0) {
       rint.hdr[ridx] = rsign * nq;
-      if (nq > 0) atomicMax(maxdegR, (limbs_bits(Qt, nq) - 1) / P.w);
+      if (nq > 0 && maxdegR) atomicMax(maxdegR, (limbs_bits(Qt, nq) - 1) / P.w);
     }
     // transform of R_p[r] (Montgomery form) for the trailing update; the
     // NTT buffer reuses the Barrett scratch when it is large enough
-    uint32_t* X = P.NW <= 4 * CY ? Pr : sm + span;
-    transform_int(P, Qt, nq, 0, rsign, X, rhat + ridx * (long long)P.NW,
-                  true, twm, err);
+    if (rhat) {
+      uint32_t* X = P.NW <= 4 * CY ? Pr : sm + span;
+      transform_int(P, Qt, nq, 0, rsign, X, rhat + ridx * (long long)P.NW,
+                    true, twm, err);
+    } else {
+      __syncthreads();
+    }
   }
 }
 

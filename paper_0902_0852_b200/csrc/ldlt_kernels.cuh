@@ -123,6 +123,19 @@ cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
 long long kernel_launch_count();
+// solve_kernels.cu (inverse iteration)
+size_t solve_axpy_smem_words(int cap, int Wv);
+size_t solve_finish_smem_words(int Wv, int Wa);
+cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
+                              IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                              int grid_cap, int* err, cudaStream_t st);
+cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                                IntBuf base, int bi, IntBuf out, int oi,
+                                IntBuf out2, int o2i, int shift_out, int* err,
+                                cudaStream_t st);
+cudaError_t launch_int_bits(IntBuf v, int idx, int stride, int k2, int* out,
+                            cudaStream_t st);
+cudaError_t configure_solve_kernels(int cap, int Wv, int Wa);
 // fold_kernels.cu
 long long fold_pivots_device(const uint32_t* plimbs, const int* plen, int n,
                              int pcap, int K, uint32_t* X0, uint32_t* X1,

@@ -1,0 +1,202 @@
+// Triangular solves with the LDL^T factors for inverse iteration (SURVEY
+// §8 a11; the north-star's step after the factorisation -- the reference
+// itself finds lambda_1 by the secant and has no solve).  With A = M - sI =
+// L D L^T, L[r][p] = R_p[r] 2^-k2 (the ratio columns of ldlt.cpp:57-58) and
+// D_p = piv_p 2^-K, a right-hand side u at F fractional bits is solved in
+// exact fixed point, truncating toward zero once per entry:
+//   forward   z_r = u_r - tdiv_2exp( sum_{p<r} R_p[r] z_p , k2 )
+//   diagonal  w_p = tdiv( z_p 2^K , piv_p )              (k_divide)
+//   back      y_p = w_p - tdiv_2exp( sum_{r>p} R_p[r] y_r , k2 )
+// The sums are accumulated column by column (one CTA per target row, exact
+// two's-complement accumulators), so each sequential step is one parallel
+// AXPY over the remaining rows.
+#include <cstdint>
+
+#include "cta_ops.cuh"
+#include "ldlt_kernels.cuh"
+
+namespace hgpu {
+
+namespace {
+
+// index of R_p[r] (p < r < n) in the packed strictly-lower store
+__device__ __forceinline__ long long lidx(int n, int p, int r) {
+  return (long long)p * (n - 1) - (long long)p * (p - 1) / 2 + (r - p - 1);
+}
+
+}  // namespace
+
+// acc_t += R(a, b) * x_j  for the targets of step j:
+//   forward (dir = 0): j = p, targets t = r in (p, n),  coefficient R_p[r]
+//   back    (dir = 1): j = r, targets t = q in [0, r),  coefficient R_q[r]
+__global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
+                             IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                             int* err) {
+  extern __shared__ uint32_t sm[];
+  const int hx = xv.hdr[xi];
+  const int nx = hx < 0 ? -hx : hx;
+  if (nx == 0) return;  // nothing to add
+  const int sx = hx < 0 ? -1 : 1;
+  uint32_t* X = sm;                 // Wv
+  uint32_t* C = X + Wv;             // cap
+  uint32_t* Pr = C + cap;           // cap + Wv
+  uint32_t* col = Pr + cap + Wv;    // 3 (cap + Wv)
+  uint32_t* red = col + 3 * (cap + Wv);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x)
+    X[i] = xv.limbs[(long long)xi * Wv + i];
+  const int t0 = dir == 0 ? j + 1 : 0;
+  const int t1 = dir == 0 ? n : j;
+  for (int t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+    const long long li = dir == 0 ? lidx(n, j, t) : lidx(n, t, j);
+    const int hc = L.hdr[li];
+    const int nc = hc < 0 ? -hc : hc;
+    if (nc == 0) continue;
+    const int sgn = (hc < 0 ? -1 : 1) * sx;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x)
+      C[i] = L.limbs[li * cap + i];
+    __syncthreads();
+    const int nP = nc + nx;
+    cta_mul(C, nc, X, nx, Pr, nP, col, red);
+    uint32_t* a = acc + (long long)t * Wa;
+    if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    cta_resolve(
+        Wa, 32,
+        [&](int k) -> int64_t {
+          const int64_t pv = k < nP ? (int64_t)Pr[k] : 0;
+          return (int64_t)a[k] + (sgn > 0 ? pv : -pv);
+        },
+        [&](int k, uint32_t d) { col[k] = d; }, red);
+    for (int k = threadIdx.x; k < Wa; k += blockDim.x) a[k] = col[k];
+    __syncthreads();
+  }
+}
+
+// out_i = base_i - tdiv_2exp(acc_i, k2)   (single CTA; acc two's complement)
+// base/out are signed limb vectors of Wv limbs; `shift_out` > 0 additionally
+// stores out_i << shift_out into out2 (the diagonal step's numerator).
+__global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                               IntBuf base, int bi, IntBuf out, int oi,
+                               IntBuf out2, int o2i, int shift_out, int* err) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* M1 = sm;           // Wa + 1
+  uint32_t* T = M1 + Wa + 1;   // Wv + 1
+  uint32_t* X = T + Wv + 1;    // Wv + 2
+  uint32_t* red = X + Wv + 2;
+  // |acc| and its sign
+  const bool neg = (acc_i[Wa - 1] & 0x80000000u) != 0;
+  cta_resolve(
+      Wa, 32,
+      [&](int k) -> int64_t {
+        return neg ? -(int64_t)acc_i[k] : (int64_t)acc_i[k];
+      },
+      [&](int k, uint32_t d) { M1[k] = d; }, red);
+  // t = sign * (|acc| >> k2)
+  const int st = neg ? -1 : 1;
+  for (int k = threadIdx.x; k <= Wv; k += blockDim.x)
+    T[k] = field32(M1, Wa, 32LL * k + k2);
+  // X = base - t   (two resolves keep every digit sum in range)
+  const int hb = base.hdr[bi];
+  const int nb = hb < 0 ? -hb : hb;
+  const int sb = hb < 0 ? -1 : 1;
+  const uint32_t* B = base.limbs + (long long)bi * Wv;
+  __syncthreads();
+  const int W2 = Wv + 2;
+  cta_resolve(
+      W2, 32,
+      [&](int k) -> int64_t {
+        const int64_t bv = k < nb ? (int64_t)B[k] : 0;
+        return sb > 0 ? bv : -bv;
+      },
+      [&](int k, uint32_t d) { X[k] = d; }, red);  // two's complement base
+  cta_resolve(
+      W2, 32,
+      [&](int k) -> int64_t {
+        const int64_t tv = k <= Wv ? (int64_t)T[k] : 0;
+        return (int64_t)X[k] - (st > 0 ? tv : -tv);
+      },
+      [&](int k, uint32_t d) { M1[k] = d; }, red);
+  const bool rneg = (M1[W2 - 1] & 0x80000000u) != 0;
+  cta_resolve(
+      W2, 32,
+      [&](int k) -> int64_t {
+        return rneg ? -(int64_t)M1[k] : (int64_t)M1[k];
+      },
+      [&](int k, uint32_t d) { X[k] = d; }, red);
+  const int len = cta_limb_len(X, W2, red);
+  if (len > Wv) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return;
+  }
+  uint32_t* O = out.limbs + (long long)oi * Wv;
+  for (int k = threadIdx.x; k < Wv; k += blockDim.x) O[k] = k < len ? X[k] : 0u;
+  if (threadIdx.x == 0) out.hdr[oi] = len == 0 ? 0 : (rneg ? -len : len);
+  if (shift_out > 0) {
+    // numerator z << shift for the diagonal division (k_divide shifts by k2
+    // itself, so the caller passes K - k2 = k2)
+    const int bits = limbs_bits(X, len) + shift_out;
+    const int n2 = len == 0 ? 0 : (bits + 31) / 32;
+    uint32_t* O2 = out2.limbs + (long long)o2i * Wv;
+    if (n2 > Wv) {
+      if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+      return;
+    }
+    for (int k = threadIdx.x; k < Wv; k += blockDim.x)
+      O2[k] = k < n2 ? field32(X, len, 32LL * k - shift_out) : 0u;
+    if (threadIdx.x == 0) out2.hdr[o2i] = n2 == 0 ? 0 : (rneg ? -n2 : n2);
+  }
+}
+
+// bits of a signed limb integer (for the reciprocal's precision)
+__global__ void k_int_bits(IntBuf v, int idx, int stride, int k2, int* out) {
+  if (threadIdx.x != 0) return;
+  const int h = v.hdr[idx];
+  const int n = h < 0 ? -h : h;
+  *out = n == 0 ? 0 : limbs_bits(v.limbs + (long long)idx * stride, n) + k2;
+}
+
+size_t solve_axpy_smem_words(int cap, int Wv) {
+  return (size_t)Wv + cap + (cap + Wv) + 3 * (size_t)(cap + Wv) + 64;
+}
+size_t solve_finish_smem_words(int Wv, int Wa) {
+  return (size_t)(Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
+}
+
+cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
+                              IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                              int grid_cap, int* err, cudaStream_t st) {
+  const int rows = dir == 0 ? n - j - 1 : j;
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = solve_axpy_smem_words(cap, Wv) * 4;
+  k_solve_axpy<<<min(rows, grid_cap), 256, smem, st>>>(n, cap, Wv, Wa, L, xv,
+                                                        xi, j, dir, acc, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                                IntBuf base, int bi, IntBuf out, int oi,
+                                IntBuf out2, int o2i, int shift_out, int* err,
+                                cudaStream_t st) {
+  const size_t smem = solve_finish_smem_words(Wv, Wa) * 4;
+  k_solve_finish<<<1, 256, smem, st>>>(Wv, Wa, k2, acc_i, base, bi, out, oi,
+                                        out2, o2i, shift_out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_int_bits(IntBuf v, int idx, int stride, int k2, int* out,
+                            cudaStream_t st) {
+  k_int_bits<<<1, 32, 0, st>>>(v, idx, stride, k2, out);
+  return cudaGetLastError();
+}
+
+cudaError_t configure_solve_kernels(int cap, int Wv, int Wa) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(
+           k_solve_axpy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+           (int)(solve_axpy_smem_words(cap, Wv) * 4))) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(k_solve_finish,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(solve_finish_smem_words(Wv, Wa) * 4));
+}
+
+}  // namespace hgpu

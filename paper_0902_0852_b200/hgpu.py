@@ -42,7 +42,7 @@ EXPORTS = (
     "hgpu_factor_det", "hgpu_factor_device_ms", "hgpu_factor_update_stats",
     "hgpu_factor_launches", "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
     "hgpu_last_zero_pivot", "hgpu_last_error", "hgpu_version",
-    "hgpu_smallest_eigenvalue", "hgpu_string_free",
+    "hgpu_smallest_eigenvalue", "hgpu_string_free", "hgpu_inverse_iteration",
 )
 
 
@@ -115,6 +115,10 @@ def load() -> ctypes.CDLL:
                                              ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64),
                                              ctypes.POINTER(ctypes.c_double)]
     lib.hgpu_string_free.argtypes = [ctypes.c_void_p]
+    lib.hgpu_inverse_iteration.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), u32p, i32, u32p,
+                                           ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
+                                           ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64),
+                                           ctypes.POINTER(ctypes.c_double)]
     _lib = lib
     return lib
 
@@ -288,6 +292,37 @@ def smallest_eigenvalue(m: "HankelMatrixGPU", digits: int = 15) -> dict:
     iterates = [tuple(int(v, 16) for v in l.split()) for l in lines if l.strip()]
     return {"eigenvalue": eig, "iterates": iterates, "iterations": it.value,
             "det_seconds": secs.value}
+
+
+def seeded_start_vector(n: int, frac_bits: int, seed: int = 0) -> list[int]:
+    """north-star start vector: numpy default_rng(seed).uniform(-1, 1, n);
+    doubles are dyadic, so they are exact at frac_bits >= 1100 or so and are
+    otherwise truncated toward zero (mantissas at frac_bits)."""
+    from fractions import Fraction
+    vals = np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+    out = []
+    for v in vals:
+        f = Fraction(float(v)) * (1 << frac_bits)
+        q = abs(f.numerator) // f.denominator
+        out.append(q if f >= 0 else -q)
+    return out
+
+
+def inverse_iteration(m: "HankelMatrixGPU", u: list[int], sigma: int = 0, max_iter: int = 40,
+                      digits: int = 15) -> dict:
+    """Inverse iteration with Rayleigh-quotient shifts on the GPU factors."""
+    lib = load()
+    sizes, limbs = pack_ints(u)
+    ss, sl = int_to_limbs(sigma)
+    ev, tr = ctypes.c_void_p(), ctypes.c_void_p()
+    it, secs = ctypes.c_long(), ctypes.c_double()
+    _check(lib.hgpu_inverse_iteration(m._h, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                      _u32p(limbs), ss, _u32p(sl), max_iter, digits,
+                                      ctypes.byref(ev), ctypes.byref(tr), ctypes.byref(it),
+                                      ctypes.byref(secs)), m.frac_bits)
+    eig = _take_string(ev)
+    rhos = [int(l, 16) for l in _take_string(tr).split("\n") if l.strip()]
+    return {"eigenvalue": eig, "rho": rhos, "iterations": it.value, "seconds": secs.value}
 
 
 def block_owner(block: int, world: int) -> int:

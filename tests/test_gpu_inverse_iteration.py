@@ -1,0 +1,102 @@
+"""GPU inverse iteration (north-star lambda_min step).
+
+The reference has no inverse iteration, so the restatement
+oracle/pyoracle.py:inverse_iteration_py defines it; the GPU path must
+reproduce every Rayleigh quotient bit for bit, and the eigenvalue it returns
+is pinned independently by the reference's own secant (15 digits) and its
+interval LDL^T sign test (40 digits, verify.cpp:8-42)."""
+import json
+import os
+
+import pytest
+
+from helpers import random_pd_hankel
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def hg():
+    from paper_0902_0852_b200 import hgpu
+    hgpu.load()
+    return hgpu
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return po.RefLib()
+
+
+def negatives(strip, x, k):
+    return sum(1 for p in po.OracleLib().ldlt(strip, x, k, capture=True).pivots if p < 0)
+
+
+@pytest.mark.parametrize("seed,n,k", [(111, 6, 256), (112, 12, 384), (113, 20, 512), (114, 33, 640)])
+def test_rho_iterates_bit_exact_random_pd(hg, seed, n, k):
+    strip = random_pd_hankel(seed, n, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
+    assert got["rho"] == want
+    assert got["iterations"] == len(want)
+    # Sylvester inertia: rho is the SMALLEST eigenvalue
+    rho = want[-1]
+    assert negatives(strip, rho - (rho >> 40), k) == 0
+    assert negatives(strip, rho + (rho >> 40), k) == 1
+
+
+def test_nonzero_start_shift(hg):
+    # phase 1 from a negative shift (the secant's x1 = -2^-16 M00 style)
+    strip = random_pd_hankel(115, 16, 512)
+    k = 512
+    sigma = -(strip[0] >> 16)
+    u = hg.seeded_start_vector(16, k, seed=3)
+    want = po.inverse_iteration_py(strip, k, u, sigma, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, sigma, 40)
+    assert got["rho"] == want
+
+
+def test_config1_inverse_iteration(hg, ref):
+    # BASELINE config 1 (N=64, beta=1, P=1024) from the seed-0 start vector
+    n, k = 64, 1024
+    strip = po.exact_strip(n, 1, 1, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40,
+                                   factor=lambda s, x, kk: ref.ldlt_serial(s, x, kk, True))
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40, digits=40)
+    assert got["rho"] == want
+    lam = got["eigenvalue"]
+    fx = {(d["n"], d["beta"]): d for d in json.load(open(os.path.join(GOLDEN, "lambda_secant.json")))}
+    sec = fx[(64, "1/1")]["eigenvalue"]  # the reference's secant, 15 digits
+    assert lam.split("e")[1] == sec.split("e")[1] and lam[:16] == sec[:16]
+    # every one of the 40 digits certified by the reference's interval LDL^T
+    assert ref.interval_sign_decimal(n, 1, 1, 2 * k, lam) == 1
+    assert ref.interval_sign_decimal(n, 1, 1, 2 * k, ref.bump_last_digit(lam)) == -1
+
+
+@pytest.mark.parametrize("n,k", [(100, 832), (30, 2048)])
+def test_fixture_matrices(hg, ref, n, k):
+    d = {(e["n"], e["frac_bits"]): e for e in json.load(open(os.path.join(GOLDEN, "lambda_secant.json")))}[(n, k)]
+    num, den = map(int, d["beta"].split("/"))
+    strip = po.exact_strip(n, num, den, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40,
+                                   factor=lambda s, x, kk: ref.ldlt_serial(s, x, kk, True))
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40, digits=15)
+    assert got["rho"] == want
+    assert got["eigenvalue"].split("e")[1] == d["eigenvalue"].split("e")[1]
+    assert got["eigenvalue"][:15] == d["eigenvalue"][:15]
+
+
+def test_config3_time_to_lambda(hg):
+    # BASELINE config 3 (N=1000, beta=1, P=24576): agrees with the GPU secant
+    # (whose iterates are bit-identical to the reference's, test_gpu_fold_secant)
+    n, k = 1000, 24576
+    m = hg.HankelMatrixGPU(po.exact_strip(n, 1, 1, k), k)
+    got = hg.inverse_iteration(m, hg.seeded_start_vector(n, k), 0, 40, digits=40)
+    print("config3 inverse iteration", got["iterations"], "steps", round(got["seconds"], 2), "s",
+          got["eigenvalue"])
+    assert got["eigenvalue"].startswith("1.0892427421041")
+    assert got["eigenvalue"].endswith("e-52")

@@ -130,3 +130,32 @@ def test_fold_restatement(orc):
     piv = po.closed_form_beta1(30, 512).pivots
     assert orc.fold(piv, 512) == po.fold_pivots(piv, 512)
     assert po.fold_pivots(piv, 512) == math.prod(math.factorial(k) ** 2 for k in range(30)) << 512
+
+
+def test_inverse_iteration_restatement_config1(ref):
+    """a11 restatement on BASELINE config 1: converges to the reference's
+    secant lambda_1 and its 40 digits pass the reference's interval test."""
+    import numpy as np
+    from fractions import Fraction
+    n, k = 64, 1024
+    strip = po.exact_strip(n, 1, 1, k)
+    u = []
+    for v in np.random.default_rng(0).uniform(-1.0, 1.0, n):
+        f = Fraction(float(v)) * (1 << k)
+        u.append(int(f) if f >= 0 else -int(-f))
+    rhos = po.inverse_iteration_py(strip, k, u, 0, 40,
+                                   factor=lambda s, x, kk: ref.ldlt_serial(s, x, kk, True))
+    assert 4 <= len(rhos) < 40
+    lam = ref.truncate_sig_digits(rhos[-1], k, 40)
+    assert lam.startswith("5.50002146863720") and lam.endswith("e-12")
+    assert ref.interval_sign_decimal(n, 1, 1, 2 * k, lam) == 1
+    assert ref.interval_sign_decimal(n, 1, 1, 2 * k, ref.bump_last_digit(lam)) == -1
+
+
+@pytest.mark.parametrize("seed,n,k", [(111, 6, 256), (113, 20, 512)])
+def test_inverse_iteration_restatement_finds_lambda1(orc, seed, n, k):
+    strip = random_pd_hankel(seed, n, k)
+    u = [((-1) ** i) << (k - 1 - i % 3) for i in range(n)]
+    rho = po.inverse_iteration_py(strip, k, u, 0, 40)[-1]
+    neg = lambda x: sum(1 for p in orc.ldlt(strip, x, k, capture=True).pivots if p < 0)
+    assert neg(rho - (rho >> 40)) == 0 and neg(rho + (rho >> 40)) == 1
