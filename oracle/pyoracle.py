@@ -357,27 +357,37 @@ def solve_py(f: LdltResult, u: list[int], k: int) -> list[int]:
     return y
 
 
-RQI_SWITCH_BITS = 32   # plain steps until the relative change is < 2^-32
-RQI_MAX_PLAIN = 64     # ... or this many plain steps
+RQI_SWITCH_BITS = 32   # phase 1 -> 2 when the relative change is < 2^-32
+RQI_MAX_PLAIN = 64     # ... or after this many phase-1 steps
 RQI_STALL = 2          # stop after this many changes not below the smallest so far
+
+
+def rqi_final_bits(k: int) -> int:
+    """phase 2 -> 3 when the relative change is < 2^-rqi_final_bits(K)"""
+    return max(64, k // 16)
 
 
 def inverse_iteration_py(strip: list[int], k: int, u: list[int], sigma: int = 0,
                          max_iter: int = 40, factor=None) -> list[int]:
-    """Shifted inverse iteration, then Rayleigh-quotient iteration (SURVEY
-    §7 hard part (iv), §0 D7); returns every rho (mantissas at k bits).
+    """Shifted inverse iteration with Rayleigh-quotient refactorisation
+    (SURVEY §7 hard part (iv), §0 D7); returns every rho (mantissas at k bits).
 
     Phase 1 keeps the factors of M - sigma I and iterates y = (M - sigma I)^-1 u
     until the Rayleigh quotient's relative change is below 2^-RQI_SWITCH_BITS
     (or RQI_MAX_PLAIN steps), which pins the iteration to the eigenvalue next to
-    sigma (lambda_1 for sigma <= 0 on a positive definite M).  Phase 2 refactors
-    at sigma = rho every step.  Stop when the relative change is below 2^-(K/2),
-    when rho repeats, or when RQI_STALL changes have failed to go below the
-    smallest change seen so far (the arithmetic noise floor).  factor(strip, x, k) defaults to ldlt_py."""
+    sigma (lambda_1 for sigma <= 0 on a positive definite M).  Phase 2
+    (Rayleigh-quotient iteration) refactors at sigma = rho every step until the
+    relative change is below 2^-rqi_final_bits(K).  Phase 3 keeps those last
+    factors: with sigma that close to lambda_1 every solve gains ~2 x
+    rqi_final_bits bits, for the price of a solve instead of a factorisation.
+    Stop when the relative change is below 2^-(K/2), when rho repeats, or when
+    RQI_STALL changes have failed to go below the smallest change seen so far
+    (the arithmetic noise floor).  factor(strip, x, k) defaults to ldlt_py."""
     factor = factor or (lambda s, x, kk: ldlt_py(s, x, kk, capture=True))
     n, k2 = len(u), k // 2
+    final_bits = rqi_final_bits(k)
     rhos, rho_prev, d_min = [], None, None
-    stall, plain, rqi = 0, 0, False
+    stall, plain, phase = 0, 0, 1
     f = None
     for _ in range(max_iter):
         if f is None:
@@ -403,13 +413,15 @@ def inverse_iteration_py(strip: list[int], k: int, u: list[int], sigma: int = 0,
                     break
             else:
                 d_min = d
-            if not rqi and ((d << RQI_SWITCH_BITS) <= abs(rho) or plain >= RQI_MAX_PLAIN):
-                rqi = True
+            if phase == 1 and ((d << RQI_SWITCH_BITS) <= abs(rho) or plain >= RQI_MAX_PLAIN):
+                phase = 2
+            elif phase == 2 and (d << final_bits) <= abs(rho):
+                phase = 3
         rho_prev = rho
-        plain += not rqi
+        plain += phase == 1
         mb = max(abs(v).bit_length() for v in y)
         sh = mb - k
         u = [tdiv_q_2exp(v, sh) if sh > 0 else v << -sh for v in y]
-        if rqi:
+        if phase == 2:
             sigma, f = rho, None
     return rhos

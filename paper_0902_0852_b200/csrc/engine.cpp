@@ -721,22 +721,29 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     sacc_ = dalloc<uint32_t>((size_t)n * sWa_);
     spair_hdr_ = dalloc<int>(2 * (size_t)n);
     spair_limbs_ = dalloc<uint32_t>(2 * (size_t)n * sWv_);
-    sbits_ = dalloc<int>(1);
-    sys_ = dalloc<int>(4);
     CU(configure_solve_kernels(P.cap, sWv_, sWa_));
   }
   // division plan: the LDL^T plan with integer capacity Wv (k_recip/k_divide
-  // with a per-step divisor, scratch in global memory, no transform)
+  // over pairs (piv_p, z_p 2^k2), scratch in global memory, no transform),
+  // batched over all n pairs on gridDim.y
   DevPlan D2 = dp_;
   D2.n = 2;
   D2.cap = sWv_;
   D2.ycap = sWv_ + k2 / 32 + 8;
   D2.tw_smem = 0;
   D2.grid_cap = 1;
+  D2.bat_vrow = 2;
+  D2.bat_rrow = 1;
+  D2.bat_ys = 4;
+  D2.bat_mb = 1;
+  D2.bat_ybuf = D2.ycap;
+  D2.bat_scr = (long long)recip_scratch_words(D2);
   if (!sybuf_) {
-    sybuf_ = dalloc<uint32_t>(D2.ycap);
-    srscr_ = dalloc<uint32_t>(recip_scratch_words(D2));
-    sdscr_ = dalloc<uint32_t>(divide_smem_words(D2) + 64);
+    sybuf_ = dalloc<uint32_t>((size_t)n * D2.ycap);
+    sys_ = dalloc<int>(4 * (size_t)n);
+    sbits_ = dalloc<int>((size_t)n);
+    srscr_ = dalloc<uint32_t>((size_t)n * D2.bat_scr);
+    sdscr_ = dalloc<uint32_t>((size_t)n * (divide_smem_words(D2) + 64));
   }
   const int Wv = sWv_, Wa = sWa_;
   IntBuf vecs{svhdr_, svlimbs_};
@@ -778,15 +785,13 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                          dp_.grid_cap, err_, st));
     nl += 2;
   }
-  // diagonal: w_p = tdiv(z_p 2^K, piv_p) with the LDL^T division kernels
-  for (int p = 0; p < n; ++p) {
-    CU(launch_int_bits(pairs, 2 * p + 1, Wv, 0, sbits_, st));
-    CU(launch_recip(D2, pairs, 2 * p, sbits_, 0, pairs, 0, sybuf_, sys_,
-                    srscr_, 1, err_, st));
-    CU(launch_divide(D2, pairs, 2 * p, 0, sybuf_, sys_, vecs, Wq + p - 1,
-                     nullptr, nullptr, sdscr_, 1, err_, st));
-    nl += 3;
-  }
+  // diagonal: w_p = tdiv(z_p 2^K, piv_p) with the LDL^T division kernels,
+  // all n independent divisions in one batched launch each
+  CU(launch_int_bits_batch(pairs, 1, 2, Wv, n, sbits_, st));
+  CU(launch_recip_batch(D2, pairs, 0, sbits_, sybuf_, sys_, srscr_, n, err_, st));
+  CU(launch_divide_batch(D2, pairs, 0, sybuf_, sys_, vecs, Wq - 1, sdscr_, n,
+                         err_, st));
+  nl += 3;
   // back: y_r = w_r - tdiv_2exp(acc'_r, k2); acc'_q += R_q[r] y_r (q < r)
   CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
   for (int r = n - 1; r >= 0; --r) {

@@ -6,7 +6,9 @@
 // Fixed point at K fractional bits throughout (K = the matrix precision).
 // Phase 1 (shifted inverse iteration) keeps the factors of M - s_0 I and only
 // re-solves; once the relative change of rho is below 2^-32 (or after 64
-// plain steps) phase 2 (Rayleigh-quotient iteration) refactors at s = rho:
+// plain steps) phase 2 (Rayleigh-quotient iteration) refactors at s = rho;
+// once it is below 2^-max(64, K/16) phase 3 keeps those factors again (each
+// solve then gains ~K/8 bits for the price of a solve, not a factorisation):
 //   factor   M - s_k I = L D L^T          (GPU LDL^T, HGPU_KEEP_L)
 //   solve    (M - s_k I) y = u_k          (GPU triangular solves, exact with
 //                                          one truncation per entry)
@@ -21,6 +23,7 @@
 // A zero last pivot means s_k is an eigenvalue at this precision (as in
 // secant.cpp:36-52); it is returned as is.
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -51,9 +54,11 @@ HostInt to_host(const Z& z) {
 Z from_host(const HostInt& h) { return Z::from_limbs(h.size, h.limbs.data()); }
 
 // phase switch and stall rule (oracle/pyoracle.py RQI_* constants)
-constexpr long kSwitchBits = 32;  // plain steps until relative change < 2^-32
-constexpr long kMaxPlain = 64;    // ... or this many plain steps
+constexpr long kSwitchBits = 32;  // phase 1 -> 2: relative change < 2^-32
+constexpr long kMaxPlain = 64;    // ... or this many phase-1 steps
 constexpr int kStall = 2;         // changes not below the smallest so far
+// phase 2 -> 3: relative change < 2^-final_bits(K)
+long final_bits(long k) { return std::max(64L, k / 16); }
 
 }  // namespace
 }  // namespace hgpu
@@ -80,12 +85,17 @@ extern "C" hgpu_status hgpu_inverse_iteration(
     }
     Z sigma = Z::from_limbs(sigma_size, sigma_limbs);
     Z rho_prev, d_min, rho;
-    bool have_prev = false, have_dmin = false, rqi = false, factored = false;
+    bool have_prev = false, have_dmin = false, factored = false;
+    int phase = 1;
+    const long fbits = final_bits(k);
     int stall = 0;
     long plain = 0;
     std::string tr;
     long it = 0;
+    const bool verbose = std::getenv("HGPU_RQI_TRACE") != nullptr;
+    double t_factor = 0, t_solve = 0;
     for (; it < max_iter; ++it) {
+      auto ta = std::chrono::steady_clock::now();
       if (!factored) {
         std::vector<uint32_t> sl;
         HostInt sx;
@@ -104,6 +114,7 @@ extern "C" hgpu_status hgpu_inverse_iteration(
         }
         factored = true;
       }
+      auto tb = std::chrono::steady_clock::now();
       std::vector<HostInt> uh(n);
       for (long i = 0; i < n; ++i) uh[i] = to_host(u[i]);
       long long nl = 0;
@@ -118,6 +129,17 @@ extern "C" hgpu_status hgpu_inverse_iteration(
       if (den.sgn() == 0) throw Error(HGPU_ERR_INTERNAL, "solve returned zero");
       rho = sigma + tdiv(shl(num, (unsigned long)k), den);
       tr += rho.hex() + "\n";
+      if (verbose) {
+        auto tc = std::chrono::steady_clock::now();
+        const double f = std::chrono::duration<double>(tb - ta).count();
+        const double sv = std::chrono::duration<double>(tc - tb).count();
+        t_factor += f;
+        t_solve += sv;
+        const Z d = rho - rho_prev;
+        std::fprintf(stderr, "rqi it %ld %s factor %.3fs solve %.3fs log2|drho/rho| %ld\n",
+                     it, phase == 1 ? "plain" : phase == 2 ? "rqi" : "final", f, sv,
+                     have_prev ? (long)(d.bits() - rho.bits()) : 0L);
+      }
       if (have_prev) {
         Z d = rho - rho_prev;
         if (d.sgn() < 0) d = Z(0) - d;
@@ -135,13 +157,15 @@ extern "C" hgpu_status hgpu_inverse_iteration(
           d_min = d;
           have_dmin = true;
         }
-        if (!rqi && (cmp(shl(d, (unsigned long)kSwitchBits), a) <= 0 ||
-                     plain >= kMaxPlain))
-          rqi = true;
+        if (phase == 1 && (cmp(shl(d, (unsigned long)kSwitchBits), a) <= 0 ||
+                           plain >= kMaxPlain))
+          phase = 2;
+        else if (phase == 2 && cmp(shl(d, (unsigned long)fbits), a) <= 0)
+          phase = 3;
       }
       rho_prev = rho;
       have_prev = true;
-      if (!rqi) ++plain;
+      if (phase == 1) ++plain;
       // next start vector: y scaled so that max |u_i| lies in [1/2, 1)
       long mb = 0;
       for (long i = 0; i < n; ++i) mb = std::max(mb, y[i].bits());
@@ -149,11 +173,13 @@ extern "C" hgpu_status hgpu_inverse_iteration(
       for (long i = 0; i < n; ++i)
         u[i] = sh > 0 ? tdiv_2exp(y[i], (unsigned long)sh)
                       : shl(y[i], (unsigned long)(-sh));
-      if (rqi) {
+      if (phase == 2) {
         sigma = rho;
         factored = false;
       }
     }
+    if (verbose)
+      std::fprintf(stderr, "rqi total factor %.3fs solve %.3fs\n", t_factor, t_solve);
     if (eigenvalue) {
       if (rho.sgn() <= 0)
         throw Error(HGPU_ERR_PRECISION_EXHAUSTED, "non-positive Rayleigh quotient");

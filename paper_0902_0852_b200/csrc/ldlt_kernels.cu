@@ -317,6 +317,14 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
   extern __shared__ uint32_t sm_dyn[];
   __shared__ uint32_t red[64];
   if (stage_aborted(err)) return;
+  {
+    const int b = blockIdx.y;  // batched instance (0 in the LDL^T)
+    prow += (long long)b * P.bat_vrow;
+    maxbitsV += b * P.bat_mb;
+    Ybuf += b * P.bat_ybuf;
+    ys += b * P.bat_ys;
+    gscratch += b * P.bat_scr;
+  }
   const int h = vint.hdr[prow];
   const int nD = h < 0 ? -h : h;
   if (nD == 0) return;  // flagged as ZeroPivot by k_extract
@@ -457,6 +465,14 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   const int cap = P.cap, ycap = P.ycap;
   const long long span = div_span_words(cap, ycap);
   const long long cta_words = span + div_extra_words(P);
+  {
+    const int b = blockIdx.y;  // batched instance (0 in the LDL^T)
+    vrow0 += (long long)b * P.bat_vrow;
+    rrow0 += (long long)b * P.bat_rrow;
+    Ybuf += b * P.bat_ybuf;
+    ys += b * P.bat_ys;
+    gscratch += (long long)b * gridDim.x * cta_words;
+  }
   uint32_t* tab = sm_dyn;
   uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * cta_words
                               : sm_dyn + (P.tw_smem ? P.NW : 0);
@@ -948,6 +964,32 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
   k_recip<<<1, recip_threads(), smem, st>>>(P, vint, prow, maxbitsV, p, piv,
                                             dmax_bits, Ybuf, ys, scratch,
                                             use_gscratch, err);
+  return post_launch(st);
+}
+
+cudaError_t launch_recip_batch(const DevPlan& P, IntBuf vint, long long prow,
+                               const int* maxbitsV, uint32_t* Ybuf, int* ys,
+                               uint32_t* scratch, int batch, int* err,
+                               cudaStream_t st) {
+  if (batch <= 0) return cudaSuccess;
+  ++g_launches;
+  k_recip<<<dim3(1, batch), recip_threads(), 0, st>>>(
+      P, vint, prow, maxbitsV, 0, IntBuf{nullptr, nullptr}, 0, Ybuf, ys,
+      scratch, 1, err);
+  return post_launch(st);
+}
+
+cudaError_t launch_divide_batch(const DevPlan& P, IntBuf vint,
+                                long long vrow0, const uint32_t* Ybuf,
+                                const int* ys, IntBuf rint, long long rrow0,
+                                uint32_t* gscratch, int batch, int* err,
+                                cudaStream_t st) {
+  if (batch <= 0 || P.n - 1 <= 0) return cudaSuccess;
+  ++g_launches;
+  k_divide<<<dim3(min(P.n - 1, P.grid_cap), batch), 256,
+             (size_t)(P.tw_smem ? P.NW : 0) * 4, st>>>(
+      P, vint, vrow0, 0, Ybuf, ys, rint, rrow0, nullptr, nullptr, gscratch, 1,
+      err);
   return post_launch(st);
 }
 

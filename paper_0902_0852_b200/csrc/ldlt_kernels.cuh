@@ -67,6 +67,11 @@ struct DevPlan {
   int tw_smem;          // 1: kernels stage the Montgomery tables in SMEM
   int grid_cap;         // CTAs for grid-stride row kernels
   int debug;            // HGPU_DEBUG bits (bisection aid), 0 in production
+  // batched division (the triangular solve's diagonal): instance b =
+  // blockIdx.y offsets its rows, reciprocal and scratch by b * these strides
+  // (all 0 in the LDL^T, where gridDim.y == 1)
+  int bat_vrow, bat_rrow, bat_ys, bat_mb;
+  long long bat_ybuf, bat_scr;
 };
 
 struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
@@ -104,6 +109,16 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          uint32_t* Ybuf, int* ys, uint32_t* scratch,
                          int use_gscratch, int* err, cudaStream_t st);
 size_t divide_smem_words(const DevPlan& P);
+// gridDim.y = batch independent reciprocal / division instances (P.bat_*)
+cudaError_t launch_recip_batch(const DevPlan& P, IntBuf vint, long long prow,
+                               const int* maxbitsV, uint32_t* Ybuf, int* ys,
+                               uint32_t* scratch, int batch, int* err,
+                               cudaStream_t st);
+cudaError_t launch_divide_batch(const DevPlan& P, IntBuf vint,
+                                long long vrow0, const uint32_t* Ybuf,
+                                const int* ys, IntBuf rint, long long rrow0,
+                                uint32_t* gscratch, int batch, int* err,
+                                cudaStream_t st);
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, const uint32_t* Ybuf, const int* ys,
                           IntBuf rint, long long rrow0, uint32_t* rhat,
@@ -133,8 +148,8 @@ cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
                                 IntBuf base, int bi, IntBuf out, int oi,
                                 IntBuf out2, int o2i, int shift_out, int* err,
                                 cudaStream_t st);
-cudaError_t launch_int_bits(IntBuf v, int idx, int stride, int k2, int* out,
-                            cudaStream_t st);
+cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
+                                  int count, int* out, cudaStream_t st);
 cudaError_t configure_solve_kernels(int cap, int Wv, int Wa);
 // fold_kernels.cu
 long long fold_pivots_device(const uint32_t* plimbs, const int* plen, int n,

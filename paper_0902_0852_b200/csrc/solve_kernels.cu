@@ -146,12 +146,16 @@ __global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
   }
 }
 
-// bits of a signed limb integer (for the reciprocal's precision)
-__global__ void k_int_bits(IntBuf v, int idx, int stride, int k2, int* out) {
-  if (threadIdx.x != 0) return;
+// bits of the signed limb integers idx0 + b*step, b < count (the
+// reciprocal's precision bound for each batched division)
+__global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
+                           int* out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= count) return;
+  const long long idx = idx0 + (long long)b * step;
   const int h = v.hdr[idx];
   const int n = h < 0 ? -h : h;
-  *out = n == 0 ? 0 : limbs_bits(v.limbs + (long long)idx * stride, n) + k2;
+  out[b] = n == 0 ? 0 : limbs_bits(v.limbs + idx * stride, n);
 }
 
 size_t solve_axpy_smem_words(int cap, int Wv) {
@@ -182,9 +186,11 @@ cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
   return cudaGetLastError();
 }
 
-cudaError_t launch_int_bits(IntBuf v, int idx, int stride, int k2, int* out,
-                            cudaStream_t st) {
-  k_int_bits<<<1, 32, 0, st>>>(v, idx, stride, k2, out);
+cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
+                                  int count, int* out, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  k_int_bits<<<(count + 127) / 128, 128, 0, st>>>(v, idx0, step, stride, count,
+                                                  out);
   return cudaGetLastError();
 }
 
