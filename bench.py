@@ -210,6 +210,22 @@ def run_gpu(args) -> None:
         del mm
     e2e_step = statistics.median(e2e_ms)
 
+    # time to lambda_min (north-star): inverse iteration with Rayleigh-quotient
+    # refactorisation from the seed-0 start vector, x = 0, to the 2^-(P/2)
+    # rule, through the public API (single rank: the solve is not sharded)
+    lam = None
+    if world == 1 and not args.no_lambda:
+        barrier()
+        t0 = time.perf_counter()
+        mm = hgpu.HankelMatrixGPU(strip, k, device=local)
+        rq = hgpu.inverse_iteration(mm, hgpu.seeded_start_vector(n, k), 0, 40, digits=40)
+        barrier()
+        lam = {"seconds": time.perf_counter() - t0, "iterations": rq["iterations"],
+               "lambda_min": rq["eigenvalue"], "digits": 40,
+               "method": "shifted inverse iteration + RQI on the GPU LDL^T (hgpu_inverse_iteration)",
+               "includes": "strip upload, every factorisation and triangular solve"}
+        del mm
+
     # roofline of the dominant kernel (trailing update): modular products per
     # launch / average launch time, against the measured IMAD.WIDE rate
     probe = probe_imad()
@@ -239,6 +255,12 @@ def run_gpu(args) -> None:
         "imad_probe": probe,
         "clocks": clk,
     }
+    if lam:
+        out["time_to_lambda_min"] = lam
+    traffic = _profiled_traffic()
+    if traffic:
+        out["roofline"]["traffic"] = traffic["dram_bytes_per_launch"]
+        out["roofline"]["traffic_source"] = traffic["source"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
@@ -246,6 +268,19 @@ def run_gpu(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def _profiled_traffic():
+    """dram bytes per k_update_tiled launch from the committed ncu --set full
+    summary (profiles/*/k_update_full.json), if present."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "k_update_full.json")))
+    if not files:
+        return None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"),
+            "source": os.path.relpath(files[-1], ROOT)}
 
 
 def probe_imad() -> dict:
@@ -331,6 +366,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lambda", action="store_true",
+                    help="skip the time-to-lambda_min measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

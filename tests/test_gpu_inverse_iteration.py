@@ -100,3 +100,25 @@ def test_config3_time_to_lambda(hg):
           got["eigenvalue"])
     assert got["eigenvalue"].startswith("1.0892427421041")
     assert got["eigenvalue"].endswith("e-52")
+
+
+def test_config2_full_size_certified_digits(hg):
+    """BASELINE config 2 (N=300, beta=7/4, P=4096) at its own precision, where
+    the secant stalls (test_gpu_fold_secant): the GPU inverse iteration ends on
+    the restatement's final Rayleigh quotient bit for bit, and its 40 digits
+    are the ones the reference's interval LDL^T certified at 12288 bits
+    (tests/golden/make_lambda_certified.py)."""
+    fx = {d["name"]: d for d in json.load(open(os.path.join(GOLDEN, "lambda_certified.json")))}
+    for name in ("config1", "config2"):
+        d = fx[name]
+        n, k = d["n"], d["frac_bits"]
+        if name == "config1":
+            strip = po.exact_strip(n, 1, 1, k)
+        else:
+            g = json.load(open(os.path.join(GOLDEN, "config2_strip.json")))
+            strip = [int(v, 16) for v in g["strip"]]
+        got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), hg.seeded_start_vector(n, k), 0, 40,
+                                   digits=40)
+        assert po.to_hex(got["rho"][-1]) == d["rho_last"]
+        assert got["iterations"] == d["iterations"]
+        assert got["eigenvalue"] == d["lambda_40"]
