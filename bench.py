@@ -261,6 +261,8 @@ def run_gpu(args) -> None:
     if traffic:
         out["roofline"]["traffic"] = traffic["dram_bytes_per_launch"]
         out["roofline"]["traffic_source"] = traffic["source"]
+        # the same kernel profiled alone: IMAD.WIDE (FMA-heavy) pipe busy %
+        out["roofline"]["ncu_imad_pipe_frac_alone"] = (traffic["pipe_pct"] or 0) / 100 or None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
@@ -280,6 +282,7 @@ def _profiled_traffic():
     with open(files[-1]) as f:
         d = json.load(f)
     return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"),
+            "pipe_pct": d.get("sm_pipe_fmaheavy_pct_of_peak_elapsed"),
             "source": os.path.relpath(files[-1], ROOT)}
 
 

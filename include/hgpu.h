@@ -112,10 +112,12 @@ void hgpu_string_free(char* s);
 /* Smallest eigenvalue by inverse iteration with Rayleigh-quotient shifts
  * (the north-star's lambda_min step; no reference counterpart -- SURVEY §0
  * D1 -- and pinned against oracle/pyoracle.py:inverse_iteration_py).  Each
- * step factors M - s_k I on the GPU (HGPU_KEEP_L), solves (M - s_k I) y = u_k
- * with the L, D factors (forward and back triangular solves, exact with one
- * truncation per entry), sets rho_k = s_k + (y.u_k)/(y.y) and stops when the
- * relative change of rho is below 2^-(frac_bits/2) or stalls.  u: n signed
+ * step solves (M - s I) y = u_k with the GPU L, D factors of M - s I
+ * (HGPU_KEEP_L; forward and back triangular solves, exact with one
+ * truncation per entry) and sets rho_k = s + (y.u_k)/(y.y).  Phase 1 keeps
+ * s = sigma until rho's relative change is < 2^-32, phase 2 refactors at
+ * s = rho_k each step until it is < 2^-max(64, frac_bits/16), phase 3 keeps
+ * those factors; stop when the change is below 2^-(frac_bits/2) or stalls.  u: n signed
  * limb vectors at frac_bits (e.g. the seed-0 uniform[-1,1] start vector);
  * sigma: the first shift (0 is fine).  Outputs as for
  * hgpu_smallest_eigenvalue; `trace` lists every rho_k in hex. */
