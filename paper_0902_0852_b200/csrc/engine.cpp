@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -468,6 +469,28 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
 
   // slot set of panel b: rows [set*kb*n, ...) of Vint/Rint/Vhat/Rhat
   auto set_row0 = [&](int b) { return (long long)(b % 2) * kb * n; };
+  const char* tl_path = std::getenv("HGPU_TIMELINE");
+  tl_.clear();
+  tl_used_ = 0;
+  // kinds: 0 col(pivot) 1 extract(pivot) 2 recip 3 col(rest) 4 extract(rest)
+  //        5 divide 6 col(all) 7 extract(all) 8 update(next panel) 9 update(rest)
+  auto TL = [&](int kind, int p, cudaStream_t s, auto&& launch) {
+    if (!tl_path) {
+      CU(launch());
+      return;
+    }
+    while (tl_pool_.size() < tl_used_ + 2) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      tl_pool_.push_back(e);
+    }
+    cudaEvent_t a = tl_pool_[tl_used_], b = tl_pool_[tl_used_ + 1];
+    tl_used_ += 2;
+    CU(cudaEventRecord(a, s));
+    CU(launch());
+    CU(cudaEventRecord(b, s));
+    tl_.push_back({kind, p, a, b});
+  };
   auto timed_update = [&](int b, int nslots, int c_begin, int c_end) {
     if (c_begin >= c_end || nslots <= 0) return;
     if (profile) {
@@ -479,8 +502,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       CU(cudaEventRecord(uev_[uev_used], st));
     }
     const long long r0 = set_row0(b);
-    CU(launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW, rhat_ + r0 * NW,
-                     slot_stride, nslots, c_begin, c_end, err_, st));
+    TL(c_begin == b * kb + kb ? 8 : 9, b, st, [&] {
+      return launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW,
+                           rhat_ + r0 * NW, slot_stride, nslots, c_begin, c_end,
+                           err_, st);
+    });
     if (profile) {
       CU(cudaEventRecord(uev_[uev_used + 1], st));
       uev_used += 2;
@@ -551,35 +577,55 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           // critical chain on the helper stream: pivot entry -> D = V_p[p]
           // -> reciprocal (precision from the PD bound), overlapping the
           // update and extraction of the other rows on the panel stream
-          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p, p,
-                               p + 1, err_, sp));
+          TL(0, p, sp, [&] {
+            return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                     p, p, p + 1, err_, sp);
+          });
           CU(cudaEventRecord(sev_[2 * p], sp));
           CU(cudaStreamWaitEvent(sh, sev_[2 * p], 0));
-          CU(launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0, piv,
-                            maxbitsV, vhat_, maxdegV, err_, sh));
-          CU(launch_recip(D, vint, row0 + p, maxbitsV, p, piv, dmax_bits_,
-                          ybuf_, ys_, rscratch_, recip_global_ ? 1 : 0, err_,
-                          sh));
+          TL(1, p, sh, [&] {
+            return launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0,
+                                  piv, maxbitsV, vhat_, maxdegV, err_, sh);
+          });
+          TL(2, p, sh, [&] {
+            return launch_recip(D, vint, row0 + p, maxbitsV, p, piv,
+                                dmax_bits_, ybuf_, ys_, rscratch_,
+                                recip_global_ ? 1 : 0, err_, sh);
+          });
           CU(cudaEventRecord(sev_[2 * p + 1], sh));
-          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p,
-                               p + 1, n, err_, sp));
-          CU(launch_extract(D, W_, colbase_, p, p + 1, n, vint, row0, piv,
-                            maxbitsV, vhat_, maxdegV, err_, sp));
+          TL(3, p, sp, [&] {
+            return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                     p, p + 1, n, err_, sp);
+          });
+          TL(4, p, sp, [&] {
+            return launch_extract(D, W_, colbase_, p, p + 1, n, vint, row0,
+                                  piv, maxbitsV, vhat_, maxdegV, err_, sp);
+          });
           CU(cudaStreamWaitEvent(sp, sev_[2 * p + 1], 0));
         } else {
           // left-looking inside the panel: column p receives stages [p0, p)
-          CU(launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s, p, p,
-                               n, err_, sp));
+          TL(6, p, sp, [&] {
+            return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                     p, p, n, err_, sp);
+          });
           // W[r][p] -> V_p[r] (+ its transform for rows r > p)
-          CU(launch_extract(D, W_, colbase_, p, p, n, vint, row0, piv,
-                            maxbitsV, vhat_, maxdegV, err_, sp));
+          TL(7, p, sp, [&] {
+            return launch_extract(D, W_, colbase_, p, p, n, vint, row0, piv,
+                                  maxbitsV, vhat_, maxdegV, err_, sp);
+          });
           if (p == n - 1) break;
-          CU(launch_recip(D, vint, row0 + p, maxbitsV, p, piv, 0, ybuf_, ys_,
-                          rscratch_, recip_global_ ? 1 : 0, err_, sp));
+          TL(2, p, sp, [&] {
+            return launch_recip(D, vint, row0 + p, maxbitsV, p, piv, 0, ybuf_,
+                                ys_, rscratch_, recip_global_ ? 1 : 0, err_,
+                                sp);
+          });
         }
         // R_p[r] (+ its Montgomery-form transform)
-        CU(launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, rhat_,
-                         maxdegR + p, dscratch_, div_global_ ? 1 : 0, err_, sp));
+        TL(5, p, sp, [&] {
+          return launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, rhat_,
+                               maxdegR + p, dscratch_, div_global_ ? 1 : 0,
+                               err_, sp);
+        });
       }
     }
     panel_broadcast(owner, p0, ns, row0set, sp);
@@ -646,6 +692,18 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, ev0_, ev1_));
   res.device_ms = ms;
+  if (tl_path) {
+    if (FILE* f = std::fopen(tl_path, "a")) {
+      std::fprintf(f, "# factorisation n=%d K=%d device_ms=%.3f\n", n, K_, ms);
+      for (const TlRec& t : tl_) {
+        float a = 0, b2 = 0;
+        CU(cudaEventElapsedTime(&a, ev0_, t.a));
+        CU(cudaEventElapsedTime(&b2, ev0_, t.b));
+        std::fprintf(f, "%d,%d,%.4f,%.4f\n", t.kind, t.p, a, b2);
+      }
+      std::fclose(f);
+    }
+  }
   if (profile) {
     for (size_t i = 0; i < uev_used; i += 2) {
       float t = 0;

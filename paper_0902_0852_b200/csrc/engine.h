@@ -141,6 +141,14 @@ class Matrix {
   int* sys_ = nullptr;
   int dmax_bits_ = 0;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+  // HGPU_TIMELINE=<file>: per-launch start/end events (scheduling analysis)
+  struct TlRec {
+    int kind, p;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> tl_pool_;
+  std::vector<TlRec> tl_;
+  size_t tl_used_ = 0;
   std::vector<cudaEvent_t> uev_;
 };
 
