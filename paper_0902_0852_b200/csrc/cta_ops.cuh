@@ -312,8 +312,9 @@ __device__ __forceinline__ uint32_t cf_of(int64_t v, int bits) {
 }
 
 // Resolves sum_{k<M} v_k 2^{bits k} into digits d_k in [0, 2^bits), where
-// getv(k) returns v_k in [-2^bits + 1, 3*2^bits - 2] (int64).  putd(k, d)
-// receives every digit.  Returns the final carry (in {-1,0,1,2}) to all
+// getv(k) returns v_k in [-2^bits + 1, 3*2^bits - 2] (int64), bits <= 48.
+// putd(k, d) receives every digit (uint64_t; callers with bits <= 32 may
+// take it as uint32_t).  Returns the final carry (in {-1,0,1,2}) to all
 // threads: the exact value is sum d_k 2^{bits k} + carry 2^{bits M}.
 // `red` needs blockDim.x/32 words.  getv must not read what putd writes.
 template <class GetV, class PutD>
@@ -331,7 +332,7 @@ __device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
   const int64_t mask = (int64_t(1) << bits) - 1;
   for (int k = k0; k < k1; ++k) {
     const int64_t v = getv(k) + c;
-    putd(k, (uint32_t)(v & mask));
+    putd(k, (uint64_t)(v & mask));  // bits <= 48: digits may exceed 32 bits
     c = (int)floor_shift(v, bits);
   }
   __syncthreads();  // digits visible to every thread on return

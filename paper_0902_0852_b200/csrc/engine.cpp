@@ -79,7 +79,7 @@ int block_owner(long block, int world) {
 Plan choose_plan(int n, int K, int bits, int min_logL) {
   Plan best;
   long long best_cost = LLONG_MAX;
-  for (int np = 2; np <= 3; ++np) {
+  for (int np = 2; np <= 4; ++np) {
     u128 Q = 1;
     for (int j = 0; j < np; ++j) Q *= kPrimes[j];
     const double log2_quarter = log2_u128(Q) - 2.0;
@@ -87,7 +87,7 @@ Plan choose_plan(int n, int K, int bits, int min_logL) {
       const int L = 1 << logL;
       // L digits of w bits must hold any product, with two digits spare
       const int w = (bits + 1 + (L - 2) - 1) / (L - 2);
-      if (w > 26) continue;
+      if (w > 48) continue;  // digits are handled in 64-bit words
       if (w < 4) continue;
       // n stages x (L/2 overlapping terms) x (2^w-1)^2 (+ slack) < Q/4
       const double lb = std::log2((double)n + 1) + std::log2((double)L / 2 + 1) +
@@ -108,7 +108,10 @@ Plan choose_plan(int n, int K, int bits, int min_logL) {
     throw Error(HGPU_ERR_CAPACITY, "no transform plan fits the value sizes");
   best.n = n;
   best.K = K;
+  // pieces of a CRT coefficient (32*np-bit two's complement): one spare for
+  // the sign, but the top piece's shift must stay inside the 128-bit value
   best.T = (32 * best.np + best.w - 1) / best.w + 1;
+  if (best.w * (best.T - 1) >= 128) --best.T;
   best.cap = (best.w * (best.L + best.T) + 31) / 32 + 2;
   best.ycap = best.cap + (K / 2) / 32 + 8;
   return best;
@@ -249,6 +252,7 @@ void Matrix::build(int min_logL) {
     c.r32 = (uint32_t)((1ULL << 32) % q);
     c.r32s = shoup_companion(c.r32, (uint32_t)q);
     c.r64 = (uint32_t)((u128)c.r32 * c.r32 % q);
+    c.one_s = shoup_companion(1u, (uint32_t)q);
     const u64 il = invmod(P.L, q);
     D.invL[j] = (uint32_t)il;
     D.invLp[j] = shoup_companion((uint32_t)il, (uint32_t)q);
@@ -261,6 +265,18 @@ void Matrix::build(int min_logL) {
   D.q0m2 = (uint32_t)(q0 % q2);
   D.q0m2p = shoup_companion(D.q0m2, (uint32_t)q2);
   D.q01 = q0 * q1;
+  if (P.np == 4) {
+    const u64 q3 = kPrimes[3];
+    const u128 q012 = (u128)q0 * q1 * q2;
+    D.g3 = (uint32_t)invmod((u64)(q012 % q3), q3);
+    D.g3p = shoup_companion(D.g3, (uint32_t)q3);
+    D.q0m3 = (uint32_t)(q0 % q3);
+    D.q0m3p = shoup_companion(D.q0m3, (uint32_t)q3);
+    D.q01m3 = (uint32_t)((u128)q0 * q1 % q3);
+    D.q01m3p = shoup_companion(D.q01m3, (uint32_t)q3);
+    D.q012lo = (u64)q012;
+    D.q012hi = (u64)(q012 >> 64);
+  }
   u128 Q = 1;
   for (int j = 0; j < P.np; ++j) Q *= kPrimes[j];
   const u128 H = (Q + 1) / 2;

@@ -61,12 +61,26 @@ __device__ void transform_int(const DevPlan& P, const uint32_t* mag, int len,
   if (bits > (long long)P.w * P.L) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapDigits);
   }
-  const uint32_t dmask = (1u << P.w) - 1u;
+  const uint64_t dmask = (1ull << P.w) - 1ull;
   for (int gi = threadIdx.x; gi < P.NW; gi += blockDim.x) {
     const int j = gi >> P.logL, i = gi & (P.L - 1);
-    const uint32_t q = P.pc[j].q;
-    const uint32_t d = field32(mag, len, (long long)P.w * i + shift) & dmask;
-    sm[gi] = (sign < 0 && d) ? q - d : d;
+    const PrimeConsts& c = P.pc[j];
+    const long long off = (long long)P.w * i + shift;
+    const uint64_t d = ((uint64_t)field32(mag, len, off) |
+                        ((uint64_t)field32(mag, len, off + 32) << 32)) & dmask;
+    // d mod q: d = dh 2^32 + dl, dh 2^32 = dh r32 (Shoup), dl = dl * 1 (Shoup)
+    uint32_t rr;
+    if (P.w <= 27) {
+      rr = (uint32_t)d;  // < 2^27 < q
+    } else {
+      const uint32_t dl = (uint32_t)d, dh = (uint32_t)(d >> 32);
+      rr = reduce_2q(mul_shoup(dl, 1u, c.one_s, c.q), c.q);
+      if (dh) {
+        rr += reduce_2q(mul_shoup(dh, c.r32, c.r32s, c.q), c.q);
+        rr = reduce_2q(rr, c.q);
+      }
+    }
+    sm[gi] = (sign < 0 && rr) ? c.q - rr : rr;
   }
   __syncthreads();
   cta_ntt_fwd16(sm, P.np, P.logL, twm, P.pc);
@@ -146,14 +160,14 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
   uint32_t* tabf = sm;
   uint32_t* tabi = sm + (P.tw_smem ? P.NW : 0);
   uint32_t* A = tabi + (P.tw_smem ? P.NW : 0);  // np*L residues -> CRT words
-  int* S = (int*)(A + P.NW);                     // M digit sums
-  uint32_t* Dg = A + P.NW + M;                   // M digits
-  uint32_t* Lb = Dg + M;                         // cap limbs of |W|
-  uint32_t* red = Lb + P.cap;                    // scan scratch
+  int64_t* S = reinterpret_cast<int64_t*>(A + P.NW);  // M digit sums
+  uint64_t* Dg = reinterpret_cast<uint64_t*>(S + M);  // M digits
+  uint32_t* Lb = reinterpret_cast<uint32_t*>(Dg + M); // cap limbs of |W|
+  uint32_t* red = Lb + P.cap;                         // scan scratch
   const uint32_t* twm;
   const uint32_t* itwm;
   stage_tables(P, tabf, tabi, &twm, &itwm);
-  const uint32_t dmask = (1u << w) - 1u;
+  const uint64_t dmask = (1ull << w) - 1ull;
 
   for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
     const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
@@ -176,7 +190,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
       const uint32_t x1 =
           reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
       unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
-      if (np == 3) {
+      if (np >= 3) {
         const uint32_t q2 = P.pc[2].q;
         const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
         uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
@@ -184,6 +198,21 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
         const uint32_t x2 =
             reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
         v += (unsigned __int128)x2 * P.q01;
+        if (np == 4) {
+          // x3 = (a3 - (x0 + x1 q0 + x2 q0 q1)) (q0 q1 q2)^-1  mod q3
+          const uint32_t q3 = P.pc[3].q;
+          const uint32_t x0m3 = x0 >= q3 ? x0 - q3 : x0;
+          const uint32_t x2m3 = x2 >= q3 ? x2 - q3 : x2;
+          uint32_t u3 = x0m3 + reduce_2q(mul_shoup(x1, P.q0m3, P.q0m3p, q3), q3);
+          u3 = reduce_2q(u3, q3);
+          u3 += reduce_2q(mul_shoup(x2m3, P.q01m3, P.q01m3p, q3), q3);
+          u3 = reduce_2q(u3, q3);
+          const uint32_t x3 =
+              reduce_2q(mul_shoup(a[3] + q3 - u3, P.g3, P.g3p, q3), q3);
+          const unsigned __int128 q012 =
+              ((unsigned __int128)P.q012hi << 64) | P.q012lo;
+          v += (unsigned __int128)x3 * q012;
+        }
       }
       const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
       const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
@@ -197,7 +226,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
     // thread owns 8 consecutive positions and decodes each coefficient that
     // reaches them once (8+T-1 decodes instead of 8T).
     for (int k0 = threadIdx.x * 8; k0 < M; k0 += blockDim.x * 8) {
-      int acc8[8];
+      int64_t acc8[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc8[u] = 0;
       const int ilo = max(0, k0 - T + 1), ihi = min(L - 1, k0 + 7);
@@ -211,7 +240,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
           const int t = k0 + u - i;  // piece index landing on position k0+u
           if (t < 0 || t >= T) continue;
           const __int128 sh = c >> (w * t);
-          acc8[u] += (t == T - 1) ? (int)sh : (int)((uint32_t)sh & dmask);
+          acc8[u] += (t == T - 1) ? (int64_t)sh : (int64_t)((uint64_t)sh & dmask);
         }
       }
 #pragma unroll
@@ -231,7 +260,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
             if (k > 0) vv += ((int64_t)sg * S[k - 1]) >> w;
             return vv;
           },
-          [&](int k, uint32_t d) { Dg[k] = d; }, red);
+          [&](int k, uint64_t d) { Dg[k] = d; }, red);
       if (carry >= 0) break;
       sg = -1;  // negative: resolve the magnitude instead
     }
@@ -239,15 +268,16 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
       if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapCrt);
       return;
     }
-    // Pack base-2^w digits into 32-bit limbs of |W|.
-    const int nl = min(P.cap, (w * M + 31) / 32);
+    // Pack base-2^w digits into 32-bit limbs of |W| (only the low 32 bits of
+    // each shifted digit matter, so u64 wrap-around is harmless).
+    const int nl = min(P.cap, (int)(((long long)w * M + 31) / 32));
     for (int m = threadIdx.x; m < P.cap; m += blockDim.x) {
       uint64_t acc = 0;
       if (m < nl) {
         const int first = (32 * m) / w;
         for (int k = first; k < M && (long long)w * k < 32LL * m + 32; ++k) {
           const int shl = w * k - 32 * m;
-          acc |= shl >= 0 ? ((uint64_t)Dg[k] << shl) : ((uint64_t)Dg[k] >> -shl);
+          acc |= shl >= 0 ? (Dg[k] << shl) : (Dg[k] >> -shl);
         }
       }
       Lb[m] = (uint32_t)acc;
@@ -868,9 +898,9 @@ k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
 __global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
                            int nstages, int* err) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  long double bound = 2.0L * (long double)(1u << P.w);
-  const long double dig2 = ((long double)((1u << P.w) - 1)) *
-                           ((long double)((1u << P.w) - 1));
+  const long double dig = (long double)((1ull << P.w) - 1ull);
+  long double bound = 2.0L * (dig + 1.0L);
+  const long double dig2 = dig * dig;
   for (int p = 0; p < nstages; ++p) {
     const int dv = maxdegV[p], dr = maxdegR[p];
     if (dv < 0 || dr < 0) continue;
@@ -922,7 +952,7 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
 
 size_t extract_smem_bytes(const DevPlan& P) {
   const int M = P.L + P.T;
-  return (size_t)((P.tw_smem ? 2 * P.NW : 0) + P.NW + 2 * M + P.cap + 64) * 4;
+  return (size_t)((P.tw_smem ? 2 * P.NW : 0) + P.NW + 4 * M + P.cap + 64) * 4;
 }
 
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,

@@ -44,7 +44,7 @@ struct DevPlan {
   int k2;       // K/2
   int np;       // primes in use (2 or 3)
   int logL, L;  // transform length
-  int w;        // digit width in bits
+  int w;        // digit width in bits (<= 48)
   int T;        // w-bit pieces per reconstructed coefficient
   int cap;      // limbs per stored integer
   int ycap;     // limbs of the per-stage reciprocal
@@ -57,6 +57,11 @@ struct DevPlan {
   uint32_t g2, g2p;          // (q0 q1)^-1 mod q2
   uint32_t q0m2, q0m2p;      // q0 mod q2
   unsigned long long q01;    // q0*q1
+  // fourth prime (np == 4)
+  uint32_t g3, g3p;          // (q0 q1 q2)^-1 mod q3
+  uint32_t q0m3, q0m3p;      // q0 mod q3
+  uint32_t q01m3, q01m3p;    // q0 q1 mod q3
+  unsigned long long q012lo, q012hi;  // q0 q1 q2 (128-bit)
   unsigned long long Qlo, Qhi, Hlo, Hhi;  // Q and Q/2 (128-bit)
   const uint32_t* tw;   // [np][Lmax]
   const uint32_t* twp;

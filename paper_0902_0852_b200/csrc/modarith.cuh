@@ -21,6 +21,7 @@ struct PrimeConsts {
   uint32_t r32;    // 2^32 mod q
   uint32_t r32s;   // Shoup companion of r32
   uint32_t r64;    // 2^64 mod q (Montgomery form of r32)
+  uint32_t one_s;  // Shoup companion of 1 (x mod q = mul_shoup(x, 1, one_s))
 };
 
 __host__ __device__ __forceinline__ uint32_t shoup_companion(uint32_t w,
