@@ -176,13 +176,14 @@ void Matrix::release() {
                   (void*)x_hdr_, (void*)x_limbs_, (void*)vhdr_, (void*)vlimbs_,
                   (void*)rhdr_, (void*)rlimbs_, (void*)vhat_, (void*)rhat_,
                   (void*)phdr_, (void*)plimbs_, (void*)ybuf_, (void*)rscratch_,
-                  (void*)dscratch_, (void*)ys_, (void*)stats_, (void*)err_})
+                  (void*)dscratch_, (void*)dscratch2_, (void*)ys_,
+                  (void*)stats_, (void*)err_})
     dfree(p);
   tw_ = W_ = that_ = xhat_ = nullptr;
   colbase_ = nullptr;
   strip_hdr_ = x_hdr_ = vhdr_ = rhdr_ = phdr_ = ys_ = stats_ = err_ = nullptr;
   strip_limbs_ = x_limbs_ = vlimbs_ = rlimbs_ = vhat_ = rhat_ = plimbs_ =
-      ybuf_ = rscratch_ = dscratch_ = nullptr;
+      ybuf_ = rscratch_ = dscratch_ = dscratch2_ = nullptr;
   plan_ = Plan{};
 }
 
@@ -392,11 +393,15 @@ void Matrix::build(int min_logL) {
   rhat_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * NW);
   phdr_ = dalloc<int>(n_);
   plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
-  ybuf_ = dalloc<uint32_t>(P.ycap);
-  ys_ = dalloc<int>(2);
+  // reciprocal of stage p in set p & 1: recip(p+1) may run while the bulk
+  // division of stage p still reads Y_p
+  ybuf_ = dalloc<uint32_t>(2 * (size_t)P.ycap);
+  ys_ = dalloc<int>(8);
   rscratch_ = dalloc<uint32_t>(recip_scratch_words(D));
-  if (div_global_)
+  if (div_global_) {
     dscratch_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
+    dscratch2_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
+  }
   stats_ = dalloc<int>(3 * (size_t)n_);
 }
 
@@ -555,7 +560,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     flush();
   };
 
-  while ((int)sev_.size() < 2 * n) {
+  while ((int)sev_.size() < 4 * n + 4) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     sev_.push_back(e);
@@ -580,35 +585,51 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
     const long long row0set = set_row0(b);
-    // ---- panel b on the high-priority stream
+    // ---- panel b on the high-priority streams
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
     if (b >= 2) CU(cudaStreamWaitEvent(sp, trail_done[b - 2], 0));
     if (owner == rank_) {
+      // Per stage p two chains run concurrently:
+      //   sh (critical): col(pivot p) -> extract(pivot p) -> recip(p) ->
+      //                  R_p[p+1] (one row)          [-> stage p+1 pivot]
+      //   sp (bulk):     col(rest p) -> extract(rest p) -> R_p[r >= p+2]
+      // Events (per stage): sev_[4p] extract(rest p) done, sev_[4p+1]
+      // recip(p) done, sev_[4p+2] bulk divide(p) done, sev_[4p+3] chain done.
+      bool chain_started = false;
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
         const long long row0 = row0set + (long long)s * n;
         const uint32_t* vh = vhat_ + row0set * NW;
         const uint32_t* rh = rhat_ + row0set * NW;
+        uint32_t* yb = ybuf_ + (size_t)(p & 1) * P.ycap;
+        int* yss = ys_ + (p & 1) * 4;
         if (recip_bound_ && p < n - 1) {
-          // critical chain on the helper stream: pivot entry -> D = V_p[p]
-          // -> reciprocal (precision from the PD bound), overlapping the
-          // update and extraction of the other rows on the panel stream
-          TL(0, p, sp, [&] {
+          if (!chain_started) {
+            // the helper stream enters the panel where the panel stream is
+            CU(cudaEventRecord(sev_[4 * n], sp));
+            CU(cudaStreamWaitEvent(sh, sev_[4 * n], 0));
+            chain_started = true;
+          } else {
+            // pivot entry of column p needs V_{p-1}[p] (extract(rest p-1))
+            // and R_{p-2}[p] (bulk divide(p-2)); R_{p-1}[p] is on sh already
+            CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 1)], 0));
+            if (p - 2 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 2) + 2], 0));
+          }
+          TL(0, p, sh, [&] {
             return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                     p, p, p + 1, err_, sp);
+                                     p, p, p + 1, err_, sh);
           });
-          CU(cudaEventRecord(sev_[2 * p], sp));
-          CU(cudaStreamWaitEvent(sh, sev_[2 * p], 0));
           TL(1, p, sh, [&] {
             return launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0,
                                   piv, maxbitsV, vhat_, maxdegV, err_, sh);
           });
           TL(2, p, sh, [&] {
             return launch_recip(D, vint, row0 + p, maxbitsV, p, piv,
-                                dmax_bits_, ybuf_, ys_, rscratch_,
+                                dmax_bits_, yb, yss, rscratch_,
                                 recip_global_ ? 1 : 0, err_, sh);
           });
-          CU(cudaEventRecord(sev_[2 * p + 1], sh));
+          CU(cudaEventRecord(sev_[4 * p + 1], sh));
+          // bulk of column p on the panel stream (rows > p)
           TL(3, p, sp, [&] {
             return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
                                      p, p + 1, n, err_, sp);
@@ -617,7 +638,27 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             return launch_extract(D, W_, colbase_, p, p + 1, n, vint, row0,
                                   piv, maxbitsV, vhat_, maxdegV, err_, sp);
           });
-          CU(cudaStreamWaitEvent(sp, sev_[2 * p + 1], 0));
+          CU(cudaEventRecord(sev_[4 * p], sp));
+          // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot)
+          CU(cudaStreamWaitEvent(sh, sev_[4 * p], 0));
+          TL(5, p, sh, [&] {
+            return launch_divide(D, vint, row0, p, p + 1, p + 2, yb, yss,
+                                 rint, row0, rhat_, maxdegR + p, dscratch_,
+                                 div_global_ ? 1 : 0, err_, sh);
+          });
+          CU(cudaEventRecord(sev_[4 * p + 3], sh));
+          // R_p[r >= p+2] on the panel stream
+          CU(cudaStreamWaitEvent(sp, sev_[4 * p + 1], 0));
+          TL(5, p, sp, [&] {
+            return launch_divide(D, vint, row0, p, p + 2, n, yb, yss, rint,
+                                 row0, rhat_, maxdegR + p, dscratch2_,
+                                 div_global_ ? 1 : 0, err_, sp);
+          });
+          CU(cudaEventRecord(sev_[4 * p + 2], sp));
+          if (p + 1 == p1 || p + 1 == n - 1) {
+            // join: the next step on sp needs R_p[p+1] as well
+            CU(cudaStreamWaitEvent(sp, sev_[4 * p + 3], 0));
+          }
         } else {
           // left-looking inside the panel: column p receives stages [p0, p)
           TL(6, p, sp, [&] {
@@ -631,17 +672,17 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           });
           if (p == n - 1) break;
           TL(2, p, sp, [&] {
-            return launch_recip(D, vint, row0 + p, maxbitsV, p, piv, 0, ybuf_,
-                                ys_, rscratch_, recip_global_ ? 1 : 0, err_,
+            return launch_recip(D, vint, row0 + p, maxbitsV, p, piv, 0, yb,
+                                yss, rscratch_, recip_global_ ? 1 : 0, err_,
                                 sp);
           });
+          // R_p[r] (+ its Montgomery-form transform)
+          TL(5, p, sp, [&] {
+            return launch_divide(D, vint, row0, p, p + 1, n, yb, yss, rint,
+                                 row0, rhat_, maxdegR + p, dscratch_,
+                                 div_global_ ? 1 : 0, err_, sp);
+          });
         }
-        // R_p[r] (+ its Montgomery-form transform)
-        TL(5, p, sp, [&] {
-          return launch_divide(D, vint, row0, p, ybuf_, ys_, rint, row0, rhat_,
-                               maxdegR + p, dscratch_, div_global_ ? 1 : 0,
-                               err_, sp);
-        });
       }
     }
     panel_broadcast(owner, p0, ns, row0set, sp);

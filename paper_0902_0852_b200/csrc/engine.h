@@ -113,7 +113,8 @@ class Matrix {
   uint32_t *vhat_ = nullptr, *rhat_ = nullptr;
   int* phdr_ = nullptr;
   uint32_t* plimbs_ = nullptr;
-  uint32_t *ybuf_ = nullptr, *rscratch_ = nullptr, *dscratch_ = nullptr;
+  uint32_t *ybuf_ = nullptr, *rscratch_ = nullptr, *dscratch_ = nullptr,
+           *dscratch2_ = nullptr;
   int* ys_ = nullptr;
   int* stats_ = nullptr;  // maxbitsV | maxdegV | maxdegR, n each
   int* err_ = nullptr;

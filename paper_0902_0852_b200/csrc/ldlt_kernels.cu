@@ -487,6 +487,7 @@ __global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
 // (e.g. exact quotients) floor(F) is within one of q and the remainder
 // window A - q~ D over nD+2 limbs decides the correction exactly.
 __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+                         int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
                          uint32_t* gscratch, int use_gscratch, int* err) {
@@ -523,7 +524,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   const uint32_t* Dg = vint.limbs + pidx * cap;
   const int n = nD ? limbs_bits(Dg, nD) : 0;
 
-  for (int r = p + 1 + blockIdx.x; r < P.n; r += gridDim.x) {
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
     const long long vidx = vrow0 + r;
     const int hv = vint.hdr[vidx];
     const int na = hv < 0 ? -hv : hv;
@@ -1018,8 +1019,8 @@ cudaError_t launch_divide_batch(const DevPlan& P, IntBuf vint,
   ++g_launches;
   k_divide<<<dim3(min(P.n - 1, P.grid_cap), batch), 256,
              (size_t)(P.tw_smem ? P.NW : 0) * 4, st>>>(
-      P, vint, vrow0, 0, Ybuf, ys, rint, rrow0, nullptr, nullptr, gscratch, 1,
-      err);
+      P, vint, vrow0, 0, 1, 2, Ybuf, ys, rint, rrow0, nullptr, nullptr,
+      gscratch, 1, err);
   return post_launch(st);
 }
 
@@ -1029,18 +1030,20 @@ size_t divide_smem_words(const DevPlan& P) {
 }
 
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
-                          int p, const uint32_t* Ybuf, const int* ys,
-                          IntBuf rint, long long rrow0, uint32_t* rhat,
-                          int* maxdegR, uint32_t* gscratch, int use_gscratch,
-                          int* err, cudaStream_t st) {
-  const int rows = P.n - p - 1;
+                          int p, int r_begin, int r_end, const uint32_t* Ybuf,
+                          const int* ys, IntBuf rint, long long rrow0,
+                          uint32_t* rhat, int* maxdegR, uint32_t* gscratch,
+                          int use_gscratch, int* err, cudaStream_t st) {
+  r_begin = max(r_begin, p + 1);
+  r_end = min(r_end, P.n);
+  const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
                                    : divide_smem_words(P) * 4;
   ++g_launches;
   k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
-      P, vint, vrow0, p, Ybuf, ys, rint, rrow0, rhat, maxdegR, gscratch,
-      use_gscratch, err);
+      P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
+      gscratch, use_gscratch, err);
   return post_launch(st);
 }
 

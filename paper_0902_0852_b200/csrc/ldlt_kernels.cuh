@@ -124,11 +124,12 @@ cudaError_t launch_divide_batch(const DevPlan& P, IntBuf vint,
                                 const int* ys, IntBuf rint, long long rrow0,
                                 uint32_t* gscratch, int batch, int* err,
                                 cudaStream_t st);
+// rows r in [max(r_begin, p+1), min(r_end, n)) of stage p
 cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
-                          int p, const uint32_t* Ybuf, const int* ys,
-                          IntBuf rint, long long rrow0, uint32_t* rhat,
-                          int* maxdegR, uint32_t* gscratch, int use_gscratch,
-                          int* err, cudaStream_t st);
+                          int p, int r_begin, int r_end, const uint32_t* Ybuf,
+                          const int* ys, IntBuf rint, long long rrow0,
+                          uint32_t* rhat, int* maxdegR, uint32_t* gscratch,
+                          int use_gscratch, int* err, cudaStream_t st);
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
