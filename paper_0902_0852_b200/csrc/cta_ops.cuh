@@ -389,13 +389,13 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
   const int M = M_end - k_begin;  // columns formed
   const int ngroups = (M + G - 1) / G;
   const int minlen = min(na, nb);
-  // split a group's i-range only when segments stay >= 64 iterations and
+  // split a group's i-range only when segments stay >= 32 iterations and
   // there are idle threads to take them
   // nseg > 1 needs 3*nseg*M words of planes plus 2*M for the reduced sums
   const int maxseg = max(1, ((col_words > 0 ? col_words : 3 * M) - 2 * M) / (3 * M));
   const int want = (2 * (int)blockDim.x + ngroups - 1) / max(ngroups, 1);
-  const int bylen = max(1, (minlen + G - 1) / 64);
-  const int nseg = max(1, min(min(min(maxseg, want), bylen), 8));
+  const int bylen = max(1, (minlen + G - 1) / 32);
+  const int nseg = max(1, min(min(min(maxseg, want), bylen), 16));
   const int seglen = (minlen + G - 1 + nseg - 1) / nseg;  // group i-range <= minlen+G-1
   const int items = ngroups * nseg;
   for (int it = threadIdx.x; it < items; it += blockDim.x) {

@@ -340,7 +340,7 @@ __device__ inline int recip_levels(int Pt, int* lv) {
   return k;
 }
 
-__global__ void k_recip(DevPlan P, IntBuf vint, long long prow,
+__global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long prow,
                         const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
                         uint32_t* Ybuf, int* ys, uint32_t* gscratch,
                         int use_gscratch, int* err) {
@@ -973,8 +973,8 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
 static int recip_threads() {
   static const int t = [] {
     const char* e = getenv("HGPU_RECIP_THREADS");
-    const int v = e ? atoi(e) : 256;
-    return (v >= 32 && v <= 1024 && v % 32 == 0) ? v : 256;
+    const int v = e ? atoi(e) : 512;
+    return (v >= 32 && v <= 512 && v % 32 == 0) ? v : 512;
   }();
   return t;
 }
@@ -1125,11 +1125,13 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                 (int)fwd)) != cudaSuccess)
     return e;
   const size_t rec = recip_scratch_words(P) * 4;
-  // the reciprocal CTA runs beside the bulk kernels: keeping its scratch in
-  // global memory (L1/L2-resident) lets it start on any SM with free warp
-  // slots instead of waiting for one with ~200 KB of free shared memory
+  // the reciprocal CTA runs beside the bulk kernels; shared-memory scratch
+  // is faster even at ~190 KB (measured at config 3: 421 -> 405 ms per
+  // factorisation), so it is used whenever it fits.  HGPU_RECIP_SMEM=0
+  // keeps the scratch in global memory (L1/L2-resident) instead.
   const char* rg = getenv("HGPU_RECIP_SMEM");
-  *recip_global = (int)rec > maxopt || !(rg && *rg == '1');
+  const bool want_smem = rg ? *rg == '1' : true;
+  *recip_global = (int)rec > maxopt || !want_smem;
   if (!*recip_global) {
     if ((e = cudaFuncSetAttribute(k_recip,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
