@@ -165,6 +165,7 @@ Matrix::~Matrix() {
   if (ev1_) cudaEventDestroy(ev1_);
   for (cudaEvent_t e : pev_) cudaEventDestroy(e);
   for (cudaEvent_t e : sev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   if (stream_helper_) cudaStreamDestroy(stream_helper_);
   if (stream_panel_) cudaStreamDestroy(stream_panel_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -179,6 +180,16 @@ void Matrix::release() {
                   (void*)dscratch_, (void*)dscratch2_, (void*)ys_,
                   (void*)stats_, (void*)err_})
     dfree(p);
+  // inverse-iteration state (sized by the plan's capacity)
+  for (void* p : {(void*)lhdr_, (void*)llimbs_, (void*)svhdr_, (void*)svlimbs_,
+                  (void*)sacc_, (void*)spair_hdr_,
+                  (void*)spair_limbs_, (void*)sbits_, (void*)sybuf_,
+                  (void*)srscr_, (void*)sdscr_, (void*)sys_})
+    dfree(p);
+  lhdr_ = svhdr_ = spair_hdr_ = sbits_ = sys_ = nullptr;
+  llimbs_ = svlimbs_ = sacc_ = spair_limbs_ = sybuf_ = srscr_ =
+      sdscr_ = nullptr;
+  have_L_ = false;
   tw_ = W_ = that_ = xhat_ = nullptr;
   colbase_ = nullptr;
   strip_hdr_ = x_hdr_ = vhdr_ = rhdr_ = phdr_ = ys_ = stats_ = err_ = nullptr;
