@@ -339,6 +339,47 @@ __device__ int cta_resolve(int M, int bits, GetV getv, PutD putd,
   return cf_apply(total, 0);
 }
 
+// ------------------------------------------- warp-level variants ---------
+// The same carry-function resolution and products for one warp (all 32
+// lanes), with __syncwarp only: the reciprocal's small Newton levels run on
+// a single warp, where block-wide barriers would cost more than the work.
+
+__device__ __forceinline__ uint32_t warp_exclusive_compose(uint32_t f,
+                                                           uint32_t* total) {
+  const int lane = threadIdx.x & 31;
+  uint32_t x = f;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = cf_compose(x, y);
+  }
+  *total = __shfl_sync(0xffffffffu, x, 31);
+  uint32_t excl = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) excl = kCfIdentity;
+  return excl;
+}
+
+template <class GetV, class PutD>
+__device__ int warp_resolve(int M, int bits, GetV getv, PutD putd) {
+  const int lane = threadIdx.x & 31;
+  const int chunk = (M + 31) / 32;
+  const int k0 = min(M, lane * chunk);
+  const int k1 = min(M, k0 + chunk);
+  uint32_t F = kCfIdentity;
+  for (int k = k0; k < k1; ++k) F = cf_compose(cf_of(getv(k), bits), F);
+  uint32_t total;
+  const uint32_t Pf = warp_exclusive_compose(F, &total);
+  int c = cf_apply(Pf, 0);
+  const int64_t mask = (int64_t(1) << bits) - 1;
+  for (int k = k0; k < k1; ++k) {
+    const int64_t v = getv(k) + c;
+    putd(k, (uint64_t)(v & mask));
+    c = (int)floor_shift(v, bits);
+  }
+  __syncwarp();
+  return cf_apply(total, 0);
+}
+
 // ------------------------------------------------------- limb helpers -----
 
 // Bits [off, off+32) of the non-negative integer a[0..n) (off may be < 0).
@@ -364,6 +405,16 @@ __device__ inline int cta_limb_len(const uint32_t* a, int n, uint32_t* red) {
   const int len = (int)red[0];
   __syncthreads();
   return len;
+}
+
+__device__ inline int warp_limb_len(const uint32_t* a, int n) {
+  int best = 0;
+  for (int i = threadIdx.x & 31; i < n; i += 32)
+    if (a[i]) best = i + 1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+    best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  return best;
 }
 
 __device__ __forceinline__ int limbs_bits(const uint32_t* a, int len) {
@@ -486,6 +537,36 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
         return v;
       },
       [&](int k, uint32_t d) { out[k] = d; }, red);
+}
+
+// Warp version of cta_mul (full product columns [0, M)): lane-strided
+// columns, one 96-bit column sum each, then a warp carry resolution.
+// col: 3*M words; out must not alias a, b or col.
+__device__ inline void warp_mul(const uint32_t* a, int na, const uint32_t* b,
+                                int nb, uint32_t* out, int M, uint32_t* col) {
+  for (int k = threadIdx.x & 31; k < M; k += 32) {
+    uint32_t c0 = 0, c1 = 0, c2 = 0;
+    const int ilo = max(0, k - nb + 1), ihi = min(k, na - 1);
+    for (int i = ilo; i <= ihi; ++i)
+      asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+          "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+          "addc.u32 %2, %2, 0;"
+          : "+r"(c0), "+r"(c1), "+r"(c2)
+          : "r"(a[i]), "r"(b[k - i]));
+    col[k] = c0;
+    col[M + k] = c1;
+    col[2 * M + k] = c2;
+  }
+  __syncwarp();
+  warp_resolve(
+      M, 32,
+      [&](int k) -> int64_t {
+        int64_t v = col[k];
+        if (k >= 1) v += col[M + k - 1];
+        if (k >= 2) v += col[2 * M + k - 2];
+        return v;
+      },
+      [&](int k, uint32_t d) { out[k] = d; });
 }
 
 }  // namespace hgpu

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
+#include <type_traits>
 
 #include "cta_ops.cuh"
 #include "ldlt_kernels.cuh"
@@ -408,64 +409,98 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
   __syncthreads();
   int nY = 2;
   const bool prof = (P.debug & 256) && p == 50 && threadIdx.x == 0;
-  long long tph[6];
-  for (int i = 0; i + 1 < nl; ++i) {
+  // one Newton level; kWarp: run by warp 0 alone (small levels)
+  auto level = [&](auto warp_tag, int i) {
+    constexpr bool kWarp = decltype(warp_tag)::value;
+    const int t0 = kWarp ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    const int ts = kWarp ? 32 : (int)blockDim.x;
+    auto sync = [] {
+      if (kWarp) __syncwarp(); else __syncthreads();
+    };
+    auto resolve = [&](int M, auto getv, auto putd) {
+      if constexpr (kWarp) return warp_resolve(M, 32, getv, putd);
+      else return cta_resolve(M, 32, getv, putd, red);
+    };
+    auto mul = [&](const uint32_t* a, int na, const uint32_t* b, int nb,
+                   uint32_t* out, int M) {
+      if constexpr (kWarp) warp_mul(a, na, b, nb, out, M, col);
+      else cta_mul(a, na, b, nb, out, M, col, red, col_words);
+    };
+    long long tph[6];
     if (prof) tph[0] = clock64();
     const int pa = lv[i], pb = lv[i + 1], dlt = pb - pa;
     const int mb = min(n, pb + G);   // bits of D'
     const int t = n - mb;
     const int nDt = (mb + 31) / 32;
-    for (int k = threadIdx.x; k < nDt; k += blockDim.x)
-      Dt[k] = field32(Dg, nD, 32LL * k + t);
-    __syncthreads();
+    for (int k = t0; k < nDt; k += ts) Dt[k] = field32(Dg, nD, 32LL * k + t);
+    sync();
     // Pr = D' * Y
     const int nP = nDt + nY;
     if (prof) tph[1] = clock64();
-    cta_mul(Dt, nDt, Y, nY, Pr, nP, col, red, col_words);
+    mul(Dt, nDt, Y, nY, Pr, nP);
     if (prof) tph[2] = clock64();
     // E = 2^(mb+pa) - Pr, signed, over nP+1 limbs
     const int nEw = nP + 1;
     const int Sb = mb + pa;
     int sgn = 1;
     for (int pass = 0; pass < 2; ++pass) {
-      const int c = cta_resolve(
-          nEw, 32,
+      const int c = resolve(
+          nEw,
           [&](int k) -> int64_t {
-            const int64_t a = (k == Sb / 32) ? (int64_t)(1u << (Sb % 32)) : 0;
-            const int64_t b = k < nP ? (int64_t)Pr[k] : 0;
-            return sgn > 0 ? a - b : b - a;
+            const int64_t av = (k == Sb / 32) ? (int64_t)(1u << (Sb % 32)) : 0;
+            const int64_t bv = k < nP ? (int64_t)Pr[k] : 0;
+            return sgn > 0 ? av - bv : bv - av;
           },
-          [&](int k, uint32_t dd) { E[k] = dd; }, red);
+          [&](int k, uint32_t dd) { E[k] = dd; });
       if (c >= 0) break;
       sgn = -1;
     }
-    const int nE = cta_limb_len(E, nEw, red);
+    const int nE = kWarp ? warp_limb_len(E, nEw) : cta_limb_len(E, nEw, red);
     if (prof) tph[3] = clock64();
     // Tm = Y * |E|
     const int nT = nY + nE;
-    if (nE > 0) cta_mul(Y, nY, E, nE, Tm, nT, col, red, col_words);
+    if (nE > 0) mul(Y, nY, E, nE, Tm, nT);
     if (prof) tph[4] = clock64();
     // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
     const int nYn = min(Lm, (pb + 2 + 31) / 32 + 1);
     const int sh = Sb - dlt;
-    cta_resolve(
-        nYn, 32,
+    resolve(
+        nYn,
         [&](int k) -> int64_t {
           const int64_t yv = field32(Y, nY, 32LL * k - dlt);
           const int64_t tv = nE > 0 ? (int64_t)field32(Tm, nT, 32LL * k + sh) : 0;
           return sgn > 0 ? yv + tv : yv - tv;
         },
-        [&](int k, uint32_t dd) { Pr[k] = dd; }, red);
-    for (int k = threadIdx.x; k < nYn; k += blockDim.x) Y[k] = Pr[k];
-    __syncthreads();
+        [&](int k, uint32_t dd) { Pr[k] = dd; });
+    for (int k = t0; k < nYn; k += ts) Y[k] = Pr[k];
+    sync();
     if (prof) {
       tph[5] = clock64();
-      printf("recip lvl %d pa=%d pb=%d nDt=%d nY=%d nE=%d: Dt %lld mul1 %lld E %lld mul2 %lld Yupd %lld\n",
-             i, pa, pb, nDt, nY, nE, tph[1] - tph[0], tph[2] - tph[1], tph[3] - tph[2],
-             tph[4] - tph[3], tph[5] - tph[4]);
+      printf("recip lvl %d%s pa=%d pb=%d nDt=%d nY=%d nE=%d: Dt %lld mul1 %lld E %lld mul2 %lld Yupd %lld\n",
+             i, kWarp ? "w" : "", pa, pb, nDt, nY, nE, tph[1] - tph[0],
+             tph[2] - tph[1], tph[3] - tph[2], tph[4] - tph[3], tph[5] - tph[4]);
     }
     nY = nYn;
+  };
+  // levels whose operands stay within kWarpLimbs run on warp 0 alone
+  constexpr int kWarpLimbs = 128;
+  __shared__ int s_next[2];
+  int i = 0;
+  if (threadIdx.x < 32) {
+    for (; i + 1 < nl; ++i) {
+      const int nDt = (min(n, lv[i + 1] + G) + 31) / 32;
+      if (nDt > kWarpLimbs || nY > kWarpLimbs) break;
+      level(std::true_type{}, i);
+    }
+    if (threadIdx.x == 0) {
+      s_next[0] = i;
+      s_next[1] = nY;
+    }
   }
+  __syncthreads();
+  i = s_next[0];
+  nY = s_next[1];
+  for (; i + 1 < nl; ++i) level(std::false_type{}, i);
   for (int k = threadIdx.x; k < P.ycap; k += blockDim.x)
     Ybuf[k] = k < nY ? Y[k] : 0u;
   if (threadIdx.x == 0) {
@@ -551,7 +586,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       const int K0 = max(0, (sh - 75) / 32);
       const int nPs = nP - K0;
       const int shs = sh - 32 * K0;
-      cta_mul(Vt, nt, Y, nY, Pr, nP, col, red, 0, K0);
+      cta_mul(Vt, nt, Y, nY, Pr, nP, col, red, 3 * CY, K0);
       const int nQ = max(0, (int)((32LL * nPs - shs + 31) / 32));
       for (int i = threadIdx.x; i < nQ; i += blockDim.x)
         Qt[i] = field32(Pr, nPs, 32LL * i + shs);
@@ -564,7 +599,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
         const int nw = nD + 2;
         uint32_t* Wa = Pr;
         uint32_t* Wb = Pr + nw;
-        cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red);
+        cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red, 3 * CY);
         cta_resolve(
             nw, 32,
             [&](int k) -> int64_t {
