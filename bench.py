@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 
 CONFIG = {"workload": "LDL^T factorisation of M - x1*I, N=1000, beta=1, P=24576",
           "n": 1000, "beta": "1", "precision_bits": 24576, "shift": "x1=-2^-16",
-          "l2": "workspace 12.3 GB >> 126 MB L2 (inputs larger than L2)"}
+          "l2": "workspace (plan.workspace_bytes, GBs) >> 126 MB L2: inputs larger than L2"}
 METRIC = "Cholesky MP-MAC/s (N=1000, beta=1, P=24576)"
 UNIT = "MP-MAC/s"
 
