@@ -37,9 +37,14 @@ typedef enum hgpu_status {
   HGPU_ERR_CAPACITY = 5,           /* a value outgrew every plan that fits */
   HGPU_ERR_INTERNAL = 6,           /* an exactness self-check failed */
   HGPU_ERR_COMM = 7,               /* heig::ChannelFailure (errors.hpp:107-111) */
-  HGPU_ERR_PRECISION_EXHAUSTED = 8 /* NoProgress / SignViolation /
-                                      RootHitAtPrecision (errors.hpp:60-80):
-                                      raise frac_bits and retry */
+  HGPU_ERR_PRECISION_EXHAUSTED = 8, /* NoProgress / SignViolation /
+                                       RootHitAtPrecision (errors.hpp:60-80):
+                                       raise frac_bits and retry */
+  HGPU_ERR_INTERVAL_STRADDLE = 9    /* interval LDL^T: a column-value bound
+                                       and a ratio bound both contain zero,
+                                       so the extreme corner of their product
+                                       depends on magnitudes (not supported
+                                       in the transform domain) */
 } hgpu_status;
 
 /* factor flags */
@@ -108,6 +113,42 @@ hgpu_status hgpu_smallest_eigenvalue(hgpu_matrix* m, int digits,
                                      char** eigenvalue, char** trace,
                                      long* iterations, double* det_seconds);
 void hgpu_string_free(char* s);
+
+/* ---- interval LDL^T (ldlt_det_interval, ldlt.cpp:79-152) ----------------
+ * An interval matrix holds the lower and upper bounds of every moment
+ * (HankelIntervalMatrix; bounds in order, same frac_bits).  It runs on one
+ * GPU.  Replaces the reference's serial interval elimination (ldlt.cpp:79). */
+hgpu_status hgpu_interval_matrix_new(long n, long frac_bits,
+                                     const int32_t* lo_sizes,
+                                     const uint32_t* lo_limbs,
+                                     const int32_t* hi_sizes,
+                                     const uint32_t* hi_limbs, int device,
+                                     hgpu_matrix** out);
+/* ldlt_det_interval(m, [xlo, xhi]): pivot intervals (hgpu_factor_pivot = lower
+ * bound, hgpu_factor_pivot_hi = upper bound) and, with HGPU_FOLD, the exact
+ * determinant interval (hgpu_factor_det / hgpu_factor_det_hi, folded with
+ * FixedInterval::mul semantics).  ZeroPivot(p) when [V.lo, V.hi][p] contains
+ * zero (ldlt.cpp:110-111); HGPU_ERR_INTERVAL_STRADDLE when a column-value bound
+ * and a ratio bound both contain zero. */
+hgpu_status hgpu_ldlt_interval(hgpu_matrix* m, int32_t xlo_size,
+                               const uint32_t* xlo_limbs, int32_t xhi_size,
+                               const uint32_t* xhi_limbs, long x_frac_bits,
+                               unsigned flags, hgpu_factor** out);
+hgpu_status hgpu_factor_pivot_hi(const hgpu_factor* f, long p, int32_t* size,
+                                 const uint32_t** limbs);
+hgpu_status hgpu_factor_det_hi(const hgpu_factor* f, int32_t* size,
+                               const uint32_t** limbs);
+/* FixedInterval::sign of the determinant interval: 1, -1, 0 (indeterminate) */
+int hgpu_factor_det_sign(const hgpu_factor* f);
+/* verify_eigenvalue (verify.cpp:8-42) on an interval matrix at its own
+ * frac_bits: a = x truncated to `digits` significant digits (the reference
+ * uses 15), b = a + 1 ulp in the last digit; status 0 verified (det(M-aI) > 0,
+ * det(M-bI) < 0), 1 refuted, 2 inconclusive; signs 1/-1/0; probes are
+ * malloc'd strings (hgpu_string_free). */
+hgpu_status hgpu_verify_eigenvalue(hgpu_matrix* m, const char* x_decimal,
+                                   int digits, int* status, int* lower_sign,
+                                   int* upper_sign, char** probe_low,
+                                   char** probe_high);
 
 /* Smallest eigenvalue by inverse iteration with Rayleigh-quotient shifts
  * (the north-star's lambda_min step; no reference counterpart -- SURVEY §0

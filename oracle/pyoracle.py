@@ -163,6 +163,67 @@ def ldlt_py(strip: list[int], x: int, k: int, capture: bool = True) -> LdltResul
     return LdltResult(det=fold_pivots(pivots, k), pivots=pivots, ratios=ratios)
 
 
+def fdiv_q(a: int, b: int) -> int:
+    return a // b
+
+
+def cdiv_q(a: int, b: int) -> int:
+    return -((-a) // b)
+
+
+@dataclass
+class IntervalLdlt:
+    det: tuple            # (lo, hi) at k bits
+    pivots: list          # [(lo, hi)] per stage (workspace precision k)
+
+
+def interval_mul(a: tuple, b: tuple, k: int) -> tuple:
+    """FixedInterval::mul (fixed_interval.cpp): 4 corners, outward rounding."""
+    c = [a[0] * b[0], a[0] * b[1], a[1] * b[0], a[1] * b[1]]
+    return (min(c) >> k, -((-max(c)) >> k))
+
+
+def ldlt_interval_py(lo: list[int], hi: list[int], k: int, x_lo: int, x_hi: int) -> IntervalLdlt:
+    """ldlt_det_interval (ldlt.cpp:79-152) restated with Python ints."""
+    n = (len(lo) + 1) // 2
+    k2 = k // 2
+    cols = [[[lo[r + c], hi[r + c]] for r in range(c, n)] for c in range(n)]
+    for c in range(n):
+        cols[c][0][0] -= x_hi
+        cols[c][0][1] -= x_lo
+    det = (1 << k, 1 << k)
+    pivots = []
+    for p in range(n):
+        pv = tuple(cols[p][0])
+        pivots.append(pv)
+        det = interval_mul(det, pv, k)
+        if p == n - 1:
+            break
+        vals = [None] * n
+        for r in range(p, n):
+            a, b = cols[p][r - p]
+            vals[r] = (a >> k2, -((-b) >> k2))          # floor, ceil
+        if vals[p][0] <= 0 <= vals[p][1]:
+            raise ZeroPivotError(p, k)
+        rat = [None] * n
+        for r in range(p + 1, n):
+            qs_f, qs_c = [], []
+            for num in vals[r]:
+                for den in vals[p]:
+                    sc = num << k2
+                    qs_f.append(fdiv_q(sc, den))
+                    qs_c.append(cdiv_q(sc, den))
+            rat[r] = (min(qs_f), max(qs_c))
+        for c in range(p + 1, n):
+            m = vals[c]
+            col = cols[c]
+            for r in range(c, n):
+                cs = [m[0] * rat[r][0], m[0] * rat[r][1], m[1] * rat[r][0], m[1] * rat[r][1]]
+                col[r - c][0] -= max(cs)
+                col[r - c][1] -= min(cs)
+    return IntervalLdlt(det=det, pivots=pivots)
+
+
 def closed_form_beta1(n: int, k: int) -> LdltResult:
     """Known answer for beta=1, x=0: D_p=(p!)^2 exactly, and the
     ratios are integers so every truncation is exact:
@@ -283,6 +344,50 @@ class RefLib(_TextLib):
         if text.startswith("error"):
             raise RuntimeError(text)
         return int(text)
+
+    def build_interval_strip(self, n: int, beta_num: int, beta_den: int, k: int):
+        """build_interval_matrix (hankel_matrix.cpp) -> (lo strip, hi strip)."""
+        text = self._call("oref_build_interval_strip",
+                          [ctypes.c_long, ctypes.c_ulong, ctypes.c_ulong, ctypes.c_long],
+                          n, beta_num, beta_den, k)
+        if text.startswith("error"):
+            raise RuntimeError(text)
+        lo, hi = [], []
+        for line in text.splitlines():
+            _, a, b = line.split()
+            lo.append(int(a, 16))
+            hi.append(int(b, 16))
+        return lo, hi
+
+    def ldlt_interval(self, lo: list[int], hi: list[int], k: int, x_lo: int, x_hi: int):
+        """ldlt_det_interval (ldlt.cpp:79-152) -> (det_lo, det_hi)."""
+        strip = "".join(f"{to_hex(a)} {to_hex(b)}\n" for a, b in zip(lo, hi))
+        text = self._call("oref_ldlt_interval",
+                          [ctypes.c_char_p, ctypes.c_long, ctypes.c_char_p, ctypes.c_char_p],
+                          strip.encode(), k, to_hex(x_lo).encode(), to_hex(x_hi).encode())
+        if text.startswith("error"):
+            parse_ldlt_text(text)  # raises ZeroPivotError / RuntimeError
+        _, a, b = text.split()
+        return int(a, 16), int(b, 16)
+
+    def decimal_to_interval(self, decimal: str, k: int) -> tuple[int, int]:
+        text = self._call("oref_decimal_to_interval", [ctypes.c_char_p, ctypes.c_long],
+                          decimal.encode(), k)
+        if text.startswith("error"):
+            raise RuntimeError(text)
+        a, b = text.split()
+        return int(a, 16), int(b, 16)
+
+    def verify(self, n: int, beta_num: int, beta_den: int, kv: int, x_decimal: str) -> dict:
+        """verify_eigenvalue (verify.cpp:8-42) on build_interval_matrix(n, beta, kv)."""
+        text = self._call("oref_verify",
+                          [ctypes.c_long, ctypes.c_ulong, ctypes.c_ulong, ctypes.c_long, ctypes.c_char_p],
+                          n, beta_num, beta_den, kv, x_decimal.encode())
+        if text.startswith("error"):
+            raise RuntimeError(text)
+        st, lo, hi, a, b = text.split()
+        return {"status": ("verified", "refuted", "inconclusive")[int(st)],
+                "lower_sign": int(lo), "upper_sign": int(hi), "probe_low": a, "probe_high": b}
 
     def truncate_sig_digits(self, x: int, frac_bits: int, digits: int) -> str:
         return self._call("oref_truncate_sig_digits", [ctypes.c_char_p, ctypes.c_long, ctypes.c_int],

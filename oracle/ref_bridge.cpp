@@ -19,9 +19,9 @@
 #include "driver.hpp"
 #include "hankel_matrix.hpp"
 #include "ldlt.hpp"
+#include "verify.hpp"
 #include "secant.hpp"
 #include "timing.hpp"
-#include "verify.hpp"
 
 using namespace heig;
 
@@ -147,6 +147,57 @@ char* oref_interval_sign_decimal(long n, unsigned long bnum, unsigned long bden,
     Sign s = FixedInterval::sign(det);
     return std::string(s == Sign::Positive ? "1"
                                            : (s == Sign::Negative ? "-1" : "0"));
+  });
+}
+
+// ldlt_det_interval (ldlt.cpp:79-152) on a given interval strip.  `strip`
+// lines: "<lo_hex> <hi_hex>" per anti-diagonal at k fractional bits; the
+// shift is [xlo, xhi].  Output: "det <lo_hex> <hi_hex>" (or the error line).
+char* oref_ldlt_interval(const char* strip, long k, const char* xlo_hex,
+                         const char* xhi_hex) {
+  return guarded([&] {
+    std::istringstream is(strip);
+    std::vector<FixedInterval> ad;
+    std::string lo, hi;
+    while (is >> lo >> hi)
+      ad.emplace_back(fixed_from_hex(lo.c_str(), k), fixed_from_hex(hi.c_str(), k));
+    const long n = ((long)ad.size() + 1) / 2;
+    HankelIntervalMatrix m(n, Rational(1, 1), k, std::move(ad));
+    FixedInterval x(fixed_from_hex(xlo_hex, k), fixed_from_hex(xhi_hex, k));
+    FixedInterval det = ldlt_det_interval(m, x);
+    std::ostringstream os;
+    os << "det " << det.lo().mantissa().get_str(16) << " "
+       << det.hi().mantissa().get_str(16) << "\n";
+    return os.str();
+  });
+}
+
+// decimal_to_interval (decimal.cpp:166-180): "<lo_hex> <hi_hex>".
+char* oref_decimal_to_interval(const char* s, long frac_bits) {
+  return guarded([&] {
+    FixedInterval v = decimal_to_interval(s, frac_bits);
+    return v.lo().mantissa().get_str(16) + " " + v.hi().mantissa().get_str(16);
+  });
+}
+
+// verify_eigenvalue (verify.cpp:8-42) on build_interval_matrix(n, beta, kv):
+// "<status> <lower_sign> <upper_sign> <probe_low> <probe_high>" with status
+// 0 verified, 1 refuted, 2 inconclusive and signs 1/-1/0 (0: indeterminate).
+char* oref_verify(long n, unsigned long bnum, unsigned long bden, long kv,
+                  const char* x_decimal) {
+  return guarded([&] {
+    HankelIntervalMatrix m = build_interval_matrix(n, Rational(bnum, bden), kv);
+    FixedPoint x = decimal_to_fixed_floor(x_decimal, kv);
+    VerifyOutcome o = verify_eigenvalue(m, x);
+    auto sg = [](Sign s) {
+      return s == Sign::Positive ? "1" : (s == Sign::Negative ? "-1" : "0");
+    };
+    std::ostringstream os;
+    os << (o.status == VerifyStatus::Verified ? 0
+           : o.status == VerifyStatus::Refuted ? 1 : 2)
+       << " " << sg(o.lower_sign) << " " << sg(o.upper_sign) << " "
+       << o.probe_low << " " << o.probe_high;
+    return os.str();
   });
 }
 

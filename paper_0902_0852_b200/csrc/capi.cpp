@@ -89,6 +89,66 @@ hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,
 
 void hgpu_matrix_free(hgpu_matrix* m) { delete m; }
 
+hgpu_status hgpu_interval_matrix_new(long n, long frac_bits,
+                                     const int32_t* lo_sizes,
+                                     const uint32_t* lo_limbs,
+                                     const int32_t* hi_sizes,
+                                     const uint32_t* hi_limbs, int device,
+                                     hgpu_matrix** out) {
+  return guarded([&] {
+    if (!out || !lo_sizes || !hi_sizes)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    if (n < 1 || n > 100000)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "order out of range");
+    auto m = std::make_unique<hgpu_matrix>();
+    m->impl = std::make_unique<hgpu::Matrix>((int)n, (int)frac_bits, lo_sizes,
+                                             lo_limbs, device);
+    m->impl->set_interval_hi(hi_sizes, hi_limbs);
+    *out = m.release();
+  });
+}
+
+hgpu_status hgpu_ldlt_interval(hgpu_matrix* m, int32_t xlo_size,
+                               const uint32_t* xlo_limbs, int32_t xhi_size,
+                               const uint32_t* xhi_limbs, long x_frac_bits,
+                               unsigned flags, hgpu_factor** out) {
+  return guarded([&] {
+    if (!m || !out) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    if (x_frac_bits != m->impl->frac_bits())
+      throw hgpu::Error(HGPU_ERR_PRECISION_MISMATCH,
+                        "fractional precision mismatch");
+    auto f = std::make_unique<hgpu_factor>();
+    f->res = m->impl->factor_interval(make_int(xlo_size, xlo_limbs),
+                                      make_int(xhi_size, xhi_limbs), flags);
+    *out = f.release();
+  });
+}
+
+hgpu_status hgpu_factor_pivot_hi(const hgpu_factor* f, long p, int32_t* size,
+                                 const uint32_t** limbs) {
+  return guarded([&] {
+    if (!f || !size || !limbs || !f->res.interval || p < 0 ||
+        p >= (long)f->res.pivots_hi.size())
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad pivot index");
+    *size = f->res.pivots_hi[p].size;
+    *limbs = f->res.pivots_hi[p].limbs.data();
+  });
+}
+
+hgpu_status hgpu_factor_det_hi(const hgpu_factor* f, int32_t* size,
+                               const uint32_t** limbs) {
+  return guarded([&] {
+    if (!f || !size || !limbs || !f->res.interval || !f->res.have_det)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "no folded interval det");
+    *size = f->res.det_hi.size;
+    *limbs = f->res.det_hi.limbs.data();
+  });
+}
+
+int hgpu_factor_det_sign(const hgpu_factor* f) {
+  return f && f->res.interval ? f->res.det_sign : 0;
+}
+
 hgpu_status hgpu_nccl_unique_id(unsigned char out[128]) {
   return guarded([&] {
     ncclUniqueId id;

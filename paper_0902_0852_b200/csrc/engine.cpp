@@ -180,6 +180,7 @@ void Matrix::release() {
                   (void*)dscratch_, (void*)dscratch2_, (void*)ys_,
                   (void*)stats_, (void*)err_})
     dfree(p);
+  release_interval();
   // inverse-iteration state (sized by the plan's capacity)
   for (void* p : {(void*)lhdr_, (void*)llimbs_, (void*)svhdr_, (void*)svlimbs_,
                   (void*)sacc_, (void*)spair_hdr_,
@@ -414,6 +415,7 @@ void Matrix::build(int min_logL) {
     dscratch2_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
   }
   stats_ = dalloc<int>(3 * (size_t)n_);
+  if (interval_) build_interval();
 }
 
 void Matrix::panel_broadcast(int owner, int p0, int ns, long long row0,

@@ -52,6 +52,13 @@ struct FactorResult {
   double update_ms = 0, update_products = 0;
   long long launches = 0;  // our kernels launched by the factorisation
   double fold_ms = 0;
+  // interval factorisation (ldlt_det_interval): pivots = lower bounds,
+  // pivots_hi = upper bounds; det = [det, det_hi] when folded; det_sign
+  // (+1 / -1 / 0 indeterminate) as FixedInterval::sign (fixed_interval.cpp)
+  bool interval = false;
+  std::vector<HostInt> pivots_hi;
+  HostInt det_hi;
+  int det_sign = 0;
 };
 
 class Matrix {
@@ -80,6 +87,13 @@ class Matrix {
   std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
   int order() const { return n_; }
   const HostInt& strip_entry(int s) const { return strip_[s]; }
+  // Interval mode (iv_engine.cpp): the constructor's strip holds the lower
+  // bounds; this supplies the upper bounds (HankelIntervalMatrix).
+  void set_interval_hi(const int32_t* sizes, const uint32_t* limbs);
+  bool is_interval() const { return interval_; }
+  // ldlt_det_interval (ldlt.cpp:79-152) at the shift [xlo, xhi].
+  FactorResult factor_interval(const HostInt& xlo, const HostInt& xhi,
+                               unsigned flags);
 
  private:
   void build(int min_logL);
@@ -89,6 +103,10 @@ class Matrix {
                        cudaStream_t st);
   void fold(FactorResult& res);
   void keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st);
+  void build_interval();
+  void release_interval();
+  void run_interval(const HostInt& xlo, const HostInt& xhi, unsigned flags,
+                    FactorResult& res);
 
   int n_, K_, device_;
   std::vector<HostInt> strip_;
@@ -141,6 +159,20 @@ class Matrix {
   uint32_t *sybuf_ = nullptr, *srscr_ = nullptr, *sdscr_ = nullptr;
   int* sys_ = nullptr;
   int dmax_bits_ = 0;
+  // interval mode: upper-bound copies of the per-entry buffers (the point
+  // buffers hold the lower bounds) and the sign classes of V, R bounds
+  bool interval_ = false;
+  std::vector<HostInt> strip_hi_;
+  uint32_t *W2_ = nullptr, *that2_ = nullptr, *xhat2_ = nullptr;
+  int* strip2_hdr_ = nullptr;
+  uint32_t* strip2_limbs_ = nullptr;
+  int* x2_hdr_ = nullptr;
+  uint32_t* x2_limbs_ = nullptr;
+  int *vhdr2_ = nullptr, *rhdr2_ = nullptr, *phdr2_ = nullptr;
+  uint32_t *vlimbs2_ = nullptr, *rlimbs2_ = nullptr, *plimbs2_ = nullptr;
+  uint32_t *vhat2_ = nullptr, *rhat2_ = nullptr, *ybuf2_ = nullptr;
+  int* ys2_ = nullptr;
+  int8_t *clsv_ = nullptr, *clsr_ = nullptr;
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   // HGPU_TIMELINE=<file>: per-launch start/end events (scheduling analysis)
   struct TlRec {

@@ -36,6 +36,7 @@ void __gmpz_tdiv_q(hg_mpz_ptr, hg_mpz_srcptr, hg_mpz_srcptr);
 void __gmpz_tdiv_q_2exp(hg_mpz_ptr, hg_mpz_srcptr, unsigned long);
 void __gmpz_fdiv_q(hg_mpz_ptr, hg_mpz_srcptr, hg_mpz_srcptr);
 void __gmpz_fdiv_q_2exp(hg_mpz_ptr, hg_mpz_srcptr, unsigned long);
+void __gmpz_cdiv_q_2exp(hg_mpz_ptr, hg_mpz_srcptr, unsigned long);
 void __gmpz_cdiv_q(hg_mpz_ptr, hg_mpz_srcptr, hg_mpz_srcptr);
 int __gmpz_cmp(hg_mpz_srcptr, hg_mpz_srcptr);
 size_t __gmpz_sizeinbase(hg_mpz_srcptr, int);

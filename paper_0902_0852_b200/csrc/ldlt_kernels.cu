@@ -153,8 +153,9 @@ __global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
 __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, int r_begin, int r_end, IntBuf vint,
                           long long vrow0, IntBuf piv, int* maxbitsV,
-                          uint32_t* vhat, int* maxdegV, int* err) {
+                          uint32_t* vhat, int* maxdegV, int* err, int round) {
   extern __shared__ uint32_t sm[];
+  __shared__ int s_bump;
   if (stage_aborted(err)) return;
   const int L = P.L, np = P.np, T = P.T, w = P.w;
   const int M = L + T;
@@ -295,18 +296,46 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
     if (r == p) {  // pivot
       if (threadIdx.x == 0) {
         piv.hdr[p] = wsign * len;
-        if (len == 0) atomicMin(&err[kErrZeroPivot], p);
+        // the interval elimination checks only V_p (ldlt.cpp:110-111)
+        if (len == 0 && round == 0) atomicMin(&err[kErrZeroPivot], p);
       }
       uint32_t* dst = piv.limbs + (long long)p * P.cap;
       for (int m = threadIdx.x; m < P.cap; m += blockDim.x) dst[m] = Lb[m];
     }
-    // V = |W| >> k2 with the sign kept (tdiv_q_2exp).
+    // V = W >> k2: truncated toward zero (round 0, tdiv_q_2exp), or toward
+    // -inf / +inf (round 1 / 2: the interval bounds, ldlt.cpp:105-108).  The
+    // magnitude is |W| >> k2, plus one when the rounding moves away from zero
+    // and a bit below k2 is set.  Built in Vb (the digit buffer is dead now).
+    uint32_t* Vb = reinterpret_cast<uint32_t*>(Dg);
+    if (threadIdx.x == 0) s_bump = 0;
+    __syncthreads();
+    if ((round == 1 && wsign < 0) || (round == 2 && wsign > 0)) {
+      const int full = P.k2 / 32, rb = P.k2 % 32;
+      bool any = false;
+      for (int m = threadIdx.x; m < min(full, len); m += blockDim.x)
+        any |= Lb[m] != 0u;
+      if (threadIdx.x == 0 && rb && full < len && (Lb[full] & ((1u << rb) - 1u)))
+        any = true;
+      if (any) s_bump = 1;
+    }
+    __syncthreads();
+    if (s_bump) {
+      cta_resolve(
+          P.cap, 32,
+          [&](int k) -> int64_t {
+            return (int64_t)field32(Lb, len, 32LL * k + P.k2) + (k == 0 ? 1 : 0);
+          },
+          [&](int k, uint32_t d) { Vb[k] = d; }, red);
+    } else {
+      for (int m = threadIdx.x; m < P.cap; m += blockDim.x)
+        Vb[m] = field32(Lb, len, 32LL * m + P.k2);
+      __syncthreads();
+    }
     const long long vidx = vrow0 + r;
     uint32_t* vdst = vint.limbs + vidx * P.cap;
-    for (int m = threadIdx.x; m < P.cap; m += blockDim.x)
-      vdst[m] = field32(Lb, len, 32LL * m + P.k2);
-    const int vbits = max(0, limbs_bits(Lb, len) - P.k2);
-    const int vlen = (vbits + 31) / 32;
+    for (int m = threadIdx.x; m < P.cap; m += blockDim.x) vdst[m] = Vb[m];
+    const int vlen = cta_limb_len(Vb, P.cap, red);
+    const int vbits = limbs_bits(Vb, vlen);
     const int vsign = vlen == 0 ? 0 : wsign;
     if (threadIdx.x == 0) {
       vint.hdr[vidx] = vsign * vlen;
@@ -318,8 +347,8 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
     }
     // transform of V_p[r] for the trailing update (rows r > p)
     if (r > p)
-      transform_int(P, Lb, len, P.k2, vsign, A,
-                    vhat + vidx * (long long)P.NW, false, twm, err);
+      transform_int(P, Vb, vlen, 0, vsign, A, vhat + vidx * (long long)P.NW,
+                    false, twm, err);
     __syncthreads();
   }
 }
@@ -525,7 +554,8 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
                          int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
-                         uint32_t* gscratch, int use_gscratch, int* err) {
+                         uint32_t* gscratch, int use_gscratch, int* err,
+                         IvDiv iv) {
   extern __shared__ uint32_t sm_dyn[];
   if (stage_aborted(err)) return;
   const int cap = P.cap, ycap = P.ycap;
@@ -551,20 +581,37 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   uint32_t* col = Pr + CY;           // 3 CY
   uint32_t* red = col + 3 * CY;      // 64
   uint32_t* Qt = Vt;
-  const int S = ys[0], nY = ys[1], amax_used = ys[2];
   const long long pidx = vrow0 + p;
-  const int hd = vint.hdr[pidx];
-  const int nD = hd < 0 ? -hd : hd;
-  const int sD = hd < 0 ? -1 : (hd > 0);
-  const uint32_t* Dg = vint.limbs + pidx * cap;
-  const int n = nD ? limbs_bits(Dg, nD) : 0;
+  // interval mode: the pivot interval [D.lo, D.hi] is sign-definite (else
+  // ZeroPivot aborted the stage); sd is its sign
+  const int sd = iv.mode == 0 ? 0 : (vint.hdr[pidx] > 0 ? 1 : -1);
 
   for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
     const long long vidx = vrow0 + r;
-    const int hv = vint.hdr[vidx];
+    // numerator bound and divisor (ldlt.cpp:113-131 restated per corner):
+    //   R.lo = floor(min corner): N = sd > 0 ? V.lo : V.hi, D = N > 0 ? D.hi : D.lo
+    //   R.hi = ceil(max corner):  N = sd > 0 ? V.hi : V.lo, D = N > 0 ? D.lo : D.hi
+    IntBuf nb = vint;
+    bool use_hi_div = false;
+    if (iv.mode != 0) {
+      const bool n_lo = (iv.mode == 1) == (sd > 0);
+      nb = n_lo ? vint : iv.vhi;
+      const int hn = nb.hdr[vidx];
+      use_hi_div = (iv.mode == 1) == (hn > 0);
+    }
+    const IntBuf db = use_hi_div ? iv.vhi : vint;
+    const uint32_t* Yb = use_hi_div ? iv.yhi : Ybuf;
+    const int* yb = use_hi_div ? iv.yshi : ys;
+    const int S = yb[0], nY = yb[1], amax_used = yb[2];
+    const int hd = db.hdr[pidx];
+    const int nD = hd < 0 ? -hd : hd;
+    const int sD = hd < 0 ? -1 : (hd > 0);
+    const uint32_t* Dg = db.limbs + pidx * cap;
+    const int n = nD ? limbs_bits(Dg, nD) : 0;
+    const int hv = nb.hdr[vidx];
     const int na = hv < 0 ? -hv : hv;
     const int sV = hv < 0 ? -1 : (hv > 0);
-    const uint32_t* Vg = vint.limbs + vidx * cap;   // global, read-only
+    const uint32_t* Vg = nb.limbs + vidx * cap;   // global, read-only
     const long long ridx = rrow0 + r;
     uint32_t* dst = rint.limbs + ridx * cap;
     int nq = 0;
@@ -578,7 +625,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       const int nt = max(0, (vbits - tv + 31) / 32);
       for (int i = threadIdx.x; i < nt; i += blockDim.x)
         Vt[i] = field32(Vg, na, 32LL * i + tv);
-      for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Ybuf[i];
+      for (int i = threadIdx.x; i < nY; i += blockDim.x) Y[i] = Yb[i];
       __syncthreads();
       const int nP = nt + nY;
       const int sh = S - P.k2 - tv;
@@ -594,6 +641,10 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       __syncthreads();
       nq = cta_limb_len(Qt, nQ, red);
       const bool exact_needed = shs < 32 || frac < 4u || frac > 0xFFFFFFFAu;
+      // interval rounding: one more unit of magnitude when the exact quotient
+      // is not an integer and the rounding points away from zero
+      const bool away = (iv.mode == 1 && sV * sD < 0) || (iv.mode == 2 && sV * sD > 0);
+      int bump = (away && !exact_needed) ? 1 : 0;  // fast path: never exact
       if (exact_needed) {
         // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
         const int nw = nD + 2;
@@ -628,6 +679,23 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
               atomicOr(&err[kErrInternal], kIntDivision);
           }
         }
+        if (away) {
+          // remainder: Wa (adj 0), Wb (adj +1), Wa + D (adj -1)
+          const uint32_t* rem = adj == 1 ? Wb : Wa;
+          if (adj == -1) {
+            __syncthreads();
+            cta_resolve(
+                nw, 32,
+                [&](int k) -> int64_t {
+                  return (int64_t)Wa[k] + (int64_t)(k < nD ? Dg[k] : 0u);
+                },
+                [&](int k, uint32_t d) { Wb[k] = d; }, red);
+            rem = Wb;
+          }
+          bump = cta_limb_len(rem, nw, red) != 0 ? 1 : 0;
+        }
+        adj += bump;
+        bump = 0;
         if (adj != 0) {
           const int nn = nq + 1;
           cta_resolve(
@@ -642,6 +710,18 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
         }
         // every thread has read the window signs before Pr is reused below
         __syncthreads();
+      }
+      if (bump) {
+        const int nn = nq + 1;
+        cta_resolve(
+            nn, 32,
+            [&](int k) -> int64_t {
+              return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? 1 : 0);
+            },
+            [&](int k, uint32_t d) { col[k] = d; }, red);
+        for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
+        __syncthreads();
+        nq = cta_limb_len(Qt, nn, red);
       }
       if (nq > cap) {
         if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
@@ -995,13 +1075,13 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, int r_begin,
                            int r_end, IntBuf vint, long long vrow0, IntBuf piv,
                            int* maxbitsV, uint32_t* vhat, int* maxdegV,
-                           int* err, cudaStream_t st) {
+                           int* err, cudaStream_t st, int round) {
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
   k_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
       P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
-      maxdegV, err);
+      maxdegV, err, round);
   return post_launch(st);
 }
 
@@ -1055,7 +1135,7 @@ cudaError_t launch_divide_batch(const DevPlan& P, IntBuf vint,
   k_divide<<<dim3(min(P.n - 1, P.grid_cap), batch), 256,
              (size_t)(P.tw_smem ? P.NW : 0) * 4, st>>>(
       P, vint, vrow0, 0, 1, 2, Ybuf, ys, rint, rrow0, nullptr, nullptr,
-      gscratch, 1, err);
+      gscratch, 1, err, IvDiv{});
   return post_launch(st);
 }
 
@@ -1068,7 +1148,8 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, int r_begin, int r_end, const uint32_t* Ybuf,
                           const int* ys, IntBuf rint, long long rrow0,
                           uint32_t* rhat, int* maxdegR, uint32_t* gscratch,
-                          int use_gscratch, int* err, cudaStream_t st) {
+                          int use_gscratch, int* err, cudaStream_t st,
+                          const IvDiv* iv) {
   r_begin = max(r_begin, p + 1);
   r_end = min(r_end, P.n);
   const int rows = r_end - r_begin;
@@ -1078,7 +1159,7 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   ++g_launches;
   k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
       P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
-      gscratch, use_gscratch, err);
+      gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
   return post_launch(st);
 }
 

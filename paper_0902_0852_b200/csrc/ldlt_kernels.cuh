@@ -34,6 +34,7 @@ enum : int {
   kCapDegree = 8,     // deg V + deg R >= L somewhere
   kCapCoeff = 16,     // accumulated coefficient bound reaches Q/2
   kCapAmax = 32,      // PD bound on the ratio sizes violated (non-PD shift)
+  kCapStraddle = 64,  // interval update: both bounds straddle zero
   kIntDivision = 1,   // quotient correction out of range
   kIntRecip = 2,      // reciprocal did not converge
 };
@@ -84,6 +85,17 @@ struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
   uint32_t* limbs;
 };
 
+// Interval division (ldlt_det_interval, ldlt.cpp:113-131): mode 1 gives the
+// lower ratio bound floor(min corner), mode 2 the upper bound ceil(max
+// corner).  The launch's vint/Ybuf/ys hold the lower bounds V.lo and the
+// reciprocal of |D.lo|; vhi/yhi/yshi the upper bounds and that of |D.hi|.
+struct IvDiv {
+  int mode;  // 0: point LDL^T (tdiv_q)
+  IntBuf vhi;
+  const uint32_t* yhi;
+  const int* yshi;
+};
+
 // Shared-memory words of one k_divide CTA (layout in ldlt_kernels.cu).
 __host__ __device__ inline long long div_span_words(int cap, int ycap) {
   const long long CY = ((long long)cap + ycap + 2 + 3) & ~3LL;
@@ -107,7 +119,7 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, int r_begin,
                            int r_end, IntBuf vint, long long vrow0, IntBuf piv,
                            int* maxbitsV, uint32_t* vhat, int* maxdegV,
-                           int* err, cudaStream_t st);
+                           int* err, cudaStream_t st, int round = 0);
 size_t recip_scratch_words(const DevPlan& P);
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
@@ -129,7 +141,8 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           int p, int r_begin, int r_end, const uint32_t* Ybuf,
                           const int* ys, IntBuf rint, long long rrow0,
                           uint32_t* rhat, int* maxdegR, uint32_t* gscratch,
-                          int use_gscratch, int* err, cudaStream_t st);
+                          int use_gscratch, int* err, cudaStream_t st,
+                          const IvDiv* iv = nullptr);
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
@@ -144,6 +157,18 @@ cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
 long long kernel_launch_count();
+// iv_kernels.cu (interval LDL^T)
+cudaError_t launch_iv_classify(IntBuf lo, IntBuf hi, long long row0,
+                               int r_begin, int r_end, int8_t* cls, int p,
+                               int check_pivot, int n, int* err,
+                               cudaStream_t st);
+cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
+                             const long long* colbase, const uint32_t* Vlo,
+                             const uint32_t* Vhi, const uint32_t* Rlo,
+                             const uint32_t* Rhi, const int8_t* clsV,
+                             const int8_t* clsR, int s_begin, int s_end,
+                             int c_begin, int c_end, int r_min, int* err,
+                             cudaStream_t st);
 // solve_kernels.cu (inverse iteration)
 size_t solve_axpy_smem_words(int cap, int Wv);
 size_t solve_finish_smem_words(int Wv, int Wa);

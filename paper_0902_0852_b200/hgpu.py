@@ -31,7 +31,7 @@ HGPU_PROFILE = 4
 STATUS = {
     0: "ok", 1: "invalid argument", 2: "zero pivot", 3: "precision mismatch",
     4: "cuda", 5: "capacity", 6: "internal", 7: "communication",
-    8: "precision exhausted",
+    8: "precision exhausted", 9: "interval straddle",
 }
 
 # every symbol include/hgpu.h declares
@@ -43,6 +43,8 @@ EXPORTS = (
     "hgpu_factor_launches", "hgpu_factor_free", "hgpu_matrix_plan", "hgpu_block_owner",
     "hgpu_last_zero_pivot", "hgpu_last_error", "hgpu_version",
     "hgpu_smallest_eigenvalue", "hgpu_string_free", "hgpu_inverse_iteration",
+    "hgpu_interval_matrix_new", "hgpu_ldlt_interval", "hgpu_factor_pivot_hi",
+    "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
 )
 
 
@@ -119,6 +121,17 @@ def load() -> ctypes.CDLL:
                                            ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                            ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(i64),
                                            ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_interval_matrix_new.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int32), u32p,
+                                             ctypes.POINTER(ctypes.c_int32), u32p, ctypes.c_int,
+                                             ctypes.POINTER(vp)]
+    lib.hgpu_ldlt_interval.argtypes = [vp, i32, u32p, i32, u32p, i64, ctypes.c_uint, ctypes.POINTER(vp)]
+    lib.hgpu_factor_pivot_hi.argtypes = [vp, i64, ctypes.POINTER(i32), ctypes.POINTER(u32p)]
+    lib.hgpu_factor_det_hi.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(u32p)]
+    lib.hgpu_factor_det_sign.argtypes = [vp]
+    lib.hgpu_factor_det_sign.restype = ctypes.c_int
+    lib.hgpu_verify_eigenvalue.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                           ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
     _lib = lib
     return lib
 
@@ -267,6 +280,66 @@ class HankelMatrixGPU:
             return res
         finally:
             lib.hgpu_factor_free(f)
+
+
+class IntervalMatrixGPU(HankelMatrixGPU):
+    """HankelIntervalMatrix (hankel_matrix.hpp:42) on one B200: lower and
+    upper bounds of every moment, for ldlt_det_interval (ldlt.cpp:79-152)
+    and verify_eigenvalue (verify.cpp:8-42)."""
+
+    def __init__(self, lo: list[int], hi: list[int], frac_bits: int, device: int = 0):
+        lib = load()
+        if len(lo) != len(hi) or len(lo) % 2 == 0 or not lo:
+            raise ValueError("strips must hold 2n-1 anti-diagonals each")
+        self.n = (len(lo) + 1) // 2
+        self.frac_bits = frac_bits
+        ls, ll = pack_ints(lo)
+        hs, hl = pack_ints(hi)
+        h = ctypes.c_void_p()
+        _check(lib.hgpu_interval_matrix_new(self.n, frac_bits,
+                                            ls.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _u32p(ll),
+                                            hs.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), _u32p(hl),
+                                            device, ctypes.byref(h)))
+        self._h = h
+
+    def ldlt_interval(self, x_lo: int, x_hi: int, fold: bool = False) -> dict:
+        """pivot intervals [(lo, hi)], det sign and (fold) det interval."""
+        lib = load()
+        a, al = int_to_limbs(x_lo)
+        b, bl = int_to_limbs(x_hi)
+        f = ctypes.c_void_p()
+        _check(lib.hgpu_ldlt_interval(self._h, a, _u32p(al), b, _u32p(bl), self.frac_bits,
+                                      HGPU_FOLD if fold else 0, ctypes.byref(f)), self.frac_bits)
+        try:
+            size = ctypes.c_int32()
+            ptr = ctypes.POINTER(ctypes.c_uint32)()
+            piv = []
+            for p in range(self.n):
+                _check(lib.hgpu_factor_pivot(f, p, ctypes.byref(size), ctypes.byref(ptr)))
+                lo = limbs_to_int(size.value, ptr)
+                _check(lib.hgpu_factor_pivot_hi(f, p, ctypes.byref(size), ctypes.byref(ptr)))
+                piv.append((lo, limbs_to_int(size.value, ptr)))
+            out = {"pivots": piv, "det_sign": int(lib.hgpu_factor_det_sign(f)),
+                   "device_ms": lib.hgpu_factor_device_ms(f)}
+            if fold:
+                _check(lib.hgpu_factor_det(f, ctypes.byref(size), ctypes.byref(ptr)))
+                lo = limbs_to_int(size.value, ptr)
+                _check(lib.hgpu_factor_det_hi(f, ctypes.byref(size), ctypes.byref(ptr)))
+                out["det"] = (lo, limbs_to_int(size.value, ptr))
+            return out
+        finally:
+            lib.hgpu_factor_free(f)
+
+
+def verify_eigenvalue(m: IntervalMatrixGPU, x_decimal: str, digits: int = 15) -> dict:
+    """verify_eigenvalue (verify.cpp:8-42) on the GPU interval LDL^T."""
+    lib = load()
+    st, ls, us = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib.hgpu_verify_eigenvalue(m._h, x_decimal.encode(), digits, ctypes.byref(st), ctypes.byref(ls),
+                                      ctypes.byref(us), ctypes.byref(a), ctypes.byref(b)), m.frac_bits)
+    return {"status": ("verified", "refuted", "inconclusive")[st.value], "lower_sign": ls.value,
+            "upper_sign": us.value, "probe_low": _take_string(a), "probe_high": _take_string(b)}
 
 
 def _take_string(ptr: ctypes.c_void_p) -> str:

@@ -159,3 +159,20 @@ def test_inverse_iteration_restatement_finds_lambda1(orc, seed, n, k):
     rho = po.inverse_iteration_py(strip, k, u, 0, 40)[-1]
     neg = lambda x: sum(1 for p in orc.ldlt(strip, x, k, capture=True).pivots if p < 0)
     assert neg(rho - (rho >> 40)) == 0 and neg(rho + (rho >> 40)) == 1
+
+
+@pytest.mark.parametrize("n,bn,bd,k", [(8, 7, 4, 256), (12, 3, 2, 512), (10, 1, 2, 384), (30, 7, 4, 1024)])
+def test_interval_restatement_matches_reference(ref, n, bn, bd, k):
+    """ldlt_interval_py (row f1's checker) against the reference's own
+    ldlt_det_interval on its certified interval strips."""
+    lo, hi = ref.build_interval_strip(n, bn, bd, k)
+    for dec in ("1e-300", "1e-30", "3.5e-10", "5e-1", "1.2e0"):
+        xl, xh = ref.decimal_to_interval(dec, k)
+        try:
+            want = ref.ldlt_interval(lo, hi, k, xl, xh)
+        except po.ZeroPivotError as e:
+            with pytest.raises(po.ZeroPivotError) as got:
+                po.ldlt_interval_py(lo, hi, k, xl, xh)
+            assert got.value.pivot_index == e.pivot_index
+            continue
+        assert po.ldlt_interval_py(lo, hi, k, xl, xh).det == want
