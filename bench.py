@@ -225,6 +225,21 @@ def run_gpu(args) -> None:
                "method": "shifted inverse iteration + RQI on the GPU LDL^T (hgpu_inverse_iteration)",
                "includes": "strip upload, every factorisation and triangular solve"}
         del mm
+        # certification of those digits (verify_eigenvalue on the GPU
+        # interval LDL^T at Kv = 2P, row f1): two interval factorisations
+        barrier()
+        t0 = time.perf_counter()
+        kv = 2 * k
+        sv = config_strip(n, kv)
+        im = hgpu.IntervalMatrixGPU(sv, sv, kv, device=local)
+        vr = hgpu.verify_eigenvalue(im, rq["eigenvalue"], 40)
+        barrier()
+        lam["certification"] = {
+            "seconds": time.perf_counter() - t0, "status": vr["status"], "digits": 40,
+            "kv_bits": kv, "probe_low": vr["probe_low"], "probe_high": vr["probe_high"],
+            "method": "verify_eigenvalue (verify.cpp:8-42) on the GPU interval LDL^T "
+                      "(hgpu_verify_eigenvalue), strip upload included"}
+        del im
 
     # roofline of the dominant kernel (trailing update): modular products per
     # launch / average launch time, against the measured IMAD.WIDE rate

@@ -114,6 +114,21 @@ hgpu_status hgpu_smallest_eigenvalue(hgpu_matrix* m, int digits,
                                      long* iterations, double* det_seconds);
 void hgpu_string_free(char* s);
 
+/* ---- moments (build_matrix / build_interval_matrix, hankel_matrix.cpp) ----
+ * The 2n-1 anti-diagonals (1/beta) Gamma((1+s)/beta), beta = beta_num /
+ * beta_den, at frac_bits: interval == 0 gives build_matrix's round-to-nearest
+ * strip in lo (hi = lo if requested), interval != 0 the certified
+ * [floor, ceil] bounds of build_interval_matrix.  Host code (all threads),
+ * bit-identical to the reference's Gamma enclosures (gamma.cpp:101-230).
+ * Outputs are malloc'd; release each with hgpu_buffer_free.  hi_* may be
+ * null when interval == 0. */
+hgpu_status hgpu_build_moments(long n, unsigned long beta_num,
+                               unsigned long beta_den, long frac_bits,
+                               int interval, int32_t** lo_sizes,
+                               uint32_t** lo_limbs, int32_t** hi_sizes,
+                               uint32_t** hi_limbs);
+void hgpu_buffer_free(void* p);
+
 /* ---- interval LDL^T (ldlt_det_interval, ldlt.cpp:79-152) ----------------
  * An interval matrix holds the lower and upper bounds of every moment
  * (HankelIntervalMatrix; bounds in order, same frac_bits).  It runs on one

@@ -23,6 +23,10 @@
 
 namespace hgpu {
 
+// host/moments.cpp
+void build_moments(long n, unsigned long bnum, unsigned long bden, long k,
+                   bool interval, std::vector<Z>& lo, std::vector<Z>& hi);
+
 namespace {
 
 struct Rational {
@@ -83,6 +87,9 @@ struct InvalidConfig : std::runtime_error {
 struct PrecisionCap : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct Refuted : std::runtime_error {  // errors.hpp:102-105
+  using std::runtime_error::runtime_error;
+};
 
 // choose_initial_precision (driver.cpp:15-21): max(512, 8n, 4n ceil(1/beta)),
 // rounded up to a multiple of 64.
@@ -112,23 +119,13 @@ long escalate(long k, long cap) {
 // Moments (1/beta) Gamma((1+s)/beta) at K bits when the Gamma arguments are
 // integers (1/beta = m integral): m * (m(1+s)-1)!, exact, which is what the
 // reference's build_matrix yields there (hankel_matrix.cpp:13-31).
+// build_matrix (hankel_matrix.cpp:13-31): every beta, through the Gamma
+// enclosures restated in host/moments.cpp (exact factorials when 1/beta is
+// integral).
 std::vector<Z> exact_moments(long n, const Rational& b, long k) {
-  if (b.den % b.num != 0)
-    throw InvalidConfig(
-        "beta=" + b.str() +
-        ": non-integer Gamma arguments need the certified Gamma series "
-        "(gamma.cpp), which this GPU build does not generate; pass the "
-        "strip through hgpu_matrix_new instead");
-  const unsigned long m = b.den / b.num;
-  std::vector<Z> strip;
-  strip.reserve(2 * n - 1);
-  for (long s = 0; s < 2 * n - 1; ++s) {
-    Z f;
-    __gmpz_fac_ui(f.p(), m * (unsigned long)(1 + s) - 1);
-    Z mm((long)m);
-    strip.push_back(shl(f * mm, (unsigned long)k));
-  }
-  return strip;
+  std::vector<Z> lo, hi;
+  build_moments(n, b.num, b.den, k, false, lo, hi);
+  return lo;
 }
 
 std::unique_ptr<Matrix> upload(const std::vector<Z>& strip, long k, int device) {
@@ -228,10 +225,51 @@ RunResult run(const RunConfig& cfg) {
     for (size_t s = 0; s < strip.size(); ++s)
       os << "s=" << s << " hex=" << strip[s].hex() << " fracbits=" << k << "\n";
   }
-  if (cfg.verify)
-    res.diagnosis =
-        "interval verification (ldlt_det_interval) is not run by the B200 "
-        "build; the value is not certified";
+  if (cfg.verify) {
+    // driver.cpp:140-175: certify on the interval matrix at Kv = 2K, doubling
+    // Kv while inconclusive.  The exact moments make lo = hi.
+    long kv = 2 * k;
+    for (;;) {
+      // build_interval_matrix (hankel_matrix.cpp:33-50)
+      std::vector<Z> vlo, vhi;
+      build_moments(cfg.n, cfg.beta.num, cfg.beta.den, kv, true, vlo, vhi);
+      std::vector<int32_t> sizes, sizes_hi;
+      std::vector<uint32_t> limbs, limbs_hi, tmp;
+      for (size_t i = 0; i < vlo.size(); ++i) {
+        sizes.push_back(vlo[i].to_limbs(tmp));
+        limbs.insert(limbs.end(), tmp.begin(), tmp.end());
+        sizes_hi.push_back(vhi[i].to_limbs(tmp));
+        limbs_hi.insert(limbs_hi.end(), tmp.begin(), tmp.end());
+      }
+      const auto tv = std::chrono::steady_clock::now();
+      hgpu_matrix* im = nullptr;
+      hgpu_status hs = hgpu_interval_matrix_new(
+          cfg.n, kv, sizes.data(), limbs.data(), sizes_hi.data(),
+          limbs_hi.data(), device_from_env(), &im);
+      int st = 2, ls = 0, us = 0;
+      char *pa = nullptr, *pb = nullptr;
+      if (hs == HGPU_OK)
+        hs = hgpu_verify_eigenvalue(im, res.eigenvalue.c_str(), 15, &st, &ls,
+                                    &us, &pa, &pb);
+      hgpu_matrix_free(im);
+      const std::string probe_low = pa ? pa : "";
+      hgpu_string_free(pa);
+      hgpu_string_free(pb);
+      if (hs != HGPU_OK) throw std::runtime_error(hgpu_last_error());
+      res.compute_s += std::chrono::duration<double>(
+                           std::chrono::steady_clock::now() - tv).count();
+      res.kv_bits = kv;
+      if (st == 0) {
+        res.verified = true;
+        break;
+      }
+      if (st == 1)
+        throw Refuted(
+            "refuted: interval verification contradicted the converged value at " +
+            probe_low);
+      kv = escalate(kv, cap);
+    }
+  }
   // condition_lower_bound (driver.cpp:48-54): M[n-1][n-1] / lambda_1
   res.condition_lower_bound =
       sig_digits(fx_div(strip[2 * cfg.n - 2], lam, k), k, 3, true);
@@ -470,6 +508,8 @@ heig_status heig_run(const heig_config* cfg, heig_result** result_out) {
     return heig_fail(HEIG_ERR_INVALID_ARGUMENT, e.what());
   } catch (const hgpu::PrecisionCap& e) {
     return heig_fail(HEIG_ERR_PRECISION_CAP, e.what());
+  } catch (const hgpu::Refuted& e) {
+    return heig_fail(HEIG_ERR_REFUTED, e.what());
   } catch (const std::exception& e) {
     return heig_fail(HEIG_ERR_INTERNAL, e.what());
   }

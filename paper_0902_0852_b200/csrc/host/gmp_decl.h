@@ -21,6 +21,9 @@ void __gmpz_init_set_si(hg_mpz_ptr, long);
 void __gmpz_clear(hg_mpz_ptr);
 void __gmpz_set(hg_mpz_ptr, hg_mpz_srcptr);
 void __gmpz_set_si(hg_mpz_ptr, long);
+void __gmpz_set_ui(hg_mpz_ptr, unsigned long);
+int __gmpz_root(hg_mpz_ptr, hg_mpz_srcptr, unsigned long);
+unsigned long __gmpz_fdiv_q_ui(hg_mpz_ptr, hg_mpz_srcptr, unsigned long);
 int __gmpz_set_str(hg_mpz_ptr, const char*, int);
 void __gmpz_swap(hg_mpz_ptr, hg_mpz_ptr);
 char* __gmpz_get_str(char*, int, hg_mpz_srcptr);

@@ -45,6 +45,7 @@ EXPORTS = (
     "hgpu_smallest_eigenvalue", "hgpu_string_free", "hgpu_inverse_iteration",
     "hgpu_interval_matrix_new", "hgpu_ldlt_interval", "hgpu_factor_pivot_hi",
     "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
+    "hgpu_build_moments", "hgpu_buffer_free",
 )
 
 
@@ -132,6 +133,11 @@ def load() -> ctypes.CDLL:
     lib.hgpu_verify_eigenvalue.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+    pp32 = ctypes.POINTER(ctypes.POINTER(ctypes.c_int32))
+    ppu32 = ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32))
+    lib.hgpu_build_moments.argtypes = [i64, ctypes.c_ulong, ctypes.c_ulong, i64, ctypes.c_int,
+                                       pp32, ppu32, pp32, ppu32]
+    lib.hgpu_buffer_free.argtypes = [ctypes.c_void_p]
     _lib = lib
     return lib
 
@@ -280,6 +286,35 @@ class HankelMatrixGPU:
             return res
         finally:
             lib.hgpu_factor_free(f)
+
+
+def build_moments(n: int, beta_num: int, beta_den: int, frac_bits: int, interval: bool = False):
+    """build_matrix / build_interval_matrix (hankel_matrix.cpp:13-50) on the
+    host: the strip (interval=False) or the (lo, hi) bound strips."""
+    lib = load()
+    ls, ll = ctypes.POINTER(ctypes.c_int32)(), ctypes.POINTER(ctypes.c_uint32)()
+    hs, hl = ctypes.POINTER(ctypes.c_int32)(), ctypes.POINTER(ctypes.c_uint32)()
+    _check(lib.hgpu_build_moments(n, beta_num, beta_den, frac_bits, int(interval), ctypes.byref(ls),
+                                  ctypes.byref(ll), ctypes.byref(hs), ctypes.byref(hl)))
+
+    def unpack(sz, lb):
+        out, off = [], 0
+        for s in range(2 * n - 1):
+            k = sz[s]
+            m = abs(k)
+            v = 0
+            for i in range(m - 1, -1, -1):
+                v = (v << 32) | lb[off + i]
+            off += m
+            out.append(-v if k < 0 else v)
+        return out
+
+    try:
+        lo, hi = unpack(ls, ll), unpack(hs, hl)
+    finally:
+        for p in (ls, ll, hs, hl):
+            lib.hgpu_buffer_free(ctypes.cast(p, ctypes.c_void_p))
+    return (lo, hi) if interval else lo
 
 
 class IntervalMatrixGPU(HankelMatrixGPU):

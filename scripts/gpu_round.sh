@@ -11,4 +11,4 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name k_update_tiled \
   --launch-skip 20 --launch-count 1 -o $out/k_update_full -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-lambda > $out/ncu_full.log 2>&1
 fi
-tail -3 $out/gpu_tests.log; cat $out/bench.json; tail -2 $out/bench.err; cat $out/bench_ref.json; tail -2 $out/ncu_launch.log $out/ncu_full.log
+tail -n 3 $out/gpu_tests.log; cat $out/bench.json; tail -n 2 $out/bench.err; cat $out/bench_ref.json; tail -n 2 $out/ncu_launch.log; tail -n 2 $out/ncu_full.log

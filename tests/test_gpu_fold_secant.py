@@ -121,7 +121,7 @@ def _heig_run(path, n, beta, k=0, verify=False):
     return 0, out
 
 
-@pytest.mark.parametrize("n,beta", [(4, "1/1"), (100, "1"), (40, "1/2")])
+@pytest.mark.parametrize("n,beta", [(4, "1/1"), (100, "1"), (40, "1/2"), (40, "7/4"), (30, "3/2")])
 def test_heig_run_c_abi_matches_reference(hg, n, beta):
     ours = _heig_run(hg.LIB_PATH, n, beta)
     theirs = _heig_run(po.REF_SO, n, beta)
@@ -130,6 +130,18 @@ def test_heig_run_c_abi_matches_reference(hg, n, beta):
         assert ours[1][key] == theirs[1][key], key
     assert set(ours[1]) == set(theirs[1])
     assert set(ours[1]["timing"]) == set(theirs[1]["timing"])
+
+
+@pytest.mark.parametrize("n,beta", [(4, "1/1"), (100, "1"), (40, "1/2"), (40, "7/4")])
+def test_heig_run_verify_matches_reference(hg, n, beta):
+    """heig_run with verification (driver.cpp:140-175): the GPU interval LDL^T
+    certifies the same value at the same Kv as the reference."""
+    ours = _heig_run(hg.LIB_PATH, n, beta, verify=True)
+    theirs = _heig_run(po.REF_SO, n, beta, verify=True)
+    assert ours[0] == 0 and theirs[0] == 0, (ours, theirs)
+    for key in ("eigenvalue", "k_bits", "kv_bits", "verified", "diagnosis"):
+        assert ours[1][key] == theirs[1][key], key
+    assert ours[1]["verified"] is True
 
 
 def test_heig_run_status_codes(hg):
