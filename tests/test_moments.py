@@ -41,3 +41,15 @@ def test_config2_moments_match_golden(hg):
 def test_moments_bad_arguments(hg):
     with pytest.raises(hg.HgpuError):
         hg.build_moments(0, 1, 1, 64)
+
+
+def test_config5_moments_digest(hg):
+    """BASELINE config 5 (N=2000, beta=3/2, P=32768): 3999 certified Gamma
+    moments, digest of the reference's own build_matrix output."""
+    d = json.load(open(os.path.join(GOLDEN, "moments_digests.json")))[0]
+    num, den = map(int, d["beta"].split("/"))
+    strip = hg.build_moments(d["n"], num, den, d["frac_bits"])
+    h = hashlib.sha256()
+    for v in strip:
+        h.update(po.to_hex(v).encode() + b"\n")
+    assert h.hexdigest() == d["strip_sha256"]
