@@ -40,8 +40,8 @@ __global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
   uint32_t* X = sm;                 // Wv
   uint32_t* C = X + Wv;             // cap
   uint32_t* Pr = C + cap;           // cap + Wv
-  uint32_t* col = Pr + cap + Wv;    // 3 (cap + Wv)
-  uint32_t* red = col + 3 * (cap + Wv);
+  uint32_t* col = Pr + cap + Wv;    // 4 (cap + Wv): room for 2+ segments
+  uint32_t* red = col + 4 * (cap + Wv);
   for (int i = threadIdx.x; i < nx; i += blockDim.x)
     X[i] = xv.limbs[(long long)xi * Wv + i];
   const int t0 = dir == 0 ? j + 1 : 0;
@@ -56,7 +56,7 @@ __global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
       C[i] = L.limbs[li * cap + i];
     __syncthreads();
     const int nP = nc + nx;
-    cta_mul(C, nc, X, nx, Pr, nP, col, red);
+    cta_mul(C, nc, X, nx, Pr, nP, col, red, 4 * (cap + Wv));
     uint32_t* a = acc + (long long)t * Wa;
     if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     cta_resolve(
@@ -159,7 +159,7 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
 }
 
 size_t solve_axpy_smem_words(int cap, int Wv) {
-  return (size_t)Wv + cap + (cap + Wv) + 3 * (size_t)(cap + Wv) + 64;
+  return (size_t)Wv + cap + (cap + Wv) + 4 * (size_t)(cap + Wv) + 64;
 }
 size_t solve_finish_smem_words(int Wv, int Wa) {
   return (size_t)(Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
