@@ -183,12 +183,12 @@ void Matrix::release() {
   release_interval();
   // inverse-iteration state (sized by the plan's capacity)
   for (void* p : {(void*)lhdr_, (void*)llimbs_, (void*)svhdr_, (void*)svlimbs_,
-                  (void*)sacc_, (void*)spair_hdr_,
+                  (void*)sacc_, (void*)sgscr_, (void*)spair_hdr_,
                   (void*)spair_limbs_, (void*)sbits_, (void*)sybuf_,
                   (void*)srscr_, (void*)sdscr_, (void*)sys_})
     dfree(p);
   lhdr_ = svhdr_ = spair_hdr_ = sbits_ = sys_ = nullptr;
-  llimbs_ = svlimbs_ = sacc_ = spair_limbs_ = sybuf_ = srscr_ =
+  llimbs_ = svlimbs_ = sacc_ = sgscr_ = spair_limbs_ = sybuf_ = srscr_ =
       sdscr_ = nullptr;
   have_L_ = false;
   tw_ = W_ = that_ = xhat_ = nullptr;
@@ -397,12 +397,14 @@ void Matrix::build(int min_logL) {
 
   // two slot sets: panel b uses set b%2 (lookahead needs b+1 while the
   // trailing update of b still reads b)
-  vhdr_ = dalloc<int>(2 * (size_t)kb * n_);
-  rhdr_ = dalloc<int>(2 * (size_t)kb * n_);
-  vlimbs_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
-  rlimbs_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
-  vhat_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * NW);
-  rhat_ = dalloc<uint32_t>(2 * (size_t)kb * n_ * NW);
+  // (the interval path has no lookahead: one slot set)
+  const size_t nsets = interval_ ? 1 : 2;
+  vhdr_ = dalloc<int>(nsets * kb * n_);
+  rhdr_ = dalloc<int>(nsets * kb * n_);
+  vlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
+  rlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
+  vhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
+  rhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
   phdr_ = dalloc<int>(n_);
   plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
   // reciprocal of stage p in set p & 1: recip(p+1) may run while the bulk
@@ -849,7 +851,11 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     sacc_ = dalloc<uint32_t>((size_t)n * sWa_);
     spair_hdr_ = dalloc<int>(2 * (size_t)n);
     spair_limbs_ = dalloc<uint32_t>(2 * (size_t)n * sWv_);
-    CU(configure_solve_kernels(P.cap, sWv_, sWa_));
+    bool axpy_global = false;
+    CU(configure_solve_kernels(P.cap, sWv_, sWa_, &axpy_global));
+    if (axpy_global)
+      sgscr_ = dalloc<uint32_t>((size_t)dp_.grid_cap *
+                                solve_axpy_smem_words(P.cap, sWv_));
   }
   // division plan: the LDL^T plan with integer capacity Wv (k_recip/k_divide
   // over pairs (piv_p, z_p 2^k2), scratch in global memory, no transform),
@@ -909,7 +915,7 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
   for (int p = 0; p < n; ++p) {
     CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)p * Wa, vecs, U + p,
                            vecs, Z + p, pairs, 2 * p + 1, k2, err_, st));
-    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Z + p, p, 0, sacc_,
+    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Z + p, p, 0, sacc_, sgscr_,
                          dp_.grid_cap, err_, st));
     nl += 2;
   }
@@ -925,7 +931,7 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
   for (int r = n - 1; r >= 0; --r) {
     CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)r * Wa, vecs, Wq + r,
                            vecs, Y + r, vecs, 0, 0, err_, st));
-    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Y + r, r, 1, sacc_,
+    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Y + r, r, 1, sacc_, sgscr_,
                          dp_.grid_cap, err_, st));
     nl += 2;
   }

@@ -153,6 +153,7 @@ class Matrix {
   int* svhdr_ = nullptr;        // vectors u | z | w | y (4n rows)
   uint32_t* svlimbs_ = nullptr;
   uint32_t* sacc_ = nullptr;    // n x Wa two's complement
+  uint32_t* sgscr_ = nullptr;   // k_solve_axpy scratch when SMEM is too small
   int* spair_hdr_ = nullptr;    // (piv_p, z_p 2^k2) pairs, 2n rows
   uint32_t* spair_limbs_ = nullptr;
   int* sbits_ = nullptr;

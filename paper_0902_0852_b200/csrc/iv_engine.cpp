@@ -132,18 +132,18 @@ void Matrix::build_interval() {
   x2_limbs_ = ialloc<uint32_t>(P.cap);
   ck(launch_fwd_ints(D, IntBuf{strip2_hdr_, strip2_limbs_}, 0, that2_, 0, ns, 0,
                      nullptr, err_, stream_));
-  vhdr2_ = ialloc<int>(2 * (size_t)kb * n_);
-  rhdr2_ = ialloc<int>(2 * (size_t)kb * n_);
-  vlimbs2_ = ialloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
-  rlimbs2_ = ialloc<uint32_t>(2 * (size_t)kb * n_ * P.cap);
-  vhat2_ = ialloc<uint32_t>(2 * (size_t)kb * n_ * NW);
-  rhat2_ = ialloc<uint32_t>(2 * (size_t)kb * n_ * NW);
+  vhdr2_ = ialloc<int>((size_t)kb * n_);
+  rhdr2_ = ialloc<int>((size_t)kb * n_);
+  vlimbs2_ = ialloc<uint32_t>((size_t)kb * n_ * P.cap);
+  rlimbs2_ = ialloc<uint32_t>((size_t)kb * n_ * P.cap);
+  vhat2_ = ialloc<uint32_t>((size_t)kb * n_ * NW);
+  rhat2_ = ialloc<uint32_t>((size_t)kb * n_ * NW);
   phdr2_ = ialloc<int>(n_);
   plimbs2_ = ialloc<uint32_t>((size_t)n_ * P.cap);
   ybuf2_ = ialloc<uint32_t>((size_t)P.ycap);
   ys2_ = ialloc<int>(4);
-  clsv_ = ialloc<int8_t>(2 * (size_t)kb * n_);
-  clsr_ = ialloc<int8_t>(2 * (size_t)kb * n_);
+  clsv_ = ialloc<int8_t>((size_t)kb * n_);
+  clsr_ = ialloc<int8_t>((size_t)kb * n_);
   int herr[kErrWords];
   ck(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, stream_));
   ck(cudaStreamSynchronize(stream_));

@@ -172,16 +172,19 @@ cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
 // solve_kernels.cu (inverse iteration)
 size_t solve_axpy_smem_words(int cap, int Wv);
 size_t solve_finish_smem_words(int Wv, int Wa);
+// gscratch: null (shared-memory operands) or solve_axpy_smem_words(cap, Wv)
+// words per CTA of global scratch (plans too large for shared memory)
 cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
                               IntBuf xv, int xi, int j, int dir, uint32_t* acc,
-                              int grid_cap, int* err, cudaStream_t st);
+                              uint32_t* gscratch, int grid_cap, int* err,
+                              cudaStream_t st);
 cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
                                 IntBuf base, int bi, IntBuf out, int oi,
                                 IntBuf out2, int o2i, int shift_out, int* err,
                                 cudaStream_t st);
 cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
                                   int count, int* out, cudaStream_t st);
-cudaError_t configure_solve_kernels(int cap, int Wv, int Wa);
+cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global);
 // fold_kernels.cu
 long long fold_pivots_device(const uint32_t* plimbs, const int* plen, int n,
                              int pcap, int K, uint32_t* X0, uint32_t* X1,

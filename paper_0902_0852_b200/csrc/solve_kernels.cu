@@ -19,6 +19,12 @@ namespace hgpu {
 
 namespace {
 
+// words of one k_solve_axpy CTA: X (Wv) | C (cap) | Pr (cap + Wv) |
+// col 3 (cap + Wv) | red 64
+__host__ __device__ inline long long solve_axpy_words(int cap, int Wv) {
+  return (long long)Wv + cap + (cap + Wv) + 3LL * (cap + Wv) + 64;
+}
+
 // index of R_p[r] (p < r < n) in the packed strictly-lower store
 __device__ __forceinline__ long long lidx(int n, int p, int r) {
   return (long long)p * (n - 1) - (long long)p * (p - 1) / 2 + (r - p - 1);
@@ -31,8 +37,13 @@ __device__ __forceinline__ long long lidx(int n, int p, int r) {
 //   back    (dir = 1): j = r, targets t = q in [0, r),  coefficient R_q[r]
 __global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
                              IntBuf xv, int xi, int j, int dir, uint32_t* acc,
-                             int* err) {
-  extern __shared__ uint32_t sm[];
+                             uint32_t* gscratch, int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  // operands and product scratch in shared memory, or (large plans) in this
+  // CTA's slice of a global scratch (L1/L2-resident)
+  uint32_t* sm = gscratch ? gscratch + (long long)blockIdx.x *
+                                           (long long)solve_axpy_words(cap, Wv)
+                          : sm_dyn;
   const int hx = xv.hdr[xi];
   const int nx = hx < 0 ? -hx : hx;
   if (nx == 0) return;  // nothing to add
@@ -40,8 +51,8 @@ __global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
   uint32_t* X = sm;                 // Wv
   uint32_t* C = X + Wv;             // cap
   uint32_t* Pr = C + cap;           // cap + Wv
-  uint32_t* col = Pr + cap + Wv;    // 4 (cap + Wv): room for 2+ segments
-  uint32_t* red = col + 4 * (cap + Wv);
+  uint32_t* col = Pr + cap + Wv;    // 3 (cap + Wv)
+  uint32_t* red = col + 3 * (cap + Wv);
   for (int i = threadIdx.x; i < nx; i += blockDim.x)
     X[i] = xv.limbs[(long long)xi * Wv + i];
   const int t0 = dir == 0 ? j + 1 : 0;
@@ -56,7 +67,7 @@ __global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
       C[i] = L.limbs[li * cap + i];
     __syncthreads();
     const int nP = nc + nx;
-    cta_mul(C, nc, X, nx, Pr, nP, col, red, 4 * (cap + Wv));
+    cta_mul(C, nc, X, nx, Pr, nP, col, red);
     uint32_t* a = acc + (long long)t * Wa;
     if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     cta_resolve(
@@ -159,7 +170,7 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
 }
 
 size_t solve_axpy_smem_words(int cap, int Wv) {
-  return (size_t)Wv + cap + (cap + Wv) + 4 * (size_t)(cap + Wv) + 64;
+  return (size_t)solve_axpy_words(cap, Wv);
 }
 size_t solve_finish_smem_words(int Wv, int Wa) {
   return (size_t)(Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
@@ -167,12 +178,13 @@ size_t solve_finish_smem_words(int Wv, int Wa) {
 
 cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
                               IntBuf xv, int xi, int j, int dir, uint32_t* acc,
-                              int grid_cap, int* err, cudaStream_t st) {
+                              uint32_t* gscratch, int grid_cap, int* err,
+                              cudaStream_t st) {
   const int rows = dir == 0 ? n - j - 1 : j;
   if (rows <= 0) return cudaSuccess;
-  const size_t smem = solve_axpy_smem_words(cap, Wv) * 4;
-  k_solve_axpy<<<min(rows, grid_cap), 256, smem, st>>>(n, cap, Wv, Wa, L, xv,
-                                                        xi, j, dir, acc, err);
+  const size_t smem = gscratch ? 0 : solve_axpy_smem_words(cap, Wv) * 4;
+  k_solve_axpy<<<min(rows, grid_cap), 256, smem, st>>>(
+      n, cap, Wv, Wa, L, xv, xi, j, dir, acc, gscratch, err);
   return cudaGetLastError();
 }
 
@@ -194,9 +206,14 @@ cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
   return cudaGetLastError();
 }
 
-cudaError_t configure_solve_kernels(int cap, int Wv, int Wa) {
+cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(
+  int dev = 0, maxopt = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  *axpy_global = solve_axpy_smem_words(cap, Wv) * 4 > (size_t)maxopt;
+  if (!*axpy_global &&
+      (e = cudaFuncSetAttribute(
            k_solve_axpy, cudaFuncAttributeMaxDynamicSharedMemorySize,
            (int)(solve_axpy_smem_words(cap, Wv) * 4))) != cudaSuccess)
     return e;
