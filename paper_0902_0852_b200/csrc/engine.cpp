@@ -855,7 +855,7 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     CU(configure_solve_kernels(P.cap, sWv_, sWa_, &axpy_global));
     if (axpy_global)
       sgscr_ = dalloc<uint32_t>((size_t)dp_.grid_cap *
-                                solve_axpy_smem_words(P.cap, sWv_));
+                                solve_axpy_smem_words(sWv_, P.cap, sWv_, sWa_));
   }
   // division plan: the LDL^T plan with integer capacity Wv (k_recip/k_divide
   // over pairs (piv_p, z_p 2^k2), scratch in global memory, no transform),
@@ -900,49 +900,62 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                        cudaMemcpyHostToDevice, st));
     CU(cudaStreamSynchronize(st));
   }
-  int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
-  CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
-  // pivots into the even rows of the pair buffer
-  CU(cudaMemcpy2DAsync(spair_hdr_, 2 * sizeof(int), phdr_, sizeof(int),
-                       sizeof(int), n, cudaMemcpyDeviceToDevice, st));
-  CU(cudaMemsetAsync(spair_limbs_, 0, 2 * (size_t)n * Wv * 4, st));
-  CU(cudaMemcpy2DAsync(spair_limbs_, 2 * (size_t)Wv * 4, plimbs_,
-                       (size_t)P.cap * 4, (size_t)P.cap * 4, n,
-                       cudaMemcpyDeviceToDevice, st));
+  // the AXPY's shared-memory layout at full operand capacities (measured:
+  // layouts sized to the operands actually met let the block scheduler pack
+  // more CTAs per SM and ran slower on this grid)
+  const int capX = Wv, capC = P.cap;
+  const int sgrid = dp_.grid_cap;
   long long nl = 0;
-  // forward: z_p = u_p - tdiv_2exp(acc_p, k2); acc_r += R_p[r] z_p (r > p)
-  CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
-  for (int p = 0; p < n; ++p) {
-    CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)p * Wa, vecs, U + p,
-                           vecs, Z + p, pairs, 2 * p + 1, k2, err_, st));
-    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Z + p, p, 0, sacc_, sgscr_,
-                         dp_.grid_cap, err_, st));
-    nl += 2;
-  }
-  // diagonal: w_p = tdiv(z_p 2^K, piv_p) with the LDL^T division kernels,
-  // all n independent divisions in one batched launch each
-  CU(launch_int_bits_batch(pairs, 1, 2, Wv, n, sbits_, st));
-  CU(launch_recip_batch(D2, pairs, 0, sbits_, sybuf_, sys_, srscr_, n, err_, st));
-  CU(launch_divide_batch(D2, pairs, 0, sybuf_, sys_, vecs, Wq - 1, sdscr_, n,
-                         err_, st));
-  nl += 3;
-  // back: y_r = w_r - tdiv_2exp(acc'_r, k2); acc'_q += R_q[r] y_r (q < r)
-  CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
-  for (int r = n - 1; r >= 0; --r) {
-    CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)r * Wa, vecs, Wq + r,
-                           vecs, Y + r, vecs, 0, 0, err_, st));
-    CU(launch_solve_axpy(n, P.cap, Wv, Wa, L, vecs, Y + r, r, 1, sacc_, sgscr_,
-                         dp_.grid_cap, err_, st));
-    nl += 2;
-  }
   int herr[kErrWords];
-  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
-  std::vector<int> yh(n);
+  std::vector<int> vh(4 * (size_t)n);
   std::vector<uint32_t> yl((size_t)n * Wv);
-  CU(cudaMemcpyAsync(yh.data(), svhdr_ + Y, n * 4, cudaMemcpyDeviceToHost, st));
-  CU(cudaMemcpyAsync(yl.data(), svlimbs_ + (size_t)Y * Wv, yl.size() * 4,
-                     cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  {
+    int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
+    CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+    // pivots into the even rows of the pair buffer
+    CU(cudaMemcpy2DAsync(spair_hdr_, 2 * sizeof(int), phdr_, sizeof(int),
+                         sizeof(int), n, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemsetAsync(spair_limbs_, 0, 2 * (size_t)n * Wv * 4, st));
+    CU(cudaMemcpy2DAsync(spair_limbs_, 2 * (size_t)Wv * 4, plimbs_,
+                         (size_t)P.cap * 4, (size_t)P.cap * 4, n,
+                         cudaMemcpyDeviceToDevice, st));
+    // forward: z_p = u_p - tdiv_2exp(acc_p, k2); acc_r += R_p[r] z_p (r > p)
+    CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
+    // (each step also finishes the next row, so one launch per step)
+    CU(launch_solve_finish(Wv, Wa, k2, sacc_,
+                           Finish{vecs, U, vecs, Z, pairs, 1, k2}, err_, st));
+    ++nl;
+    for (int p = 0; p + 1 < n; ++p) {
+      const Finish f{vecs, U + p + 1, vecs, Z + p + 1, pairs, 2 * (p + 1) + 1, k2};
+      CU(launch_solve_axpy(n, P.cap, Wv, Wa, k2, L, vecs, Z + p, p, 0, sacc_, f,
+                           capX, capC, sgscr_, sgrid, err_, st));
+      ++nl;
+    }
+    // diagonal: w_p = tdiv(z_p 2^K, piv_p) with the LDL^T division kernels,
+    // all n independent divisions in one batched launch each
+    CU(launch_int_bits_batch(pairs, 1, 2, Wv, n, sbits_, st));
+    CU(launch_recip_batch(D2, pairs, 0, sbits_, sybuf_, sys_, srscr_, n, err_, st));
+    CU(launch_divide_batch(D2, pairs, 0, sybuf_, sys_, vecs, Wq - 1, sdscr_, n,
+                           err_, st));
+    nl += 3;
+    // back: y_r = w_r - tdiv_2exp(acc'_r, k2); acc'_q += R_q[r] y_r (q < r)
+    CU(cudaMemsetAsync(sacc_, 0, (size_t)n * Wa * 4, st));
+    CU(launch_solve_finish(Wv, Wa, k2, sacc_ + (size_t)(n - 1) * Wa,
+                           Finish{vecs, Wq + n - 1, vecs, Y + n - 1, vecs, 0, 0},
+                           err_, st));
+    ++nl;
+    for (int r = n - 1; r >= 1; --r) {
+      const Finish f{vecs, Wq + r - 1, vecs, Y + r - 1, vecs, 0, 0};
+      CU(launch_solve_axpy(n, P.cap, Wv, Wa, k2, L, vecs, Y + r, r, 1, sacc_, f,
+                           capX, capC, sgscr_, sgrid, err_, st));
+      ++nl;
+    }
+    CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(vh.data(), svhdr_, vh.size() * 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(yl.data(), svlimbs_ + (size_t)Y * Wv, yl.size() * 4,
+                       cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
   if (launches) *launches += nl;
   if (herr[kErrCapacity])
     throw Error(HGPU_ERR_CAPACITY, "solve capacity exceeded (flags " +
@@ -951,6 +964,7 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     throw Error(HGPU_ERR_INTERNAL, "solve exactness self-check failed");
   if (herr[kErrZeroPivot] != INT_MAX)
     throw Error(HGPU_ERR_INTERNAL, "zero divisor in the diagonal solve");
+  std::vector<int> yh(vh.begin() + Y, vh.begin() + Y + n);
   std::vector<HostInt> y(n);
   for (int i = 0; i < n; ++i) {
     y[i].size = yh[i];

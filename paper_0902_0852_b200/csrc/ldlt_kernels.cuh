@@ -170,18 +170,31 @@ cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
                              int c_begin, int c_end, int r_min, int* err,
                              cudaStream_t st);
 // solve_kernels.cu (inverse iteration)
-size_t solve_axpy_smem_words(int cap, int Wv);
+size_t solve_axpy_smem_words(int capX, int capC, int Wv, int Wa);
 size_t solve_finish_smem_words(int Wv, int Wa);
-// gscratch: null (shared-memory operands) or solve_axpy_smem_words(cap, Wv)
-// words per CTA of global scratch (plans too large for shared memory)
-cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
+// One row's finish: out[oi] = base[bi] - tdiv_2exp(acc_row, k2) and, with
+// shift_out > 0, out2[o2i] = out[oi] << shift_out (the diagonal numerator).
+struct Finish {
+  IntBuf base;
+  int bi;
+  IntBuf out;
+  int oi;
+  IntBuf out2;
+  int o2i, shift_out;
+};
+// One solve step: every target row accumulates R * x_j; the first target's
+// finish (`fin`) runs in the same launch.  gscratch: null (shared-memory
+// operands) or solve_axpy_smem_words(cap, Wv) words per CTA of global
+// scratch (plans too large for shared memory).
+// capX / capC: the smem layout's operand capacities (x, R limbs); a larger
+// operand raises kCapLimbs and the host reruns with the full capacities
+cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
                               IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                              const Finish& fin, int capX, int capC,
                               uint32_t* gscratch, int grid_cap, int* err,
                               cudaStream_t st);
 cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
-                                IntBuf base, int bi, IntBuf out, int oi,
-                                IntBuf out2, int o2i, int shift_out, int* err,
-                                cudaStream_t st);
+                                const Finish& fin, int* err, cudaStream_t st);
 cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
                                   int count, int* out, cudaStream_t st);
 cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global);

@@ -19,10 +19,17 @@ namespace hgpu {
 
 namespace {
 
-// words of one k_solve_axpy CTA: X (Wv) | C (cap) | Pr (cap + Wv) |
-// col 3 (cap + Wv) | red 64
-__host__ __device__ inline long long solve_axpy_words(int cap, int Wv) {
-  return (long long)Wv + cap + (cap + Wv) + 3LL * (cap + Wv) + 64;
+// words of one k_solve_axpy CTA sized for operands of at most capX (x) and
+// capC (R) limbs: X | C | max(Pr (capX + capC) + col 3 (capX + capC), the
+// finish's scratch) | red 64
+__host__ __device__ inline long long solve_finish_words(int Wv, int Wa) {
+  return (long long)(Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
+}
+__host__ __device__ inline long long solve_axpy_words(int capX, int capC,
+                                                      int Wv, int Wa) {
+  const long long prod = 4LL * (capX + capC);
+  const long long fin = solve_finish_words(Wv, Wa);
+  return (long long)capX + capC + (prod > fin ? prod : fin) + 64;
 }
 
 // index of R_p[r] (p < r < n) in the packed strictly-lower store
@@ -32,63 +39,17 @@ __device__ __forceinline__ long long lidx(int n, int p, int r) {
 
 }  // namespace
 
-// acc_t += R(a, b) * x_j  for the targets of step j:
-//   forward (dir = 0): j = p, targets t = r in (p, n),  coefficient R_p[r]
-//   back    (dir = 1): j = r, targets t = q in [0, r),  coefficient R_q[r]
-__global__ void k_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
-                             IntBuf xv, int xi, int j, int dir, uint32_t* acc,
-                             uint32_t* gscratch, int* err) {
-  extern __shared__ uint32_t sm_dyn[];
-  // operands and product scratch in shared memory, or (large plans) in this
-  // CTA's slice of a global scratch (L1/L2-resident)
-  uint32_t* sm = gscratch ? gscratch + (long long)blockIdx.x *
-                                           (long long)solve_axpy_words(cap, Wv)
-                          : sm_dyn;
-  const int hx = xv.hdr[xi];
-  const int nx = hx < 0 ? -hx : hx;
-  if (nx == 0) return;  // nothing to add
-  const int sx = hx < 0 ? -1 : 1;
-  uint32_t* X = sm;                 // Wv
-  uint32_t* C = X + Wv;             // cap
-  uint32_t* Pr = C + cap;           // cap + Wv
-  uint32_t* col = Pr + cap + Wv;    // 3 (cap + Wv)
-  uint32_t* red = col + 3 * (cap + Wv);
-  for (int i = threadIdx.x; i < nx; i += blockDim.x)
-    X[i] = xv.limbs[(long long)xi * Wv + i];
-  const int t0 = dir == 0 ? j + 1 : 0;
-  const int t1 = dir == 0 ? n : j;
-  for (int t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-    const long long li = dir == 0 ? lidx(n, j, t) : lidx(n, t, j);
-    const int hc = L.hdr[li];
-    const int nc = hc < 0 ? -hc : hc;
-    if (nc == 0) continue;
-    const int sgn = (hc < 0 ? -1 : 1) * sx;
-    for (int i = threadIdx.x; i < nc; i += blockDim.x)
-      C[i] = L.limbs[li * cap + i];
-    __syncthreads();
-    const int nP = nc + nx;
-    cta_mul(C, nc, X, nx, Pr, nP, col, red);
-    uint32_t* a = acc + (long long)t * Wa;
-    if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
-    cta_resolve(
-        Wa, 32,
-        [&](int k) -> int64_t {
-          const int64_t pv = k < nP ? (int64_t)Pr[k] : 0;
-          return (int64_t)a[k] + (sgn > 0 ? pv : -pv);
-        },
-        [&](int k, uint32_t d) { col[k] = d; }, red);
-    for (int k = threadIdx.x; k < Wa; k += blockDim.x) a[k] = col[k];
-    __syncthreads();
-  }
-}
-
 // out_i = base_i - tdiv_2exp(acc_i, k2)   (single CTA; acc two's complement)
 // base/out are signed limb vectors of Wv limbs; `shift_out` > 0 additionally
 // stores out_i << shift_out into out2 (the diagonal step's numerator).
-__global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
-                               IntBuf base, int bi, IntBuf out, int oi,
-                               IntBuf out2, int o2i, int shift_out, int* err) {
-  extern __shared__ uint32_t sm[];
+__device__ void solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                             const Finish& f, uint32_t* sm, int* err) {
+  const IntBuf& base = f.base;
+  const int bi = f.bi;
+  const IntBuf& out = f.out;
+  const int oi = f.oi;
+  const IntBuf& out2 = f.out2;
+  const int o2i = f.o2i, shift_out = f.shift_out;
   uint32_t* M1 = sm;           // Wa + 1
   uint32_t* T = M1 + Wa + 1;   // Wv + 1
   uint32_t* X = T + Wv + 1;    // Wv + 2
@@ -157,6 +118,78 @@ __global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
   }
 }
 
+__global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                               Finish f, int* err) {
+  extern __shared__ uint32_t sm[];
+  solve_finish(Wv, Wa, k2, acc_i, f, sm, err);
+}
+
+// acc_t += R(a, b) * x_j  for the targets of step j:
+//   forward (dir = 0): j = p, targets t = r in (p, n),  coefficient R_p[r]
+//   back    (dir = 1): j = r, targets t = q in [0, r),  coefficient R_q[r]
+// The first target (p+1, resp. r-1) is complete after this step: CTA 0
+// takes it first and finishes it (solve_finish with `fin`), so the next
+// step's operand is ready without a separate launch.
+__global__ void __launch_bounds__(256) k_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
+                             IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                             Finish fin, int capX, int capC, uint32_t* gscratch,
+                             int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  // operands and product scratch in shared memory, or (large plans) in this
+  // CTA's slice of a global scratch (L1/L2-resident)
+  uint32_t* sm =
+      gscratch ? gscratch + (long long)blockIdx.x * solve_axpy_words(capX, capC, Wv, Wa)
+               : sm_dyn;
+  const int hx = xv.hdr[xi];
+  const int nx = hx < 0 ? -hx : hx;
+  const int sx = hx < 0 ? -1 : 1;
+  uint32_t* X = sm;                   // capX
+  uint32_t* C = X + capX;             // capC
+  uint32_t* Pr = C + capC;            // capX + capC (also the finish scratch)
+  uint32_t* col = Pr + capX + capC;   // 3 (capX + capC)
+  uint32_t* red = Pr + max(4LL * (capX + capC), solve_finish_words(Wv, Wa));
+  if (nx > capX) {  // the host sized the layout too small: it reruns
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return;
+  }
+  for (int i = threadIdx.x; i < nx; i += blockDim.x)
+    X[i] = xv.limbs[(long long)xi * Wv + i];
+  // targets in critical-first order: k = 0 is the row finished here
+  const int ntg = dir == 0 ? n - j - 1 : j;
+  for (int kk = blockIdx.x; kk < ntg; kk += gridDim.x) {
+    const int t = dir == 0 ? j + 1 + kk : j - 1 - kk;
+    const long long li = dir == 0 ? lidx(n, j, t) : lidx(n, t, j);
+    const int hc = L.hdr[li];
+    const int nc = hc < 0 ? -hc : hc;
+    if (nc == 0 || nx == 0) {
+      if (kk == 0) solve_finish(Wv, Wa, k2, acc + (long long)t * Wa, fin, Pr, err);
+      continue;
+    }
+    if (nc > capC) {
+      if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+      return;
+    }
+    const int sgn = (hc < 0 ? -1 : 1) * sx;
+    for (int i = threadIdx.x; i < nc; i += blockDim.x)
+      C[i] = L.limbs[li * cap + i];
+    __syncthreads();
+    const int nP = nc + nx;
+    cta_mul(C, nc, X, nx, Pr, nP, col, red);  // one segment per group (measured fastest here)
+    uint32_t* a = acc + (long long)t * Wa;
+    if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    cta_resolve(
+        Wa, 32,
+        [&](int k) -> int64_t {
+          const int64_t pv = k < nP ? (int64_t)Pr[k] : 0;
+          return (int64_t)a[k] + (sgn > 0 ? pv : -pv);
+        },
+        [&](int k, uint32_t d) { col[k] = d; }, red);
+    for (int k = threadIdx.x; k < Wa; k += blockDim.x) a[k] = col[k];
+    __syncthreads();
+    if (kk == 0) solve_finish(Wv, Wa, k2, a, fin, Pr, err);
+  }
+}
+
 // bits of the signed limb integers idx0 + b*step, b < count (the
 // reciprocal's precision bound for each batched division)
 __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
@@ -169,32 +202,32 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
   out[b] = n == 0 ? 0 : limbs_bits(v.limbs + idx * stride, n);
 }
 
-size_t solve_axpy_smem_words(int cap, int Wv) {
-  return (size_t)solve_axpy_words(cap, Wv);
+size_t solve_axpy_smem_words(int capX, int capC, int Wv, int Wa) {
+  return (size_t)solve_axpy_words(capX, capC, Wv, Wa);
 }
 size_t solve_finish_smem_words(int Wv, int Wa) {
-  return (size_t)(Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
+  return (size_t)solve_finish_words(Wv, Wa);
 }
 
-cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, IntBuf L,
+cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
                               IntBuf xv, int xi, int j, int dir, uint32_t* acc,
+                              const Finish& fin, int capX, int capC,
                               uint32_t* gscratch, int grid_cap, int* err,
                               cudaStream_t st) {
   const int rows = dir == 0 ? n - j - 1 : j;
   if (rows <= 0) return cudaSuccess;
-  const size_t smem = gscratch ? 0 : solve_axpy_smem_words(cap, Wv) * 4;
+  const size_t smem =
+      gscratch ? 0 : solve_axpy_smem_words(capX, capC, Wv, Wa) * 4;
   k_solve_axpy<<<min(rows, grid_cap), 256, smem, st>>>(
-      n, cap, Wv, Wa, L, xv, xi, j, dir, acc, gscratch, err);
+      n, cap, Wv, Wa, k2, L, xv, xi, j, dir, acc, fin, capX, capC, gscratch,
+      err);
   return cudaGetLastError();
 }
 
 cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
-                                IntBuf base, int bi, IntBuf out, int oi,
-                                IntBuf out2, int o2i, int shift_out, int* err,
-                                cudaStream_t st) {
+                                const Finish& fin, int* err, cudaStream_t st) {
   const size_t smem = solve_finish_smem_words(Wv, Wa) * 4;
-  k_solve_finish<<<1, 256, smem, st>>>(Wv, Wa, k2, acc_i, base, bi, out, oi,
-                                        out2, o2i, shift_out, err);
+  k_solve_finish<<<1, 256, smem, st>>>(Wv, Wa, k2, acc_i, fin, err);
   return cudaGetLastError();
 }
 
@@ -211,11 +244,13 @@ cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global) 
   int dev = 0, maxopt = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  *axpy_global = solve_axpy_smem_words(cap, Wv) * 4 > (size_t)maxopt;
+  // the attribute admits the worst-case layout; launches use the layout of
+  // the operand sizes actually met (more CTAs per SM)
+  *axpy_global = solve_axpy_smem_words(Wv, cap, Wv, Wa) * 4 > (size_t)maxopt;
   if (!*axpy_global &&
       (e = cudaFuncSetAttribute(
            k_solve_axpy, cudaFuncAttributeMaxDynamicSharedMemorySize,
-           (int)(solve_axpy_smem_words(cap, Wv) * 4))) != cudaSuccess)
+           (int)(solve_axpy_smem_words(Wv, cap, Wv, Wa) * 4))) != cudaSuccess)
     return e;
   return cudaFuncSetAttribute(k_solve_finish,
                               cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhgpu.so")
+LIB_PATH = os.environ.get("HGPU_LIB") or os.path.join(_HERE, "libhgpu.so")
 
 HGPU_CAPTURE = 1
 HGPU_FOLD = 2
