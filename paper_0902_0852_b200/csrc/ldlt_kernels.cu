@@ -1079,7 +1079,8 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
-  k_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
+  // a single row is on the pivot chain: give it more threads
+  k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, extract_smem_bytes(P), st>>>(
       P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
       maxdegV, err, round);
   return post_launch(st);
@@ -1157,7 +1158,7 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
                                    : divide_smem_words(P) * 4;
   ++g_launches;
-  k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
+  k_divide<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, smem, st>>>(
       P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
       gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
   return post_launch(st);
