@@ -58,17 +58,48 @@ double log2_u128(u128 v) {
 
 template <typename T>
 T* dalloc(size_t count) {
-  void* p = nullptr;
   if (count == 0) count = 1;
-  CU(cudaMalloc(&p, count * sizeof(T)));
-  return static_cast<T*>(p);
+  return static_cast<T*>(dev_alloc(count * sizeof(T)));
 }
 
-void dfree(void* p) {
-  if (p) cudaFree(p);
-}
+void dfree(void* p) { dev_free(p); }
 
 }  // namespace
+
+void* dev_alloc(size_t bytes) {
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  CU(cudaDeviceGetDefaultMemPool(&pool, dev));
+  static thread_local int configured = -1;
+  if (configured != dev) {
+    uint64_t keep = UINT64_MAX;  // keep freed blocks in the pool
+    CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    configured = dev;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, 0);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemPoolTrimTo(pool, 0));
+    e = cudaMallocFromPoolAsync(&p, bytes, pool, 0);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(HGPU_ERR_CUDA, std::string("device allocation failed: ") +
+                                   cudaGetErrorString(e));
+  }
+  // the legacy stream orders the allocation; our streams are non-blocking
+  CU(cudaStreamSynchronize(0));
+  return p;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();  // no stream may still use it
+  cudaFreeAsync(p, 0);
+}
 
 int block_owner(long block, int world) {
   // reflected round-robin, assignment.hpp:15-23, over column blocks

@@ -21,6 +21,13 @@ struct Error : std::runtime_error {
       : std::runtime_error(what), status(s) {}
 };
 
+// Device memory from the device's stream-ordered pool, which keeps freed
+// blocks for reuse: building a matrix (GBs of workspace) after another one
+// costs no cudaMalloc.  On exhaustion the pool is trimmed and the
+// allocation retried.  dev_free waits for the device first.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p);
+
 // Signed limb integer (GMP-style size) on the host.
 struct HostInt {
   int32_t size = 0;

@@ -30,15 +30,10 @@ namespace {
 
 template <class T>
 T* ialloc(size_t count) {
-  void* p = nullptr;
-  if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess)
-    throw Error(HGPU_ERR_CUDA, "device allocation failed");
-  return static_cast<T*>(p);
+  return static_cast<T*>(dev_alloc(std::max<size_t>(count, 1) * sizeof(T)));
 }
 
-void ifree(void* p) {
-  if (p) cudaFree(p);
-}
+void ifree(void* p) { dev_free(p); }
 
 void ck(cudaError_t e) {
   if (e != cudaSuccess) throw Error(HGPU_ERR_CUDA, cudaGetErrorString(e));
