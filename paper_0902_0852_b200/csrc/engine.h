@@ -181,6 +181,7 @@ class Matrix {
   uint32_t *vhat2_ = nullptr, *rhat2_ = nullptr, *ybuf2_ = nullptr;
   int* ys2_ = nullptr;
   int8_t *clsv_ = nullptr, *clsr_ = nullptr;
+  int* ivgate_ = nullptr;  // {INT_MAX, nonpositive bound seen, 0, 0}
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
   // HGPU_TIMELINE=<file>: per-launch start/end events (scheduling analysis)
   struct TlRec {

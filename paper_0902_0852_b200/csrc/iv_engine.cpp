@@ -139,6 +139,7 @@ void Matrix::build_interval() {
   ys2_ = ialloc<int>(4);
   clsv_ = ialloc<int8_t>((size_t)kb * n_);
   clsr_ = ialloc<int8_t>((size_t)kb * n_);
+  ivgate_ = ialloc<int>(4);
   int herr[kErrWords];
   ck(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, stream_));
   ck(cudaStreamSynchronize(stream_));
@@ -152,8 +153,9 @@ void Matrix::release_interval() {
                   (void*)vhdr2_, (void*)rhdr2_, (void*)phdr2_, (void*)vlimbs2_,
                   (void*)rlimbs2_, (void*)plimbs2_, (void*)vhat2_,
                   (void*)rhat2_, (void*)ybuf2_, (void*)ys2_, (void*)clsv_,
-                  (void*)clsr_})
+                  (void*)clsr_, (void*)ivgate_})
     ifree(p);
+  ivgate_ = nullptr;
   W2_ = that2_ = xhat2_ = strip2_limbs_ = x2_limbs_ = vlimbs2_ = rlimbs2_ =
       plimbs2_ = vhat2_ = rhat2_ = ybuf2_ = nullptr;
   strip2_hdr_ = x2_hdr_ = vhdr2_ = rhdr2_ = phdr2_ = ys2_ = nullptr;
@@ -201,22 +203,52 @@ void Matrix::run_interval(const HostInt& xlo, const HostInt& xhi,
   IntBuf rlo{rhdr_, rlimbs_}, rhi{rhdr2_, rlimbs2_};
   IntBuf plo{phdr_, plimbs_}, phi{phdr2_, plimbs2_};
   const long long slot_stride = (long long)n * NW;
-  (void)slot_stride;
+  // Panels whose V and R bounds are all positive (the common case: Hankel
+  // moment matrices are totally positive) take the tiled point kernels with
+  // the operand bounds swapped -- W.lo -= V.hi R.hi, W.hi -= V.lo R.lo, the
+  // max / min corners for positive intervals -- and the selecting kernel
+  // otherwise.  ivgate_ = {INT_MAX, nonpositive-seen, 0, 0} reads as an error
+  // word for the point kernels (they skip when it is set) and as the gate of
+  // k_update_iv (it runs only when it is set).
+  {
+    const int g[4] = {INT_MAX, 0, 0, 0};
+    ck(cudaMemcpyAsync(ivgate_, g, sizeof(g), cudaMemcpyHostToDevice, st));
+    ck(cudaStreamSynchronize(st));
+  }
+  int* nonpos = ivgate_ + kErrCapacity;
+  auto iv_update = [&](int s_end, int c_begin, int c_end, bool col) {
+    if (s_end <= 0) return;
+    if (col) {
+      ck(launch_update_col(D, W_, colbase_, vhat2_, rhat2_, slot_stride, s_end,
+                           c_begin, c_begin, n, ivgate_, st));
+      ck(launch_update_col(D, W2_, colbase_, vhat_, rhat_, slot_stride, s_end,
+                           c_begin, c_begin, n, ivgate_, st));
+    } else {
+      ck(launch_update(D, P.tile, W_, colbase_, vhat2_, rhat2_, slot_stride,
+                       s_end, c_begin, c_end, ivgate_, st));
+      ck(launch_update(D, P.tile, W2_, colbase_, vhat_, rhat_, slot_stride,
+                       s_end, c_begin, c_end, ivgate_, st));
+    }
+    ck(launch_update_iv(D, W_, W2_, colbase_, vhat_, vhat2_, rhat_, rhat2_,
+                        clsv_, clsr_, 0, s_end, c_begin, c_end, c_begin, nonpos,
+                        err_, st));
+  };
   const int nblocks = (n + kb - 1) / kb;
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb);
     const long long row0set = 0;  // one slot set: no lookahead here
+    ck(cudaMemsetAsync(nonpos, 0, sizeof(int), st));
     for (int p = p0; p < p1; ++p) {
       const int s = p - p0;
       const long long row0 = row0set + (long long)s * n;
       // column p receives the panel's earlier stages (left-looking)
-      ck(launch_update_iv(D, W_, W2_, colbase_, vhat_, vhat2_, rhat_, rhat2_,
-                          clsv_, clsr_, 0, s, p, p + 1, p, err_, st));
+      iv_update(s, p, p + 1, true);
       ck(launch_extract(D, W_, colbase_, p, p, n, vlo, row0, plo, maxbitsV,
                         vhat_, maxdegV, err_, st, 1));
       ck(launch_extract(D, W2_, colbase_, p, p, n, vhi, row0, phi, maxbitsV,
                         vhat2_, maxdegV, err_, st, 2));
-      ck(launch_iv_classify(vlo, vhi, row0, p, n, clsv_, p, 1, n, err_, st));
+      ck(launch_iv_classify(vlo, vhi, row0, p, n, clsv_, p, 1, n, err_, nonpos,
+                            st));
       if (p == n - 1) break;
       ck(launch_recip(D, vlo, row0 + p, maxbitsV, p, plo, 0, ybuf_, ys_,
                       rscratch_, recip_global_ ? 1 : 0, err_, st));
@@ -230,13 +262,12 @@ void Matrix::run_interval(const HostInt& xlo, const HostInt& xhi,
       ck(launch_divide(D, vlo, row0, p, p + 1, n, ybuf_, ys_, rhi, row0, rhat2_,
                        maxdegR + p, dscratch_, div_global_ ? 1 : 0, err_, st,
                        &ivh));
-      ck(launch_iv_classify(rlo, rhi, row0, p + 1, n, clsr_, p, 0, n, err_, st));
+      ck(launch_iv_classify(rlo, rhi, row0, p + 1, n, clsr_, p, 0, n, err_,
+                            nonpos, st));
     }
     // trailing update of the panel's stages on every column to its right
     const int nsl = std::min(kb, n - 1 - p0);
-    if (p1 < n && nsl > 0)
-      ck(launch_update_iv(D, W_, W2_, colbase_, vhat_, vhat2_, rhat_, rhat2_,
-                          clsv_, clsr_, 0, nsl, p1, n, p1, err_, st));
+    if (p1 < n && nsl > 0) iv_update(nsl, p1, n, false);
   }
   ck(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));
   ck(cudaEventRecord(ev1_, st));

@@ -42,11 +42,12 @@ __device__ __forceinline__ int sel_min(int cv, int cr) {
 // (ldlt.cpp:110-111: ZeroPivot).
 __global__ void k_iv_classify(IntBuf lo, IntBuf hi, long long row0, int r_begin,
                               int r_end, int8_t* cls, int p, int check_pivot,
-                              int n, int* err) {
+                              int n, int* err, int* nonpos) {
   for (int r = r_begin + blockIdx.x * blockDim.x + threadIdx.x; r < r_end;
        r += gridDim.x * blockDim.x) {
     const int c = iv_class(lo.hdr[row0 + r], hi.hdr[row0 + r]);
     cls[row0 + r] = (int8_t)c;
+    if (c <= 0 && nonpos) atomicOr(nonpos, 1);
     if (check_pivot && r == p && c == 0 && p < n - 1)
       atomicMin(&err[kErrZeroPivot], p);
   }
@@ -64,10 +65,12 @@ k_update_iv(DevPlan P, uint32_t* Wlo, uint32_t* Whi, const long long* colbase,
             const uint32_t* Vlo, const uint32_t* Vhi, const uint32_t* Rlo,
             const uint32_t* Rhi, const int8_t* clsV, const int8_t* clsR,
             int s_begin, int s_end, int c_begin, int c_end, int r_min,
-            int nrt, int* err) {
+            int nrt, const int* gate, int* err) {
   if (*(volatile const int*)&err[kErrZeroPivot] != INT_MAX ||
       *(volatile const int*)&err[kErrCapacity] != 0)
     return;
+  // all-positive panels take the tiled point kernels instead (iv_engine.cpp)
+  if (gate && *(volatile const int*)gate == 0) return;
   const int wd = blockIdx.y * blockDim.x + threadIdx.x;
   if (wd >= P.NW) return;
   const int n = P.n;
@@ -134,12 +137,12 @@ k_update_iv(DevPlan P, uint32_t* Wlo, uint32_t* Whi, const long long* colbase,
 
 cudaError_t launch_iv_classify(IntBuf lo, IntBuf hi, long long row0,
                                int r_begin, int r_end, int8_t* cls, int p,
-                               int check_pivot, int n, int* err,
+                               int check_pivot, int n, int* err, int* nonpos,
                                cudaStream_t st) {
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   k_iv_classify<<<(rows + 255) / 256, 256, 0, st>>>(
-      lo, hi, row0, r_begin, r_end, cls, p, check_pivot, n, err);
+      lo, hi, row0, r_begin, r_end, cls, p, check_pivot, n, err, nonpos);
   return cudaGetLastError();
 }
 
@@ -148,8 +151,8 @@ cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
                              const uint32_t* Vhi, const uint32_t* Rlo,
                              const uint32_t* Rhi, const int8_t* clsV,
                              const int8_t* clsR, int s_begin, int s_end,
-                             int c_begin, int c_end, int r_min, int* err,
-                             cudaStream_t st) {
+                             int c_begin, int c_end, int r_min,
+                             const int* gate, int* err, cudaStream_t st) {
   if (c_begin >= c_end || s_begin >= s_end) return cudaSuccess;
   const int rbase = std::max(c_begin, r_min);
   if (rbase >= P.n) return cudaSuccess;
@@ -158,7 +161,7 @@ cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
   const dim3 grid((unsigned)(nct * nrt), (unsigned)((P.NW + 127) / 128));
   k_update_iv<<<grid, 128, 0, st>>>(P, Wlo, Whi, colbase, Vlo, Vhi, Rlo, Rhi,
                                     clsV, clsR, s_begin, s_end, c_begin, c_end,
-                                    r_min, nrt, err);
+                                    r_min, nrt, gate, err);
   return cudaGetLastError();
 }
 

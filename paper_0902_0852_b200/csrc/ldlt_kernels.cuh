@@ -158,17 +158,18 @@ cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             cudaStream_t st);
 long long kernel_launch_count();
 // iv_kernels.cu (interval LDL^T)
+// nonpos (optional): set to 1 when some class is not +1
 cudaError_t launch_iv_classify(IntBuf lo, IntBuf hi, long long row0,
                                int r_begin, int r_end, int8_t* cls, int p,
-                               int check_pivot, int n, int* err,
+                               int check_pivot, int n, int* err, int* nonpos,
                                cudaStream_t st);
 cudaError_t launch_update_iv(const DevPlan& P, uint32_t* Wlo, uint32_t* Whi,
                              const long long* colbase, const uint32_t* Vlo,
                              const uint32_t* Vhi, const uint32_t* Rlo,
                              const uint32_t* Rhi, const int8_t* clsV,
                              const int8_t* clsR, int s_begin, int s_end,
-                             int c_begin, int c_end, int r_min, int* err,
-                             cudaStream_t st);
+                             int c_begin, int c_end, int r_min,
+                             const int* gate, int* err, cudaStream_t st);
 // solve_kernels.cu (inverse iteration)
 size_t solve_axpy_smem_words(int capX, int capC, int Wv, int Wa);
 size_t solve_finish_smem_words(int Wv, int Wa);
