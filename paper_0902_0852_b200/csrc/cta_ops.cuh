@@ -421,11 +421,44 @@ __device__ __forceinline__ int limbs_bits(const uint32_t* a, int len) {
   return len == 0 ? 0 : 32 * (len - 1) + (32 - __clz(a[len - 1]));
 }
 
+// Column sums of a*b for the G columns k0..k0+G-1 over i in [ilo, ihi]:
+// acc[t] + cc[t] 2^64 += sum_i a[i] b[k0+t-i].  The i-loop is unrolled by G,
+// so the b-window sits in static registers (2G-1 values per block) and every
+// product is one IMAD.WIDE.U32 with carry-out plus one IMAD.X, with G
+// independent accumulator chains (measured 2x the throughput of the rolled
+// loop, whose window shifts and CC chains cost register moves).
+template <int G>
+__device__ __forceinline__ void col_block(const uint32_t* a, const uint32_t* b,
+                                          int nb, int k0, int ilo, int ihi,
+                                          uint64_t* acc, uint32_t* cc) {
+  for (int i = ilo; i <= ihi; i += G) {
+    uint32_t av[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) av[u] = (i + u <= ihi) ? a[i + u] : 0u;
+    uint32_t bw[2 * G - 1];  // bw[m] = b[k0 - i - (G-1) + m]
+#pragma unroll
+    for (int m = 0; m < 2 * G - 1; ++m) {
+      const int j = k0 - i - (G - 1) + m;
+      bw[m] = (j >= 0 && j < nb) ? b[j] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+#pragma unroll
+      for (int t = 0; t < G; ++t)
+        asm("{\n\t.reg .u64 pr;\n\t"
+            "mul.wide.u32 pr, %2, %3;\n\t"
+            "add.cc.u64 %0, %0, pr;\n\t"
+            "addc.u32 %1, %1, 0;\n\t}"
+            : "+l"(acc[t]), "+r"(cc[t])
+            : "r"(av[u]), "r"(bw[G - 1 + t - u]));
+  }
+}
+
 // out[0..M) = low M limbs of a*b (M <= na+nb gives the exact product when
 // M == na+nb).  Product scanning: a work item is a group of 8 consecutive
 // output columns times one segment of its i-range, so long middle columns
 // are split across threads (load balance); each item keeps 96-bit column
-// sums on PTX carry chains and writes them to its segment's planes.
+// sums (col_block) and writes them to its segment's planes.
 // col: scratch of `col_words` >= 3*M words (more words allow more segments);
 // out must not alias a, b or col.  red: blockDim/32+1 words.
 // With k_begin > 0 only columns [k_begin, M) are formed (a "short product"):
@@ -452,46 +485,24 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int g = nseg == 1 ? it : it / nseg, sgi = it - g * nseg;
     const int k0 = k_begin + g * G;
-    uint32_t c0[G], c1[G], c2[G];
+    uint64_t acc[G];
+    uint32_t c2[G];
 #pragma unroll
-    for (int t = 0; t < G; ++t) c0[t] = c1[t] = c2[t] = 0u;
+    for (int t = 0; t < G; ++t) acc[t] = 0ull, c2[t] = 0u;
     if (na > 0 && nb > 0) {
       const int glo = max(0, k0 - nb + 1);
       const int ghi = min(k0 + G - 1, na - 1);
       const int ilo = glo + sgi * seglen;
       const int ihi = min(ghi, ilo + seglen - 1);
-      if (ilo <= ihi) {
-        // window w[t] = b[k0 + t - i]
-        uint32_t w[G];
-#pragma unroll
-        for (int t = 0; t < G; ++t) {
-          const int j = k0 + t - ilo;
-          w[t] = (j >= 0 && j < nb) ? b[j] : 0u;
-        }
-        for (int i = ilo; i <= ihi; ++i) {
-          const uint32_t ai = a[i];
-#pragma unroll
-          for (int t = 0; t < G; ++t) {
-            asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
-                "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
-                "addc.u32 %2, %2, 0;"
-                : "+r"(c0[t]), "+r"(c1[t]), "+r"(c2[t])
-                : "r"(ai), "r"(w[t]));
-          }
-#pragma unroll
-          for (int t = G - 1; t > 0; --t) w[t] = w[t - 1];
-          const int j = k0 - i - 1;
-          w[0] = (j >= 0 && j < nb) ? b[j] : 0u;
-        }
-      }
+      if (ilo <= ihi) col_block<G>(a, b, nb, k0, ilo, ihi, acc, c2);
     }
     uint32_t* pl = col + (size_t)sgi * 3 * M;
 #pragma unroll
     for (int t = 0; t < G; ++t) {
       const int k = k0 + t - k_begin;
       if (k < M) {
-        pl[k] = c0[t];
-        pl[M + k] = c1[t];
+        pl[k] = (uint32_t)acc[t];
+        pl[M + k] = (uint32_t)(acc[t] >> 32);
         pl[2 * M + k] = c2[t];
       }
     }
@@ -539,23 +550,28 @@ __device__ inline void cta_mul(const uint32_t* a, int na, const uint32_t* b,
       [&](int k, uint32_t d) { out[k] = d; }, red);
 }
 
-// Warp version of cta_mul (full product columns [0, M)): lane-strided
-// columns, one 96-bit column sum each, then a warp carry resolution.
+// Warp version of cta_mul (full product columns [0, M)): each lane forms
+// groups of 4 consecutive columns (col_block), then a warp carry resolution.
 // col: 3*M words; out must not alias a, b or col.
 __device__ inline void warp_mul(const uint32_t* a, int na, const uint32_t* b,
                                 int nb, uint32_t* out, int M, uint32_t* col) {
-  for (int k = threadIdx.x & 31; k < M; k += 32) {
-    uint32_t c0 = 0, c1 = 0, c2 = 0;
-    const int ilo = max(0, k - nb + 1), ihi = min(k, na - 1);
-    for (int i = ilo; i <= ihi; ++i)
-      asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
-          "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
-          "addc.u32 %2, %2, 0;"
-          : "+r"(c0), "+r"(c1), "+r"(c2)
-          : "r"(a[i]), "r"(b[k - i]));
-    col[k] = c0;
-    col[M + k] = c1;
-    col[2 * M + k] = c2;
+  constexpr int G = 4;
+  for (int k0 = (threadIdx.x & 31) * G; k0 < M; k0 += 32 * G) {
+    uint64_t acc[G];
+    uint32_t c2[G];
+#pragma unroll
+    for (int t = 0; t < G; ++t) acc[t] = 0ull, c2[t] = 0u;
+    const int ilo = max(0, k0 - nb + 1), ihi = min(k0 + G - 1, na - 1);
+    if (ilo <= ihi) col_block<G>(a, b, nb, k0, ilo, ihi, acc, c2);
+#pragma unroll
+    for (int t = 0; t < G; ++t) {
+      const int k = k0 + t;
+      if (k < M) {
+        col[k] = (uint32_t)acc[t];
+        col[M + k] = (uint32_t)(acc[t] >> 32);
+        col[2 * M + k] = c2[t];
+      }
+    }
   }
   __syncwarp();
   warp_resolve(

@@ -1,6 +1,8 @@
 // Host side of the B200 LDL^T engine (see engine.h).
 #include "engine.h"
 
+#include <cublas_v2.h>
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -9,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 namespace hgpu {
 
@@ -54,6 +57,89 @@ int bitrev(int x, int bits) {
 double log2_u128(u128 v) {
   return std::log2((double)(u64)(v >> 64) * 18446744073709551616.0 +
                    (double)(u64)v);
+}
+
+// ---- SM partition (green contexts) ---------------------------------------
+// The pivot chain (one-row update, extraction, reciprocal, one-row division)
+// is a sequence of single-CTA, latency-bound kernels: on an SM shared with
+// trailing-update CTAs (which keep the IMAD pipe ~80 % busy) every one of its
+// dependent instructions waits for issue, and each launch first queues for a
+// free slot.  The chain therefore runs on a reserved group of SMs (a green
+// context) and the trailing update on the rest.  Driver entry points are
+// fetched through the runtime, so the library does not link libcuda.
+// HGPU_SM_SPLIT=<chain SMs>[:<panel stream on a (chain group) | b (update
+// group) | p (primary context, every SM)>], "0" disables.
+struct GreenSplit {
+  bool ok = false;
+  int chain_sms = 0, rest_sms = 0;
+  char panel = 'a';
+  CUgreenCtx ga = nullptr, gb = nullptr;
+};
+
+GreenSplit make_green_split(int device) {
+  GreenSplit g;
+  int want = 0;  // off by default: measured slower at config 3
+  if (const char* s = std::getenv("HGPU_SM_SPLIT")) {
+    want = std::atoi(s);
+    if (const char* c = std::strchr(s, ':')) g.panel = c[1];
+  }
+  if (want <= 0) return g;
+  auto sym = [](const char* name) -> void* {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return fn;
+  };
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*,
+                             CUdevResource*, unsigned, unsigned);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+  using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+  auto get_res = (GetRes)sym("cuDeviceGetDevResource");
+  auto split = (Split)sym("cuDevSmResourceSplitByCount");
+  auto gen = (GenDesc)sym("cuDevResourceGenerateDesc");
+  auto create = (Create)sym("cuGreenCtxCreate");
+  if (!get_res || !split || !gen || !create) return g;
+  CUdevResource all, grp, rest;
+  if (get_res((CUdevice)device, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return g;
+  unsigned ng = 1;
+  if (split(&grp, &ng, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || ng != 1)
+    return g;
+  CUdevResourceDesc da, db;
+  if (gen(&da, &grp, 1) != CUDA_SUCCESS || gen(&db, &rest, 1) != CUDA_SUCCESS) return g;
+  if (create(&g.ga, da, (CUdevice)device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      create(&g.gb, db, (CUdevice)device, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return g;
+  g.chain_sms = (int)grp.sm.smCount;
+  g.rest_sms = (int)rest.sm.smCount;
+  g.ok = true;
+  return g;
+}
+
+// One split per device for the process (green contexts are kept alive).
+const GreenSplit& green_split(int device) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, GreenSplit>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : cache)
+    if (e.first == device) return e.second;
+  cache.emplace_back(device, make_green_split(device));
+  return cache.back().second;
+}
+
+cudaStream_t green_stream(CUgreenCtx g, int priority) {
+  using SCreate = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuGreenCtxStreamCreate", &fn, cudaEnableDefault, &q) !=
+          cudaSuccess || q != cudaDriverEntryPointSuccess)
+    throw Error(HGPU_ERR_CUDA, "cuGreenCtxStreamCreate unavailable");
+  CUstream s = nullptr;
+  if (((SCreate)fn)(&s, g, CU_STREAM_NON_BLOCKING, priority) != CUDA_SUCCESS)
+    throw Error(HGPU_ERR_CUDA, "cuGreenCtxStreamCreate failed");
+  return (cudaStream_t)s;
 }
 
 template <typename T>
@@ -176,15 +262,38 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (device < 0 || device >= ndev)
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad device index");
   CU(cudaSetDevice(device_));
-  CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
-    CU(cudaStreamCreateWithPriority(&stream_helper_, cudaStreamNonBlocking, hi));
+    const GreenSplit& g = green_split(device_);
+    if (g.ok) {
+      // bulk stream on the large group, pivot chain on the reserved SMs;
+      // the panel stream where HGPU_SM_SPLIT places it
+      stream_ = green_stream(g.gb, 0);
+      stream_helper_ = green_stream(g.ga, hi);
+      stream_far_ = green_stream(g.gb, hi);
+      if (g.panel == 'b')
+        stream_panel_ = green_stream(g.gb, hi);
+      else if (g.panel == 'a')
+        stream_panel_ = green_stream(g.ga, hi);
+      else
+        CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
+      chain_sms_ = g.chain_sms;
+    } else {
+      CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+      CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&stream_helper_, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&stream_far_, cudaStreamNonBlocking, hi));
+    }
   }
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
+  if (const char* e = std::getenv("HGPU_NEAR")) near_rows_ = std::max(2, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_RATIO_GEMM")) ratio_gemm_ = std::atoi(e);
+  if (ratio_gemm_)
+    for (int i = 0; i < 2; ++i)
+      if (cublasCreate((cublasHandle_t*)&blas_[i]) != CUBLAS_STATUS_SUCCESS)
+        throw Error(HGPU_ERR_CUDA, "cublasCreate failed");
 }
 
 Matrix::~Matrix() {
@@ -197,6 +306,9 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : pev_) cudaEventDestroy(e);
   for (cudaEvent_t e : sev_) cudaEventDestroy(e);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
+  for (void* h : blas_)
+    if (h) cublasDestroy((cublasHandle_t)h);
+  if (stream_far_) cudaStreamDestroy(stream_far_);
   if (stream_helper_) cudaStreamDestroy(stream_helper_);
   if (stream_panel_) cudaStreamDestroy(stream_panel_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -208,7 +320,9 @@ void Matrix::release() {
                   (void*)x_hdr_, (void*)x_limbs_, (void*)vhdr_, (void*)vlimbs_,
                   (void*)rhdr_, (void*)rlimbs_, (void*)vhat_, (void*)rhat_,
                   (void*)phdr_, (void*)plimbs_, (void*)ybuf_, (void*)rscratch_,
-                  (void*)dscratch_, (void*)dscratch2_, (void*)ys_,
+                  (void*)dscratch_, (void*)dscratch2_, (void*)dscratch3_, (void*)ys_,
+                  (void*)vdig_, (void*)rg_t_[0], (void*)rg_t_[1], (void*)rg_c_[0],
+                  (void*)rg_c_[1], (void*)rg_ws_[0], (void*)rg_ws_[1],
                   (void*)stats_, (void*)err_})
     dfree(p);
   release_interval();
@@ -226,7 +340,11 @@ void Matrix::release() {
   colbase_ = nullptr;
   strip_hdr_ = x_hdr_ = vhdr_ = rhdr_ = phdr_ = ys_ = stats_ = err_ = nullptr;
   strip_limbs_ = x_limbs_ = vlimbs_ = rlimbs_ = vhat_ = rhat_ = plimbs_ =
-      ybuf_ = rscratch_ = dscratch_ = dscratch2_ = nullptr;
+      ybuf_ = rscratch_ = dscratch_ = dscratch2_ = dscratch3_ = nullptr;
+  vdig_ = rg_t_[0] = rg_t_[1] = nullptr;
+  rg_ws_[0] = rg_ws_[1] = nullptr;
+  rg_c_[0] = rg_c_[1] = nullptr;
+  rg_kd_ = rg_ncols_ = 0;
   plan_ = Plan{};
 }
 
@@ -378,7 +496,9 @@ void Matrix::build(int min_logL) {
     int dev = 0, nsm = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    D.grid_cap = 2 * nsm;
+    int per_sm = 2;
+    if (const char* g = std::getenv("HGPU_GRID")) per_sm = std::max(1, std::atoi(g));
+    D.grid_cap = per_sm * nsm;
     if (const char* dbg = std::getenv("HGPU_DEBUG")) D.debug = std::atoi(dbg);
   }
 
@@ -438,17 +558,74 @@ void Matrix::build(int min_logL) {
   rhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
   phdr_ = dalloc<int>(n_);
   plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
-  // reciprocal of stage p in set p & 1: recip(p+1) may run while the bulk
-  // division of stage p still reads Y_p
-  ybuf_ = dalloc<uint32_t>(2 * (size_t)P.ycap);
-  ys_ = dalloc<int>(8);
+  // reciprocals in a ring of kYRing stage sets: the far-row divisions of
+  // stage p may lag the pivot chain by up to a panel
+  ybuf_ = dalloc<uint32_t>(kYRing * (size_t)P.ycap);
+  ys_ = dalloc<int>(4 * kYRing);
   rscratch_ = dalloc<uint32_t>(recip_scratch_words(D));
   if (div_global_) {
     dscratch_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
     dscratch2_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
+    dscratch3_ = dalloc<uint32_t>((size_t)D.grid_cap * divide_smem_words(D));
   }
   stats_ = dalloc<int>(3 * (size_t)n_);
+  if (ratio_gemm_ && !interval_) {
+    // ratio GEMM operands, sized for the PD bounds of any shift whose
+    // diagonal stays within strip_bits_ + 64 bits (run() checks its own)
+    const int db = strip_bits_ + 64;
+    rg_kd_ = ratio_gemm_kd(db);
+    rg_ncols_ = ratio_gemm_ncols(db);
+    vdig_ = dalloc<uint8_t>((size_t)n_ * rg_kd_);
+    for (int i = 0; i < 2; ++i) {
+      rg_t_[i] = dalloc<uint8_t>((size_t)rg_ncols_ * rg_kd_);
+      rg_c_[i] = dalloc<int32_t>((size_t)n_ * rg_ncols_);
+      rg_ws_[i] = dalloc<uint8_t>(kBlasWorkspace);
+      if (cublasSetWorkspace((cublasHandle_t)blas_[i], rg_ws_[i], kBlasWorkspace) !=
+          CUBLAS_STATUS_SUCCESS)
+        throw Error(HGPU_ERR_CUDA, "cublasSetWorkspace failed");
+    }
+  }
   if (interval_) build_interval();
+}
+
+// 7-bit digit columns of |V| (K of the ratio GEMM) and quotient columns (M)
+// for diagonal entries of at most db bits: |V| <= dmax + 3 - k2 bits (PD
+// bound, k_recip's amax), and the columns needed above K0d are
+// (e + 282) / 7 + 3 with e <= (db + 1) / 2 + k2 + 5 (k_ratio_finish checks
+// every row against its actual operands).
+int Matrix::ratio_gemm_kd(int db) const {
+  const int vb = std::min(db + 3 - K_ / 2, 32 * plan_.cap - K_ / 2);
+  return ((vb + 6) / 7 + 15) & ~15;
+}
+int Matrix::ratio_gemm_ncols(int db) const {
+  const int e = (db + 1) / 2 + K_ / 2 + 5;
+  return ((e + 282) / 7 + 3 + 15) & ~15;
+}
+
+void Matrix::ratio_gemm(int which, int p, int r_begin, int r_end, IntBuf vint,
+                        long long row0, const uint32_t* yb, const int* yss,
+                        IntBuf rint, int* maxdegR, uint32_t* dscr,
+                        cudaStream_t s) {
+  const DevPlan& D = dp_;
+  r_begin = std::max(r_begin, p + 1);
+  const int rows = r_end - r_begin;
+  if (rows <= 0) return;
+  cublasHandle_t h = (cublasHandle_t)blas_[which];
+  CU(launch_toeplitz(D, yb, yss, rg_kd_, rg_ncols_, rg_t_[which], err_, s));
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS)
+    throw Error(HGPU_ERR_CUDA, "cublasSetStream failed");
+  const int32_t one = 1, zero = 0;
+  const cublasStatus_t bs = cublasGemmEx(
+      h, CUBLAS_OP_T, CUBLAS_OP_N, rg_ncols_, rows, rg_kd_, &one, rg_t_[which],
+      CUDA_R_8I, rg_kd_, vdig_ + (size_t)r_begin * rg_kd_, CUDA_R_8I, rg_kd_,
+      &zero, rg_c_[which], CUDA_R_32I, rg_ncols_, CUBLAS_COMPUTE_32I,
+      CUBLAS_GEMM_DEFAULT);
+  if (bs != CUBLAS_STATUS_SUCCESS)
+    throw Error(HGPU_ERR_CUDA, "int8 ratio GEMM failed (cublas status " +
+                                   std::to_string((int)bs) + ")");
+  CU(launch_ratio_finish(D, vint, row0, p, r_begin, r_end, yb, yss,
+                         rg_c_[which], rg_ncols_, rint, row0, rhat_, maxdegR,
+                         dscr, div_global_ ? 1 : 0, err_, s));
 }
 
 void Matrix::panel_broadcast(int owner, int p0, int ns, long long row0,
@@ -606,12 +783,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     flush();
   };
 
-  while ((int)sev_.size() < 4 * n + 4) {
+  while ((int)sev_.size() < 4 * n + 4) {  // + panel entry / far join
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     sev_.push_back(e);
   }
   cudaStream_t sh = stream_helper_;
+  cudaStream_t sf = stream_far_;
   {
     // bits bound of any diagonal Schur complement W_rr (PD: <= M_rr - x)
     int db = 0;
@@ -635,20 +813,37 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
     if (b >= 2) CU(cudaStreamWaitEvent(sp, trail_done[b - 2], 0));
     if (owner == rank_) {
-      // Per stage p two chains run concurrently:
+      // Per stage p three chains run concurrently:
       //   sh (critical): col(pivot p) -> extract(pivot p) -> recip(p) ->
       //                  R_p[p+1] (one row)          [-> stage p+1 pivot]
-      //   sp (bulk):     col(rest p) -> extract(rest p) -> R_p[r >= p+2]
-      // Events (per stage): sev_[4p] extract(rest p) done, sev_[4p+1]
-      // recip(p) done, sev_[4p+2] bulk divide(p) done, sev_[4p+3] chain done.
+      //   sp (near):     col, extract, R_p for rows p+1 < r < near_end
+      //   sf (far):      col, extract, R_p for rows r >= near_end
+      // The pivot chain reads only near rows (row p+2 at stage p feeds the
+      // stage-(p+1) divide, and so on inside the window), so the far rows run
+      // behind it on their own stream and only have to be done before the
+      // trailing update of the panel.  near_end = p0 + near_rows_.
+      // Events (per stage): sev_[4p] extract(near p) done, sev_[4p+1]
+      // recip(p) done, sev_[4p+2] near divide(p) done, sev_[4p+3] chain done.
+      const int near_end = std::min(n, p0 + near_rows_);
+      const bool far = near_end < n && recip_bound_;
+      // ratio GEMM for this run's operand bounds (else k_divide)
+      const bool rg_ok = ratio_gemm_ && rg_kd_ > 0 &&
+                         ratio_gemm_kd(dmax_bits_) <= rg_kd_ &&
+                         ratio_gemm_ncols(dmax_bits_) <= rg_ncols_;
+      const bool rg_near = rg_ok && (ratio_gemm_ & 2);
+      const bool rg_far = rg_ok && (ratio_gemm_ & 1);
       bool chain_started = false;
+      if (far) {
+        CU(cudaEventRecord(sev_[4 * n + 1], sp));
+        CU(cudaStreamWaitEvent(sf, sev_[4 * n + 1], 0));
+      }
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
         const long long row0 = row0set + (long long)s * n;
         const uint32_t* vh = vhat_ + row0set * NW;
         const uint32_t* rh = rhat_ + row0set * NW;
-        uint32_t* yb = ybuf_ + (size_t)(p & 1) * P.ycap;
-        int* yss = ys_ + (p & 1) * 4;
+        uint32_t* yb = ybuf_ + (size_t)(p % kYRing) * P.ycap;
+        int* yss = ys_ + (p % kYRing) * 4;
         if (recip_bound_ && p < n - 1) {
           if (!chain_started) {
             // the helper stream enters the panel where the panel stream is
@@ -656,8 +851,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             CU(cudaStreamWaitEvent(sh, sev_[4 * n], 0));
             chain_started = true;
           } else {
-            // pivot entry of column p needs V_{p-1}[p] (extract(rest p-1))
-            // and R_{p-2}[p] (bulk divide(p-2)); R_{p-1}[p] is on sh already
+            // pivot entry of column p needs V_{p-1}[p] (extract(near p-1))
+            // and R_{p-2}[p] (near divide(p-2)); R_{p-1}[p] is on sh already
             CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 1)], 0));
             if (p - 2 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 2) + 2], 0));
           }
@@ -675,14 +870,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                                 recip_global_ ? 1 : 0, err_, sh);
           });
           CU(cudaEventRecord(sev_[4 * p + 1], sh));
-          // bulk of column p on the panel stream (rows > p)
+          // near rows of column p on the panel stream (rows > p)
+          const int rn = far ? near_end : n;
           TL(3, p, sp, [&] {
             return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                     p, p + 1, n, err_, sp);
+                                     p, p + 1, rn, err_, sp);
           });
           TL(4, p, sp, [&] {
-            return launch_extract(D, W_, colbase_, p, p + 1, n, vint, row0,
-                                  piv, maxbitsV, vhat_, maxdegV, err_, sp);
+            return launch_extract(D, W_, colbase_, p, p + 1, rn, vint, row0,
+                                  piv, maxbitsV, vhat_, maxdegV, err_, sp, 0,
+                                  rg_near ? vdig_ : nullptr, rg_kd_);
           });
           CU(cudaEventRecord(sev_[4 * p], sp));
           // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot)
@@ -693,17 +890,58 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                                  div_global_ ? 1 : 0, err_, sh);
           });
           CU(cudaEventRecord(sev_[4 * p + 3], sh));
-          // R_p[r >= p+2] on the panel stream
+          // R_p[p+1 < r < rn] on the panel stream
           CU(cudaStreamWaitEvent(sp, sev_[4 * p + 1], 0));
-          TL(5, p, sp, [&] {
-            return launch_divide(D, vint, row0, p, p + 2, n, yb, yss, rint,
-                                 row0, rhat_, maxdegR + p, dscratch2_,
-                                 div_global_ ? 1 : 0, err_, sp);
-          });
+          if (rg_near) {
+            TL(5, p, sp, [&] {
+              ratio_gemm(0, p, p + 2, rn, vint, row0, yb, yss, rint, maxdegR + p,
+                         dscratch2_, sp);
+              return cudaSuccess;
+            });
+          } else {
+            TL(5, p, sp, [&] {
+              return launch_divide(D, vint, row0, p, p + 2, rn, yb, yss, rint,
+                                   row0, rhat_, maxdegR + p, dscratch2_,
+                                   div_global_ ? 1 : 0, err_, sp);
+            });
+          }
           CU(cudaEventRecord(sev_[4 * p + 2], sp));
+          if (far) {
+            // far rows: column p receives stages [p0, p) (V^_s[p] of the
+            // near rows, extract(near p-1) done; their own R^_s on sf), then
+            // extraction and, once recip(p) is done, the ratios
+            if (p > p0) CU(cudaStreamWaitEvent(sf, sev_[4 * (p - 1)], 0));
+            TL(10, p, sf, [&] {
+              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                       p, near_end, n, err_, sf);
+            });
+            TL(11, p, sf, [&] {
+              return launch_extract(D, W_, colbase_, p, near_end, n, vint, row0,
+                                    piv, maxbitsV, vhat_, maxdegV, err_, sf, 0,
+                                    rg_far ? vdig_ : nullptr, rg_kd_);
+            });
+            CU(cudaStreamWaitEvent(sf, sev_[4 * p + 1], 0));
+            if (rg_far) {
+              TL(12, p, sf, [&] {
+                ratio_gemm(1, p, near_end, n, vint, row0, yb, yss, rint,
+                           maxdegR + p, dscratch3_, sf);
+                return cudaSuccess;
+              });
+            } else {
+              TL(12, p, sf, [&] {
+                return launch_divide(D, vint, row0, p, near_end, n, yb, yss, rint,
+                                     row0, rhat_, maxdegR + p, dscratch3_,
+                                     div_global_ ? 1 : 0, err_, sf);
+              });
+            }
+          }
           if (p + 1 == p1 || p + 1 == n - 1) {
             // join: the next step on sp needs R_p[p+1] as well
             CU(cudaStreamWaitEvent(sp, sev_[4 * p + 3], 0));
+            if (far) {
+              CU(cudaEventRecord(sev_[4 * n + 2], sf));
+              CU(cudaStreamWaitEvent(sp, sev_[4 * n + 2], 0));
+            }
           }
         } else {
           // left-looking inside the panel: column p receives stages [p0, p)
@@ -776,7 +1014,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       const int p2 = std::min(n, p1 + kb);
       trailing(b, p1, p2);
       CU(cudaEventRecord(next_ready[b + 1], st));
-      trailing(b, p2, n);
+      if (!(D.debug & 512)) trailing(b, p2, n);  // 512: timing experiment only
     } else {
       CU(cudaEventRecord(next_ready[b + 1], st));
     }

@@ -89,6 +89,7 @@ class Matrix {
     return plan_;
   }
   int frac_bits() const { return K_; }
+  int chain_sms() const { return chain_sms_; }
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
   std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
@@ -109,6 +110,13 @@ class Matrix {
   void panel_broadcast(int owner, int p0, int ns, long long row0,
                        cudaStream_t st);
   void fold(FactorResult& res);
+  int ratio_gemm_kd(int db) const;
+  int ratio_gemm_ncols(int db) const;
+  // R_p[r] for rows [max(r_begin, p+1), r_end) by the int8 ratio GEMM on
+  // stream s with operand set `which` (0 near, 1 far)
+  void ratio_gemm(int which, int p, int r_begin, int r_end, IntBuf vint,
+                  long long row0, const uint32_t* yb, const int* yss,
+                  IntBuf rint, int* maxdegR, uint32_t* dscr, cudaStream_t s);
   void keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st);
   void build_interval();
   void release_interval();
@@ -139,7 +147,21 @@ class Matrix {
   int* phdr_ = nullptr;
   uint32_t* plimbs_ = nullptr;
   uint32_t *ybuf_ = nullptr, *rscratch_ = nullptr, *dscratch_ = nullptr,
-           *dscratch2_ = nullptr;
+           *dscratch2_ = nullptr, *dscratch3_ = nullptr;
+  static constexpr int kYRing = 64;
+  // rows [p0, p0 + near_rows_) of a panel run in step with the pivot chain,
+  // the rest on the far stream (HGPU_NEAR, default two panels)
+  int near_rows_ = 64;
+  // ratio GEMM (HGPU_RATIO_GEMM bits: 1 far rows, 2 near rows; 0 = k_divide,
+  // the default: the int8 path is exact but measured slower end to end)
+  int ratio_gemm_ = 0;
+  int rg_kd_ = 0, rg_ncols_ = 0;
+  uint8_t* vdig_ = nullptr;             // n x kd digits of |V_p[r]|
+  uint8_t* rg_t_[2] = {nullptr, nullptr};  // per stream (near, far): T
+  int32_t* rg_c_[2] = {nullptr, nullptr};  // per stream: GEMM output
+  uint8_t* rg_ws_[2] = {nullptr, nullptr};
+  void* blas_[2] = {nullptr, nullptr};     // cublasHandle_t per stream
+  static constexpr size_t kBlasWorkspace = 32u << 20;
   int* ys_ = nullptr;
   int* stats_ = nullptr;  // maxbitsV | maxdegV | maxdegR, n each
   int* err_ = nullptr;
@@ -149,6 +171,8 @@ class Matrix {
   cudaStream_t stream_ = nullptr;        // bulk (trailing updates)
   cudaStream_t stream_panel_ = nullptr;  // panel factorisation, high priority
   cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
+  cudaStream_t stream_far_ = nullptr;    // far rows of the panel (may lag)
+  int chain_sms_ = 0;  // SMs reserved for the pivot chain (green context), 0 = none
   std::vector<cudaEvent_t> pev_, sev_;
   bool recip_bound_ = true;  // reciprocal precision from the PD bound
   // whole L factor (HGPU_KEEP_L): R_p[r], p < r, packed strictly lower

@@ -2,6 +2,7 @@
 // it reproduces (/root/reference/proj/src/ldlt.cpp).  Arithmetic is exact:
 // the only roundings are the reference's own truncations (tdiv_q_2exp for the
 // column values, tdiv_q for the ratios), so results are bit-identical.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -153,7 +154,8 @@ __global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
 __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, int r_begin, int r_end, IntBuf vint,
                           long long vrow0, IntBuf piv, int* maxbitsV,
-                          uint32_t* vhat, int* maxdegV, int* err, int round) {
+                          uint32_t* vhat, int* maxdegV, int* err, int round,
+                          uint8_t* vdig, int kd) {
   extern __shared__ uint32_t sm[];
   __shared__ int s_bump;
   if (stage_aborted(err)) return;
@@ -336,6 +338,16 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
     for (int m = threadIdx.x; m < P.cap; m += blockDim.x) vdst[m] = Vb[m];
     const int vlen = cta_limb_len(Vb, P.cap, red);
     const int vbits = limbs_bits(Vb, vlen);
+    if (vdig && r > p) {  // 7-bit digits of |V| for the ratio GEMM
+      uint32_t* drow = reinterpret_cast<uint32_t*>(vdig + (long long)r * kd);
+      for (int i = threadIdx.x; i < kd / 4; i += blockDim.x) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          wv |= (field32(Vb, vlen, 7LL * (4 * i + u)) & 127u) << (8 * u);
+        drow[i] = wv;
+      }
+    }
     const int vsign = vlen == 0 ? 0 : wsign;
     if (threadIdx.x == 0) {
       vint.hdr[vidx] = vsign * vlen;
@@ -539,6 +551,114 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
   }
 }
 
+// Quotient from the top of the product.  Pr[0, nPs) holds the product
+// columns from limb K0 on, i.e. F 2^shs with F = |V| Y / 2^sh lowered by
+// < 2^-32 (dropped columns) and within 2^-31.9 of |V| 2^k2 / |D| (k_recip's
+// |Y - 2^S/D| <= 3), shs = sh - 32 K0 >= 32.  When the 32 fraction bits of F
+// lie in [4, 2^32-5], q = floor(F) exactly; otherwise floor(F) is within one
+// of q and the remainder window |V| 2^k2 - q~ D over nD+2 limbs decides the
+// correction exactly.  `away`: interval rounding bumps a non-integer
+// quotient away from zero.  Writes |q| to Qt (Qt may alias neither Pr nor
+// col); Pr is reused as the window scratch.  Returns the limb count of |q|,
+// or -1 after raising kCapLimbs.
+__device__ int ratio_quotient(const DevPlan& P, uint32_t* Pr, int nPs, int shs,
+                              uint32_t* Qt, uint32_t* col, uint32_t* red, int CY,
+                              const uint32_t* Vg, int na, const uint32_t* Dg,
+                              int nD, bool away, int* err) {
+  int nq;
+  const int nQ = max(0, (int)((32LL * nPs - shs + 31) / 32));
+  for (int i = threadIdx.x; i < nQ; i += blockDim.x)
+    Qt[i] = field32(Pr, nPs, 32LL * i + shs);
+  const uint32_t frac = field32(Pr, nPs, (long long)shs - 32);
+  __syncthreads();
+  nq = cta_limb_len(Qt, nQ, red);
+  const bool exact_needed = shs < 32 || frac < 4u || frac > 0xFFFFFFFAu;
+  int bump = (away && !exact_needed) ? 1 : 0;  // fast path: never exact
+  if (exact_needed) {
+    // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
+    const int nw = nD + 2;
+    uint32_t* Wa = Pr;
+    uint32_t* Wb = Pr + nw;
+    cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red, 3 * CY);
+    cta_resolve(
+        nw, 32,
+        [&](int k) -> int64_t {
+          return (int64_t)field32(Vg, na, 32LL * k - P.k2) - (int64_t)Wb[k];
+        },
+        [&](int k, uint32_t d) { Wa[k] = d; }, red);
+    int adj = 0;
+    if (Wa[nw - 1] & 0x80000000u) {
+      adj = -1;  // remainder negative: q~ was one too large
+    } else {
+      cta_resolve(
+          nw, 32,
+          [&](int k) -> int64_t {
+            return (int64_t)Wa[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+          },
+          [&](int k, uint32_t d) { Wb[k] = d; }, red);
+      if (!(Wb[nw - 1] & 0x80000000u)) {
+        adj = 1;
+        cta_resolve(
+            nw, 32,
+            [&](int k) -> int64_t {
+              return (int64_t)Wb[k] - (int64_t)(k < nD ? Dg[k] : 0u);
+            },
+            [&](int k, uint32_t d) { Wa[k] = d; }, red);
+        if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
+          atomicOr(&err[kErrInternal], kIntDivision);
+      }
+    }
+    if (away) {
+      // remainder: Wa (adj 0), Wb (adj +1), Wa + D (adj -1)
+      const uint32_t* rem = adj == 1 ? Wb : Wa;
+      if (adj == -1) {
+        __syncthreads();
+        cta_resolve(
+            nw, 32,
+            [&](int k) -> int64_t {
+              return (int64_t)Wa[k] + (int64_t)(k < nD ? Dg[k] : 0u);
+            },
+            [&](int k, uint32_t d) { Wb[k] = d; }, red);
+        rem = Wb;
+      }
+      bump = cta_limb_len(rem, nw, red) != 0 ? 1 : 0;
+    }
+    adj += bump;
+    bump = 0;
+    if (adj != 0) {
+      const int nn = nq + 1;
+      cta_resolve(
+          nn, 32,
+          [&](int k) -> int64_t {
+            return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
+          },
+          [&](int k, uint32_t d) { col[k] = d; }, red);
+      for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
+      __syncthreads();
+      nq = cta_limb_len(Qt, nn, red);
+    }
+    // every thread has read the window signs before Pr is reused below
+    __syncthreads();
+  }
+  if (bump) {
+    const int nn = nq + 1;
+    cta_resolve(
+        nn, 32,
+        [&](int k) -> int64_t {
+          return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? 1 : 0);
+        },
+        [&](int k, uint32_t d) { col[k] = d; }, red);
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
+    __syncthreads();
+    nq = cta_limb_len(Qt, nn, red);
+  }
+  if (nq > P.cap) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return -1;
+  }
+  return nq;
+}
+
 // ---------------------------------------------------------------- ratios ---
 // Stage p, rows r in (p, n):  R_p[r] = tdiv_q(V_p[r] << K/2, V_p[p])
 // (ldlt.cpp:15-20, 57-58).  With A = |V_r| 2^{K/2}, D = |V_p|, n = bits(D):
@@ -634,99 +754,11 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       const int nPs = nP - K0;
       const int shs = sh - 32 * K0;
       cta_mul(Vt, nt, Y, nY, Pr, nP, col, red, 3 * CY, K0);
-      const int nQ = max(0, (int)((32LL * nPs - shs + 31) / 32));
-      for (int i = threadIdx.x; i < nQ; i += blockDim.x)
-        Qt[i] = field32(Pr, nPs, 32LL * i + shs);
-      const uint32_t frac = field32(Pr, nPs, (long long)shs - 32);
-      __syncthreads();
-      nq = cta_limb_len(Qt, nQ, red);
-      const bool exact_needed = shs < 32 || frac < 4u || frac > 0xFFFFFFFAu;
       // interval rounding: one more unit of magnitude when the exact quotient
       // is not an integer and the rounding points away from zero
       const bool away = (iv.mode == 1 && sV * sD < 0) || (iv.mode == 2 && sV * sD > 0);
-      int bump = (away && !exact_needed) ? 1 : 0;  // fast path: never exact
-      if (exact_needed) {
-        // remainder window: |V| 2^k2 - q~ D  (mod 2^(32 nw)), nw = nD + 2
-        const int nw = nD + 2;
-        uint32_t* Wa = Pr;
-        uint32_t* Wb = Pr + nw;
-        cta_mul(Qt, nq, Dg, nD, Wb, nw, col, red, 3 * CY);
-        cta_resolve(
-            nw, 32,
-            [&](int k) -> int64_t {
-              return (int64_t)field32(Vg, na, 32LL * k - P.k2) - (int64_t)Wb[k];
-            },
-            [&](int k, uint32_t d) { Wa[k] = d; }, red);
-        int adj = 0;
-        if (Wa[nw - 1] & 0x80000000u) {
-          adj = -1;  // remainder negative: q~ was one too large
-        } else {
-          cta_resolve(
-              nw, 32,
-              [&](int k) -> int64_t {
-                return (int64_t)Wa[k] - (int64_t)(k < nD ? Dg[k] : 0u);
-              },
-              [&](int k, uint32_t d) { Wb[k] = d; }, red);
-          if (!(Wb[nw - 1] & 0x80000000u)) {
-            adj = 1;
-            cta_resolve(
-                nw, 32,
-                [&](int k) -> int64_t {
-                  return (int64_t)Wb[k] - (int64_t)(k < nD ? Dg[k] : 0u);
-                },
-                [&](int k, uint32_t d) { Wa[k] = d; }, red);
-            if (!(Wa[nw - 1] & 0x80000000u) && threadIdx.x == 0)
-              atomicOr(&err[kErrInternal], kIntDivision);
-          }
-        }
-        if (away) {
-          // remainder: Wa (adj 0), Wb (adj +1), Wa + D (adj -1)
-          const uint32_t* rem = adj == 1 ? Wb : Wa;
-          if (adj == -1) {
-            __syncthreads();
-            cta_resolve(
-                nw, 32,
-                [&](int k) -> int64_t {
-                  return (int64_t)Wa[k] + (int64_t)(k < nD ? Dg[k] : 0u);
-                },
-                [&](int k, uint32_t d) { Wb[k] = d; }, red);
-            rem = Wb;
-          }
-          bump = cta_limb_len(rem, nw, red) != 0 ? 1 : 0;
-        }
-        adj += bump;
-        bump = 0;
-        if (adj != 0) {
-          const int nn = nq + 1;
-          cta_resolve(
-              nn, 32,
-              [&](int k) -> int64_t {
-                return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? adj : 0);
-              },
-              [&](int k, uint32_t d) { col[k] = d; }, red);
-          for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
-          __syncthreads();
-          nq = cta_limb_len(Qt, nn, red);
-        }
-        // every thread has read the window signs before Pr is reused below
-        __syncthreads();
-      }
-      if (bump) {
-        const int nn = nq + 1;
-        cta_resolve(
-            nn, 32,
-            [&](int k) -> int64_t {
-              return (int64_t)(k < nq ? Qt[k] : 0u) + (k == 0 ? 1 : 0);
-            },
-            [&](int k, uint32_t d) { col[k] = d; }, red);
-        for (int i = threadIdx.x; i < nn; i += blockDim.x) Qt[i] = col[i];
-        __syncthreads();
-        nq = cta_limb_len(Qt, nn, red);
-      }
-      if (nq > cap) {
-        if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
-        return;
-      }
+      nq = ratio_quotient(P, Pr, nPs, shs, Qt, col, red, CY, Vg, na, Dg, nD, away, err);
+      if (nq < 0) return;
     }
     const int rsign = nq == 0 ? 0 : sV * sD;
     for (int i = threadIdx.x; i < cap; i += blockDim.x)
@@ -737,6 +769,160 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
     }
     // transform of R_p[r] (Montgomery form) for the trailing update; the
     // NTT buffer reuses the Barrett scratch when it is large enough
+    if (rhat) {
+      uint32_t* X = P.NW <= 4 * CY ? Pr : sm + span;
+      transform_int(P, Qt, nq, 0, rsign, X, rhat + ridx * (long long)P.NW,
+                    true, twm, err);
+    } else {
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------- ratios on the tensor cores ---
+// The stage's bulk division R_p[r] = tdiv_q(V_p[r] 2^k2, V_p[p]) for many
+// rows is one product of every |V_p[r]| with the stage's reciprocal Y, i.e. a
+// limb convolution with a common operand: a GEMM.  In 7-bit digits
+//   C[r][k'] = sum_i vdig[r][i] * T[k'][i],   T[k'][i] = ydig[K0d + k' - i],
+// is column K0d + k' of |V_r| Y (products < 2^14, sums over <= 2^13 digits
+// stay < 2^27: exact in int32), computed by an int8 x int8 -> int32 tensor
+// core GEMM.  k_ratio_finish turns each row's columns back into limbs and
+// applies ratio_quotient, so the results equal k_divide's bit for bit.
+// K0d = ((sh - 59) / 7) rounded down to a multiple of 32 (7 K0d is a whole
+// limb offset): the dropped columns sum to < 2^26.1 2^(7 K0d) <= 2^(sh-32),
+// so F is lowered by < 2^-32 as in k_divide (there with V truncated; here V
+// is whole, sh = S - k2).
+__device__ __forceinline__ int ratio_k0d(int sh) {
+  return sh < 59 ? 0 : ((sh - 59) / 7) & ~31;
+}
+
+// T[k'][i] (ncols x kd bytes, row k' contiguous) for the stage's Y.  One
+// thread per 16 bytes.
+__global__ void k_toeplitz(const uint32_t* Ybuf, const int* ys, int k2, int kd,
+                           int ncols, uint8_t* T, const int* err) {
+  extern __shared__ uint32_t ysm[];
+  if (stage_aborted(err)) return;
+  const int nY = ys[1];
+  const int k0d = ratio_k0d(ys[0] - k2);
+  for (int i = threadIdx.x; i < nY; i += blockDim.x) ysm[i] = Ybuf[i];
+  __syncthreads();
+  const int per_row = kd / 16;
+  const long long total = (long long)ncols * per_row;
+  const long long nyd = (32LL * nY + 6) / 7;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int kc = (int)(idx / per_row);
+    const int i0 = (int)(idx - (long long)kc * per_row) * 16;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const long long j = (long long)k0d + kc - (i0 + u);
+      if (j >= 0 && j < nyd) {
+        const uint32_t d = field32(ysm, nY, 7 * j) & 127u;
+        w[u >> 2] |= d << (8 * (u & 3));
+      }
+    }
+    reinterpret_cast<uint4*>(T + (long long)kc * kd)[i0 / 16] =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Rows r in [r_begin, r_end) of stage p from the GEMM's columns
+// C[(r - r_begin) * ncols + k'] (see above); same outputs as k_divide.
+__global__ void k_ratio_finish(DevPlan P, IntBuf vint, long long vrow0, int p,
+                               int r_begin, int r_end, const uint32_t* Ybuf,
+                               const int* ys, const int32_t* C, int ncols,
+                               IntBuf rint, long long rrow0, uint32_t* rhat,
+                               int* maxdegR, uint32_t* gscratch,
+                               int use_gscratch, int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  if (stage_aborted(err)) return;
+  const int cap = P.cap, ycap = P.ycap;
+  const long long span = div_span_words(cap, ycap);
+  const long long cta_words = span + div_extra_words(P);
+  uint32_t* tab = sm_dyn;
+  uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * cta_words
+                              : sm_dyn + (P.tw_smem ? P.NW : 0);
+  const uint32_t* twm;
+  stage_tables(P, tab, nullptr, &twm, nullptr);
+  const int CY = (cap + ycap + 2 + 3) & ~3;
+  uint32_t* Qt = sm;                 // cap + ycap: digits, then |q|
+  uint32_t* Pr = sm + CY;            // CY: product top, windows, NTT
+  uint32_t* col = Pr + CY;           // 3 CY: super-digits, then scratch
+  uint32_t* red = col + 3 * CY;      // 64
+  const long long pidx = vrow0 + p;
+  const int S = ys[0], nY = ys[1], amax_used = ys[2];
+  const int ybits = limbs_bits(Ybuf, nY);
+  const int sh = S - P.k2;
+  const int k0d = ratio_k0d(sh);
+  const int shs = sh - 7 * k0d;
+  const int J = ncols / 4;  // 28-bit super-digits
+  const uint64_t m28 = (1ull << 28) - 1ull;
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
+    const long long vidx = vrow0 + r;
+    const int hd = vint.hdr[pidx];
+    const int nD = hd < 0 ? -hd : hd;
+    const int sD = hd < 0 ? -1 : (hd > 0);
+    const uint32_t* Dg = vint.limbs + pidx * cap;
+    const int hv = vint.hdr[vidx];
+    const int na = hv < 0 ? -hv : hv;
+    const int sV = hv < 0 ? -1 : (hv > 0);
+    const uint32_t* Vg = vint.limbs + vidx * cap;
+    const long long ridx = rrow0 + r;
+    uint32_t* dst = rint.limbs + ridx * cap;
+    int nq = 0;
+    if (na > 0 && nD > 0) {
+      const int vbits = limbs_bits(Vg, na);
+      if (vbits + P.k2 > amax_used) {  // reciprocal too short for this row
+        if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapAmax);
+        return;
+      }
+      // every nonzero column of |V| Y lies below K0d + ncols
+      if ((vbits + ybits + 6) / 7 + 1 > k0d + ncols) {
+        if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+        return;
+      }
+      const int32_t* Cr = C + (long long)(r - r_begin) * ncols;
+      uint64_t* Dsd = reinterpret_cast<uint64_t*>(col);
+      for (int j = threadIdx.x; j < J; j += blockDim.x) {
+        const int4 c4 = reinterpret_cast<const int4*>(Cr)[j];
+        Dsd[j] = (uint64_t)(uint32_t)c4.x + ((uint64_t)(uint32_t)c4.y << 7) +
+                 ((uint64_t)(uint32_t)c4.z << 14) + ((uint64_t)(uint32_t)c4.w << 21);
+      }
+      __syncthreads();
+      const int carry = cta_resolve(
+          J + 1, 28,
+          [&](int j) -> int64_t {
+            int64_t v = j < J ? (int64_t)(Dsd[j] & m28) : 0;
+            if (j > 0) v += (int64_t)(Dsd[j - 1] >> 28);
+            return v;
+          },
+          [&](int j, uint64_t d) { Qt[j] = (uint32_t)d; }, red);
+      if (carry != 0) {
+        if (threadIdx.x == 0) atomicOr(&err[kErrInternal], kIntDivision);
+        return;
+      }
+      const int nPs = (28 * (J + 1) + 31) / 32;
+      for (int m = threadIdx.x; m < nPs; m += blockDim.x) {
+        uint64_t acc = 0;
+        for (int k = (32 * m) / 28; k <= J && 28 * k < 32 * m + 32; ++k) {
+          const int shl = 28 * k - 32 * m;
+          acc |= shl >= 0 ? ((uint64_t)Qt[k] << shl) : ((uint64_t)Qt[k] >> -shl);
+        }
+        Pr[m] = (uint32_t)acc;
+      }
+      __syncthreads();
+      nq = ratio_quotient(P, Pr, nPs, shs, Qt, col, red, CY, Vg, na, Dg, nD,
+                          false, err);
+      if (nq < 0) return;
+    }
+    const int rsign = nq == 0 ? 0 : sV * sD;
+    for (int i = threadIdx.x; i < cap; i += blockDim.x)
+      dst[i] = i < nq ? Qt[i] : 0u;
+    if (threadIdx.x == 0) {
+      rint.hdr[ridx] = rsign * nq;
+      if (nq > 0 && maxdegR) atomicMax(maxdegR, (limbs_bits(Qt, nq) - 1) / P.w);
+    }
     if (rhat) {
       uint32_t* X = P.NW <= 4 * CY ? Pr : sm + span;
       transform_int(P, Qt, nq, 0, rsign, X, rhat + ridx * (long long)P.NW,
@@ -1075,14 +1261,15 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, int r_begin,
                            int r_end, IntBuf vint, long long vrow0, IntBuf piv,
                            int* maxbitsV, uint32_t* vhat, int* maxdegV,
-                           int* err, cudaStream_t st, int round) {
+                           int* err, cudaStream_t st, int round,
+                           uint8_t* vdig, int kd) {
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
   // a single row is on the pivot chain: give it more threads
   k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, extract_smem_bytes(P), st>>>(
       P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
-      maxdegV, err, round);
+      maxdegV, err, round, vdig, kd);
   return post_launch(st);
 }
 
@@ -1161,6 +1348,35 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   k_divide<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, smem, st>>>(
       P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
       gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
+  return post_launch(st);
+}
+
+cudaError_t launch_toeplitz(const DevPlan& P, const uint32_t* Ybuf,
+                            const int* ys, int kd, int ncols, uint8_t* T,
+                            const int* err, cudaStream_t st) {
+  ++g_launches;
+  const long long words = (long long)ncols * (kd / 16);
+  const int blocks = (int)std::min<long long>((words + 255) / 256, 4096);
+  k_toeplitz<<<blocks, 256, (size_t)P.ycap * 4, st>>>(Ybuf, ys, P.k2, kd, ncols,
+                                                      T, err);
+  return post_launch(st);
+}
+
+cudaError_t launch_ratio_finish(const DevPlan& P, IntBuf vint, long long vrow0,
+                                int p, int r_begin, int r_end,
+                                const uint32_t* Ybuf, const int* ys,
+                                const int32_t* C, int ncols, IntBuf rint,
+                                long long rrow0, uint32_t* rhat, int* maxdegR,
+                                uint32_t* gscratch, int use_gscratch, int* err,
+                                cudaStream_t st) {
+  const int rows = r_end - r_begin;
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
+                                   : divide_smem_words(P) * 4;
+  ++g_launches;
+  k_ratio_finish<<<min(rows, P.grid_cap), 256, smem, st>>>(
+      P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, C, ncols, rint, rrow0, rhat,
+      maxdegR, gscratch, use_gscratch, err);
   return post_launch(st);
 }
 
@@ -1264,8 +1480,16 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   tab)) != cudaSuccess)
       return e;
+    if ((e = cudaFuncSetAttribute(k_ratio_finish,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  tab)) != cudaSuccess)
+      return e;
   } else {
     if ((e = cudaFuncSetAttribute(k_divide,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)div)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(k_ratio_finish,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)div)) != cudaSuccess)
       return e;

@@ -119,7 +119,8 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
                            const long long* colbase, int p, int r_begin,
                            int r_end, IntBuf vint, long long vrow0, IntBuf piv,
                            int* maxbitsV, uint32_t* vhat, int* maxdegV,
-                           int* err, cudaStream_t st, int round = 0);
+                           int* err, cudaStream_t st, int round = 0,
+                           uint8_t* vdig = nullptr, int kd = 0);
 size_t recip_scratch_words(const DevPlan& P);
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
@@ -143,6 +144,19 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                           uint32_t* rhat, int* maxdegR, uint32_t* gscratch,
                           int use_gscratch, int* err, cudaStream_t st,
                           const IvDiv* iv = nullptr);
+// Ratio GEMM: T[k'][i] = 7-bit digit K0d + k' - i of the
+// stage's reciprocal; C = T^T vdig on the tensor cores (cuBLAS int8); the
+// finish kernel gives the same R_p[r] (and R^) as launch_divide.
+cudaError_t launch_toeplitz(const DevPlan& P, const uint32_t* Ybuf,
+                            const int* ys, int kd, int ncols, uint8_t* T,
+                            const int* err, cudaStream_t st);
+cudaError_t launch_ratio_finish(const DevPlan& P, IntBuf vint, long long vrow0,
+                                int p, int r_begin, int r_end,
+                                const uint32_t* Ybuf, const int* ys,
+                                const int32_t* C, int ncols, IntBuf rint,
+                                long long rrow0, uint32_t* rhat, int* maxdegR,
+                                uint32_t* gscratch, int use_gscratch, int* err,
+                                cudaStream_t st);
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
