@@ -462,10 +462,11 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
       if constexpr (kWarp) return warp_resolve(M, 32, getv, putd);
       else return cta_resolve(M, 32, getv, putd, red);
     };
+    // out = columns [k_begin, M) of a*b (the warp path forms all of [0, M))
     auto mul = [&](const uint32_t* a, int na, const uint32_t* b, int nb,
-                   uint32_t* out, int M) {
+                   uint32_t* out, int M, int k_begin) {
       if constexpr (kWarp) warp_mul(a, na, b, nb, out, M, col);
-      else cta_mul(a, na, b, nb, out, M, col, red, col_words);
+      else cta_mul(a, na, b, nb, out, M, col, red, col_words, k_begin);
     };
     long long tph[6];
     if (prof) tph[0] = clock64();
@@ -475,41 +476,48 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
     const int nDt = (mb + 31) / 32;
     for (int k = t0; k < nDt; k += ts) Dt[k] = field32(Dg, nD, 32LL * k + t);
     sync();
-    // Pr = D' * Y
-    const int nP = nDt + nY;
+    // E = 2^Sb - D' Y, Sb = mb + pa.  Y is within a few units at precision
+    // pa, so |E| < 2^(mb+3) <= 2^(32 nDt + 3): the low nL = nDt + 1 limbs of
+    // the product (a low short product) determine E, read as a two's
+    // complement number mod 2^(32 nL).
+    const int nL = nDt + 1;
     if (prof) tph[1] = clock64();
-    mul(Dt, nDt, Y, nY, Pr, nP);
+    mul(Dt, nDt, Y, nY, Pr, nL, 0);
     if (prof) tph[2] = clock64();
-    // E = 2^(mb+pa) - Pr, signed, over nP+1 limbs
-    const int nEw = nP + 1;
     const int Sb = mb + pa;
-    int sgn = 1;
-    for (int pass = 0; pass < 2; ++pass) {
-      const int c = resolve(
-          nEw,
-          [&](int k) -> int64_t {
-            const int64_t av = (k == Sb / 32) ? (int64_t)(1u << (Sb % 32)) : 0;
-            const int64_t bv = k < nP ? (int64_t)Pr[k] : 0;
-            return sgn > 0 ? av - bv : bv - av;
-          },
-          [&](int k, uint32_t dd) { E[k] = dd; });
-      if (c >= 0) break;
-      sgn = -1;
+    resolve(
+        nL,
+        [&](int k) -> int64_t {
+          const int64_t av = (k == Sb / 32) ? (int64_t)(1u << (Sb % 32)) : 0;
+          return av - (int64_t)Pr[k];
+        },
+        [&](int k, uint32_t dd) { E[k] = dd; });
+    const int sgn = (E[nL - 1] & 0x80000000u) ? -1 : 1;
+    uint32_t* Ev = E;
+    if (sgn < 0) {  // |E| = 2^(32 nL) - E
+      resolve(
+          nL, [&](int k) -> int64_t { return -(int64_t)E[k]; },
+          [&](int k, uint32_t dd) { Pr[k] = dd; });
+      Ev = Pr;
     }
-    const int nE = kWarp ? warp_limb_len(E, nEw) : cta_limb_len(E, nEw, red);
+    const int nE = kWarp ? warp_limb_len(Ev, nL) : cta_limb_len(Ev, nL, red);
     if (prof) tph[3] = clock64();
-    // Tm = Y * |E|
-    const int nT = nY + nE;
-    if (nE > 0) mul(Y, nY, E, nE, Tm, nT);
-    if (prof) tph[4] = clock64();
-    // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
+    // Tm = Y |E|, only from column K0 on: Y' below uses Tm >> sh, and the
+    // dropped columns sum to < min(nY,nE) 2^(32 K0 + 33) <= 2^(sh - 21), so
+    // Y' moves by at most one unit (|Y - 2^S/D| <= 4 at the last level)
     const int nYn = min(Lm, (pb + 2 + 31) / 32 + 1);
     const int sh = Sb - dlt;
+    const int K0 = kWarp ? 0 : max(0, (sh - 64) / 32);
+    const int nT = nY + nE;
+    if (nE > 0) mul(Y, nY, Ev, nE, Tm, nT, K0);
+    if (prof) tph[4] = clock64();
+    // Y' = Y 2^dlt +- Tm >> (Sb - dlt)
     resolve(
         nYn,
         [&](int k) -> int64_t {
           const int64_t yv = field32(Y, nY, 32LL * k - dlt);
-          const int64_t tv = nE > 0 ? (int64_t)field32(Tm, nT, 32LL * k + sh) : 0;
+          const int64_t tv =
+              nE > 0 ? (int64_t)field32(Tm, nT - K0, 32LL * k + sh - 32LL * K0) : 0;
           return sgn > 0 ? yv + tv : yv - tv;
         },
         [&](int k, uint32_t dd) { Pr[k] = dd; });
@@ -553,8 +561,8 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
 
 // Quotient from the top of the product.  Pr[0, nPs) holds the product
 // columns from limb K0 on, i.e. F 2^shs with F = |V| Y / 2^sh lowered by
-// < 2^-32 (dropped columns) and within 2^-31.9 of |V| 2^k2 / |D| (k_recip's
-// |Y - 2^S/D| <= 3), shs = sh - 32 K0 >= 32.  When the 32 fraction bits of F
+// < 2^-32 (dropped columns) and within 2^-32 of |V| 2^k2 / |D| (k_recip's
+// |Y - 2^S/D| <= 4), shs = sh - 32 K0 >= 32.  When the 32 fraction bits of F
 // lie in [4, 2^32-5], q = floor(F) exactly; otherwise floor(F) is within one
 // of q and the remainder window |V| 2^k2 - q~ D over nD+2 limbs decides the
 // correction exactly.  `away`: interval rounding bumps a non-integer
@@ -663,11 +671,11 @@ __device__ int ratio_quotient(const DevPlan& P, uint32_t* Pr, int nPs, int shs,
 // Stage p, rows r in (p, n):  R_p[r] = tdiv_q(V_p[r] << K/2, V_p[p])
 // (ldlt.cpp:15-20, 57-58).  With A = |V_r| 2^{K/2}, D = |V_p|, n = bits(D):
 //   F = (|V_r| >> t) * Y / 2^{S-K/2-t},   t = max(0, n - K/2 - 40),
-// differs from A/D by < 2^-31.9 (|Y - 2^S/D| <= 3 from k_recip; the dropped
-// low bits of V cost < 2^-39), and the product is formed only from column
-// K0 = (sh-75)/32 up, which lowers F by < 2^-32 more.  So when the 32 fraction
-// bits of F lie in [4, 2^32-5], q = floor(F) exactly and no remainder is
-// needed.  Otherwise
+// differs from A/D by <= 2^-32 (|Y - 2^S/D| <= 4 from k_recip, and
+// S = n + e + 32 with 2^e >= 4 A/D; the dropped low bits of V cost < 2^-39),
+// and the product is formed only from column K0 = (sh-75)/32 up, which
+// lowers F by < 2^-32 more.  So when the 32 fraction bits of F lie in
+// [4, 2^32-5], q = floor(F) exactly and no remainder is needed.  Otherwise
 // (e.g. exact quotients) floor(F) is within one of q and the remainder
 // window A - q~ D over nD+2 limbs decides the correction exactly.
 __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
