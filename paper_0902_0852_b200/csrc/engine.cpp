@@ -72,17 +72,11 @@ double log2_u128(u128 v) {
 struct GreenSplit {
   bool ok = false;
   int chain_sms = 0, rest_sms = 0;
-  char panel = 'a';
   CUgreenCtx ga = nullptr, gb = nullptr;
 };
 
-GreenSplit make_green_split(int device) {
+GreenSplit make_green_split(int device, int want) {
   GreenSplit g;
-  int want = 0;  // off by default: measured slower at config 3
-  if (const char* s = std::getenv("HGPU_SM_SPLIT")) {
-    want = std::atoi(s);
-    if (const char* c = std::strchr(s, ':')) g.panel = c[1];
-  }
   if (want <= 0) return g;
   auto sym = [](const char* name) -> void* {
     void* fn = nullptr;
@@ -118,14 +112,16 @@ GreenSplit make_green_split(int device) {
   return g;
 }
 
-// One split per device for the process (green contexts are kept alive).
-const GreenSplit& green_split(int device) {
+// One split per (device, group size) for the process (green contexts are
+// kept alive).
+const GreenSplit& green_split(int device, int want) {
   static std::mutex mu;
-  static std::vector<std::pair<int, GreenSplit>> cache;
+  static std::vector<std::pair<long long, GreenSplit>> cache;
   std::lock_guard<std::mutex> lk(mu);
+  const long long key = ((long long)device << 32) | (unsigned)want;
   for (auto& e : cache)
-    if (e.first == device) return e.second;
-  cache.emplace_back(device, make_green_split(device));
+    if (e.first == key) return e.second;
+  cache.emplace_back(key, make_green_split(device, want));
   return cache.back().second;
 }
 
@@ -265,16 +261,22 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const GreenSplit& g = green_split(device_);
+    int want = 0;  // off by default: measured slower at config 3
+    char panel = 'a';
+    if (const char* e = std::getenv("HGPU_SM_SPLIT")) {
+      want = std::atoi(e);
+      if (const char* c = std::strchr(e, ':')) panel = c[1];
+    }
+    const GreenSplit& g = green_split(device_, want);
     if (g.ok) {
       // bulk stream on the large group, pivot chain on the reserved SMs;
       // the panel stream where HGPU_SM_SPLIT places it
       stream_ = green_stream(g.gb, 0);
       stream_helper_ = green_stream(g.ga, hi);
       stream_far_ = green_stream(g.gb, hi);
-      if (g.panel == 'b')
+      if (panel == 'b')
         stream_panel_ = green_stream(g.gb, hi);
-      else if (g.panel == 'a')
+      else if (panel == 'a')
         stream_panel_ = green_stream(g.ga, hi);
       else
         CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
@@ -286,8 +288,33 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       CU(cudaStreamCreateWithPriority(&stream_far_, cudaStreamNonBlocking, hi));
     }
   }
+  {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream_upd1_, cudaStreamNonBlocking, hi));
+    // HGPU_UPD_SMS=k: the deferred update runs on k SMs only (green context)
+    int upd_sms = 0;
+    if (const char* e = std::getenv("HGPU_UPD_SMS")) upd_sms = std::atoi(e);
+    const GreenSplit& gu = green_split(device_, upd_sms);
+    if (gu.ok)
+      stream_upd2_ = green_stream(gu.ga, lo);
+    else
+      CU(cudaStreamCreateWithPriority(&stream_upd2_, cudaStreamNonBlocking, lo));
+  }
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
+  if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_FAR_LANES"))
+    far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
+  {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    far_streams_[0] = stream_far_;
+    for (int l = 1; l < kMaxFarLanes; ++l)
+      CU(cudaStreamCreateWithPriority(&far_streams_[l], cudaStreamNonBlocking, hi));
+    for (int l = 0; l < kMaxFarLanes; ++l)
+      CU(cudaEventCreateWithFlags(&far_ev_[l], cudaEventDisableTiming));
+  }
   if (const char* e = std::getenv("HGPU_NEAR")) near_rows_ = std::max(2, std::atoi(e));
   if (const char* e = std::getenv("HGPU_RATIO_GEMM")) ratio_gemm_ = std::atoi(e);
   if (ratio_gemm_)
@@ -308,7 +335,13 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
     if (h) cublasDestroy((cublasHandle_t)h);
+  for (int l = 1; l < kMaxFarLanes; ++l)
+    if (far_streams_[l]) cudaStreamDestroy(far_streams_[l]);
+  for (cudaEvent_t e : far_ev_)
+    if (e) cudaEventDestroy(e);
   if (stream_far_) cudaStreamDestroy(stream_far_);
+  if (stream_upd1_) cudaStreamDestroy(stream_upd1_);
+  if (stream_upd2_) cudaStreamDestroy(stream_upd2_);
   if (stream_helper_) cudaStreamDestroy(stream_helper_);
   if (stream_panel_) cudaStreamDestroy(stream_panel_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -549,7 +582,17 @@ void Matrix::build(int min_logL) {
   // two slot sets: panel b uses set b%2 (lookahead needs b+1 while the
   // trailing update of b still reads b)
   // (the interval path has no lookahead: one slot set)
-  const size_t nsets = interval_ ? 1 : 2;
+  // slot sets: 2 + deferral depth (HGPU_DEFER, default 4), fewer when the
+  // device memory would not hold them beside the workspace
+  size_t nsets = 1;
+  if (!interval_) {
+    nsets = 2 + (size_t)std::max(0, defer_);
+    const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    while (nsets > 2 && per_set * nsets > 0.5 * (double)free_b) --nsets;
+  }
+  nsets_ = (int)nsets;
   vhdr_ = dalloc<int>(nsets * kb * n_);
   rhdr_ = dalloc<int>(nsets * kb * n_);
   vlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
@@ -700,7 +743,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   std::vector<uint32_t> hr_limbs;
   size_t uev_used = 0;
   const int nblocks = (n + kb - 1) / kb;
-  while ((int)pev_.size() < 3 * nblocks + 3) {
+  while ((int)pev_.size() < 4 * nblocks + 4) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pev_.push_back(e);
@@ -710,9 +753,25 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   cudaEvent_t* panel_done = pev_.data();
   cudaEvent_t* next_ready = pev_.data() + nblocks + 1;
   cudaEvent_t* trail_done = pev_.data() + 2 * nblocks + 2;
+  // rest_done[b]: the deferred part of panel b's trailing update (stream su2)
+  cudaEvent_t* rest_done = pev_.data() + 3 * nblocks + 3;
 
   // slot set of panel b: rows [set*kb*n, ...) of Vint/Rint/Vhat/Rhat
-  auto set_row0 = [&](int b) { return (long long)(b % 2) * kb * n; };
+  const int nsets = nsets_;
+  auto set_row0 = [&](int b) { return (long long)(b % nsets) * kb * n; };
+  // Trailing update of panel b, by band j (columns
+  // [j kb, (j+1) kb)):
+  //   j = b+1          at the end of panel b on su1 (gates panel b+1),
+  //   b+2 <= j <= b+s  caught up on su1 at the start of panel j-1, while
+  //                    panel j-1 factorises (band j is idle then),
+  //   j >= b+1+s       at the end of panel b on su2, lowest priority.
+  // su2's update of panel b may lag up to s panels: early panels (much
+  // trailing work, short pivot chain) hand work to late ones (little work,
+  // the chain alone).  Band j is touched by su2 up to panel j-1-s, then by
+  // su1, which waits for rest_done[j-1-s] first.  Slot sets are reused after
+  // nsets = s + 2 panels.
+  const int sdef = std::max(1, nsets - 2);
+  cudaStream_t su1 = stream_upd1_, su2 = stream_upd2_;
   const char* tl_path = std::getenv("HGPU_TIMELINE");
   tl_.clear();
   tl_used_ = 0;
@@ -735,7 +794,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaEventRecord(b, s));
     tl_.push_back({kind, p, a, b});
   };
-  auto timed_update = [&](int b, int nslots, int c_begin, int c_end) {
+  auto timed_update = [&](int b, int nslots, int c_begin, int c_end,
+                          cudaStream_t us, int kind) {
     if (c_begin >= c_end || nslots <= 0) return;
     if (profile) {
       while (uev_.size() < uev_used + 2) {
@@ -743,16 +803,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         CU(cudaEventCreate(&e));
         uev_.push_back(e);
       }
-      CU(cudaEventRecord(uev_[uev_used], st));
+      CU(cudaEventRecord(uev_[uev_used], us));
     }
     const long long r0 = set_row0(b);
-    TL(c_begin == b * kb + kb ? 8 : 9, b, st, [&] {
+    TL(kind, b, us, [&] {
       return launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW,
                            rhat_ + r0 * NW, slot_stride, nslots, c_begin, c_end,
-                           err_, st);
+                           err_, us);
     });
     if (profile) {
-      CU(cudaEventRecord(uev_[uev_used + 1], st));
+      CU(cudaEventRecord(uev_[uev_used + 1], us));
       uev_used += 2;
       double pairs = 0;
       for (int c = c_begin; c < c_end; ++c) pairs += n - c;
@@ -761,12 +821,12 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     }
   };
   // trailing update of panel b restricted to owned columns in [lo, hi)
-  auto trailing = [&](int b, int lo, int hi) {
+  auto trailing = [&](int b, int lo, int hi, cudaStream_t us, int kind) {
     const int p0 = b * kb, nsl = std::min(kb, n - 1 - p0);
     int run_begin = -1, run_end = -1;
     auto flush = [&]() {
       if (run_begin >= 0 && run_begin < run_end)
-        timed_update(b, nsl, run_begin, run_end);
+        timed_update(b, nsl, run_begin, run_end, us, kind);
       run_begin = run_end = -1;
     };
     for (int ob : owned_blocks_) {
@@ -789,7 +849,6 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     sev_.push_back(e);
   }
   cudaStream_t sh = stream_helper_;
-  cudaStream_t sf = stream_far_;
   {
     // bits bound of any diagonal Schur complement W_rr (PD: <= M_rr - x)
     int db = 0;
@@ -805,13 +864,23 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     dmax_bits_ = db + 1;
   }
   CU(cudaEventRecord(next_ready[0], st));  // init done
+  CU(cudaStreamWaitEvent(su1, next_ready[0], 0));
+  CU(cudaStreamWaitEvent(su2, next_ready[0], 0));
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
     const long long row0set = set_row0(b);
     // ---- panel b on the high-priority streams
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
-    if (b >= 2) CU(cudaStreamWaitEvent(sp, trail_done[b - 2], 0));
+    // slot set reuse: su1's last use of panel b - nsets precedes next_ready[b]
+    if (b >= nsets) CU(cudaStreamWaitEvent(sp, rest_done[b - nsets], 0));
+    // catch-up of band b+1 with panels [b+1-s, b-1] on su1 (after su2's
+    // last touch of the band, panel b-s), overlapping panel b
+    if (p1 < n) {
+      if (b - sdef >= 0) CU(cudaStreamWaitEvent(su1, rest_done[b - sdef], 0));
+      for (int bb = std::max(0, b + 1 - sdef); bb <= b - 1; ++bb)
+        trailing(bb, p1, std::min(n, p1 + kb), su1, 13);
+    }
     if (owner == rank_) {
       // Per stage p three chains run concurrently:
       //   sh (critical): col(pivot p) -> extract(pivot p) -> recip(p) ->
@@ -833,9 +902,12 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       const bool rg_near = rg_ok && (ratio_gemm_ & 2);
       const bool rg_far = rg_ok && (ratio_gemm_ & 1);
       bool chain_started = false;
+      // far lanes (one when the divisions use global scratch or the GEMM)
+      const int nlanes = (div_global_ || rg_far) ? 1 : far_lanes_;
       if (far) {
         CU(cudaEventRecord(sev_[4 * n + 1], sp));
-        CU(cudaStreamWaitEvent(sf, sev_[4 * n + 1], 0));
+        for (int l = 0; l < nlanes; ++l)
+          CU(cudaStreamWaitEvent(far_streams_[l], sev_[4 * n + 1], 0));
       }
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
@@ -908,40 +980,49 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           CU(cudaEventRecord(sev_[4 * p + 2], sp));
           if (far) {
             // far rows: column p receives stages [p0, p) (V^_s[p] of the
-            // near rows, extract(near p-1) done; their own R^_s on sf), then
-            // extraction and, once recip(p) is done, the ratios
-            if (p > p0) CU(cudaStreamWaitEvent(sf, sev_[4 * (p - 1)], 0));
-            TL(10, p, sf, [&] {
-              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                       p, near_end, n, err_, sf);
-            });
-            TL(11, p, sf, [&] {
-              return launch_extract(D, W_, colbase_, p, near_end, n, vint, row0,
-                                    piv, maxbitsV, vhat_, maxdegV, err_, sf, 0,
-                                    rg_far ? vdig_ : nullptr, rg_kd_);
-            });
-            CU(cudaStreamWaitEvent(sf, sev_[4 * p + 1], 0));
-            if (rg_far) {
-              TL(12, p, sf, [&] {
-                ratio_gemm(1, p, near_end, n, vint, row0, yb, yss, rint,
-                           maxdegR + p, dscratch3_, sf);
-                return cudaSuccess;
+            // near rows, extract(near p-1) done; their own R^_s on the lane's
+            // stream), then extraction and, once recip(p) is done, the
+            // ratios.  The far rows are split into lanes on separate streams
+            // so that one lane's division overlaps another's extraction.
+            for (int l = 0; l < nlanes; ++l) {
+              cudaStream_t fs = far_streams_[l];
+              const int lo = near_end + (int)((long long)(n - near_end) * l / nlanes);
+              const int hi = near_end + (int)((long long)(n - near_end) * (l + 1) / nlanes);
+              if (lo >= hi) continue;
+              if (p > p0) CU(cudaStreamWaitEvent(fs, sev_[4 * (p - 1)], 0));
+              TL(10, p, fs, [&] {
+                return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                         p, lo, hi, err_, fs);
               });
-            } else {
-              TL(12, p, sf, [&] {
-                return launch_divide(D, vint, row0, p, near_end, n, yb, yss, rint,
-                                     row0, rhat_, maxdegR + p, dscratch3_,
-                                     div_global_ ? 1 : 0, err_, sf);
+              TL(11, p, fs, [&] {
+                return launch_extract(D, W_, colbase_, p, lo, hi, vint, row0,
+                                      piv, maxbitsV, vhat_, maxdegV, err_, fs, 0,
+                                      rg_far ? vdig_ : nullptr, rg_kd_);
               });
+              CU(cudaStreamWaitEvent(fs, sev_[4 * p + 1], 0));
+              if (rg_far) {
+                TL(12, p, fs, [&] {
+                  ratio_gemm(1, p, lo, hi, vint, row0, yb, yss, rint,
+                             maxdegR + p, dscratch3_, fs);
+                  return cudaSuccess;
+                });
+              } else {
+                TL(12, p, fs, [&] {
+                  return launch_divide(D, vint, row0, p, lo, hi, yb, yss, rint,
+                                       row0, rhat_, maxdegR + p, dscratch3_,
+                                       div_global_ ? 1 : 0, err_, fs);
+                });
+              }
             }
           }
           if (p + 1 == p1 || p + 1 == n - 1) {
             // join: the next step on sp needs R_p[p+1] as well
             CU(cudaStreamWaitEvent(sp, sev_[4 * p + 3], 0));
-            if (far) {
-              CU(cudaEventRecord(sev_[4 * n + 2], sf));
-              CU(cudaStreamWaitEvent(sp, sev_[4 * n + 2], 0));
-            }
+            if (far)
+              for (int l = 0; l < nlanes; ++l) {
+                CU(cudaEventRecord(far_ev_[l], far_streams_[l]));
+                CU(cudaStreamWaitEvent(sp, far_ev_[l], 0));
+              }
           }
         } else {
           // left-looking inside the panel: column p receives stages [p0, p)
@@ -1009,20 +1090,26 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     // ---- trailing update of panel b on the bulk stream: the next panel's
     // columns first (they gate panel b+1), then everything to their right,
     // which overlaps panel b+1's factorisation
-    CU(cudaStreamWaitEvent(st, panel_done[b], 0));
+    CU(cudaStreamWaitEvent(su1, panel_done[b], 0));
+    CU(cudaStreamWaitEvent(su2, panel_done[b], 0));
     if (p1 < n) {
       const int p2 = std::min(n, p1 + kb);
-      trailing(b, p1, p2);
-      CU(cudaEventRecord(next_ready[b + 1], st));
-      if (!(D.debug & 512)) trailing(b, p2, n);  // 512: timing experiment only
+      trailing(b, p1, p2, su1, 8);
+      CU(cudaEventRecord(next_ready[b + 1], su1));
+      const int pr = std::min(n, (b + 1 + sdef) * kb);
+      if (!(D.debug & 512)) trailing(b, pr, n, su2, 9);  // 512: timing experiment only
     } else {
-      CU(cudaEventRecord(next_ready[b + 1], st));
+      CU(cudaEventRecord(next_ready[b + 1], su1));
     }
-    CU(cudaEventRecord(trail_done[b], st));
+    CU(cudaEventRecord(rest_done[b], su2));
   }
-  // join the panel stream back into the bulk stream
+  // join the panel and update streams back into the bulk stream
   CU(cudaEventRecord(panel_done[nblocks], sp));
   CU(cudaStreamWaitEvent(st, panel_done[nblocks], 0));
+  CU(cudaEventRecord(trail_done[0], su1));
+  CU(cudaStreamWaitEvent(st, trail_done[0], 0));
+  CU(cudaEventRecord(trail_done[1], su2));
+  CU(cudaStreamWaitEvent(st, trail_done[1], 0));
   CU(launch_validate(D, maxdegV, maxdegR, n - 1, err_, st));
   CU(cudaEventRecord(ev1_, st));
   res.launches = kernel_launch_count() - launches0;

@@ -172,6 +172,14 @@ class Matrix {
   cudaStream_t stream_panel_ = nullptr;  // panel factorisation, high priority
   cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
   cudaStream_t stream_far_ = nullptr;    // far rows of the panel (may lag)
+  static constexpr int kMaxFarLanes = 4;
+  int far_lanes_ = 2;  // far-row streams (HGPU_FAR_LANES)
+  cudaStream_t far_streams_[kMaxFarLanes] = {};  // [0] = stream_far_
+  cudaEvent_t far_ev_[kMaxFarLanes] = {};
+  cudaStream_t stream_upd1_ = nullptr;   // trailing update: next band, catch-up
+  cudaStream_t stream_upd2_ = nullptr;   // trailing update: deferred bands
+  int defer_ = 4;   // panels the deferred trailing update may lag (HGPU_DEFER)
+  int nsets_ = 2;   // V/R slot sets (2 + deferral, memory permitting)
   int chain_sms_ = 0;  // SMs reserved for the pivot chain (green context), 0 = none
   std::vector<cudaEvent_t> pev_, sev_;
   bool recip_bound_ = true;  // reciprocal precision from the PD bound
