@@ -1,0 +1,57 @@
+"""GPU parity of the scheduling variants and opt-in arithmetic paths.
+
+The factorisation's results may not depend on how the panel work is spread
+over streams (near/far rows, far lanes, deferred trailing update, SM split)
+nor on how the stage's ratios are formed (k_divide or the int8 tensor-core
+ratio GEMM): every variant must equal the reference's ldlt_det_serial
+(ldlt.cpp:31-77) bit for bit.  The knobs are environment variables read when
+a matrix is created (engine.cpp).  N is chosen so that the matrix has far
+rows (N > 64) and several panels (kb = 32).
+"""
+import os
+
+import pytest
+
+import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [
+    {},
+    {"HGPU_FAR_LANES": "1", "HGPU_DEFER": "0"},
+    {"HGPU_FAR_LANES": "3", "HGPU_DEFER": "6", "HGPU_NEAR": "40"},
+    {"HGPU_RATIO_GEMM": "3"},
+    {"HGPU_RATIO_GEMM": "1", "HGPU_FAR_LANES": "1"},
+    {"HGPU_SM_SPLIT": "8:b"},
+    {"HGPU_UPD_SMS": "96", "HGPU_GRID": "3"},
+]
+
+
+@pytest.fixture(scope="module")
+def hg():
+    from paper_0902_0852_b200 import hgpu
+    hgpu.load()
+    return hgpu
+
+
+@pytest.fixture(scope="module")
+def case():
+    # config-2 shape at reduced size: beta = 7/4, certified-rounded moments
+    n, k = 150, 1024
+    ref = po.OracleLib()
+    strip = ref.build_strip(n, 7, 4, k)
+    x = -(1 << (k - 16))
+    want = ref.ldlt(strip, x, k, capture=True)
+    return n, k, strip, x, want
+
+
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
+def test_variant_bit_exact(hg, case, env, monkeypatch):
+    n, k, strip, x, want = case
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    m = hg.HankelMatrixGPU(strip, k)
+    got = m.ldlt(x, capture=True)
+    assert got.pivots == want.pivots
+    bad = [key for key in want.ratios if got.ratios[key] != want.ratios[key]]
+    assert not bad, f"{len(bad)} ratios differ under {env}, first {bad[:3]}"
