@@ -38,10 +38,9 @@ def hg():
 def case():
     # config-2 shape at reduced size: beta = 7/4, certified-rounded moments
     n, k = 150, 1024
-    ref = po.OracleLib()
-    strip = ref.build_strip(n, 7, 4, k)
+    strip = po.RefLib().build_strip(n, 7, 4, k)
     x = -(1 << (k - 16))
-    want = ref.ldlt(strip, x, k, capture=True)
+    want = po.OracleLib().ldlt(strip, x, k, capture=True)
     return n, k, strip, x, want
 
 
