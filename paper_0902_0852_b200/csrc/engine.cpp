@@ -304,6 +304,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
   if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
   {
@@ -928,19 +929,29 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 1)], 0));
             if (p - 2 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 2) + 2], 0));
           }
-          TL(0, p, sh, [&] {
-            return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                     p, p, p + 1, err_, sh);
-          });
-          TL(1, p, sh, [&] {
-            return launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0,
-                                  piv, maxbitsV, vhat_, maxdegV, err_, sh);
-          });
-          TL(2, p, sh, [&] {
-            return launch_recip(D, vint, row0 + p, maxbitsV, p, piv,
-                                dmax_bits_, yb, yss, rscratch_,
-                                recip_global_ ? 1 : 0, err_, sh);
-          });
+          if (fused_pivot_) {
+            // pivot-entry update, extraction and reciprocal in one CTA
+            TL(2, p, sh, [&] {
+              return launch_pivot(D, W_, colbase_, vh, rh, slot_stride, s, p,
+                                  vint, row0, piv, maxbitsV, vhat_, maxdegV,
+                                  dmax_bits_, yb, yss, rscratch_,
+                                  recip_global_ ? 1 : 0, err_, sh);
+            });
+          } else {
+            TL(0, p, sh, [&] {
+              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                       p, p, p + 1, err_, sh);
+            });
+            TL(1, p, sh, [&] {
+              return launch_extract(D, W_, colbase_, p, p, p + 1, vint, row0,
+                                    piv, maxbitsV, vhat_, maxdegV, err_, sh);
+            });
+            TL(2, p, sh, [&] {
+              return launch_recip(D, vint, row0 + p, maxbitsV, p, piv,
+                                  dmax_bits_, yb, yss, rscratch_,
+                                  recip_global_ ? 1 : 0, err_, sh);
+            });
+          }
           CU(cudaEventRecord(sev_[4 * p + 1], sh));
           // near rows of column p on the panel stream (rows > p)
           const int rn = far ? near_end : n;

@@ -151,11 +151,11 @@ __global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
 //   V_p[r] = tdiv_q_2exp(W[r][p], K/2)                 (ldlt.cpp:54-55)
 //   ZeroPivot if V_p[p] == 0 and p < n-1               (ldlt.cpp:56)
 // V goes to vint[slot][r]; the full pivot to piv[p].
-__global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
-                          int p, int r_begin, int r_end, IntBuf vint,
-                          long long vrow0, IntBuf piv, int* maxbitsV,
-                          uint32_t* vhat, int* maxdegV, int* err, int round,
-                          uint8_t* vdig, int kd) {
+__device__ void extract_body(const DevPlan& P, const uint32_t* W, const long long* colbase,
+                             int p, int r_begin, int r_end, IntBuf vint,
+                             long long vrow0, IntBuf piv, int* maxbitsV,
+                             uint32_t* vhat, int* maxdegV, int* err, int round,
+                             uint8_t* vdig, int kd, int bx, int gx) {
   extern __shared__ uint32_t sm[];
   __shared__ int s_bump;
   if (stage_aborted(err)) return;
@@ -173,7 +173,7 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
   stage_tables(P, tabf, tabi, &twm, &itwm);
   const uint64_t dmask = (1ull << w) - 1ull;
 
-  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
+  for (int r = r_begin + bx; r < r_end; r += gx) {
     const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
     for (int i = threadIdx.x; i < P.NW / 4; i += blockDim.x)
       reinterpret_cast<uint4*>(A)[i] = reinterpret_cast<const uint4*>(src)[i];
@@ -365,6 +365,15 @@ __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase
   }
 }
 
+__global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
+                          int p, int r_begin, int r_end, IntBuf vint,
+                          long long vrow0, IntBuf piv, int* maxbitsV,
+                          uint32_t* vhat, int* maxdegV, int* err, int round,
+                          uint8_t* vdig, int kd) {
+  extract_body(P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV,
+               vhat, maxdegV, err, round, vdig, kd, blockIdx.x, gridDim.x);
+}
+
 // ------------------------------------------------------------- reciprocal --
 // Per stage, one CTA: Y ~ 2^S / |V_p| within a few units, S = n + Pt with
 // n = bits(V_p) and Pt = e + 32, where e bounds the bits of every ratio of the
@@ -382,15 +391,15 @@ __device__ inline int recip_levels(int Pt, int* lv) {
   return k;
 }
 
-__global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long prow,
-                        const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
-                        uint32_t* Ybuf, int* ys, uint32_t* gscratch,
-                        int use_gscratch, int* err) {
+__device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
+                           const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
+                           uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+                           int use_gscratch, int* err, int b) {
   extern __shared__ uint32_t sm_dyn[];
   __shared__ uint32_t red[64];
   if (stage_aborted(err)) return;
   {
-    const int b = blockIdx.y;  // batched instance (0 in the LDL^T)
+    // b: batched instance (0 in the LDL^T)
     prow += (long long)b * P.bat_vrow;
     maxbitsV += b * P.bat_mb;
     Ybuf += b * P.bat_ybuf;
@@ -557,6 +566,51 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
     ys[1] = nY;
     ys[2] = amax;
   }
+}
+
+__global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long prow,
+                        const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
+                        uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+                        int use_gscratch, int* err) {
+  recip_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, gscratch,
+             use_gscratch, err, blockIdx.y);
+}
+
+// Pivot chain of stage p in one CTA (the three steps of the helper stream,
+// fused to save two launches per stage): column p's pivot entry receives the
+// panel's stages [0, s) (as k_update_col), is extracted (k_extract, row p:
+// pivot, V_p[p], ZeroPivot) and the stage's reciprocal is formed (k_recip).
+__global__ void __launch_bounds__(512)
+k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+        const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
+        IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
+        int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+        int use_gscratch, int* err) {
+  if (stage_aborted(err)) return;
+  if (nslots > 0) {
+    const long long NW = P.NW;
+    uint32_t* dst = W + colbase[p] * NW;
+    const uint32_t* vp = Vhat + (long long)p * NW;
+    const uint32_t* rp = Rhat + (long long)p * NW;
+    for (int wd = threadIdx.x; wd < P.NW; wd += blockDim.x) {
+      uint64_t acc = 0;
+      for (int s = 0; s < nslots; ++s) {
+        const long long off = s * row_stride_slot + wd;
+        acc += (uint64_t)__ldg(vp + off) * __ldg(rp + off);
+      }
+      const PrimeConsts& pc = P.pc[wd / P.L];
+      const uint32_t t32 = reduce_sum64(acc, pc);
+      const uint32_t old = dst[wd];
+      dst[wd] = old >= t32 ? old - t32 : old + pc.q - t32;
+    }
+    __syncthreads();
+  }
+  extract_body(P, W, colbase, p, p, p + 1, vint, vrow0, piv, maxbitsV, vhat,
+               maxdegV, err, 0, nullptr, 0, 0, 1);
+  __syncthreads();
+  if (p < P.n - 1)
+    recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
+               gscratch, use_gscratch, err, 0);
 }
 
 // Quotient from the top of the product.  Pr[0, nPs) holds the product
@@ -1309,6 +1363,22 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
   return post_launch(st);
 }
 
+cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase,
+                         const uint32_t* Vhat, const uint32_t* Rhat,
+                         long long row_stride_slot, int nslots, int p,
+                         IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV,
+                         uint32_t* vhat, int* maxdegV, int dmax_bits,
+                         uint32_t* Ybuf, int* ys, uint32_t* scratch,
+                         int use_gscratch, int* err, cudaStream_t st) {
+  ++g_launches;
+  const size_t smem = std::max(extract_smem_bytes(P),
+                               use_gscratch ? (size_t)0 : recip_scratch_words(P) * 4);
+  k_pivot<<<1, 512, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
+                                p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
+                                dmax_bits, Ybuf, ys, scratch, use_gscratch, err);
+  return post_launch(st);
+}
+
 cudaError_t launch_recip_batch(const DevPlan& P, IntBuf vint, long long prow,
                                const int* maxbitsV, uint32_t* Ybuf, int* ys,
                                uint32_t* scratch, int batch, int* err,
@@ -1466,6 +1536,12 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                 (int)fwd)) != cudaSuccess)
     return e;
   const size_t rec = recip_scratch_words(P) * 4;
+  {
+    const size_t piv_smem = std::max(ext, (int)rec > maxopt ? (size_t)0 : rec);
+    if ((e = cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)piv_smem)) != cudaSuccess)
+      return e;
+  }
   // the reciprocal CTA runs beside the bulk kernels; shared-memory scratch
   // is faster even at ~190 KB (measured at config 3: 421 -> 405 ms per
   // factorisation), so it is used whenever it fits.  HGPU_RECIP_SMEM=0

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 VARIANTS = [
     {},
-    {"HGPU_FAR_LANES": "1", "HGPU_DEFER": "0"},
+    {"HGPU_FAR_LANES": "1", "HGPU_DEFER": "0", "HGPU_FUSED_PIVOT": "0"},
     {"HGPU_FAR_LANES": "3", "HGPU_DEFER": "6", "HGPU_NEAR": "40"},
     {"HGPU_RATIO_GEMM": "3"},
     {"HGPU_RATIO_GEMM": "1", "HGPU_FAR_LANES": "1"},
