@@ -930,12 +930,25 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             if (p - 2 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 2) + 2], 0));
           }
           if (fused_pivot_) {
-            // pivot-entry update, extraction and reciprocal in one CTA
+            // R_{p-1}[p] (inside the panel), pivot-entry update, extraction
+            // and reciprocal in one CTA
+            PivotDiv pd{};
+            if (p > p0) {
+              pd.on = 1;
+              pd.vrow0 = row0 - n;  // stage p-1 of this panel's slot set
+              pd.Ybuf = ybuf_ + (size_t)((p - 1) % kYRing) * P.ycap;
+              pd.ys = ys_ + ((p - 1) % kYRing) * 4;
+              pd.rint = rint;
+              pd.rhat = rhat_;
+              pd.maxdegR = maxdegR + (p - 1);
+              pd.dscr = dscratch_;
+              pd.use_dscr = div_global_ ? 1 : 0;
+            }
             TL(2, p, sh, [&] {
               return launch_pivot(D, W_, colbase_, vh, rh, slot_stride, s, p,
                                   vint, row0, piv, maxbitsV, vhat_, maxdegV,
                                   dmax_bits_, yb, yss, rscratch_,
-                                  recip_global_ ? 1 : 0, err_, sh);
+                                  recip_global_ ? 1 : 0, err_, sh, pd);
             });
           } else {
             TL(0, p, sh, [&] {
@@ -965,13 +978,17 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                                   rg_near ? vdig_ : nullptr, rg_kd_);
           });
           CU(cudaEventRecord(sev_[4 * p], sp));
-          // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot)
+          // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot):
+          // inside the next stage's k_pivot, except at the panel's last stage
+          // (the trailing update reads it)
           CU(cudaStreamWaitEvent(sh, sev_[4 * p], 0));
-          TL(5, p, sh, [&] {
-            return launch_divide(D, vint, row0, p, p + 1, p + 2, yb, yss,
-                                 rint, row0, rhat_, maxdegR + p, dscratch_,
-                                 div_global_ ? 1 : 0, err_, sh);
-          });
+          if (!fused_pivot_ || p + 1 == p1 || p + 1 == n - 1) {
+            TL(5, p, sh, [&] {
+              return launch_divide(D, vint, row0, p, p + 1, p + 2, yb, yss,
+                                   rint, row0, rhat_, maxdegR + p, dscratch_,
+                                   div_global_ ? 1 : 0, err_, sh);
+            });
+          }
           CU(cudaEventRecord(sev_[4 * p + 3], sh));
           // R_p[p+1 < r < rn] on the panel stream
           CU(cudaStreamWaitEvent(sp, sev_[4 * p + 1], 0));

@@ -576,42 +576,6 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
              use_gscratch, err, blockIdx.y);
 }
 
-// Pivot chain of stage p in one CTA (the three steps of the helper stream,
-// fused to save two launches per stage): column p's pivot entry receives the
-// panel's stages [0, s) (as k_update_col), is extracted (k_extract, row p:
-// pivot, V_p[p], ZeroPivot) and the stage's reciprocal is formed (k_recip).
-__global__ void __launch_bounds__(512)
-k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
-        const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
-        IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
-        int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
-        int use_gscratch, int* err) {
-  if (stage_aborted(err)) return;
-  if (nslots > 0) {
-    const long long NW = P.NW;
-    uint32_t* dst = W + colbase[p] * NW;
-    const uint32_t* vp = Vhat + (long long)p * NW;
-    const uint32_t* rp = Rhat + (long long)p * NW;
-    for (int wd = threadIdx.x; wd < P.NW; wd += blockDim.x) {
-      uint64_t acc = 0;
-      for (int s = 0; s < nslots; ++s) {
-        const long long off = s * row_stride_slot + wd;
-        acc += (uint64_t)__ldg(vp + off) * __ldg(rp + off);
-      }
-      const PrimeConsts& pc = P.pc[wd / P.L];
-      const uint32_t t32 = reduce_sum64(acc, pc);
-      const uint32_t old = dst[wd];
-      dst[wd] = old >= t32 ? old - t32 : old + pc.q - t32;
-    }
-    __syncthreads();
-  }
-  extract_body(P, W, colbase, p, p, p + 1, vint, vrow0, piv, maxbitsV, vhat,
-               maxdegV, err, 0, nullptr, 0, 0, 1);
-  __syncthreads();
-  if (p < P.n - 1)
-    recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
-               gscratch, use_gscratch, err, 0);
-}
 
 // Quotient from the top of the product.  Pr[0, nPs) holds the product
 // columns from limb K0 on, i.e. F 2^shs with F = |V| Y / 2^sh lowered by
@@ -732,27 +696,27 @@ __device__ int ratio_quotient(const DevPlan& P, uint32_t* Pr, int nPs, int shs,
 // [4, 2^32-5], q = floor(F) exactly and no remainder is needed.  Otherwise
 // (e.g. exact quotients) floor(F) is within one of q and the remainder
 // window A - q~ D over nD+2 limbs decides the correction exactly.
-__global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
-                         int r_begin, int r_end,
-                         const uint32_t* Ybuf, const int* ys, IntBuf rint,
-                         long long rrow0, uint32_t* rhat, int* maxdegR,
-                         uint32_t* gscratch, int use_gscratch, int* err,
-                         IvDiv iv) {
+__device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int p,
+                            int r_begin, int r_end,
+                            const uint32_t* Ybuf, const int* ys, IntBuf rint,
+                            long long rrow0, uint32_t* rhat, int* maxdegR,
+                            uint32_t* gscratch, int use_gscratch, int* err,
+                            IvDiv iv, int bx, int gx, int b) {
   extern __shared__ uint32_t sm_dyn[];
   if (stage_aborted(err)) return;
   const int cap = P.cap, ycap = P.ycap;
   const long long span = div_span_words(cap, ycap);
   const long long cta_words = span + div_extra_words(P);
   {
-    const int b = blockIdx.y;  // batched instance (0 in the LDL^T)
+    // b: batched instance (0 in the LDL^T)
     vrow0 += (long long)b * P.bat_vrow;
     rrow0 += (long long)b * P.bat_rrow;
     Ybuf += b * P.bat_ybuf;
     ys += b * P.bat_ys;
-    gscratch += (long long)b * gridDim.x * cta_words;
+    gscratch += (long long)b * gx * cta_words;
   }
   uint32_t* tab = sm_dyn;
-  uint32_t* sm = use_gscratch ? gscratch + (long long)blockIdx.x * cta_words
+  uint32_t* sm = use_gscratch ? gscratch + (long long)bx * cta_words
                               : sm_dyn + (P.tw_smem ? P.NW : 0);
   const uint32_t* twm;
   stage_tables(P, tab, nullptr, &twm, nullptr);
@@ -768,7 +732,7 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
   // ZeroPivot aborted the stage); sd is its sign
   const int sd = iv.mode == 0 ? 0 : (vint.hdr[pidx] > 0 ? 1 : -1);
 
-  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
+  for (int r = r_begin + bx; r < r_end; r += gx) {
     const long long vidx = vrow0 + r;
     // numerator bound and divisor (ldlt.cpp:113-131 restated per corner):
     //   R.lo = floor(min corner): N = sd > 0 ? V.lo : V.hi, D = N > 0 ? D.hi : D.lo
@@ -839,6 +803,62 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
       __syncthreads();
     }
   }
+}
+
+__global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+                         int r_begin, int r_end,
+                         const uint32_t* Ybuf, const int* ys, IntBuf rint,
+                         long long rrow0, uint32_t* rhat, int* maxdegR,
+                         uint32_t* gscratch, int use_gscratch, int* err,
+                         IvDiv iv) {
+  divide_body(P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat,
+              maxdegR, gscratch, use_gscratch, err, iv, blockIdx.x, gridDim.x,
+              blockIdx.y);
+}
+
+// Pivot chain of stage p in one CTA (the three steps of the helper stream,
+// fused to save two launches per stage): column p's pivot entry receives the
+// panel's stages [0, s) (as k_update_col), is extracted (k_extract, row p:
+// pivot, V_p[p], ZeroPivot) and the stage's reciprocal is formed (k_recip).
+__global__ void __launch_bounds__(512)
+k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+        const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
+        IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
+        int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+        int use_gscratch, int* err, PivotDiv pd) {
+  if (stage_aborted(err)) return;
+  if (pd.on) {
+    // R_{p-1}[p] of the previous stage of the panel (k_divide, one row)
+    divide_body(P, vint, pd.vrow0, p - 1, p, p + 1, pd.Ybuf, pd.ys, pd.rint,
+                pd.vrow0, pd.rhat, pd.maxdegR, pd.dscr, pd.use_dscr, err, IvDiv{},
+                0, 1, 0);
+    __syncthreads();
+    if (stage_aborted(err)) return;
+  }
+  if (nslots > 0) {
+    const long long NW = P.NW;
+    uint32_t* dst = W + colbase[p] * NW;
+    const uint32_t* vp = Vhat + (long long)p * NW;
+    const uint32_t* rp = Rhat + (long long)p * NW;
+    for (int wd = threadIdx.x; wd < P.NW; wd += blockDim.x) {
+      uint64_t acc = 0;
+      for (int s = 0; s < nslots; ++s) {
+        const long long off = s * row_stride_slot + wd;
+        acc += (uint64_t)__ldg(vp + off) * __ldg(rp + off);
+      }
+      const PrimeConsts& pc = P.pc[wd / P.L];
+      const uint32_t t32 = reduce_sum64(acc, pc);
+      const uint32_t old = dst[wd];
+      dst[wd] = old >= t32 ? old - t32 : old + pc.q - t32;
+    }
+    __syncthreads();
+  }
+  extract_body(P, W, colbase, p, p, p + 1, vint, vrow0, piv, maxbitsV, vhat,
+               maxdegV, err, 0, nullptr, 0, 0, 1);
+  __syncthreads();
+  if (p < P.n - 1)
+    recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
+               gscratch, use_gscratch, err, 0);
 }
 
 // ------------------------------------------- ratios on the tensor cores ---
@@ -1369,13 +1389,17 @@ cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase
                          IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV,
                          uint32_t* vhat, int* maxdegV, int dmax_bits,
                          uint32_t* Ybuf, int* ys, uint32_t* scratch,
-                         int use_gscratch, int* err, cudaStream_t st) {
+                         int use_gscratch, int* err, cudaStream_t st,
+                         const PivotDiv& pd) {
   ++g_launches;
-  const size_t smem = std::max(extract_smem_bytes(P),
-                               use_gscratch ? (size_t)0 : recip_scratch_words(P) * 4);
+  size_t smem = std::max(extract_smem_bytes(P),
+                         use_gscratch ? (size_t)0 : recip_scratch_words(P) * 4);
+  if (pd.on)
+    smem = std::max(smem, pd.use_dscr ? (size_t)(P.tw_smem ? P.NW : 0) * 4
+                                      : divide_smem_words(P) * 4);
   k_pivot<<<1, 512, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
                                 p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
-                                dmax_bits, Ybuf, ys, scratch, use_gscratch, err);
+                                dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
   return post_launch(st);
 }
 
@@ -1537,7 +1561,9 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
     return e;
   const size_t rec = recip_scratch_words(P) * 4;
   {
-    const size_t piv_smem = std::max(ext, (int)rec > maxopt ? (size_t)0 : rec);
+    size_t piv_smem = std::max(ext, (int)rec > maxopt ? (size_t)0 : rec);
+    const size_t dv = divide_smem_words(P) * 4;
+    if ((int)dv <= maxopt) piv_smem = std::max(piv_smem, dv);
     if ((e = cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)piv_smem)) != cudaSuccess)
       return e;

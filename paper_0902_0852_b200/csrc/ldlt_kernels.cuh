@@ -127,15 +127,30 @@ cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          uint32_t* Ybuf, int* ys, uint32_t* scratch,
                          int use_gscratch, int* err, cudaStream_t st);
 size_t divide_smem_words(const DevPlan& P);
-// stage p's pivot chain in one CTA: pivot-entry update with the panel's
-// first nslots stages, its extraction, and (p < n-1) the reciprocal
+// Optional first step of k_pivot: R_{p-1}[p] by the previous stage's
+// reciprocal (k_divide for one row), vint/rint rows at vrow0 (stage p-1)
+struct PivotDiv {
+  int on;
+  long long vrow0;
+  const uint32_t* Ybuf;
+  const int* ys;
+  IntBuf rint;
+  uint32_t* rhat;
+  int* maxdegR;
+  uint32_t* dscr;
+  int use_dscr;
+};
+// stage p's pivot chain in one CTA: (pd) the previous stage's ratio of row p,
+// the pivot-entry update with the panel's first nslots stages, its
+// extraction, and (p < n-1) the reciprocal
 cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase,
                          const uint32_t* Vhat, const uint32_t* Rhat,
                          long long row_stride_slot, int nslots, int p,
                          IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV,
                          uint32_t* vhat, int* maxdegV, int dmax_bits,
                          uint32_t* Ybuf, int* ys, uint32_t* scratch,
-                         int use_gscratch, int* err, cudaStream_t st);
+                         int use_gscratch, int* err, cudaStream_t st,
+                         const PivotDiv& pd);
 // gridDim.y = batch independent reciprocal / division instances (P.bat_*)
 cudaError_t launch_recip_batch(const DevPlan& P, IntBuf vint, long long prow,
                                const int* maxbitsV, uint32_t* Ybuf, int* ys,
