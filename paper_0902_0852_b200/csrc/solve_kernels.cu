@@ -11,6 +11,7 @@
 // two's-complement accumulators), so each sequential step is one parallel
 // AXPY over the remaining rows.
 #include <cstdint>
+#include <cstdlib>
 
 #include "cta_ops.cuh"
 #include "ldlt_kernels.cuh"
@@ -133,7 +134,7 @@ __global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
 __global__ void __launch_bounds__(256) k_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
                              IntBuf xv, int xi, int j, int dir, uint32_t* acc,
                              Finish fin, int capX, int capC, uint32_t* gscratch,
-                             int* err) {
+                             int seg, int* err) {
   extern __shared__ uint32_t sm_dyn[];
   // operands and product scratch in shared memory, or (large plans) in this
   // CTA's slice of a global scratch (L1/L2-resident)
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(256) k_solve_axpy(int n, int cap, int Wv, int 
   uint32_t* Pr = C + capC;            // capX + capC (also the finish scratch)
   uint32_t* col = Pr + capX + capC;   // 3 (capX + capC)
   uint32_t* red = Pr + max(4LL * (capX + capC), solve_finish_words(Wv, Wa));
+  const int seg_words = seg ? 3 * (capX + capC) : 0;
   if (nx > capX) {  // the host sized the layout too small: it reruns
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     return;
@@ -174,7 +176,9 @@ __global__ void __launch_bounds__(256) k_solve_axpy(int n, int cap, int Wv, int 
       C[i] = L.limbs[li * cap + i];
     __syncthreads();
     const int nP = nc + nx;
-    cta_mul(C, nc, X, nx, Pr, nP, col, red);  // one segment per group (measured fastest here)
+    // one segment per group (measured fastest here; HGPU_SOLVE_SEG=1: as
+    // many as the column scratch allows)
+    cta_mul(C, nc, X, nx, Pr, nP, col, red, seg_words);
     uint32_t* a = acc + (long long)t * Wa;
     if (nP > Wa && threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     cta_resolve(
@@ -218,9 +222,13 @@ cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
   if (rows <= 0) return cudaSuccess;
   const size_t smem =
       gscratch ? 0 : solve_axpy_smem_words(capX, capC, Wv, Wa) * 4;
+  static const int seg = [] {
+    const char* e = getenv("HGPU_SOLVE_SEG");
+    return e ? atoi(e) : 0;
+  }();
   k_solve_axpy<<<min(rows, grid_cap), 256, smem, st>>>(
       n, cap, Wv, Wa, k2, L, xv, xi, j, dir, acc, fin, capX, capC, gscratch,
-      err);
+      seg, err);
   return cudaGetLastError();
 }
 
