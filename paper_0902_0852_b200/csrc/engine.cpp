@@ -305,6 +305,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   CU(cudaEventCreate(&ev1_));
   if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
   {
@@ -933,6 +934,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             // R_{p-1}[p] (inside the panel), pivot-entry update, extraction
             // and reciprocal in one CTA
             PivotDiv pd{};
+            pd.recip_words = std::min<long long>(
+                (long long)recip_scratch_words(D), recip_words_bound(D, dmax_bits_, pivot_segs_));
             if (p > p0) {
               pd.on = 1;
               pd.vrow0 = row0 - n;  // stage p-1 of this panel's slot set

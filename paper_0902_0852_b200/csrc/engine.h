@@ -180,6 +180,7 @@ class Matrix {
   cudaStream_t stream_upd2_ = nullptr;   // trailing update: deferred bands
   int defer_ = 4;   // panels the deferred trailing update may lag (HGPU_DEFER)
   bool fused_pivot_ = true;  // k_pivot: one launch per chain stage (HGPU_FUSED_PIVOT)
+  int pivot_segs_ = 6;       // k_pivot's reciprocal product segments (HGPU_PIVOT_SEGS)
   int nsets_ = 2;   // V/R slot sets (2 + deferral, memory permitting)
   int chain_sms_ = 0;  // SMs reserved for the pivot chain (green context), 0 = none
   std::vector<cudaEvent_t> pev_, sev_;

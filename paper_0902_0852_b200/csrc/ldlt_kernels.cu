@@ -394,7 +394,8 @@ __device__ inline int recip_levels(int Pt, int* lv) {
 __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
                            const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
                            uint32_t* Ybuf, int* ys, uint32_t* gscratch,
-                           int use_gscratch, int* err, int b) {
+                           int use_gscratch, int* err, int b,
+                           long long scratch_words = 0) {
   extern __shared__ uint32_t sm_dyn[];
   __shared__ uint32_t red[64];
   if (stage_aborted(err)) return;
@@ -441,7 +442,16 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
   uint32_t* E = Pr + 2 * Lm + 1;     // 2 Lm + 2
   uint32_t* Tm = E + 2 * Lm + 2;     // 3 Lm + 2
   uint32_t* col = Tm + 3 * Lm + 2;   // 2 * 3 (3 Lm + 2)
-  const int col_words = 6 * (3 * Lm + 2);
+  // product planes: up to 6 segments' worth, fewer when the caller's scratch
+  // (scratch_words > 0) is sized to the stage's bound
+  int segs = 6;
+  if (scratch_words > 0)
+    segs = (int)min(6LL, (scratch_words - 9LL * Lm - 69) / (3LL * Lm + 2));
+  if (segs < 1) {
+    if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
+    return;
+  }
+  const int col_words = segs * (3 * Lm + 2);
   int lv[40];
   const int nl = recip_levels(Pt, lv);
   // seed: Y_0 = floor(2^(n+p0)/D) ~ (2^126/top64(D)) >> (62 - p0)
@@ -858,7 +868,7 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
   __syncthreads();
   if (p < P.n - 1)
     recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
-               gscratch, use_gscratch, err, 0);
+               gscratch, use_gscratch, err, 0, pd.recip_words);
 }
 
 // ------------------------------------------- ratios on the tensor cores ---
@@ -1364,6 +1374,13 @@ static int recip_threads() {
   return t;
 }
 
+long long recip_words_bound(const DevPlan& P, int dmax_bits, int segs) {
+  // e <= (dmax - k2)/2 + k2 + 6 (the pivot has more than k2 bits), Pt = e + 32
+  const long long e = (long long)(dmax_bits - P.k2) / 2 + P.k2 + 6;
+  const long long Lm = (e + 32 + 32 + 31) / 32 + 2;
+  return 9 * Lm + 69 + (long long)segs * (3 * Lm + 2) + 8;
+}
+
 size_t recip_scratch_words(const DevPlan& P) {
   // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
   const size_t Lm = (size_t)P.ycap + 4;
@@ -1393,11 +1410,16 @@ cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase
                          const PivotDiv& pd) {
   ++g_launches;
   size_t smem = std::max(extract_smem_bytes(P),
-                         use_gscratch ? (size_t)0 : recip_scratch_words(P) * 4);
+                         use_gscratch ? (size_t)0 : (size_t)pd.recip_words * 4);
   if (pd.on)
     smem = std::max(smem, pd.use_dscr ? (size_t)(P.tw_smem ? P.NW : 0) * 4
                                       : divide_smem_words(P) * 4);
-  k_pivot<<<1, 512, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
+  static const int threads = [] {
+    const char* e = getenv("HGPU_PIVOT_THREADS");
+    const int v = e ? atoi(e) : 512;
+    return (v >= 128 && v <= 512 && v % 32 == 0) ? v : 512;
+  }();
+  k_pivot<<<1, threads, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
                                 p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
                                 dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
   return post_launch(st);

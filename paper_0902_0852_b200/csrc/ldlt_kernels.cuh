@@ -139,7 +139,14 @@ struct PivotDiv {
   int* maxdegR;
   uint32_t* dscr;
   int use_dscr;
+  // shared-memory words for the reciprocal (recip_words_bound), which
+  // also sizes the launch's dynamic shared memory
+  long long recip_words;
 };
+// reciprocal scratch words for diagonal entries of at most dmax_bits bits
+// (PD bound on the stage's precision, as k_recip computes it) and `segs`
+// product segments
+long long recip_words_bound(const DevPlan& P, int dmax_bits, int segs);
 // stage p's pivot chain in one CTA: (pd) the previous stage's ratio of row p,
 // the pivot-entry update with the panel's first nslots stages, its
 // extraction, and (p < n-1) the reciprocal
