@@ -1351,6 +1351,13 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     throw Error(HGPU_ERR_INTERNAL, "solve exactness self-check failed");
   if (herr[kErrZeroPivot] != INT_MAX)
     throw Error(HGPU_ERR_INTERNAL, "zero divisor in the diagonal solve");
+  if (std::getenv("HGPU_SOLVE_TRACE")) {
+    int mx[4] = {0, 0, 0, 0};
+    for (int v = 0; v < 4; ++v)
+      for (int i = 0; i < n; ++i) mx[v] = std::max(mx[v], std::abs(vh[(size_t)v * n + i]));
+    std::fprintf(stderr, "solve limbs: u %d z %d w %d y %d (Wv %d, R cap %d)\n", mx[0], mx[1],
+                 mx[2], mx[3], Wv, P.cap);
+  }
   std::vector<int> yh(vh.begin() + Y, vh.begin() + Y + n);
   std::vector<HostInt> y(n);
   for (int i = 0; i < n; ++i) {
