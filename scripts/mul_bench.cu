@@ -1,5 +1,6 @@
-// Microbenchmark of the CTA-wide limb product (cta_ops.cuh: cta_mul) at the
-// reciprocal's last-level sizes: clock64 cycles per call, one CTA alone.
+// Microbenchmark of the CTA-wide limb product (cta_ops.cuh: cta_mul, G = 8)
+// against a G-column variant (cta_mul2<G>) at the reciprocal's and the
+// solve's sizes: clock64 cycles per call, one CTA alone.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
 //        -I paper_0902_0852_b200/csrc -o /tmp/mb scripts/mul_bench.cu
 #include <cstdio>
@@ -12,37 +13,11 @@
 using namespace hgpu;
 
 
-// Candidate product loop: 64-bit accumulators, the i-loop unrolled by G so the
-// b-window lives in static registers (no per-iteration moves).
 template <int G>
-__device__ __forceinline__ void col_block(const uint32_t* a, const uint32_t* b, int nb,
-                                          int k0, int ilo, int ihi, uint64_t* acc,
-                                          uint32_t* cc) {
-  for (int i = ilo; i <= ihi; i += G) {
-    uint32_t av[G];
-#pragma unroll
-    for (int u = 0; u < G; ++u) av[u] = (i + u <= ihi) ? a[i + u] : 0u;
-    uint32_t bw[2 * G - 1];
-#pragma unroll
-    for (int m = 0; m < 2 * G - 1; ++m) {
-      const int j = k0 - i - (G - 1) + m;
-      bw[m] = (j >= 0 && j < nb) ? b[j] : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < G; ++u)
-#pragma unroll
-      for (int t = 0; t < G; ++t)
-        asm("{\n\t.reg .u64 pr;\n\tmul.wide.u32 pr, %2, %3;\n\tadd.cc.u64 %0, %0, pr;\n\taddc.u32 %1, %1, 0;\n\t}"
-            : "+l"(acc[t]), "+r"(cc[t])
-            : "r"(av[u]), "r"(bw[G - 1 + t - u]));
-  }
-}
-
 __device__ inline void cta_mul2(const uint32_t* a, int na, const uint32_t* b,
                                 int nb, uint32_t* out, int M_end, uint32_t* col,
                                 uint32_t* red, int col_words = 0,
                                 int k_begin = 0) {
-  constexpr int G = 8;
   const int M = M_end - k_begin;
   const int ngroups = (M + G - 1) / G;
   const int minlen = min(na, nb);
@@ -107,14 +82,14 @@ __device__ inline void cta_mul2(const uint32_t* a, int na, const uint32_t* b,
 
 template <int VARIANT>
 __global__ void __launch_bounds__(512) k_bench(int na, int nb, int reps, long long* cyc,
-                                               uint32_t* out_g) {
+                                               uint32_t* out_g, int col_words_arg) {
   extern __shared__ uint32_t sm[];
   uint32_t* a = sm;
   uint32_t* b = a + na;
   const int M = na + nb;
   uint32_t* out = b + nb;
   uint32_t* col = out + M;
-  const int col_words = 12252;
+  const int col_words = col_words_arg;
   uint32_t* red = col + col_words;
   for (int i = threadIdx.x; i < na; i += blockDim.x) a[i] = 0x9E3779B9u * (i + 1);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) b[i] = 0x7F4A7C15u * (i + 3);
@@ -122,7 +97,7 @@ __global__ void __launch_bounds__(512) k_bench(int na, int nb, int reps, long lo
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     if (VARIANT == 0) cta_mul(a, na, b, nb, out, M, col, red, col_words);
-    else cta_mul2(a, na, b, nb, out, M, col, red, col_words);
+    else cta_mul2<16>(a, na, b, nb, out, M, col, red, col_words);
     __syncthreads();
   }
   long long t1 = clock64();
@@ -131,28 +106,28 @@ __global__ void __launch_bounds__(512) k_bench(int na, int nb, int reps, long lo
 }
 
 int main() {
-  const int sizes[][2] = {{398, 340}, {340, 171}, {171, 86}, {86, 44}, {676, 676}};
+  const int sizes[][2] = {{650, 1038}, {650, 830}, {398, 340}, {676, 676}};
   long long* cyc;
   uint32_t* outg;
   cudaMalloc(&cyc, 8);
   cudaMalloc(&outg, 4 * 4096);
-  const int smem = 4 * (4096 + 12252 + 64);
+  const int smem = 160 * 1024;
   cudaFuncSetAttribute(k_bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (auto& s : sizes) {
-    for (int threads : {256, 512}) {
+    for (int threads : {256, 512}) for (int cw : {0, 3 * (s[0] + s[1]) * 2}) {
       long long c0 = 0, c1 = 0;
       std::vector<uint32_t> r0(4096), r1(4096);
-      k_bench<0><<<1, threads, smem>>>(s[0], s[1], 5, cyc, outg);
+      k_bench<0><<<1, threads, smem>>>(s[0], s[1], 5, cyc, outg, cw);
       cudaMemcpy(&c0, cyc, 8, cudaMemcpyDeviceToHost);
       cudaMemcpy(r0.data(), outg, 4 * 4096, cudaMemcpyDeviceToHost);
-      k_bench<1><<<1, threads, smem>>>(s[0], s[1], 5, cyc, outg);
+      k_bench<1><<<1, threads, smem>>>(s[0], s[1], 5, cyc, outg, cw);
       cudaMemcpy(&c1, cyc, 8, cudaMemcpyDeviceToHost);
       cudaMemcpy(r1.data(), outg, 4 * 4096, cudaMemcpyDeviceToHost);
       bool same = true;
       for (int i = 0; i < s[0] + s[1]; ++i) same &= r0[i] == r1[i];
-      printf("%4d x %4d, %3d threads: cta_mul %7lld cycles (%.2f prod/cyc), cta_mul2 %7lld cycles (%.2f prod/cyc) %s\n",
-             s[0], s[1], threads, c0, (double)s[0] * s[1] / c0, c1, (double)s[0] * s[1] / c1, same ? "same" : "DIFFERENT");
+      printf("cw %5d %4d x %4d, %3d threads: cta_mul %7lld cycles (%.2f prod/cyc), cta_mul2 %7lld cycles (%.2f prod/cyc) %s\n",
+             cw, s[0], s[1], threads, c0, (double)s[0] * s[1] / c0, c1, (double)s[0] * s[1] / c1, same ? "same" : "DIFFERENT");
     }
   }
   cudaError_t e = cudaDeviceSynchronize();
