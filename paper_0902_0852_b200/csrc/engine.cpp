@@ -305,6 +305,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   CU(cudaEventCreate(&ev1_));
   if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_SOLVE_TC")) solve_tc_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -337,6 +338,7 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
     if (h) cublasDestroy((cublasHandle_t)h);
+  if (tc_blas_) cublasDestroy((cublasHandle_t)tc_blas_);
   for (int l = 1; l < kMaxFarLanes; ++l)
     if (far_streams_[l]) cudaStreamDestroy(far_streams_[l]);
   for (cudaEvent_t e : far_ev_)
@@ -367,6 +369,14 @@ void Matrix::release() {
                   (void*)spair_limbs_, (void*)sbits_, (void*)sybuf_,
                   (void*)srscr_, (void*)sdscr_, (void*)sys_})
     dfree(p);
+  for (void* q : {(void*)rdig_col_, (void*)rdig_row_, (void*)tc_t_, (void*)tc_c_,
+                  (void*)tc_acc_, (void*)tc_ws_})
+    dfree(q);
+  rdig_col_ = rdig_row_ = tc_t_ = tc_ws_ = nullptr;
+  tc_c_ = nullptr;
+  tc_acc_ = nullptr;
+  tc_kr_ = tc_mc_ = 0;
+  rdig_for_ = -1;
   lhdr_ = svhdr_ = spair_hdr_ = sbits_ = sys_ = nullptr;
   llimbs_ = svlimbs_ = sacc_ = sgscr_ = spair_limbs_ = sybuf_ = srscr_ =
       sdscr_ = nullptr;
@@ -1218,10 +1228,26 @@ void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st) {
                        rows * P.cap * 4, cudaMemcpyDeviceToDevice, st));
   }
   have_L_ = true;
+  ++factor_serial_;
 }
 
 std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                                    long long* launches) {
+  // tensor-core AXPY (HGPU_SOLVE_TC=1) once an earlier solve has recorded
+  // the operand widths; any capacity flag reruns the solve on the integer path
+  if (solve_tc_ && solve_xlimbs_ > 0) {
+    try {
+      return solve_impl(u, launches, true);
+    } catch (const Error& e) {
+      if (e.status != HGPU_ERR_CAPACITY) throw;
+      solve_xlimbs_ = 0;
+    }
+  }
+  return solve_impl(u, launches, false);
+}
+
+std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
+                                        long long* launches, bool tc) {
   if (!have_L_)
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve needs a HGPU_KEEP_L factorisation");
   if (world_ != 1)
@@ -1267,6 +1293,69 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     sdscr_ = dalloc<uint32_t>((size_t)n * (divide_smem_words(D2) + 64));
   }
   const int Wv = sWv_, Wa = sWa_;
+  // tensor-core AXPY operands (digits of the L entries once per factorisation)
+  int kr = 0, mc = 0;
+  if (tc) {
+    const long long ne = (long long)n * (n - 1) / 2;
+    if (rdig_for_ != factor_serial_) {
+      std::vector<int> bits(std::max<long long>(ne, 1));
+      int* dbits = dalloc<int>(std::max<long long>(ne, 1));
+      CU(launch_int_bits_batch(IntBuf{lhdr_, llimbs_}, 0, 1, P.cap, (int)ne, dbits, st));
+      CU(cudaMemcpyAsync(bits.data(), dbits, ne * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      dfree(dbits);
+      int mb = 1;
+      for (long long i = 0; i < ne; ++i) mb = std::max(mb, bits[i]);
+      const int need_kr = ((mb + 6) / 7 + 15) & ~15;
+      if (need_kr > tc_kr_ || !rdig_col_) {
+        dfree(rdig_col_);
+        dfree(rdig_row_);
+        rdig_col_ = dalloc<uint8_t>((size_t)ne * need_kr);
+        rdig_row_ = dalloc<uint8_t>((size_t)ne * need_kr);
+        tc_kr_ = need_kr;
+      }
+      CU(launch_solve_rdig(n, P.cap, IntBuf{lhdr_, llimbs_}, tc_kr_, rdig_col_, rdig_row_,
+                           err_, st));
+      rdig_for_ = factor_serial_;
+    }
+    kr = tc_kr_;
+    const int xd = ((32 * (solve_xlimbs_ + solve_xlimbs_ / 16 + 8)) + 6) / 7;
+    mc = (kr + xd + 15) & ~15;
+    if (mc > tc_mc_) {
+      dfree(tc_t_);
+      dfree(tc_c_);
+      dfree(tc_acc_);
+      tc_t_ = dalloc<uint8_t>((size_t)mc * kr);
+      tc_c_ = dalloc<int32_t>((size_t)n * mc);
+      tc_acc_ = dalloc<long long>((size_t)n * mc);
+      tc_mc_ = mc;
+    }
+    mc = tc_mc_;
+    int ok = 0;
+    CU(configure_solve_tc(Wv, Wa, mc, &ok));
+    if (!ok) throw Error(HGPU_ERR_CAPACITY, "tensor-core solve operands exceed shared memory");
+    if (!tc_blas_) {
+      if (cublasCreate((cublasHandle_t*)&tc_blas_) != CUBLAS_STATUS_SUCCESS)
+        throw Error(HGPU_ERR_CUDA, "cublasCreate failed");
+      tc_ws_ = dalloc<uint8_t>(kBlasWorkspace);
+      if (cublasSetWorkspace((cublasHandle_t)tc_blas_, tc_ws_, kBlasWorkspace) !=
+          CUBLAS_STATUS_SUCCESS)
+        throw Error(HGPU_ERR_CUDA, "cublasSetWorkspace failed");
+    }
+    if (cublasSetStream((cublasHandle_t)tc_blas_, st) != CUBLAS_STATUS_SUCCESS)
+      throw Error(HGPU_ERR_CUDA, "cublasSetStream failed");
+  }
+  // C[t][k'] = sum_i B[t][i] T[k'][i] for `rows` targets (int8 -> int32)
+  auto tc_gemm = [&](const uint8_t* B, int rows) {
+    const int32_t one = 1, zero = 0;
+    const cublasStatus_t bs = cublasGemmEx(
+        (cublasHandle_t)tc_blas_, CUBLAS_OP_T, CUBLAS_OP_N, mc, rows, kr, &one, tc_t_,
+        CUDA_R_8I, kr, B, CUDA_R_8I, kr, &zero, tc_c_, CUDA_R_32I, mc,
+        CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    if (bs != CUBLAS_STATUS_SUCCESS)
+      throw Error(HGPU_ERR_CUDA, "solve GEMM failed (cublas status " +
+                                     std::to_string((int)bs) + ")");
+  };
   IntBuf vecs{svhdr_, svlimbs_};
   IntBuf pairs{spair_hdr_, spair_limbs_};
   IntBuf L{lhdr_, llimbs_};
@@ -1312,8 +1401,18 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
     CU(launch_solve_finish(Wv, Wa, k2, sacc_,
                            Finish{vecs, U, vecs, Z, pairs, 1, k2}, err_, st));
     ++nl;
+    if (tc) CU(cudaMemsetAsync(tc_acc_, 0, (size_t)n * mc * 8, st));
     for (int p = 0; p + 1 < n; ++p) {
       const Finish f{vecs, U + p + 1, vecs, Z + p + 1, pairs, 2 * (p + 1) + 1, k2};
+      if (tc) {
+        CU(launch_solve_toeplitz(vecs, Z + p, Wv, kr, mc, tc_t_, err_, st));
+        tc_gemm(rdig_col_ + (size_t)((long long)p * (n - 1) - (long long)p * (p - 1) / 2) * kr,
+                n - 1 - p);
+        CU(launch_solve_acc_tc(n, Wv, Wa, k2, L, vecs, Z + p, p, 0, tc_c_, mc, tc_acc_, f,
+                               sgrid, err_, st));
+        nl += 3;
+        continue;
+      }
       CU(launch_solve_axpy(n, P.cap, Wv, Wa, k2, L, vecs, Z + p, p, 0, sacc_, f,
                            capX, capC, sgscr_, sgrid, err_, st));
       ++nl;
@@ -1331,8 +1430,17 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                            Finish{vecs, Wq + n - 1, vecs, Y + n - 1, vecs, 0, 0},
                            err_, st));
     ++nl;
+    if (tc) CU(cudaMemsetAsync(tc_acc_, 0, (size_t)n * mc * 8, st));
     for (int r = n - 1; r >= 1; --r) {
       const Finish f{vecs, Wq + r - 1, vecs, Y + r - 1, vecs, 0, 0};
+      if (tc) {
+        CU(launch_solve_toeplitz(vecs, Y + r, Wv, kr, mc, tc_t_, err_, st));
+        tc_gemm(rdig_row_ + (size_t)((long long)r * (r - 1) / 2) * kr, r);
+        CU(launch_solve_acc_tc(n, Wv, Wa, k2, L, vecs, Y + r, r, 1, tc_c_, mc, tc_acc_, f,
+                               sgrid, err_, st));
+        nl += 3;
+        continue;
+      }
       CU(launch_solve_axpy(n, P.cap, Wv, Wa, k2, L, vecs, Y + r, r, 1, sacc_, f,
                            capX, capC, sgscr_, sgrid, err_, st));
       ++nl;
@@ -1357,6 +1465,12 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
       for (int i = 0; i < n; ++i) mx[v] = std::max(mx[v], std::abs(vh[(size_t)v * n + i]));
     std::fprintf(stderr, "solve limbs: u %d z %d w %d y %d (Wv %d, R cap %d)\n", mx[0], mx[1],
                  mx[2], mx[3], Wv, P.cap);
+  }
+  {
+    int mx = 0;
+    for (int i = 0; i < n; ++i)
+      mx = std::max(mx, std::max(std::abs(vh[(size_t)Z + i]), std::abs(vh[(size_t)Y + i])));
+    solve_xlimbs_ = std::max(solve_xlimbs_, mx);
   }
   std::vector<int> yh(vh.begin() + Y, vh.begin() + Y + n);
   std::vector<HostInt> y(n);

@@ -93,6 +93,8 @@ class Matrix {
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
   std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
+  std::vector<HostInt> solve_impl(const std::vector<HostInt>& u, long long* launches,
+                                  bool tc);
   int order() const { return n_; }
   const HostInt& strip_entry(int s) const { return strip_[s]; }
   // Interval mode (iv_engine.cpp): the constructor's strip holds the lower
@@ -201,6 +203,18 @@ class Matrix {
   uint32_t *sybuf_ = nullptr, *srscr_ = nullptr, *sdscr_ = nullptr;
   int* sys_ = nullptr;
   int dmax_bits_ = 0;
+  // tensor-core solve AXPY (HGPU_SOLVE_TC): L digits (column and row order),
+  // Toeplitz operand, GEMM output, 7-bit-column accumulators
+  bool solve_tc_ = false;
+  int solve_xlimbs_ = 0;          // widest z / y entry of the solves so far
+  long long factor_serial_ = 0;   // KEEP_L factorisations so far
+  long long rdig_for_ = -1;       // factor_serial_ the digits belong to
+  int tc_kr_ = 0, tc_mc_ = 0;
+  uint8_t *rdig_col_ = nullptr, *rdig_row_ = nullptr, *tc_t_ = nullptr,
+          *tc_ws_ = nullptr;
+  int32_t* tc_c_ = nullptr;
+  long long* tc_acc_ = nullptr;
+  void* tc_blas_ = nullptr;
   // interval mode: upper-bound copies of the per-entry buffers (the point
   // buffers hold the lower bounds) and the sign classes of V, R bounds
   bool interval_ = false;

@@ -241,6 +241,16 @@ cudaError_t launch_solve_axpy(int n, int cap, int Wv, int Wa, int k2, IntBuf L,
                               cudaStream_t st);
 cudaError_t launch_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
                                 const Finish& fin, int* err, cudaStream_t st);
+// tensor-core AXPY of the triangular solves (solve_kernels.cu, opt-in)
+cudaError_t launch_solve_rdig(int n, int cap, IntBuf L, int kr, uint8_t* dcol,
+                              uint8_t* drow, int* err, cudaStream_t st);
+cudaError_t launch_solve_toeplitz(IntBuf xv, int xi, int Wv, int kr, int mc,
+                                  uint8_t* T, int* err, cudaStream_t st);
+cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf xv,
+                                int xi, int j, int dir, const int32_t* C, int mc,
+                                long long* acc7, const Finish& fin, int grid_cap,
+                                int* err, cudaStream_t st);
+cudaError_t configure_solve_tc(int Wv, int Wa, int mc, int* ok);
 cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
                                   int count, int* out, cudaStream_t st);
 cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global);

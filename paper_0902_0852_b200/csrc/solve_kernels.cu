@@ -10,6 +10,7 @@
 // The sums are accumulated column by column (one CTA per target row, exact
 // two's-complement accumulators), so each sequential step is one parallel
 // AXPY over the remaining rows.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -206,6 +207,181 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
   out[b] = n == 0 ? 0 : limbs_bits(v.limbs + idx * stride, n);
 }
 
+// ------------------------------------------ tensor-core AXPY (opt-in) ---
+// Every step's products R(t, j) x_j (x_j the vector entry just finished)
+// share x_j, so they form one int8 GEMM on 7-bit digits (as the ratio GEMM,
+// DESIGN.md §4): C[t][k'] = sum_i rdig(t)[i] xdig[k' - i], column k' of
+// |R| |x| (digit products < 2^14, sums over <= 2^13 digits < 2^27: exact in
+// int32).  The accumulators stay in those 7-bit columns as signed 64-bit
+// sums (|.| < n 2^27), and a row's finish converts them to two's
+// complement limbs and applies solve_finish.  Results equal k_solve_axpy's.
+
+// packed lower triangle by rows: (r, q), q < r
+__device__ __forceinline__ long long lidx_row(int r, int q) {
+  return (long long)r * (r - 1) / 2 + q;
+}
+
+// 7-bit digits of |R_p[r]| of every stored entry, in column order (forward
+// sweep: entry lidx(n,p,r)) and row order (back sweep: entry lidx_row(r,p)).
+__global__ void k_solve_rdig(int n, int cap, IntBuf L, int kr, uint8_t* dcol,
+                             uint8_t* drow, int* err) {
+  const long long ne = (long long)n * (n - 1) / 2;
+  for (long long li = blockIdx.x; li < ne; li += gridDim.x) {
+    // column p of entry li: largest p with lidx(n, p, p+1) <= li
+    int p = (int)((2.0 * n - 1 - sqrt((2.0 * n - 1) * (2.0 * n - 1) - 8.0 * li)) / 2);
+    p = max(0, min(p, n - 2));
+    while (p > 0 && lidx(n, p, p + 1) > li) --p;
+    while (p + 1 < n - 1 && lidx(n, p + 1, p + 2) <= li) ++p;
+    const int r = (int)(li - lidx(n, p, p + 1)) + p + 1;
+    const int h = L.hdr[li];
+    const int len = h < 0 ? -h : h;
+    const uint32_t* src = L.limbs + li * (long long)cap;
+    if (threadIdx.x == 0 && len > 0 && (limbs_bits(src, len) + 6) / 7 > kr)
+      atomicOr(&err[kErrCapacity], kCapLimbs);
+    uint32_t* c = reinterpret_cast<uint32_t*>(dcol + li * kr);
+    uint32_t* rw = reinterpret_cast<uint32_t*>(drow + lidx_row(r, p) * kr);
+    for (int i = threadIdx.x; i < kr / 4; i += blockDim.x) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        w |= (field32(src, len, 7LL * (4 * i + u)) & 127u) << (8 * u);
+      c[i] = w;
+      rw[i] = w;
+    }
+  }
+}
+
+// T[k'][i] = 7-bit digit k' - i of |x| (entry xi of xv), k' < mc, i < kr
+__global__ void k_solve_toeplitz(IntBuf xv, int xi, int Wv, int kr, int mc,
+                                 uint8_t* T, int* err) {
+  extern __shared__ uint32_t xs[];
+  const int h = xv.hdr[xi];
+  const int nx = h < 0 ? -h : h;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) xs[i] = xv.limbs[(long long)xi * Wv + i];
+  __syncthreads();
+  const long long nxd = nx == 0 ? 0 : (limbs_bits(xs, nx) + 6) / 7;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nxd + kr > mc)
+    atomicOr(&err[kErrCapacity], kCapLimbs);  // product columns beyond mc
+  const int per_row = kr / 16;
+  const long long total = (long long)mc * per_row;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int kc = (int)(idx / per_row);
+    const int i0 = (int)(idx - (long long)kc * per_row) * 16;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const long long jd = (long long)kc - (i0 + u);
+      if (jd >= 0 && jd < nxd)
+        w[u >> 2] |= (field32(xs, nx, 7 * jd) & 127u) << (8 * (u & 3));
+    }
+    reinterpret_cast<uint4*>(T + (long long)kc * kr)[i0 / 16] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// acc7[t] += s_t C[row(t)] for the targets of step j; the first target is
+// complete afterwards and finished here (solve_finish), as in k_solve_axpy.
+__global__ void __launch_bounds__(256)
+k_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf xv, int xi, int j,
+               int dir, const int32_t* C, int mc, long long* acc7, Finish fin,
+               int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  const int hx = xv.hdr[xi];
+  const int sx = hx < 0 ? -1 : 1;
+  const int ntg = dir == 0 ? n - j - 1 : j;
+  const int J = mc / 4;        // 28-bit super-digits
+  const int Mres = J + 2;
+  long long* Dsd = reinterpret_cast<long long*>(sm_dyn);          // J
+  uint32_t* dig = reinterpret_cast<uint32_t*>(Dsd + J);           // Mres
+  uint32_t* limbs = dig + Mres;                                   // Wa
+  uint32_t* fscr = limbs + Wa;                                    // finish
+  for (int kk = blockIdx.x; kk < ntg; kk += gridDim.x) {
+    const int t = dir == 0 ? j + 1 + kk : j - 1 - kk;
+    const long long li = dir == 0 ? lidx(n, j, t) : lidx(n, t, j);
+    const int hc = L.hdr[li];
+    long long* a = acc7 + (long long)t * mc;
+    if (hc != 0 && hx != 0) {
+      const long long crow = dir == 0 ? kk : t;
+      const int32_t* c = C + crow * mc;
+      const bool neg = (hc < 0) != (sx < 0);
+      for (int k = threadIdx.x; k < mc; k += blockDim.x)
+        a[k] += neg ? -(long long)c[k] : (long long)c[k];
+    }
+    if (kk != 0) continue;
+    __syncthreads();
+    // columns -> base-2^28 super-digit sums D_j (|D_j| < 2^58)
+    for (int q = threadIdx.x; q < J; q += blockDim.x)
+      Dsd[q] = a[4 * q] + a[4 * q + 1] * 128 + a[4 * q + 2] * 16384 + a[4 * q + 3] * 2097152;
+    __syncthreads();
+    const long long m28 = (1ll << 28) - 1;
+    const int carry = cta_resolve(
+        Mres, 28,
+        [&](int q) -> int64_t {
+          int64_t v = q < J ? (Dsd[q] & m28) : 0;
+          if (q >= 1 && q - 1 < J) v += (Dsd[q - 1] >> 28) & m28;
+          if (q >= 2 && q - 2 < J) v += Dsd[q - 2] >> 56;
+          return v;
+        },
+        [&](int q, uint64_t d) { dig[q] = (uint32_t)d; }, fscr);
+    if (carry > 0 || carry < -1) {
+      if (threadIdx.x == 0) atomicOr(&err[kErrInternal], kIntDivision);
+      return;
+    }
+    // two's complement limbs over Wa (sign-filled above the digits)
+    const long long top = 28LL * Mres;
+    for (int m = threadIdx.x; m < Wa; m += blockDim.x) {
+      uint64_t accw = 0;
+      for (int k = (32 * m) / 28; k < Mres && 28 * k < 32 * m + 32; ++k) {
+        const int shl = 28 * k - 32 * m;
+        accw |= shl >= 0 ? ((uint64_t)dig[k] << shl) : ((uint64_t)dig[k] >> -shl);
+      }
+      uint32_t v = (uint32_t)accw;
+      if (carry < 0) {
+        const long long lo = 32LL * m;
+        if (lo >= top) v = 0xFFFFFFFFu;
+        else if (lo + 32 > top) v |= 0xFFFFFFFFu << (int)(top - lo);
+      }
+      limbs[m] = v;
+    }
+    __syncthreads();
+    solve_finish(Wv, Wa, k2, limbs, fin, fscr, err);
+  }
+}
+
+size_t solve_acc_tc_smem_words(int Wv, int Wa, int mc) {
+  const long long J = mc / 4;
+  return (size_t)(2 * J + (J + 2) + Wa + solve_finish_words(Wv, Wa) + 64);
+}
+
+cudaError_t launch_solve_rdig(int n, int cap, IntBuf L, int kr, uint8_t* dcol,
+                              uint8_t* drow, int* err, cudaStream_t st) {
+  if (n < 2) return cudaSuccess;
+  const long long ne = (long long)n * (n - 1) / 2;
+  k_solve_rdig<<<(unsigned)std::min<long long>(ne, 8192), 128, 0, st>>>(n, cap, L, kr, dcol,
+                                                                    drow, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_toeplitz(IntBuf xv, int xi, int Wv, int kr, int mc,
+                                  uint8_t* T, int* err, cudaStream_t st) {
+  const long long words = (long long)mc * (kr / 16);
+  const int blocks = (int)std::min<long long>((words + 255) / 256, 2048);
+  k_solve_toeplitz<<<blocks, 256, (size_t)Wv * 4, st>>>(xv, xi, Wv, kr, mc, T, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf xv,
+                                int xi, int j, int dir, const int32_t* C, int mc,
+                                long long* acc7, const Finish& fin, int grid_cap,
+                                int* err, cudaStream_t st) {
+  const int rows = dir == 0 ? n - j - 1 : j;
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = solve_acc_tc_smem_words(Wv, Wa, mc) * 4;
+  k_solve_acc_tc<<<std::min(rows, grid_cap), 256, smem, st>>>(
+      n, Wv, Wa, k2, L, xv, xi, j, dir, C, mc, acc7, fin, err);
+  return cudaGetLastError();
+}
+
 size_t solve_axpy_smem_words(int capX, int capC, int Wv, int Wa) {
   return (size_t)solve_axpy_words(capX, capC, Wv, Wa);
 }
@@ -245,6 +421,20 @@ cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
   k_int_bits<<<(count + 127) / 128, 128, 0, st>>>(v, idx0, step, stride, count,
                                                   out);
   return cudaGetLastError();
+}
+
+cudaError_t configure_solve_tc(int Wv, int Wa, int mc, int* ok) {
+  int dev = 0, maxopt = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t smem = solve_acc_tc_smem_words(Wv, Wa, mc) * 4;
+  *ok = smem <= (size_t)maxopt && (size_t)Wv * 4 <= (size_t)maxopt;
+  if (!*ok) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_solve_acc_tc,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_solve_toeplitz, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Wv * 4);
 }
 
 cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global) {

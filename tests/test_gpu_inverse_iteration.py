@@ -122,3 +122,17 @@ def test_config2_full_size_certified_digits(hg):
         assert po.to_hex(got["rho"][-1]) == d["rho_last"]
         assert got["iterations"] == d["iterations"]
         assert got["eigenvalue"] == d["lambda_40"]
+
+
+@pytest.mark.parametrize("seed,n,k", [(115, 40, 768), (116, 70, 1024)])
+def test_tensor_core_solve_bit_exact(hg, seed, n, k, monkeypatch):
+    """The opt-in int8 tensor-core AXPY of the triangular solves
+    (HGPU_SOLVE_TC=1, solve_kernels.cu) gives the restatement's Rayleigh
+    quotients bit for bit; the solves after the first one take that path."""
+    monkeypatch.setenv("HGPU_SOLVE_TC", "1")
+    strip = random_pd_hankel(seed, n, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
+    assert got["rho"] == want
+    assert got["iterations"] == len(want)
