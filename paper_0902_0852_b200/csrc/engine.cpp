@@ -306,6 +306,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_SOLVE_TC")) solve_tc_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -916,6 +917,9 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       bool chain_started = false;
       // far lanes (one when the divisions use global scratch or the GEMM)
       const int nlanes = (div_global_ || rg_far) ? 1 : far_lanes_;
+      // far rows' in-panel update in sub-panels of fsub stages (0: plain
+      // left-looking); needs the far rows below the panel's columns
+      const int fsub = (far_sub_ > 0 && near_end >= p1 && D.NW % 32 == 0) ? far_sub_ : 0;
       if (far) {
         CU(cudaEventRecord(sev_[4 * n + 1], sp));
         for (int l = 0; l < nlanes; ++l)
@@ -1031,9 +1035,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               const int hi = near_end + (int)((long long)(n - near_end) * (l + 1) / nlanes);
               if (lo >= hi) continue;
               if (p > p0) CU(cudaStreamWaitEvent(fs, sev_[4 * (p - 1)], 0));
+              // column p receives the stages of its own sub-panel [ps, p);
+              // earlier sub-panels arrived by the rank-fsub updates below
+              const int ps = fsub > 0 ? p0 + (s / fsub) * fsub : p0;
               TL(10, p, fs, [&] {
-                return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                         p, lo, hi, err_, fs);
+                return launch_update_col(D, W_, colbase_, vh + (ps - p0) * slot_stride,
+                                         rh + (ps - p0) * slot_stride, slot_stride,
+                                         p - ps, p, lo, hi, err_, fs);
               });
               TL(11, p, fs, [&] {
                 return launch_extract(D, W_, colbase_, p, lo, hi, vint, row0,
@@ -1052,6 +1060,19 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                   return launch_divide(D, vint, row0, p, lo, hi, yb, yss, rint,
                                        row0, rhat_, maxdegR + p, dscratch3_,
                                        div_global_ ? 1 : 0, err_, fs);
+                });
+              }
+              if (fsub > 0 && (s + 1) % fsub == 0 && p + 1 < p1) {
+                // the finished sub-panel [p+1-fsub, p] on the panel's
+                // remaining columns of these rows, one tiled pass (R^ read
+                // once per tile instead of once per column); needs V^_p of
+                // those columns (near extract of stage p)
+                CU(cudaStreamWaitEvent(fs, sev_[4 * p], 0));
+                const int sb0 = p + 1 - fsub - p0;
+                TL(14, p, fs, [&] {
+                  return launch_update_rect(D, W_, colbase_, vh + sb0 * slot_stride,
+                                            rh + sb0 * slot_stride, slot_stride, fsub,
+                                            p + 1, p1, lo, hi, err_, fs);
                 });
               }
             }

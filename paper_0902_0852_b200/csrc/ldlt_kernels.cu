@@ -1136,21 +1136,28 @@ __global__ void __launch_bounds__(128, 2)
 k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
                const uint32_t* Vhat, const uint32_t* Rhat,
                long long row_stride_slot, int nslots, int c_begin, int c_end,
-               int nct, int nrt, const int* err) {
+               int nct, int nrt, const int* err, int r_lo, int r_hi, int rect) {
   __shared__ __align__(16) uint32_t sm[kUStages][2 * kUT][kUWords];
   // the tile's own workspace words, prefetched at entry so the epilogue's
   // read-modify-write never waits on HBM
   extern __shared__ __align__(16) uint32_t sW[];  // [kUT*kUT][kUWords]
   if (stage_aborted(err)) return;
   const int w0 = blockIdx.y * kUWords;
-  int t = blockIdx.x, ct = 0;
-  while (t >= nrt - ct) {
-    t -= nrt - ct;
-    ++ct;
+  // tiles: the lower triangle r >= c of columns [c_begin, c_end) (rows from
+  // r_lo = c_begin), or (rect) the rectangle [r_lo, r_hi) x [c_begin, c_end)
+  int t = blockIdx.x, ct = 0, rt;
+  if (rect) {
+    ct = t / nrt;
+    rt = t - ct * nrt;
+  } else {
+    while (t >= nrt - ct) {
+      t -= nrt - ct;
+      ++ct;
+    }
+    rt = ct + t;
   }
-  const int rt = ct + t;
   const int c0 = c_begin + ct * kUT;
-  const int r0 = c_begin + rt * kUT;
+  const int r0 = r_lo + rt * kUT;
   const long long NW = P.NW;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -1162,7 +1169,7 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
     const int chunk = tid + 128 * h;
     const int k = chunk >> 3, part = chunk & 7;
     const uint32_t* base;
-    if (k < kUT) base = Rhat + (long long)min(r0 + k, P.n - 1) * NW;
+    if (k < kUT) base = Rhat + (long long)min(r0 + k, r_hi - 1) * NW;
     else base = Vhat + (long long)min(c0 + k - kUT, c_end - 1) * NW;
     src[h] = base + w0 + part * 4;
     dst_k[h] = k;
@@ -1181,7 +1188,7 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
     const int chunk = tid + 128 * h;
     const int pair = chunk >> 3, part = chunk & 7;
     const int r = r0 + (pair >> 4), c = c0 + (pair & 15);
-    if (c < c_end && r >= c && r < P.n)
+    if (c < c_end && r >= c && r < r_hi)
       cp_async16(&sW[pair * kUWords + part * 4],
                  W + (colbase[c] + (r - c)) * NW + w0 + part * 4);
   }
@@ -1229,7 +1236,7 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int r = r0 + rm + i;
-      if (r < c || r >= P.n) continue;
+      if (r < c || r >= r_hi) continue;
       const uint32_t t32 = reduce_sum64(acc[i][j], pc);
       const uint32_t old = sW[((rm + i) * kUT + cm + j) * kUWords + lane];
       W[(base + (r - c)) * NW + wd] = old >= t32 ? old - t32 : old + pc.q - t32;
@@ -1519,7 +1526,7 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
     ++g_launches;
     k_update_tiled<<<grid, 128, kUT * kUT * kUWords * 4, st>>>(P, W, colbase, Vhat, Rhat,
                                          row_stride_slot, nslots, c_begin,
-                                         c_end, nct, nrt, err);
+                                         c_end, nct, nrt, err, c_begin, P.n, 0);
     return cudaGetLastError();
   }
   if (tile == 16) tile = 8;
@@ -1537,6 +1544,23 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
     k_update<4><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
                                       row_stride_slot, nslots, c_begin, c_end,
                                       nct, nrt, err);
+  return post_launch(st);
+}
+
+cudaError_t launch_update_rect(const DevPlan& P, uint32_t* W,
+                               const long long* colbase, const uint32_t* Vhat,
+                               const uint32_t* Rhat, long long row_stride_slot,
+                               int nslots, int c_begin, int c_end, int r_lo,
+                               int r_hi, const int* err, cudaStream_t st) {
+  if (c_begin >= c_end || r_lo >= r_hi || nslots <= 0) return cudaSuccess;
+  if (P.NW % kUWords != 0 || r_lo < c_end) return cudaErrorInvalidValue;
+  const int nct = (c_end - c_begin + kUT - 1) / kUT;
+  const int nrt = (r_hi - r_lo + kUT - 1) / kUT;
+  dim3 grid((unsigned)(nct * nrt), P.NW / kUWords);
+  ++g_launches;
+  k_update_tiled<<<grid, 128, kUT * kUT * kUWords * 4, st>>>(
+      P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c_begin, c_end, nct, nrt,
+      err, r_lo, r_hi, 1);
   return post_launch(st);
 }
 

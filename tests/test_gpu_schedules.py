@@ -24,6 +24,9 @@ VARIANTS = [
     {"HGPU_RATIO_GEMM": "1", "HGPU_FAR_LANES": "1"},
     {"HGPU_SM_SPLIT": "8:b"},
     {"HGPU_UPD_SMS": "96", "HGPU_GRID": "3"},
+    {"HGPU_FAR_SUB": "0"},
+    {"HGPU_FAR_SUB": "5", "HGPU_FAR_LANES": "3"},
+    {"HGPU_FAR_SUB": "16", "HGPU_NEAR": "100"},
 ]
 
 
