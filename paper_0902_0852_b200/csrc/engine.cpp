@@ -307,6 +307,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_SOLVE_TC")) solve_tc_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -336,6 +337,7 @@ Matrix::~Matrix() {
   if (ev1_) cudaEventDestroy(ev1_);
   for (cudaEvent_t e : pev_) cudaEventDestroy(e);
   for (cudaEvent_t e : sev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : edf_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
     if (h) cublasDestroy((cublasHandle_t)h);
@@ -599,11 +601,14 @@ void Matrix::build(int min_logL) {
   // device memory would not hold them beside the workspace
   size_t nsets = 1;
   if (!interval_) {
-    nsets = 2 + (size_t)std::max(0, defer_);
+    // EDF schedule (edf_h_ > 0): every panel's sets are kept until all of
+    // its updates ran, memory permitting (else the oldest are flushed)
+    const int nblocks = (n_ + kb - 1) / kb;
+    nsets = edf_h_ > 0 ? (size_t)nblocks + 1 : 2 + (size_t)std::max(0, defer_);
     const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
-    while (nsets > 2 && per_set * nsets > 0.5 * (double)free_b) --nsets;
+    while (nsets > 2 && per_set * nsets > 0.6 * (double)free_b) --nsets;
   }
   nsets_ = (int)nsets;
   vhdr_ = dalloc<int>(nsets * kb * n_);
@@ -785,6 +790,26 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   // nsets = s + 2 panels.
   const int sdef = std::max(1, nsets - 2);
   cudaStream_t su1 = stream_upd1_, su2 = stream_upd2_;
+  // EDF schedule of the trailing update (edf_h_ = H > 0): the update of band
+  // j by panel b' (U(b',j)) is due at panel j.  su1 runs U(b, b+1) at the
+  // end of panel b; every other pair goes to su2 in deadline order: at the
+  // end of panel b, all pending pairs with j <= b + H + 1, by band and then
+  // panel, one launch each.  Far bands are not touched before they come
+  // within H panels, so old panels' far work never blocks a near band (the
+  // FIFO trap of one launch per panel).  band_ev[j]: su2's last launch on
+  // band j (su1 waits for it); edf_next[b']: next band of panel b' to queue.
+  const bool edf = edf_h_ > 0 && nsets >= 3;
+  std::vector<int> edf_next(nblocks, INT_MAX);
+  std::vector<cudaEvent_t> band_ev(nblocks + 1, nullptr);
+  size_t edf_used = 0;
+  auto edf_event = [&]() {
+    while (edf_ev_.size() <= edf_used) {
+      cudaEvent_t e;
+      CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      edf_ev_.push_back(e);
+    }
+    return edf_ev_[edf_used++];
+  };
   const char* tl_path = std::getenv("HGPU_TIMELINE");
   tl_.clear();
   tl_used_ = 0;
@@ -856,6 +881,14 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     flush();
   };
 
+  // U(bp, j) on su2 (owned columns of band j)
+  auto edf_enqueue = [&](int bp, int j) {
+    const int c0 = j * kb, c1 = std::min(n, (j + 1) * kb);
+    if (!(D.debug & 512)) trailing(bp, c0, c1, su2, 9);  // 512: timing experiment only
+    cudaEvent_t e = edf_event();
+    CU(cudaEventRecord(e, su2));
+    band_ev[j] = e;
+  };
   while ((int)sev_.size() < 4 * n + 4) {  // + panel entry / far join
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -886,10 +919,19 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     // ---- panel b on the high-priority streams
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
     // slot set reuse: su1's last use of panel b - nsets precedes next_ready[b]
-    if (b >= nsets) CU(cudaStreamWaitEvent(sp, rest_done[b - nsets], 0));
+    if (edf && b >= nsets) {
+      // EDF: the panel whose set is reused gets its remaining bands now
+      const int bo = b - nsets;
+      for (int j = edf_next[bo]; j < nblocks; ++j) edf_enqueue(bo, j);
+      edf_next[bo] = INT_MAX;
+      CU(cudaEventRecord(rest_done[bo], su2));
+      CU(cudaStreamWaitEvent(sp, rest_done[bo], 0));
+    } else if (!edf && b >= nsets) {
+      CU(cudaStreamWaitEvent(sp, rest_done[b - nsets], 0));
+    }
     // catch-up of band b+1 with panels [b+1-s, b-1] on su1 (after su2's
     // last touch of the band, panel b-s), overlapping panel b
-    if (p1 < n) {
+    if (!edf && p1 < n) {
       if (b - sdef >= 0) CU(cudaStreamWaitEvent(su1, rest_done[b - sdef], 0));
       for (int bb = std::max(0, b + 1 - sdef); bb <= b - 1; ++bb)
         trailing(bb, p1, std::min(n, p1 + kb), su1, 13);
@@ -1154,7 +1196,22 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     // which overlaps panel b+1's factorisation
     CU(cudaStreamWaitEvent(su1, panel_done[b], 0));
     CU(cudaStreamWaitEvent(su2, panel_done[b], 0));
-    if (p1 < n) {
+    if (edf) {
+      if (p1 < n) {
+        const int p2 = std::min(n, p1 + kb);
+        if (band_ev[b + 1]) CU(cudaStreamWaitEvent(su1, band_ev[b + 1], 0));
+        trailing(b, p1, p2, su1, 8);
+      }
+      CU(cudaEventRecord(next_ready[b + 1], su1));
+      edf_next[b] = b + 2;
+      const int jmax = std::min(nblocks - 1, b + edf_h_ + 1);
+      for (int j = b + 2; j <= jmax; ++j)
+        for (int bp = 0; bp <= b; ++bp)
+          if (edf_next[bp] == j) {
+            edf_enqueue(bp, j);
+            ++edf_next[bp];
+          }
+    } else if (p1 < n) {
       const int p2 = std::min(n, p1 + kb);
       trailing(b, p1, p2, su1, 8);
       CU(cudaEventRecord(next_ready[b + 1], su1));
@@ -1163,7 +1220,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     } else {
       CU(cudaEventRecord(next_ready[b + 1], su1));
     }
-    CU(cudaEventRecord(rest_done[b], su2));
+    if (!edf) CU(cudaEventRecord(rest_done[b], su2));
   }
   // join the panel and update streams back into the bulk stream
   CU(cudaEventRecord(panel_done[nblocks], sp));

@@ -27,6 +27,8 @@ VARIANTS = [
     {"HGPU_FAR_SUB": "0"},
     {"HGPU_FAR_SUB": "5", "HGPU_FAR_LANES": "3"},
     {"HGPU_FAR_SUB": "16", "HGPU_NEAR": "100"},
+    {"HGPU_EDF": "1"},
+    {"HGPU_EDF": "3", "HGPU_FAR_LANES": "1"},
 ]
 
 
