@@ -881,13 +881,36 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     flush();
   };
 
-  // U(bp, j) on su2 (owned columns of band j)
-  auto edf_enqueue = [&](int bp, int j) {
+  // U(bp, j) for the m consecutive panels bp.. on su2 (owned columns of band
+  // j): their slot sets are adjacent, so one launch accumulates all 32 m
+  // stages (<= 256, the accumulator bound) with one pass over W
+  auto edf_enqueue = [&](int bp, int m, int j) {
     const int c0 = j * kb, c1 = std::min(n, (j + 1) * kb);
-    if (!(D.debug & 512)) trailing(bp, c0, c1, su2, 9);  // 512: timing experiment only
+    if (!(D.debug & 512)) {  // 512: timing experiment only
+      for (int ob : owned_blocks_)
+        if (ob == j) timed_update(bp, kb * m, c0, c1, su2, 9);
+    }
     cudaEvent_t e = edf_event();
     CU(cudaEventRecord(e, su2));
     band_ev[j] = e;
+  };
+  // all pending panels of band j (edf_next[bp] == j), in runs of <= 8
+  // consecutive panels whose slot sets do not wrap
+  auto edf_band = [&](int j, int bmax) {
+    int bp = 0;
+    while (bp <= bmax) {
+      if (edf_next[bp] != j) {
+        ++bp;
+        continue;
+      }
+      int m = 1;
+      while (m < 8 && bp + m <= bmax && edf_next[bp + m] == j &&
+             (bp % nsets) + m < nsets)
+        ++m;
+      edf_enqueue(bp, m, j);
+      for (int k = 0; k < m; ++k) ++edf_next[bp + k];
+      bp += m;
+    }
   };
   while ((int)sev_.size() < 4 * n + 4) {  // + panel entry / far join
     cudaEvent_t e;
@@ -922,7 +945,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     if (edf && b >= nsets) {
       // EDF: the panel whose set is reused gets its remaining bands now
       const int bo = b - nsets;
-      for (int j = edf_next[bo]; j < nblocks; ++j) edf_enqueue(bo, j);
+      for (int j = edf_next[bo]; j < nblocks; ++j) edf_enqueue(bo, 1, j);
       edf_next[bo] = INT_MAX;
       CU(cudaEventRecord(rest_done[bo], su2));
       CU(cudaStreamWaitEvent(sp, rest_done[bo], 0));
@@ -1205,12 +1228,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       CU(cudaEventRecord(next_ready[b + 1], su1));
       edf_next[b] = b + 2;
       const int jmax = std::min(nblocks - 1, b + edf_h_ + 1);
-      for (int j = b + 2; j <= jmax; ++j)
-        for (int bp = 0; bp <= b; ++bp)
-          if (edf_next[bp] == j) {
-            edf_enqueue(bp, j);
-            ++edf_next[bp];
-          }
+      for (int j = b + 2; j <= jmax; ++j) edf_band(j, b);
     } else if (p1 < n) {
       const int p2 = std::min(n, p1 + kb);
       trailing(b, p1, p2, su1, 8);
