@@ -436,6 +436,14 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
     return;
   }
   uint32_t* sm = use_gscratch ? gscratch : sm_dyn;
+  // the top Lm + 2 limbs of D: every level reads D' (its top <= 32 Lm - 64
+  // bits) from here instead of global memory
+  const int dbase = max(0, nD - (Lm + 2));
+  const int nDs = nD - dbase;
+  uint32_t* Ds = sm;                 // Lm + 2
+  for (int k = threadIdx.x; k < nDs; k += blockDim.x) Ds[k] = Dg[dbase + k];
+  __syncthreads();
+  sm += Lm + 2;
   uint32_t* Dt = sm;                 // Lm
   uint32_t* Y = Dt + Lm;             // Lm
   uint32_t* Pr = Y + Lm;             // 2 Lm + 1
@@ -446,7 +454,7 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
   // (scratch_words > 0) is sized to the stage's bound
   int segs = 6;
   if (scratch_words > 0)
-    segs = (int)min(6LL, (scratch_words - 9LL * Lm - 69) / (3LL * Lm + 2));
+    segs = (int)min(6LL, (scratch_words - 10LL * Lm - 71) / (3LL * Lm + 2));
   if (segs < 1) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     return;
@@ -457,8 +465,8 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
   // seed: Y_0 = floor(2^(n+p0)/D) ~ (2^126/top64(D)) >> (62 - p0)
   const int p0 = lv[0];
   if (threadIdx.x == 0) {
-    const uint32_t hi = field32(Dg, nD, (long long)n - 32);
-    const uint32_t lo = field32(Dg, nD, (long long)n - 64);
+    const uint32_t hi = field32(Ds, nDs, (long long)n - 32 - 32LL * dbase);
+    const uint32_t lo = field32(Ds, nDs, (long long)n - 64 - 32LL * dbase);
     const double d = ldexp((double)hi, 32) + (double)lo;  // [2^63, 2^64)
     const unsigned long long y63 =
         (unsigned long long)(ldexp(1.0, 126) / d);        // (2^62, 2^63]
@@ -493,7 +501,7 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
     const int mb = min(n, pb + G);   // bits of D'
     const int t = n - mb;
     const int nDt = (mb + 31) / 32;
-    for (int k = t0; k < nDt; k += ts) Dt[k] = field32(Dg, nD, 32LL * k + t);
+    for (int k = t0; k < nDt; k += ts) Dt[k] = field32(Ds, nDs, 32LL * k + t - 32LL * dbase);
     sync();
     // E = 2^Sb - D' Y, Sb = mb + pa.  Y is within a few units at precision
     // pa, so |E| < 2^(mb+3) <= 2^(32 nDt + 3): the low nL = nDt + 1 limbs of
@@ -1385,13 +1393,13 @@ long long recip_words_bound(const DevPlan& P, int dmax_bits, int segs) {
   // e <= (dmax - k2)/2 + k2 + 6 (the pivot has more than k2 bits), Pt = e + 32
   const long long e = (long long)(dmax_bits - P.k2) / 2 + P.k2 + 6;
   const long long Lm = (e + 32 + 32 + 31) / 32 + 2;
-  return 9 * Lm + 69 + (long long)segs * (3 * Lm + 2) + 8;
+  return 10 * Lm + 71 + (long long)segs * (3 * Lm + 2) + 8;
 }
 
 size_t recip_scratch_words(const DevPlan& P) {
   // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
   const size_t Lm = (size_t)P.ycap + 4;
-  return Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
+  return (Lm + 2) + Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
          6 * (3 * Lm + 2) + 64;
 }
 
