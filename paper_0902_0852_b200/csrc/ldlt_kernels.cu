@@ -845,6 +845,10 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
         int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
         int use_gscratch, int* err, PivotDiv pd) {
   if (stage_aborted(err)) return;
+  // HGPU_DEBUG & 4096: phase clocks of sampled stages (timing aid)
+  const bool ph = (P.debug & 4096) && p % 100 == 50 && threadIdx.x == 0;
+  long long t[5];
+  if (ph) t[0] = clock64();
   if (pd.on) {
     // R_{p-1}[p] of the previous stage of the panel (k_divide, one row)
     divide_body(P, vint, pd.vrow0, p - 1, p, p + 1, pd.Ybuf, pd.ys, pd.rint,
@@ -853,6 +857,7 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
     __syncthreads();
     if (stage_aborted(err)) return;
   }
+  if (ph) t[1] = clock64();
   if (nslots > 0) {
     const long long NW = P.NW;
     uint32_t* dst = W + colbase[p] * NW;
@@ -871,12 +876,19 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
     }
     __syncthreads();
   }
+  if (ph) t[2] = clock64();
   extract_body(P, W, colbase, p, p, p + 1, vint, vrow0, piv, maxbitsV, vhat,
                maxdegV, err, 0, nullptr, 0, 0, 1);
   __syncthreads();
+  if (ph) t[3] = clock64();
   if (p < P.n - 1)
     recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
                gscratch, use_gscratch, err, 0, pd.recip_words);
+  if (ph) {
+    t[4] = clock64();
+    printf("k_pivot p=%d div %lld col %lld extract %lld recip %lld cycles\n", p,
+           t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3]);
+  }
 }
 
 // ------------------------------------------- ratios on the tensor cores ---
