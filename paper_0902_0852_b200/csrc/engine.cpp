@@ -308,6 +308,12 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_SOLVE_TC")) solve_tc_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
+  {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream_pre_, cudaStreamNonBlocking, hi));
+  }
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -338,6 +344,8 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : pev_) cudaEventDestroy(e);
   for (cudaEvent_t e : sev_) cudaEventDestroy(e);
   for (cudaEvent_t e : edf_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : pre_ev_) cudaEventDestroy(e);
+  if (stream_pre_) cudaStreamDestroy(stream_pre_);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
     if (h) cublasDestroy((cublasHandle_t)h);
@@ -918,6 +926,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     sev_.push_back(e);
   }
   cudaStream_t sh = stream_helper_;
+  while ((int)pre_ev_.size() < n) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pre_ev_.push_back(e);
+  }
   {
     // bits bound of any diagonal Schur complement W_rr (PD: <= M_rr - x)
     int db = 0;
@@ -1026,8 +1039,23 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               pd.dscr = dscratch_;
               pd.use_dscr = div_global_ ? 1 : 0;
             }
+            // stages [p0, p-1) of the pivot entry W[p][p] ahead of the chain,
+            // on their own stream with 32 CTAs (k_pivot's single CTA is
+            // latency-bound on those reads); k_pivot applies stage p-1
+            int s_first = 0;
+            if (pre_entry_ && s >= 2) {
+              CU(cudaStreamWaitEvent(stream_pre_, sev_[4 * (p - 2) + 2], 0));
+              TL(16, p, stream_pre_, [&] {
+                return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s - 1,
+                                         p, p, p + 1, err_, stream_pre_);
+              });
+              CU(cudaEventRecord(pre_ev_[p], stream_pre_));
+              CU(cudaStreamWaitEvent(sh, pre_ev_[p], 0));
+              s_first = s - 1;
+            }
             TL(2, p, sh, [&] {
-              return launch_pivot(D, W_, colbase_, vh, rh, slot_stride, s, p,
+              return launch_pivot(D, W_, colbase_, vh + s_first * slot_stride,
+                                  rh + s_first * slot_stride, slot_stride, s - s_first, p,
                                   vint, row0, piv, maxbitsV, vhat_, maxdegV,
                                   dmax_bits_, yb, yss, rscratch_,
                                   recip_global_ ? 1 : 0, err_, sh, pd);

@@ -208,6 +208,10 @@ class Matrix {
   bool solve_tc_ = false;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
+  // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)
+  bool pre_entry_ = true;
+  cudaStream_t stream_pre_ = nullptr;
+  std::vector<cudaEvent_t> pre_ev_;
   std::vector<cudaEvent_t> edf_ev_;
   int solve_xlimbs_ = 0;          // widest z / y entry of the solves so far
   long long factor_serial_ = 0;   // KEEP_L factorisations so far
