@@ -585,87 +585,5 @@ __device__ inline void warp_mul(const uint32_t* a, int na, const uint32_t* b,
       [&](int k, uint32_t d) { out[k] = d; });
 }
 
-// out[0..M) = the product a*b (M = na + nb), balanced for long operands:
-// a work item is G=8 output columns times one SL-long stretch of their
-// i-range, so every item costs at most SL*G limb products; items are dealt
-// so that the lanes of a warp hold different column groups (item it ->
-// group it % ngroups, stretch it / ngroups), and each item adds its 96-bit
-// column sums into three shared 32-bit planes with native atomics (no two
-// lanes of a warp share an address).  col: >= 3*M words.
-__device__ inline void cta_mul_bal(const uint32_t* a, int na, const uint32_t* b,
-                                   int nb, uint32_t* out, int M, uint32_t* col,
-                                   uint32_t* red) {
-  constexpr int G = 8, SL = 48;
-  uint32_t* s0 = col;
-  uint32_t* s1 = col + M;
-  uint32_t* s2 = col + 2 * M;
-  for (int k = threadIdx.x; k < 3 * M; k += blockDim.x) col[k] = 0u;
-  __syncthreads();
-  const int ngroups = (M + G - 1) / G;
-  const int minlen = min(na, nb);
-  const int nst = (minlen + G - 1 + SL - 1) / SL;  // stretches of the longest group
-  if (na > 0 && nb > 0) {
-    for (int it = threadIdx.x; it < ngroups * nst; it += blockDim.x) {
-      const int g = it % ngroups, sgi = it / ngroups;
-      const int k0 = g * G;
-      const int glo = max(0, k0 - nb + 1);
-      const int ghi = min(k0 + G - 1, na - 1);
-      const int ilo = glo + sgi * SL;
-      const int ihi = min(ghi, ilo + SL - 1);
-      if (ilo > ihi) continue;
-      uint32_t c0[G], c1[G], c2[G];
-#pragma unroll
-      for (int t = 0; t < G; ++t) c0[t] = c1[t] = c2[t] = 0u;
-      uint32_t w[G];
-#pragma unroll
-      for (int t = 0; t < G; ++t) {
-        const int j = k0 + t - ilo;
-        w[t] = (j >= 0 && j < nb) ? b[j] : 0u;
-      }
-      for (int i = ilo; i <= ihi; ++i) {
-        const uint32_t ai = a[i];
-#pragma unroll
-        for (int t = 0; t < G; ++t) {
-          asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
-              "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
-              "addc.u32 %2, %2, 0;"
-              : "+r"(c0[t]), "+r"(c1[t]), "+r"(c2[t])
-              : "r"(ai), "r"(w[t]));
-        }
-#pragma unroll
-        for (int t = G - 1; t > 0; --t) w[t] = w[t - 1];
-        const int j = k0 - i - 1;
-        w[0] = (j >= 0 && j < nb) ? b[j] : 0u;
-      }
-#pragma unroll
-      for (int t = 0; t < G; ++t) {
-        const int k = k0 + t;
-        if (k >= M) continue;
-        // (c0, c1, c2) into (s0, s1, s2): carries move up a plane
-        const uint32_t o0 = atomicAdd(s0 + k, c0[t]);
-        const uint32_t cy0 = (o0 + c0[t] < o0) ? 1u : 0u;
-        const uint32_t v1 = c1[t] + cy0;
-        const uint32_t w1 = (cy0 && v1 == 0u) ? 1u : 0u;
-        uint32_t cy1 = 0u;
-        if (v1) {
-          const uint32_t o1 = atomicAdd(s1 + k, v1);
-          cy1 = (o1 + v1 < o1) ? 1u : 0u;
-        }
-        const uint32_t v2 = c2[t] + cy1 + w1;
-        if (v2) atomicAdd(s2 + k, v2);
-      }
-    }
-  }
-  __syncthreads();
-  cta_resolve(
-      M, 32,
-      [&](int k) -> int64_t {
-        int64_t v = s0[k];
-        if (k >= 1) v += s1[k - 1];
-        if (k >= 2) v += s2[k - 2];
-        return v;
-      },
-      [&](int k, uint32_t d) { out[k] = d; }, red);
-}
 
 }  // namespace hgpu

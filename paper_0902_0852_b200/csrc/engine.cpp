@@ -985,7 +985,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       // Events (per stage): sev_[4p] extract(near p) done, sev_[4p+1]
       // recip(p) done, sev_[4p+2] near divide(p) done, sev_[4p+3] chain done.
       const int near_end = std::min(n, p0 + near_rows_);
-      const bool far = near_end < n && recip_bound_ && !(D.debug & 1024);  // 1024: timing experiment only
+      const bool far = near_end < n && recip_bound_;
       // ratio GEMM for this run's operand bounds (else k_divide)
       const bool rg_ok = ratio_gemm_ && rg_kd_ > 0 &&
                          ratio_gemm_kd(dmax_bits_) <= rg_kd_ &&
