@@ -309,10 +309,12 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CU(cudaStreamCreateWithPriority(&stream_pre_, cudaStreamNonBlocking, hi));
+    CU(cudaStreamCreateWithPriority(&stream_next_, cudaStreamNonBlocking, hi));
   }
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
@@ -345,6 +347,8 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : sev_) cudaEventDestroy(e);
   for (cudaEvent_t e : edf_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : pre_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : sn_ev_) cudaEventDestroy(e);
+  if (stream_next_) cudaStreamDestroy(stream_next_);
   if (stream_pre_) cudaStreamDestroy(stream_pre_);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
@@ -926,6 +930,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     sev_.push_back(e);
   }
   cudaStream_t sh = stream_helper_;
+  while ((int)sn_ev_.size() < n) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sn_ev_.push_back(e);
+  }
   while ((int)pre_ev_.size() < n) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -995,6 +1004,10 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       bool chain_started = false;
       // far lanes (one when the divisions use global scratch or the GEMM)
       const int nlanes = (div_global_ || rg_far) ? 1 : far_lanes_;
+      // next-row stream (HGPU_NEXT_ROW): the chain's next row apart from the
+      // bulk near rows (fused chain, shared-memory divisions, >= 3 near rows)
+      const bool nr = next_row_ && fused_pivot_ && !div_global_ && !rg_near &&
+                      (far ? near_end : n) - p0 >= 3 && recip_bound_;
       // far rows' in-panel update in sub-panels of fsub stages (0: plain
       // left-looking); needs the far rows below the panel's columns
       const int fsub = (far_sub_ > 0 && near_end >= p1 && D.NW % 32 == 0) ? far_sub_ : 0;
@@ -1016,6 +1029,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             CU(cudaEventRecord(sev_[4 * n], sp));
             CU(cudaStreamWaitEvent(sh, sev_[4 * n], 0));
             chain_started = true;
+          } else if (nr) {
+            // next-row stream: V_{p-1}[p] and R_{p-2}[p] come from sn(p-1),
+            // V^_{p-2}[p] from the bulk extraction (p-2) and older ratios
+            // from the bulk divisions (p-3)
+            CU(cudaStreamWaitEvent(sh, sn_ev_[p - 1], 0));
+            if (p - 2 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 2)], 0));
+            if (p - 3 >= p0) CU(cudaStreamWaitEvent(sh, sev_[4 * (p - 3) + 2], 0));
           } else {
             // pivot entry of column p needs V_{p-1}[p] (extract(near p-1))
             // and R_{p-2}[p] (near divide(p-2)); R_{p-1}[p] is on sh already
@@ -1044,7 +1064,17 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             // latency-bound on those reads); k_pivot applies stage p-1
             int s_first = 0;
             if (pre_entry_ && s >= 2) {
-              CU(cudaStreamWaitEvent(stream_pre_, sev_[4 * (p - 2) + 2], 0));
+              if (nr) {
+                // stages <= p-2 of W[p][p]: R_{p-2}[p] from sn(p-1), older
+                // ratios from the bulk divisions (p-3), V^_{p-2}[p] from the
+                // bulk extraction (p-2)
+                CU(cudaStreamWaitEvent(stream_pre_, sn_ev_[p - 1], 0));
+                CU(cudaStreamWaitEvent(stream_pre_, sev_[4 * (p - 2)], 0));
+                if (p - 3 >= p0)
+                  CU(cudaStreamWaitEvent(stream_pre_, sev_[4 * (p - 3) + 2], 0));
+              } else {
+                CU(cudaStreamWaitEvent(stream_pre_, sev_[4 * (p - 2) + 2], 0));
+              }
               TL(16, p, stream_pre_, [&] {
                 return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s - 1,
                                          p, p, p + 1, err_, stream_pre_);
@@ -1076,14 +1106,48 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             });
           }
           CU(cudaEventRecord(sev_[4 * p + 1], sh));
-          // near rows of column p on the panel stream (rows > p)
           const int rn = far ? near_end : n;
+          if (nr) {
+            // sn(p): row p+1 of column p, which the chain needs next --
+            // (i) R_{p-1}[p+1], (ii) its entry update with stages [p0, p),
+            // (iii) its extraction -- off the bulk near rows' stream
+            cudaStream_t sn = stream_next_;
+            if (s == 0) {
+              CU(cudaEventRecord(sev_[4 * n + 3], sp));  // panel entry
+              CU(cudaStreamWaitEvent(sn, sev_[4 * n + 3], 0));
+            }
+            if (s >= 1) {
+              CU(cudaStreamWaitEvent(sn, sev_[4 * (p - 1) + 1], 0));  // Y_{p-1}
+              CU(cudaStreamWaitEvent(sn, sev_[4 * (p - 1)], 0));      // V_{p-1}[p+1]
+              if (s >= 2) CU(cudaStreamWaitEvent(sn, sev_[4 * (p - 2) + 2], 0));
+              TL(17, p, sn, [&] {
+                return launch_divide(D, vint, row0 - n, p - 1, p + 1, p + 2,
+                                     ybuf_ + (size_t)((p - 1) % kYRing) * P.ycap,
+                                     ys_ + ((p - 1) % kYRing) * 4, rint, row0 - n, rhat_,
+                                     maxdegR + (p - 1), dscratch_, 0, err_, sn);
+              });
+              TL(17, p, sn, [&] {
+                return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                         p, p + 1, p + 2, err_, sn);
+              });
+            }
+            TL(17, p, sn, [&] {
+              return launch_extract(D, W_, colbase_, p, p + 1, p + 2, vint, row0,
+                                    piv, maxbitsV, vhat_, maxdegV, err_, sn, 0,
+                                    rg_near ? vdig_ : nullptr, rg_kd_);
+            });
+            CU(cudaEventRecord(sn_ev_[p], sn));
+            // bulk near rows [p+2, rn): V^_{p-1}[p] comes from sn(p-1)
+            if (s >= 1) CU(cudaStreamWaitEvent(sp, sn_ev_[p - 1], 0));
+          }
+          // near rows of column p on the panel stream (rows > p)
+          const int rb = nr ? p + 2 : p + 1;
           TL(3, p, sp, [&] {
             return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                     p, p + 1, rn, err_, sp);
+                                     p, rb, rn, err_, sp);
           });
           TL(4, p, sp, [&] {
-            return launch_extract(D, W_, colbase_, p, p + 1, rn, vint, row0,
+            return launch_extract(D, W_, colbase_, p, rb, rn, vint, row0,
                                   piv, maxbitsV, vhat_, maxdegV, err_, sp, 0,
                                   rg_near ? vdig_ : nullptr, rg_kd_);
           });
@@ -1091,7 +1155,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot):
           // inside the next stage's k_pivot, except at the panel's last stage
           // (the trailing update reads it)
-          CU(cudaStreamWaitEvent(sh, sev_[4 * p], 0));
+          CU(cudaStreamWaitEvent(sh, nr ? sn_ev_[p] : sev_[4 * p], 0));
           if (!fused_pivot_ || p + 1 == p1 || p + 1 == n - 1) {
             TL(5, p, sh, [&] {
               return launch_divide(D, vint, row0, p, p + 1, p + 2, yb, yss,
@@ -1109,8 +1173,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               return cudaSuccess;
             });
           } else {
+            // with sn, row p+2 of stage p is sn(p+1)'s first task (inside
+            // the panel)
+            const int db0 = (nr && p + 1 < p1 && p + 1 < n - 1) ? p + 3 : p + 2;
             TL(5, p, sp, [&] {
-              return launch_divide(D, vint, row0, p, p + 2, rn, yb, yss, rint,
+              return launch_divide(D, vint, row0, p, db0, rn, yb, yss, rint,
                                    row0, rhat_, maxdegR + p, dscratch2_,
                                    div_global_ ? 1 : 0, err_, sp);
             });
@@ -1128,6 +1195,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               const int hi = near_end + (int)((long long)(n - near_end) * (l + 1) / nlanes);
               if (lo >= hi) continue;
               if (p > p0) CU(cudaStreamWaitEvent(fs, sev_[4 * (p - 1)], 0));
+              if (nr && p > p0) CU(cudaStreamWaitEvent(fs, sn_ev_[p - 1], 0));
               // column p receives the stages of its own sub-panel [ps, p);
               // earlier sub-panels arrived by the rank-fsub updates below
               const int ps = fsub > 0 ? p0 + (s / fsub) * fsub : p0;
@@ -1161,6 +1229,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                 // once per tile instead of once per column); needs V^_p of
                 // those columns (near extract of stage p)
                 CU(cudaStreamWaitEvent(fs, sev_[4 * p], 0));
+                if (nr) CU(cudaStreamWaitEvent(fs, sn_ev_[p], 0));
                 const int sb0 = p + 1 - fsub - p0;
                 TL(14, p, fs, [&] {
                   return launch_update_rect(D, W_, colbase_, vh + sb0 * slot_stride,
@@ -1173,6 +1242,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           if (p + 1 == p1 || p + 1 == n - 1) {
             // join: the next step on sp needs R_p[p+1] as well
             CU(cudaStreamWaitEvent(sp, sev_[4 * p + 3], 0));
+            if (nr) CU(cudaStreamWaitEvent(sp, sn_ev_[p], 0));
             if (far)
               for (int l = 0; l < nlanes; ++l) {
                 CU(cudaEventRecord(far_ev_[l], far_streams_[l]));

@@ -210,6 +210,10 @@ class Matrix {
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
   // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)
   bool pre_entry_ = true;
+  // the chain's next row on its own stream (HGPU_NEXT_ROW)
+  bool next_row_ = false;
+  cudaStream_t stream_next_ = nullptr;
+  std::vector<cudaEvent_t> sn_ev_;
   cudaStream_t stream_pre_ = nullptr;
   std::vector<cudaEvent_t> pre_ev_;
   std::vector<cudaEvent_t> edf_ev_;

@@ -29,6 +29,9 @@ VARIANTS = [
     {"HGPU_FAR_SUB": "16", "HGPU_NEAR": "100"},
     {"HGPU_EDF": "1"},
     {"HGPU_EDF": "3", "HGPU_FAR_LANES": "1"},
+    {"HGPU_NEXT_ROW": "1"},
+    {"HGPU_NEXT_ROW": "1", "HGPU_PRE_ENTRY": "0", "HGPU_FAR_SUB": "0"},
+    {"HGPU_NEXT_ROW": "1", "HGPU_NEAR": "100", "HGPU_EDF": "0"},
 ]
 
 
