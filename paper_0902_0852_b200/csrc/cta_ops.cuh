@@ -204,13 +204,17 @@ __device__ inline void inv_pass(uint32_t* x, int np, int logL, int lt0,
 
 // Forward: natural in (< 4q), bit-reversed out (< q).  twm: [np][L] table
 // T[m+i] in Montgomery form (any memory; shared memory when it fits).
+// RM (16, 8 or 4): the widest pass; narrower passes use more threads per
+// transform (the single-transform chains of the solve prefer them).
+template <int RM = 16>
 __device__ inline void cta_ntt_fwd16(uint32_t* x, int np, int logL,
                                      const uint32_t* twm, const PrimeConsts* pc) {
   // first pass takes logL mod 4 levels (large stride), then passes of 4;
   // the last pass (s = 1) moves contiguous 16-word units
+  constexpr int rb = RM == 16 ? 4 : (RM == 8 ? 3 : 2);
   int lm = 0;
   while (lm < logL) {
-    const int r = (lm == 0 && logL % 4) ? logL % 4 : 4;
+    const int r = (lm == 0 && logL % rb) ? logL % rb : rb;
     switch (r) {
       case 1: fwd_pass<2>(x, np, logL, lm, twm, pc); break;
       case 2: fwd_pass<4>(x, np, logL, lm, twm, pc); break;
@@ -230,12 +234,14 @@ __device__ inline void cta_ntt_fwd16(uint32_t* x, int np, int logL,
 }
 
 // Inverse without 1/L: bit-reversed in (< 2q), natural out (< 2q).
+template <int RM = 16>
 __device__ inline void cta_ntt_inv16(uint32_t* x, int np, int logL,
                                      const uint32_t* itwm, const PrimeConsts* pc) {
   // passes of 4 from the contiguous end (S = 1); the last takes the rest
+  constexpr int rb = RM == 16 ? 4 : (RM == 8 ? 3 : 2);
   int lt = 0;
   while (lt < logL) {
-    const int r = logL - lt >= 4 ? 4 : logL - lt;
+    const int r = logL - lt >= rb ? rb : logL - lt;
     switch (r) {
       case 1: inv_pass<2>(x, np, logL, lt, itwm, pc); break;
       case 2: inv_pass<4>(x, np, logL, lt, itwm, pc); break;

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -230,6 +231,118 @@ Plan choose_plan(int n, int K, int bits, int min_logL) {
   return best;
 }
 
+// Prime constants, Garner constants and the twiddle tables (host copy:
+// Shoup forward/inverse pairs, then the Montgomery forms) of plan P.
+static std::vector<uint32_t> transform_tables(DevPlan& D, const Plan& P) {
+  const size_t npl = (size_t)P.np * P.L;
+  D.Lmax = P.L;
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    PrimeConsts& c = D.pc[j];
+    c.q = (uint32_t)q;
+    // -q^-1 mod 2^32 by Newton
+    uint32_t inv = 1;
+    for (int i = 0; i < 6; ++i) inv *= 2u - (uint32_t)q * inv;
+    c.qneg = (uint32_t)(0u - inv);
+    c.r32 = (uint32_t)((1ULL << 32) % q);
+    c.r32s = shoup_companion(c.r32, (uint32_t)q);
+    c.r64 = (uint32_t)((u128)c.r32 * c.r32 % q);
+    c.one_s = shoup_companion(1u, (uint32_t)q);
+    const u64 il = invmod(P.L, q);
+    D.invL[j] = (uint32_t)il;
+    D.invLp[j] = shoup_companion((uint32_t)il, (uint32_t)q);
+  }
+  const u64 q0 = kPrimes[0], q1 = kPrimes[1], q2 = kPrimes[2];
+  D.g1 = (uint32_t)invmod(q0 % q1, q1);
+  D.g1p = shoup_companion(D.g1, (uint32_t)q1);
+  D.g2 = (uint32_t)invmod((u128)q0 * q1 % q2, q2);
+  D.g2p = shoup_companion(D.g2, (uint32_t)q2);
+  D.q0m2 = (uint32_t)(q0 % q2);
+  D.q0m2p = shoup_companion(D.q0m2, (uint32_t)q2);
+  D.q01 = q0 * q1;
+  if (P.np == 4) {
+    const u64 q3 = kPrimes[3];
+    const u128 q012 = (u128)q0 * q1 * q2;
+    D.g3 = (uint32_t)invmod((u64)(q012 % q3), q3);
+    D.g3p = shoup_companion(D.g3, (uint32_t)q3);
+    D.q0m3 = (uint32_t)(q0 % q3);
+    D.q0m3p = shoup_companion(D.q0m3, (uint32_t)q3);
+    D.q01m3 = (uint32_t)((u128)q0 * q1 % q3);
+    D.q01m3p = shoup_companion(D.q01m3, (uint32_t)q3);
+    D.q012lo = (u64)q012;
+    D.q012hi = (u64)(q012 >> 64);
+  }
+  u128 Q = 1;
+  for (int j = 0; j < P.np; ++j) Q *= kPrimes[j];
+  const u128 H = (Q + 1) / 2;
+  D.Qlo = (u64)Q;
+  D.Qhi = (u64)(Q >> 64);
+  D.Hlo = (u64)H;
+  D.Hhi = (u64)(H >> 64);
+
+  // twiddles: T[m+i] = w^{(L/2m) bitrev_m(i)}, w a primitive L-th root
+  std::vector<uint32_t> tab(4 * (size_t)P.np * P.L, 0);
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    const u64 wL = powmod(kPrimRoots[j], (q - 1) / P.L, q);
+    uint32_t* tw = &tab[(0 * P.np + j) * (size_t)P.L];
+    uint32_t* twp = &tab[(1 * P.np + j) * (size_t)P.L];
+    uint32_t* itw = &tab[(2 * P.np + j) * (size_t)P.L];
+    uint32_t* itwp = &tab[(3 * P.np + j) * (size_t)P.L];
+    for (int lm = 0; (1 << lm) < P.L; ++lm) {
+      const int m = 1 << lm;
+      for (int i = 0; i < m; ++i) {
+        const u64 e = (u64)(P.L / (2 * m)) * bitrev(i, lm);
+        const u64 v = powmod(wL, e, q);
+        const u64 iv = invmod(v, q);
+        tw[m + i] = (uint32_t)v;
+        twp[m + i] = shoup_companion((uint32_t)v, (uint32_t)q);
+        itw[m + i] = (uint32_t)iv;
+        itwp[m + i] = shoup_companion((uint32_t)iv, (uint32_t)q);
+      }
+    }
+  }
+  // Montgomery-form copies (w 2^32 mod q) for the radix-16 transforms
+  tab.resize(6 * npl, 0);
+  for (int j = 0; j < P.np; ++j) {
+    const u64 q = kPrimes[j];
+    for (int k = 1; k < P.L; ++k) {
+      tab[4 * npl + j * (size_t)P.L + k] =
+          (uint32_t)(((u128)tab[0 * npl + j * (size_t)P.L + k] << 32) % q);
+      tab[5 * npl + j * (size_t)P.L + k] =
+          (uint32_t)(((u128)tab[2 * npl + j * (size_t)P.L + k] << 32) % q);
+    }
+  }
+  return tab;
+}
+
+// Transform plan of the solve's AXPY: 32-bit digits (a digit is a limb, so
+// the conversions are word copies), the shortest length holding a product
+// of `bits` bits with two digits spare, and the fewest primes keeping n
+// products of L/2 overlapping digit pairs below Q/4.
+Plan solve_plan(int n, int K, int bits) {
+  Plan P;
+  P.w = 32;
+  P.logL = 5;
+  while (32LL * ((1 << P.logL) - 2) < (long long)bits + 1) ++P.logL;
+  if (P.logL > kMaxLogL) throw Error(HGPU_ERR_CAPACITY, "solve transform too long");
+  P.L = 1 << P.logL;
+  for (P.np = 2; P.np <= kMaxPrimes; ++P.np) {
+    u128 Q = 1;
+    for (int j = 0; j < P.np; ++j) Q *= kPrimes[j];
+    const double lb = std::log2((double)n + 1) + std::log2((double)P.L / 2 + 1) + 64.1;
+    if (lb < log2_u128(Q) - 2.0) break;
+  }
+  if (P.np > kMaxPrimes) throw Error(HGPU_ERR_CAPACITY, "no solve transform plan fits");
+  P.n = n;
+  P.K = K;
+  P.T = (32 * P.np + P.w - 1) / P.w + 1;
+  if (P.w * (P.T - 1) >= 128) --P.T;
+  P.cap = (P.w * (P.L + P.T) + 31) / 32 + 2;
+  P.ycap = P.cap + (K / 2) / 32 + 8;
+  return P;
+}
+
 Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
                int device)
     : n_(n), K_(K), device_(device) {
@@ -306,6 +419,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_DEFER")) defer_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_FUSED_PIVOT")) fused_pivot_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_SOLVE_TC")) solve_tc_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_SOLVE_NTT")) solve_ntt_ = std::atoi(e);
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
@@ -385,8 +499,12 @@ void Matrix::release() {
                   (void*)srscr_, (void*)sdscr_, (void*)sys_})
     dfree(p);
   for (void* q : {(void*)rdig_col_, (void*)rdig_row_, (void*)tc_t_, (void*)tc_c_,
-                  (void*)tc_acc_, (void*)tc_ws_})
+                  (void*)tc_acc_, (void*)tc_ws_, (void*)stw_, (void*)lhat_, (void*)acch_,
+                  (void*)sxhat_})
     dfree(q);
+  stw_ = lhat_ = acch_ = sxhat_ = nullptr;
+  sdp_bits_ = sdp_xbits_ = 0;
+  lhat_for_ = -1;
   rdig_col_ = rdig_row_ = tc_t_ = tc_ws_ = nullptr;
   tc_c_ = nullptr;
   tc_acc_ = nullptr;
@@ -462,85 +580,8 @@ void Matrix::build(int min_logL) {
   D.cap = P.cap;
   D.ycap = P.ycap;
   D.NW = P.np * P.L;
-  D.Lmax = P.L;
-  for (int j = 0; j < P.np; ++j) {
-    const u64 q = kPrimes[j];
-    PrimeConsts& c = D.pc[j];
-    c.q = (uint32_t)q;
-    // -q^-1 mod 2^32 by Newton
-    uint32_t inv = 1;
-    for (int i = 0; i < 6; ++i) inv *= 2u - (uint32_t)q * inv;
-    c.qneg = (uint32_t)(0u - inv);
-    c.r32 = (uint32_t)((1ULL << 32) % q);
-    c.r32s = shoup_companion(c.r32, (uint32_t)q);
-    c.r64 = (uint32_t)((u128)c.r32 * c.r32 % q);
-    c.one_s = shoup_companion(1u, (uint32_t)q);
-    const u64 il = invmod(P.L, q);
-    D.invL[j] = (uint32_t)il;
-    D.invLp[j] = shoup_companion((uint32_t)il, (uint32_t)q);
-  }
-  const u64 q0 = kPrimes[0], q1 = kPrimes[1], q2 = kPrimes[2];
-  D.g1 = (uint32_t)invmod(q0 % q1, q1);
-  D.g1p = shoup_companion(D.g1, (uint32_t)q1);
-  D.g2 = (uint32_t)invmod((u128)q0 * q1 % q2, q2);
-  D.g2p = shoup_companion(D.g2, (uint32_t)q2);
-  D.q0m2 = (uint32_t)(q0 % q2);
-  D.q0m2p = shoup_companion(D.q0m2, (uint32_t)q2);
-  D.q01 = q0 * q1;
-  if (P.np == 4) {
-    const u64 q3 = kPrimes[3];
-    const u128 q012 = (u128)q0 * q1 * q2;
-    D.g3 = (uint32_t)invmod((u64)(q012 % q3), q3);
-    D.g3p = shoup_companion(D.g3, (uint32_t)q3);
-    D.q0m3 = (uint32_t)(q0 % q3);
-    D.q0m3p = shoup_companion(D.q0m3, (uint32_t)q3);
-    D.q01m3 = (uint32_t)((u128)q0 * q1 % q3);
-    D.q01m3p = shoup_companion(D.q01m3, (uint32_t)q3);
-    D.q012lo = (u64)q012;
-    D.q012hi = (u64)(q012 >> 64);
-  }
-  u128 Q = 1;
-  for (int j = 0; j < P.np; ++j) Q *= kPrimes[j];
-  const u128 H = (Q + 1) / 2;
-  D.Qlo = (u64)Q;
-  D.Qhi = (u64)(Q >> 64);
-  D.Hlo = (u64)H;
-  D.Hhi = (u64)(H >> 64);
-
-  // twiddles: T[m+i] = w^{(L/2m) bitrev_m(i)}, w a primitive L-th root
-  std::vector<uint32_t> tab(4 * (size_t)P.np * P.L, 0);
-  for (int j = 0; j < P.np; ++j) {
-    const u64 q = kPrimes[j];
-    const u64 wL = powmod(kPrimRoots[j], (q - 1) / P.L, q);
-    uint32_t* tw = &tab[(0 * P.np + j) * (size_t)P.L];
-    uint32_t* twp = &tab[(1 * P.np + j) * (size_t)P.L];
-    uint32_t* itw = &tab[(2 * P.np + j) * (size_t)P.L];
-    uint32_t* itwp = &tab[(3 * P.np + j) * (size_t)P.L];
-    for (int lm = 0; (1 << lm) < P.L; ++lm) {
-      const int m = 1 << lm;
-      for (int i = 0; i < m; ++i) {
-        const u64 e = (u64)(P.L / (2 * m)) * bitrev(i, lm);
-        const u64 v = powmod(wL, e, q);
-        const u64 iv = invmod(v, q);
-        tw[m + i] = (uint32_t)v;
-        twp[m + i] = shoup_companion((uint32_t)v, (uint32_t)q);
-        itw[m + i] = (uint32_t)iv;
-        itwp[m + i] = shoup_companion((uint32_t)iv, (uint32_t)q);
-      }
-    }
-  }
-  // Montgomery-form copies (w 2^32 mod q) for the radix-16 transforms
+  std::vector<uint32_t> tab = transform_tables(D, P);
   const size_t npl = (size_t)P.np * P.L;
-  tab.resize(6 * npl, 0);
-  for (int j = 0; j < P.np; ++j) {
-    const u64 q = kPrimes[j];
-    for (int k = 1; k < P.L; ++k) {
-      tab[4 * npl + j * (size_t)P.L + k] =
-          (uint32_t)(((u128)tab[0 * npl + j * (size_t)P.L + k] << 32) % q);
-      tab[5 * npl + j * (size_t)P.L + k] =
-          (uint32_t)(((u128)tab[2 * npl + j * (size_t)P.L + k] << 32) % q);
-    }
-  }
   tw_ = dalloc<uint32_t>(tab.size());
   CU(cudaMemcpy(tw_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
   D.tw = tw_;
@@ -1429,19 +1470,30 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                                    long long* launches) {
   // tensor-core AXPY (HGPU_SOLVE_TC=1) once an earlier solve has recorded
   // the operand widths; any capacity flag reruns the solve on the integer path
+  if (solve_ntt_) {
+    try {
+      return solve_impl(u, launches, 2);
+    } catch (const Error& e) {
+      if (e.status != HGPU_ERR_CAPACITY || solve_ntt_ == 2) throw;
+      sdp_bits_ = 0;  // re-plan from the widths the integer path records
+      lhat_for_ = -1;
+    }
+  }
   if (solve_tc_ && solve_xlimbs_ > 0) {
     try {
-      return solve_impl(u, launches, true);
+      return solve_impl(u, launches, 1);
     } catch (const Error& e) {
       if (e.status != HGPU_ERR_CAPACITY) throw;
       solve_xlimbs_ = 0;
     }
   }
-  return solve_impl(u, launches, false);
+  return solve_impl(u, launches, 0);
 }
 
 std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
-                                        long long* launches, bool tc) {
+                                        long long* launches, int mode) {
+  const bool tc = mode == 1, ntt = mode == 2;
+  const auto t_start = std::chrono::steady_clock::now();
   if (!have_L_)
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve needs a HGPU_KEEP_L factorisation");
   if (world_ != 1)
@@ -1539,6 +1591,75 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
     if (cublasSetStream((cublasHandle_t)tc_blas_, st) != CUBLAS_STATUS_SUCCESS)
       throw Error(HGPU_ERR_CUDA, "cublasSetStream failed");
   }
+  // transform-domain AXPY: plan for |R| < 2^mbR and |x| < 2^xb, transforms
+  // of every L entry once per factorisation
+  const long long ne = (long long)n * (n - 1) / 2;
+  int xbmax = 0;
+  if (ntt) {
+    if (lhat_for_ != factor_serial_) {
+      std::vector<int> bits(std::max<long long>(ne, 1));
+      int* dbits = dalloc<int>(std::max<long long>(ne, 1));
+      CU(launch_int_bits_batch(IntBuf{lhdr_, llimbs_}, 0, 1, P.cap, (int)ne, dbits, st));
+      CU(cudaMemcpyAsync(bits.data(), dbits, ne * 4, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      dfree(dbits);
+      int mb = 1;
+      for (long long i = 0; i < ne; ++i) mb = std::max(mb, bits[i]);
+      const int xb = 32 * std::max(P.cap, solve_xlimbs_ + 16);
+      if (mb + xb != sdp_bits_) {
+        // bits of one product; choose_plan adds the column count n to the
+        // coefficient bound and keeps two spare digits
+        const Plan SP = solve_plan(n, K_, mb + xb);
+        dfree(stw_);
+        dfree(lhat_);
+        dfree(acch_);
+        dfree(sxhat_);
+        stw_ = lhat_ = acch_ = sxhat_ = nullptr;
+        DevPlan S{};
+        S.n = n;
+        S.K = K_;
+        S.k2 = k2;
+        S.np = SP.np;
+        S.logL = SP.logL;
+        S.L = SP.L;
+        S.w = SP.w;
+        S.T = SP.T;
+        S.cap = SP.cap;
+        S.ycap = SP.ycap;
+        S.NW = SP.np * SP.L;
+        const std::vector<uint32_t> tab = transform_tables(S, SP);
+        const size_t npl = (size_t)SP.np * SP.L;
+        stw_ = dalloc<uint32_t>(tab.size());
+        CU(cudaMemcpy(stw_, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+        S.tw = stw_;
+        S.twp = stw_ + npl;
+        S.itw = stw_ + 2 * npl;
+        S.itwp = stw_ + 3 * npl;
+        S.twm = stw_ + 4 * npl;
+        S.itwm = stw_ + 5 * npl;
+        S.tw_smem = 0;
+        S.grid_cap = dp_.grid_cap;
+        S.debug = dp_.debug;
+        int ok = 0;
+        CU(configure_solve_ntt(S, P.cap, Wv, Wa, &ok));
+        size_t fr = 0, tot = 0;
+        CU(cudaMemGetInfo(&fr, &tot));
+        const size_t need = ((size_t)ne + n + 2) * S.NW * 4;
+        if (!ok || need + (1ull << 30) > fr)
+          throw Error(HGPU_ERR_CAPACITY, "transform-domain solve does not fit");
+        lhat_ = dalloc<uint32_t>(std::max<size_t>((size_t)ne * S.NW, 1));
+        acch_ = dalloc<uint32_t>((size_t)n * S.NW);
+        sxhat_ = dalloc<uint32_t>(2 * (size_t)S.NW);
+        sdp_ = S;
+        sdp_bits_ = mb + xb;
+        sdp_xbits_ = xb;
+      }
+      CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, ne, lhat_, dp_.grid_cap, err_,
+                           st));
+      lhat_for_ = factor_serial_;
+    }
+    xbmax = sdp_xbits_;
+  }
   // C[t][k'] = sum_i B[t][i] T[k'][i] for `rows` targets (int8 -> int32)
   auto tc_gemm = [&](const uint8_t* B, int rows) {
     const int32_t one = 1, zero = 0;
@@ -1596,8 +1717,26 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
                            Finish{vecs, U, vecs, Z, pairs, 1, k2}, err_, st));
     ++nl;
     if (tc) CU(cudaMemsetAsync(tc_acc_, 0, (size_t)n * mc * 8, st));
+    const int SNW = sdp_.NW;
+    // one resident CTA per SM (the critical CTA's shared memory): block 0
+    // plus one pointwise CTA on every other SM
+    int nsm = 148;
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device_));
+    const int ntt_grid = std::max(1, nsm - 1);
+    if (ntt) {
+      CU(cudaMemsetAsync(acch_, 0, (size_t)n * SNW * 4, st));
+      CU(launch_solve_xhat(sdp_, vecs, Z, Wv, sxhat_, xbmax, err_, st));
+      ++nl;
+    }
     for (int p = 0; p + 1 < n; ++p) {
       const Finish f{vecs, U + p + 1, vecs, Z + p + 1, pairs, 2 * (p + 1) + 1, k2};
+      if (ntt) {
+        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_, sxhat_ + (size_t)(p & 1) * SNW,
+                            sxhat_ + (size_t)((p + 1) & 1) * SNW, acch_, p, 0, f, ntt_grid, xbmax,
+                            err_, st));
+        ++nl;
+        continue;
+      }
       if (tc) {
         CU(launch_solve_toeplitz(vecs, Z + p, Wv, kr, mc, tc_t_, err_, st));
         tc_gemm(rdig_col_ + (size_t)((long long)p * (n - 1) - (long long)p * (p - 1) / 2) * kr,
@@ -1625,8 +1764,21 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
                            err_, st));
     ++nl;
     if (tc) CU(cudaMemsetAsync(tc_acc_, 0, (size_t)n * mc * 8, st));
+    if (ntt) {
+      CU(cudaMemsetAsync(acch_, 0, (size_t)n * SNW * 4, st));
+      CU(launch_solve_xhat(sdp_, vecs, Y + n - 1, Wv, sxhat_, xbmax, err_, st));
+      ++nl;
+    }
     for (int r = n - 1; r >= 1; --r) {
       const Finish f{vecs, Wq + r - 1, vecs, Y + r - 1, vecs, 0, 0};
+      if (ntt) {
+        const int par = (n - 1 - r) & 1;
+        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_, sxhat_ + (size_t)par * SNW,
+                            sxhat_ + (size_t)(par ^ 1) * SNW, acch_, r, 1, f, ntt_grid, xbmax,
+                            err_, st));
+        ++nl;
+        continue;
+      }
       if (tc) {
         CU(launch_solve_toeplitz(vecs, Y + r, Wv, kr, mc, tc_t_, err_, st));
         tc_gemm(rdig_row_ + (size_t)((long long)r * (r - 1) / 2) * kr, r);
@@ -1657,8 +1809,11 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
     int mx[4] = {0, 0, 0, 0};
     for (int v = 0; v < 4; ++v)
       for (int i = 0; i < n; ++i) mx[v] = std::max(mx[v], std::abs(vh[(size_t)v * n + i]));
-    std::fprintf(stderr, "solve limbs: u %d z %d w %d y %d (Wv %d, R cap %d)\n", mx[0], mx[1],
-                 mx[2], mx[3], Wv, P.cap);
+    std::fprintf(stderr, "solve mode %d %.3f ms; limbs: u %d z %d w %d y %d (Wv %d, R cap %d)\n",
+                 mode,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                           t_start).count(),
+                 mx[0], mx[1], mx[2], mx[3], Wv, P.cap);
   }
   {
     int mx = 0;

@@ -93,8 +93,9 @@ class Matrix {
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
   std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
+  // mode 0: integer AXPY, 1: tensor-core AXPY, 2: transform-domain AXPY
   std::vector<HostInt> solve_impl(const std::vector<HostInt>& u, long long* launches,
-                                  bool tc);
+                                  int mode);
   int order() const { return n_; }
   const HostInt& strip_entry(int s) const { return strip_[s]; }
   // Interval mode (iv_engine.cpp): the constructor's strip holds the lower
@@ -206,6 +207,13 @@ class Matrix {
   // tensor-core solve AXPY (HGPU_SOLVE_TC): L digits (column and row order),
   // Toeplitz operand, GEMM output, 7-bit-column accumulators
   bool solve_tc_ = false;
+  // transform-domain solve AXPY (HGPU_SOLVE_NTT): solve plan, transforms of
+  // the L entries (per factorisation), accumulators, double-buffered x-hat
+  int solve_ntt_ = 1;  // 0: off, 1: with fallback to the integer AXPY, 2: strict
+  DevPlan sdp_{};
+  int sdp_bits_ = 0, sdp_xbits_ = 0;
+  uint32_t *stw_ = nullptr, *lhat_ = nullptr, *acch_ = nullptr, *sxhat_ = nullptr;
+  long long lhat_for_ = -1;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
   // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)

@@ -256,6 +256,19 @@ cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf 
                                 int xi, int j, int dir, const int32_t* C, int mc,
                                 long long* acc7, const Finish& fin, int grid_cap,
                                 int* err, cudaStream_t st);
+// transform-domain AXPY of the triangular solves (solve_kernels.cu, opt-in):
+// plan S, per-factorisation transforms of L, per-step launch
+size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa);
+cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* ok);
+cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
+                              uint32_t* rhat, int grid_cap, int* err, cudaStream_t st);
+cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint32_t* xhat,
+                              int xbmax, int* err, cudaStream_t st);
+cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
+                             const uint32_t* rhat, const uint32_t* xhat_in,
+                             uint32_t* xhat_out, uint32_t* acch, int j, int dir,
+                             const Finish& fin, int grid, int xbmax, int* err,
+                             cudaStream_t st);
 cudaError_t configure_solve_tc(int Wv, int Wa, int mc, int* ok);
 cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
                                   int count, int* out, cudaStream_t st);

@@ -12,10 +12,12 @@
 // AXPY over the remaining rows.
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "cta_ops.cuh"
 #include "ldlt_kernels.cuh"
+#include "transform_ops.cuh"
 
 namespace hgpu {
 
@@ -44,58 +46,44 @@ __device__ __forceinline__ long long lidx(int n, int p, int r) {
 // out_i = base_i - tdiv_2exp(acc_i, k2)   (single CTA; acc two's complement)
 // base/out are signed limb vectors of Wv limbs; `shift_out` > 0 additionally
 // stores out_i << shift_out into out2 (the diagonal step's numerator).
-__device__ void solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
-                             const Finish& f, uint32_t* sm, int* err) {
+// The same from |acc| (M1, Wa limbs, zero padded; Wa + 1 words of storage,
+// reused as scratch) and its sign; T: Wv + 1, X: Wv + 2 words.
+__device__ void solve_finish_mag(int Wv, int Wa, int k2, uint32_t* M1, bool neg,
+                                 const Finish& f, uint32_t* T, uint32_t* X,
+                                 uint32_t* red, int* err) {
   const IntBuf& base = f.base;
   const int bi = f.bi;
   const IntBuf& out = f.out;
   const int oi = f.oi;
   const IntBuf& out2 = f.out2;
   const int o2i = f.o2i, shift_out = f.shift_out;
-  uint32_t* M1 = sm;           // Wa + 1
-  uint32_t* T = M1 + Wa + 1;   // Wv + 1
-  uint32_t* X = T + Wv + 1;    // Wv + 2
-  uint32_t* red = X + Wv + 2;
-  // |acc| and its sign
-  const bool neg = (acc_i[Wa - 1] & 0x80000000u) != 0;
-  cta_resolve(
-      Wa, 32,
-      [&](int k) -> int64_t {
-        return neg ? -(int64_t)acc_i[k] : (int64_t)acc_i[k];
-      },
-      [&](int k, uint32_t d) { M1[k] = d; }, red);
   // t = sign * (|acc| >> k2)
   const int st = neg ? -1 : 1;
   for (int k = threadIdx.x; k <= Wv; k += blockDim.x)
     T[k] = field32(M1, Wa, 32LL * k + k2);
-  // X = base - t   (two resolves keep every digit sum in range)
+  // X = |base - t|: with base = sb |B| and t = st |T|, base - t =
+  // sb (|B| - sb st |T|), whose limb-wise digit sums stay in (-2^32, 2^33):
+  // one resolve, and a second (negated) one only when |B| < |T| under the
+  // subtraction.
   const int hb = base.hdr[bi];
   const int nb = hb < 0 ? -hb : hb;
   const int sb = hb < 0 ? -1 : 1;
+  const int sbt = sb * st;
   const uint32_t* B = base.limbs + (long long)bi * Wv;
   __syncthreads();
   const int W2 = Wv + 2;
-  cta_resolve(
-      W2, 32,
-      [&](int k) -> int64_t {
-        const int64_t bv = k < nb ? (int64_t)B[k] : 0;
-        return sb > 0 ? bv : -bv;
-      },
-      [&](int k, uint32_t d) { X[k] = d; }, red);  // two's complement base
-  cta_resolve(
-      W2, 32,
-      [&](int k) -> int64_t {
-        const int64_t tv = k <= Wv ? (int64_t)T[k] : 0;
-        return (int64_t)X[k] - (st > 0 ? tv : -tv);
-      },
-      [&](int k, uint32_t d) { M1[k] = d; }, red);
-  const bool rneg = (M1[W2 - 1] & 0x80000000u) != 0;
-  cta_resolve(
-      W2, 32,
-      [&](int k) -> int64_t {
-        return rneg ? -(int64_t)M1[k] : (int64_t)M1[k];
-      },
-      [&](int k, uint32_t d) { X[k] = d; }, red);
+  auto inner = [&](int k) -> int64_t {
+    const int64_t bv = k < nb ? (int64_t)B[k] : 0;
+    const int64_t tv = k <= Wv ? (int64_t)T[k] : 0;
+    return sbt > 0 ? bv - tv : bv + tv;
+  };
+  const bool ineg =
+      cta_resolve(W2, 32, inner, [&](int k, uint32_t d) { X[k] = d; }, red) < 0;
+  if (ineg)
+    cta_resolve(
+        W2, 32, [&](int k) -> int64_t { return -inner(k); },
+        [&](int k, uint32_t d) { X[k] = d; }, red);
+  const bool rneg = (sb < 0) != ineg;
   const int len = cta_limb_len(X, W2, red);
   if (len > Wv) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
@@ -118,6 +106,23 @@ __device__ void solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
       O2[k] = k < n2 ? field32(X, len, 32LL * k - shift_out) : 0u;
     if (threadIdx.x == 0) out2.hdr[o2i] = n2 == 0 ? 0 : (rneg ? -n2 : n2);
   }
+}
+
+__device__ void solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
+                             const Finish& f, uint32_t* sm, int* err) {
+  uint32_t* M1 = sm;           // Wa + 1
+  uint32_t* T = M1 + Wa + 1;   // Wv + 1
+  uint32_t* X = T + Wv + 1;    // Wv + 2
+  uint32_t* red = X + Wv + 2;
+  // |acc| and its sign
+  const bool neg = (acc_i[Wa - 1] & 0x80000000u) != 0;
+  cta_resolve(
+      Wa, 32,
+      [&](int k) -> int64_t {
+        return neg ? -(int64_t)acc_i[k] : (int64_t)acc_i[k];
+      },
+      [&](int k, uint32_t d) { M1[k] = d; }, red);
+  solve_finish_mag(Wv, Wa, k2, M1, neg, f, T, X, red, err);
 }
 
 __global__ void k_solve_finish(int Wv, int Wa, int k2, const uint32_t* acc_i,
@@ -205,6 +210,154 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
   const int h = v.hdr[idx];
   const int n = h < 0 ? -h : h;
   out[b] = n == 0 ? 0 : limbs_bits(v.limbs + idx * stride, n);
+}
+
+// ------------------------------------ transform-domain AXPY (opt-in) ---
+// The step's products R(t, j) x_j are pointwise in the residue-number NTT
+// domain of a solve plan S (its own primes / length / digit width, chosen
+// so that a whole column of products sums exactly: n * (L/2) * 2^(2w) <
+// Q/4 and deg R + deg x < L).  Once per factorisation every L entry is
+// transformed (Montgomery form, k_solve_rhat); per step the accumulators of
+// all targets take one pointwise multiply-add (HBM-streaming), and the
+// critical target alone is brought back to an exact integer (inverse NTT,
+// Garner, carry resolution: reconstruct_int), finished (solve_finish_mag)
+// and its new vector entry transformed for the next step.  The integer
+// result of every accumulator equals k_solve_axpy's, so the solve is bit
+// identical.
+
+// shared-memory words of the critical CTA: A NW | forward, inverse twiddles
+// NW each (staged while the pointwise update runs: from L2 they stall every
+// butterfly) | S, Dg (L+T) x 2 words each | M1 Wa + 1 | T Wv + 1 | X Wv + 2 |
+// red 64
+__host__ __device__ inline long long solve_ntt_words(const DevPlan& S, int Wv, int Wa) {
+  const long long M = S.L + S.T;
+  return 3LL * S.NW + 4 * M + (Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
+}
+constexpr int kSolveNttThreads = 1024;
+
+// every L entry (packed like L) -> its transform in Montgomery form
+__global__ void __launch_bounds__(256) k_solve_rhat(DevPlan S, int cap, IntBuf L,
+                                                    long long count, uint32_t* rhat,
+                                                    int* err) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* buf = sm;           // NW
+  uint32_t* mag = buf + S.NW;   // cap
+  for (long long e = blockIdx.x; e < count; e += gridDim.x) {
+    int len;
+    const int sign = load_int(L, e, cap, mag, &len);
+    transform_int(S, mag, len, 0, sign, buf, rhat + e * (long long)S.NW, true, S.twm, err);
+  }
+}
+
+// transform of the signed limb integer xv[xi] (stride Wv) -> xhat
+__global__ void __launch_bounds__(512) k_solve_xhat(DevPlan S, IntBuf xv, int xi, int Wv,
+                                                    uint32_t* xhat, int xbmax, int* err) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* buf = sm;
+  uint32_t* mag = buf + S.NW;
+  int len;
+  const int sign = load_int(xv, xi, Wv, mag, &len);
+  if (threadIdx.x == 0 && limbs_bits(mag, len) > xbmax)
+    atomicOr(&err[kErrCapacity], kCapDegree);
+  transform_int(S, mag, len, 0, sign, buf, xhat, false, S.twm, err);
+}
+
+// a + mont(x, r) mod q for 4 words of one prime
+__device__ __forceinline__ uint4 pw_madd(uint4 a, uint4 x, uint4 r, const PrimeConsts& c) {
+  auto f = [&](uint32_t av, uint32_t xv, uint32_t rv) {
+    const uint32_t v = av + reduce_2q(mont_mul(xv, rv, c.q, c.qneg), c.q);
+    return v >= c.q ? v - c.q : v;
+  };
+  return make_uint4(f(a.x, x.x, r.x), f(a.y, x.y, r.y), f(a.z, x.z, r.z), f(a.w, x.w, r.w));
+}
+
+// One step j (dir 0: forward, targets t > j, coefficient R_j[t]; dir 1:
+// back, targets t < j, coefficient R_t[j]).  Block 0 finishes the critical
+// target (t = j+1 resp. j-1) and writes xhat_out; blocks >= 1 stream the
+// pointwise updates of the other targets.
+template <int RM>
+__global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n, int Wv, int Wa, int k2,
+                                                   const uint32_t* __restrict__ rhat,
+                                                   const uint32_t* __restrict__ xhat_in,
+                                                   uint32_t* xhat_out, uint32_t* acch,
+                                                   int j, int dir, Finish fin, int xbmax,
+                                                   int* err) {
+  extern __shared__ uint32_t sm[];
+  const int NW = S.NW;
+  const int ntg = dir == 0 ? n - j - 1 : j;
+  auto target = [&](int kk) { return dir == 0 ? j + 1 + kk : j - 1 - kk; };
+  auto ridx = [&](int t) { return dir == 0 ? lidx(n, j, t) : lidx(n, t, j); };
+  if (blockIdx.x > 0) {
+    if (S.debug & 16384) return;  // timing aid: skip the pointwise updates
+    // pointwise: items (kk >= 1, 4-word group), grid-stride over blocks >= 1
+    const int g4 = NW / 4;
+    const long long items = (long long)(ntg - 1) * g4;
+    const long long stride = (long long)(gridDim.x - 1) * blockDim.x;
+    for (long long it = (long long)(blockIdx.x - 1) * blockDim.x + threadIdx.x; it < items;
+         it += stride) {
+      const int kk = 1 + (int)(it / g4);
+      const int q4 = (int)(it - (long long)(kk - 1) * g4);
+      const int t = target(kk);
+      const PrimeConsts& c = S.pc[(4 * q4) >> S.logL];
+      uint4* a = reinterpret_cast<uint4*>(acch + (long long)t * NW) + q4;
+      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW) + q4);
+      const uint4 x = reinterpret_cast<const uint4*>(xhat_in)[q4];
+      *a = pw_madd(*a, x, r, c);
+    }
+    return;
+  }
+  if (ntg <= 0 || (S.debug & 32768)) return;  // (timing aid: skip the critical row)
+  const int t = target(0);
+  const int M = S.L + S.T;
+  uint32_t* A = sm;
+  uint32_t* twf = A + NW;
+  uint32_t* twi = twf + NW;
+  int64_t* Ssum = reinterpret_cast<int64_t*>(twi + NW);
+  uint64_t* Dg = reinterpret_cast<uint64_t*>(Ssum + M);
+  uint32_t* M1 = reinterpret_cast<uint32_t*>(Dg + M);
+  uint32_t* T = M1 + Wa + 1;
+  uint32_t* X = T + Wv + 1;
+  uint32_t* red = X + Wv + 2;
+  for (int i = threadIdx.x; i < NW / 4; i += blockDim.x) {
+    reinterpret_cast<uint4*>(twf)[i] = reinterpret_cast<const uint4*>(S.twm)[i];
+    reinterpret_cast<uint4*>(twi)[i] = reinterpret_cast<const uint4*>(S.itwm)[i];
+  }
+  const bool stamp = (S.debug & 8192) && (j == 500 || j == 501) && threadIdx.x == 0;
+  long long c0 = stamp ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
+  unsigned long long g0 = 0;
+  if (stamp) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  {
+    const uint4* a = reinterpret_cast<const uint4*>(acch + (long long)t * NW);
+    const uint4* r = reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW);
+    const uint4* x = reinterpret_cast<const uint4*>(xhat_in);
+    for (int q4 = threadIdx.x; q4 < NW / 4; q4 += blockDim.x)
+      reinterpret_cast<uint4*>(A)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), S.pc[(4 * q4) >> S.logL]);
+  }
+  __syncthreads();
+  if (stamp) c1 = clock64();
+  int len = 0;
+  long long rs[4] = {0, 0, 0, 0};
+  const int sg = reconstruct_int<RM>(S, A, Ssum, Dg, M1, Wa, red, twi, err, &len,
+                                 stamp ? rs : nullptr);
+  if (sg == 0) return;
+  if (threadIdx.x == 0) M1[Wa] = 0u;
+  __syncthreads();
+  if (stamp) c2 = clock64();
+  solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err);
+  __syncthreads();
+  if (stamp) c3 = clock64();
+  // the finished entry, transformed for the next step
+  int xl;
+  const int xs = load_int(fin.out, fin.oi, Wv, X, &xl);
+  if (threadIdx.x == 0 && limbs_bits(X, xl) > xbmax) atomicOr(&err[kErrCapacity], kCapDegree);
+  transform_int<RM>(S, X, xl, 0, xs, A, xhat_out, false, twf, err);
+  unsigned long long g1 = 0;
+  if (stamp) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  if (stamp)
+    printf("solve_ntt j=%d dir=%d ns %llu..%llu (%llu) clk %lld: pointwise %lld reconstruct %lld (intt %lld garner %lld "
+           "digits %lld resolve+pack %lld) finish %lld transform %lld\n",
+           j, dir, g0, g1, g1 - g0, clock64() - c0, c1 - c0, c2 - c1, rs[0] - c1, rs[1] - rs[0], rs[2] - rs[1], c2 - rs[2],
+           c3 - c2, clock64() - c3);
 }
 
 // ------------------------------------------ tensor-core AXPY (opt-in) ---
@@ -420,6 +573,65 @@ cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
   if (count <= 0) return cudaSuccess;
   k_int_bits<<<(count + 127) / 128, 128, 0, st>>>(v, idx0, step, stride, count,
                                                   out);
+  return cudaGetLastError();
+}
+
+size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa) {
+  return (size_t)solve_ntt_words(S, Wv, Wa);
+}
+
+cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* ok) {
+  int dev = 0, maxopt = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t step = solve_ntt_words(S, Wv, Wa) * 4;
+  const size_t rh = ((size_t)S.NW + cap) * 4, xh = ((size_t)S.NW + Wv) * 4;
+  *ok = step <= (size_t)maxopt && rh <= (size_t)maxopt && xh <= (size_t)maxopt;
+  if (!*ok) return cudaSuccess;
+  cudaError_t e;
+  for (auto k : {k_solve_ntt<16>, k_solve_ntt<8>, k_solve_ntt<4>})
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step)) !=
+        cudaSuccess)
+      return e;
+  if ((e = cudaFuncSetAttribute(k_solve_rhat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)rh)) != cudaSuccess)
+    return e;
+  return cudaFuncSetAttribute(k_solve_xhat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)xh);
+}
+
+cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
+                              uint32_t* rhat, int grid_cap, int* err, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  k_solve_rhat<<<(int)std::min<long long>(count, grid_cap), 256,
+                 ((size_t)S.NW + cap) * 4, st>>>(S, cap, L, count, rhat, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint32_t* xhat,
+                              int xbmax, int* err, cudaStream_t st) {
+  k_solve_xhat<<<1, 512, ((size_t)S.NW + Wv) * 4, st>>>(S, xv, xi, Wv, xhat, xbmax, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
+                             const uint32_t* rhat, const uint32_t* xhat_in,
+                             uint32_t* xhat_out, uint32_t* acch, int j, int dir,
+                             const Finish& fin, int grid, int xbmax, int* err,
+                             cudaStream_t st) {
+  const int ntg = dir == 0 ? n - j - 1 : j;
+  if (ntg <= 0) return cudaSuccess;
+  const long long items = (long long)(ntg - 1) * (S.NW / 4);
+  const int pw = (int)std::min<long long>((items + kSolveNttThreads - 1) / kSolveNttThreads,
+                                          grid);
+  // widest NTT pass of the critical row's transforms (HGPU_SOLVE_RADIX)
+  static const int radix = [] {
+    const char* e = getenv("HGPU_SOLVE_RADIX");
+    return e ? atoi(e) : 8;
+  }();
+  auto kern = radix == 16 ? k_solve_ntt<16> : (radix == 4 ? k_solve_ntt<4> : k_solve_ntt<8>);
+  kern<<<1 + pw, kSolveNttThreads, solve_ntt_words(S, Wv, Wa) * 4, st>>>(
+      S, n, Wv, Wa, k2, rhat, xhat_in, xhat_out, acch, j, dir, fin, xbmax, err);
   return cudaGetLastError();
 }
 

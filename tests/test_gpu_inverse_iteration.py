@@ -130,9 +130,51 @@ def test_tensor_core_solve_bit_exact(hg, seed, n, k, monkeypatch):
     (HGPU_SOLVE_TC=1, solve_kernels.cu) gives the restatement's Rayleigh
     quotients bit for bit; the solves after the first one take that path."""
     monkeypatch.setenv("HGPU_SOLVE_TC", "1")
+    monkeypatch.setenv("HGPU_SOLVE_NTT", "0")
     strip = random_pd_hankel(seed, n, k)
     u = hg.seeded_start_vector(n, k)
     want = po.inverse_iteration_py(strip, k, u, 0, 40)
     got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
     assert got["rho"] == want
     assert got["iterations"] == len(want)
+
+
+@pytest.mark.parametrize("seed,n,k", [(117, 40, 768), (118, 70, 1024), (119, 130, 2048)])
+def test_transform_domain_solve_bit_exact(hg, seed, n, k, monkeypatch):
+    """The transform-domain AXPY of the triangular solves (HGPU_SOLVE_NTT=1,
+    k_solve_ntt): every accumulator is the same exact integer, so the
+    Rayleigh quotients equal the restatement's bit for bit."""
+    monkeypatch.setenv("HGPU_SOLVE_NTT", "2")
+    strip = random_pd_hankel(seed, n, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
+    assert got["rho"] == want
+    assert got["iterations"] == len(want)
+
+
+def test_transform_domain_solve_config2(hg, monkeypatch):
+    """Config 2 at full size through the transform-domain solve: the final
+    Rayleigh quotient and the certified 40 digits of the golden fixture."""
+    monkeypatch.setenv("HGPU_SOLVE_NTT", "2")
+    d = {e["name"]: e for e in json.load(open(os.path.join(GOLDEN, "lambda_certified.json")))}["config2"]
+    g = json.load(open(os.path.join(GOLDEN, "config2_strip.json")))
+    strip = [int(v, 16) for v in g["strip"]]
+    n, k = d["n"], d["frac_bits"]
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), hg.seeded_start_vector(n, k), 0, 40,
+                               digits=40)
+    assert po.to_hex(got["rho"][-1]) == d["rho_last"]
+    assert got["iterations"] == d["iterations"]
+    assert got["eigenvalue"] == d["lambda_40"]
+
+
+@pytest.mark.parametrize("seed,n,k", [(120, 40, 768), (121, 90, 1536)])
+def test_integer_solve_bit_exact(hg, seed, n, k, monkeypatch):
+    """The schoolbook AXPY (HGPU_SOLVE_NTT=0, k_solve_axpy), kept as the
+    fallback of the transform-domain solve, gives the same quotients."""
+    monkeypatch.setenv("HGPU_SOLVE_NTT", "0")
+    strip = random_pd_hankel(seed, n, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
+    assert got["rho"] == want
