@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../../include/hgpu.h"
@@ -121,10 +122,27 @@ extern "C" hgpu_status hgpu_inverse_iteration(
       const std::vector<HostInt> yh = mm->solve(uh, &nl);
       std::vector<Z> y(n);
       Z num, den;
-      for (long i = 0; i < n; ++i) {
-        y[i] = from_host(yh[i]);
-        num = num + y[i] * u[i];
-        den = den + y[i] * y[i];
+      {
+        // u.y and y.y: n products of ~K-bit integers each, split over host
+        // threads (GMP objects are per thread; the partial sums are exact)
+        const long nth = std::max(1L, std::min<long>(
+                                          16, std::min<long>((long)std::thread::hardware_concurrency(),
+                                                             n / 32 + 1)));
+        std::vector<Z> pn(nth), pd(nth);
+        std::vector<std::thread> pool;
+        for (long t = 0; t < nth; ++t)
+          pool.emplace_back([&, t] {
+            for (long i = t; i < n; i += nth) {
+              y[i] = from_host(yh[i]);
+              pn[t] = pn[t] + y[i] * u[i];
+              pd[t] = pd[t] + y[i] * y[i];
+            }
+          });
+        for (std::thread& th : pool) th.join();
+        for (long t = 0; t < nth; ++t) {
+          num = num + pn[t];
+          den = den + pd[t];
+        }
       }
       if (den.sgn() == 0) throw Error(HGPU_ERR_INTERNAL, "solve returned zero");
       rho = sigma + tdiv(shl(num, (unsigned long)k), den);

@@ -603,8 +603,15 @@ cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* 
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
                               uint32_t* rhat, int grid_cap, int* err, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
-  k_solve_rhat<<<(int)std::min<long long>(count, grid_cap), 256,
-                 ((size_t)S.NW + cap) * 4, st>>>(S, cap, L, count, rhat, err);
+  // every resident CTA slot (each transform is a latency-bound chain)
+  const size_t smem = ((size_t)S.NW + cap) * 4;
+  int dev = 0, nsm = 1, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_rhat, 256, smem);
+  const long long grid = std::max<long long>(grid_cap, (long long)nsm * std::max(1, per_sm));
+  k_solve_rhat<<<(int)std::min<long long>(count, grid), 256, smem, st>>>(S, cap, L, count,
+                                                                        rhat, err);
   return cudaGetLastError();
 }
 
