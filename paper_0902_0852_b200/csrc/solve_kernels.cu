@@ -634,9 +634,9 @@ cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
   // widest NTT pass of the critical row's transforms (HGPU_SOLVE_RADIX)
   static const int radix = [] {
     const char* e = getenv("HGPU_SOLVE_RADIX");
-    return e ? atoi(e) : 8;
+    return e ? atoi(e) : 16;
   }();
-  auto kern = radix == 16 ? k_solve_ntt<16> : (radix == 4 ? k_solve_ntt<4> : k_solve_ntt<8>);
+  auto kern = radix == 8 ? k_solve_ntt<8> : (radix == 4 ? k_solve_ntt<4> : k_solve_ntt<16>);
   kern<<<1 + pw, kSolveNttThreads, solve_ntt_words(S, Wv, Wa) * 4, st>>>(
       S, n, Wv, Wa, k2, rhat, xhat_in, xhat_out, acch, j, dir, fin, xbmax, err);
   return cudaGetLastError();
