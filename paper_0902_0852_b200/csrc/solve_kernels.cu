@@ -19,6 +19,8 @@
 #include "ldlt_kernels.cuh"
 #include "transform_ops.cuh"
 
+#include <cooperative_groups.h>
+
 namespace hgpu {
 
 namespace {
@@ -360,6 +362,110 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
            c3 - c2, clock64() - c3);
 }
 
+// The same step with the critical row spread over a cluster of np CTAs (one
+// prime each): every CTA updates and inverse-transforms its prime's slice
+// of the critical accumulator and stores it into CTA 0's shared memory
+// (DSMEM); CTA 0 runs Garner, the carry resolution and the finish; then
+// every CTA transforms the new entry for its prime.  Both transforms of the
+// chain run np-wide in parallel instead of np in a row.  Needs w = 32 (the
+// solve plan's digits).
+template <int RM>
+__global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
+    DevPlan S, int n, int Wv, int Wa, int k2, const uint32_t* __restrict__ rhat,
+    const uint32_t* __restrict__ xhat_in, uint32_t* xhat_out, uint32_t* acch, int j, int dir,
+    Finish fin, int xbmax, int* err) {
+  namespace cg = cooperative_groups;
+  extern __shared__ uint32_t sm[];
+  const int NW = S.NW, L = S.L, np = S.np;
+  const int ntg = dir == 0 ? n - j - 1 : j;
+  auto target = [&](int kk) { return dir == 0 ? j + 1 + kk : j - 1 - kk; };
+  auto ridx = [&](int t) { return dir == 0 ? lidx(n, j, t) : lidx(n, t, j); };
+  const int nc = np;  // CTAs of the critical cluster (cluster 0)
+  if ((int)blockIdx.x >= nc) {
+    if (S.debug & 16384) return;
+    const int g4 = NW / 4;
+    const long long items = (long long)(ntg - 1) * g4;
+    const long long stride = (long long)(gridDim.x - nc) * blockDim.x;
+    for (long long it = (long long)(blockIdx.x - nc) * blockDim.x + threadIdx.x; it < items;
+         it += stride) {
+      const int kk = 1 + (int)(it / g4);
+      const int q4 = (int)(it - (long long)(kk - 1) * g4);
+      const int t = target(kk);
+      const PrimeConsts& c = S.pc[(4 * q4) >> S.logL];
+      uint4* a = reinterpret_cast<uint4*>(acch + (long long)t * NW) + q4;
+      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW) + q4);
+      const uint4 x = reinterpret_cast<const uint4*>(xhat_in)[q4];
+      *a = pw_madd(*a, x, r, c);
+    }
+    return;
+  }
+  // every CTA of cluster 0 reaches every cluster barrier (no early return)
+  cg::cluster_group cl = cg::this_cluster();
+  const int rk = (int)blockIdx.x;  // prime handled by this CTA
+  const bool live = ntg > 0 && !(S.debug & 32768);
+  const int t = live ? target(0) : 0;
+  const int M = L + S.T;
+  uint32_t* A = sm;
+  uint32_t* twf = A + NW;
+  uint32_t* twi = twf + NW;
+  int64_t* Ssum = reinterpret_cast<int64_t*>(twi + NW);
+  uint64_t* Dg = reinterpret_cast<uint64_t*>(Ssum + M);
+  uint32_t* M1 = reinterpret_cast<uint32_t*>(Dg + M);
+  uint32_t* T = M1 + Wa + 1;
+  uint32_t* X = T + Wv + 1;
+  uint32_t* red = X + Wv + 2;
+  const PrimeConsts& c = S.pc[rk];
+  uint32_t* Ar = A + rk * L;
+  if (live) {
+    for (int i = threadIdx.x; i < L / 4; i += blockDim.x) {
+      reinterpret_cast<uint4*>(twf + rk * L)[i] = reinterpret_cast<const uint4*>(S.twm + rk * L)[i];
+      reinterpret_cast<uint4*>(twi + rk * L)[i] = reinterpret_cast<const uint4*>(S.itwm + rk * L)[i];
+    }
+    const uint4* a = reinterpret_cast<const uint4*>(acch + (long long)t * NW + rk * L);
+    const uint4* r = reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW + rk * L);
+    const uint4* x = reinterpret_cast<const uint4*>(xhat_in + rk * L);
+    for (int q4 = threadIdx.x; q4 < L / 4; q4 += blockDim.x)
+      reinterpret_cast<uint4*>(Ar)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), c);
+    __syncthreads();
+    cta_ntt_inv16<RM>(Ar, 1, S.logL, twi + rk * L, &c);
+    if (rk != 0) {
+      uint32_t* A0 = cl.map_shared_rank(A, 0) + rk * L;
+      for (int i = threadIdx.x; i < L / 4; i += blockDim.x)
+        reinterpret_cast<uint4*>(A0)[i] = reinterpret_cast<const uint4*>(Ar)[i];
+    }
+  }
+  cl.sync();
+  if (live && rk == 0) {
+    int len = 0;
+    const int sg = reconstruct_int<RM>(S, A, Ssum, Dg, M1, Wa, red, twi, err, &len, nullptr, true);
+    if (sg != 0) {
+      if (threadIdx.x == 0) M1[Wa] = 0u;
+      __syncthreads();
+      solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err);
+    }
+    __threadfence();
+  }
+  cl.sync();
+  if (live) {
+    // the finished entry (global, written by CTA 0), transformed for prime rk
+    int xl;
+    const int xs = load_int(fin.out, fin.oi, Wv, X, &xl);
+    if (threadIdx.x == 0 && rk == 0) {
+      if (limbs_bits(X, xl) > xbmax) atomicOr(&err[kErrCapacity], kCapDegree);
+      if (xl > L) atomicOr(&err[kErrCapacity], kCapDigits);
+    }
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      const uint32_t d = i < xl ? X[i] : 0u;
+      const uint32_t rr = reduce_2q(mul_shoup(d, 1u, c.one_s, c.q), c.q);
+      Ar[i] = (xs < 0 && rr) ? c.q - rr : rr;
+    }
+    __syncthreads();
+    cta_ntt_fwd16<RM>(Ar, 1, S.logL, twf + rk * L, &c);
+    for (int i = threadIdx.x; i < L / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(xhat_out + rk * L)[i] = reinterpret_cast<const uint4*>(Ar)[i];
+  }
+}
+
 // ------------------------------------------ tensor-core AXPY (opt-in) ---
 // Every step's products R(t, j) x_j (x_j the vector entry just finished)
 // share x_j, so they form one int8 GEMM on 7-bit digits (as the ratio GEMM,
@@ -589,7 +695,8 @@ cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* 
   *ok = step <= (size_t)maxopt && rh <= (size_t)maxopt && xh <= (size_t)maxopt;
   if (!*ok) return cudaSuccess;
   cudaError_t e;
-  for (auto k : {k_solve_ntt<16>, k_solve_ntt<8>, k_solve_ntt<4>})
+  for (auto k : {k_solve_ntt<16>, k_solve_ntt<8>, k_solve_ntt<4>, k_solve_ntt_cl<16>,
+                 k_solve_ntt_cl<8>, k_solve_ntt_cl<4>})
     if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step)) !=
         cudaSuccess)
       return e;
@@ -636,8 +743,34 @@ cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
     const char* e = getenv("HGPU_SOLVE_RADIX");
     return e ? atoi(e) : 16;
   }();
+  // the critical row on a cluster of np CTAs (HGPU_SOLVE_CLUSTER, 32-bit
+  // digits only)
+  static const int use_cl = [] {
+    const char* e = getenv("HGPU_SOLVE_CLUSTER");
+    return e ? atoi(e) : 1;
+  }();
+  const size_t smem = solve_ntt_words(S, Wv, Wa) * 4;
+  if (use_cl && S.w == 32 && S.np > 1) {
+    auto kc = radix == 8 ? k_solve_ntt_cl<8> : (radix == 4 ? k_solve_ntt_cl<4> : k_solve_ntt_cl<16>);
+    const int nc = S.np;
+    const int grid_pw = ((pw + nc - 1) / nc) * nc;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nc + grid_pw);
+    cfg.blockDim = dim3(kSolveNttThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kc, S, n, Wv, Wa, k2, rhat, xhat_in, xhat_out, acch, j, dir,
+                              fin, xbmax, err);
+  }
   auto kern = radix == 8 ? k_solve_ntt<8> : (radix == 4 ? k_solve_ntt<4> : k_solve_ntt<16>);
-  kern<<<1 + pw, kSolveNttThreads, solve_ntt_words(S, Wv, Wa) * 4, st>>>(
+  kern<<<1 + pw, kSolveNttThreads, smem, st>>>(
       S, n, Wv, Wa, k2, rhat, xhat_in, xhat_out, acch, j, dir, fin, xbmax, err);
   return cudaGetLastError();
 }

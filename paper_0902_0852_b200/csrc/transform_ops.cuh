@@ -80,18 +80,19 @@ __device__ inline void transform_int(const DevPlan& P, const uint32_t* mag, int 
 // Inverse transform of A (np*L residues, bit-reversed, shared memory) back
 // to the exact signed integer it represents: |value| in Lb[0, lcap) (zero
 // padded), *len_out its limb length; returns the sign (+1 / -1), or 0 after
-// flagging kCapCrt (coefficients out of the CRT range).  Scratch: S and Dg
+// flagging kCapCrt (coefficients out of the CRT range).  ntt_done: A already
+// holds the inverse transforms (computed elsewhere).  Scratch: S and Dg
 // hold L + T digit sums / digits; red is the scan scratch.  A is clobbered.
 template <int RM = 16>
 __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
                                       uint64_t* Dg, uint32_t* Lb, int lcap,
                                       uint32_t* red, const uint32_t* itwm,
                                       int* err, int* len_out,
-                                      long long* stamps = nullptr) {
+                                      long long* stamps = nullptr, bool ntt_done = false) {
   const int L = P.L, np = P.np, T = P.T, w = P.w;
   const int M = L + T;
   const uint64_t dmask = (1ull << w) - 1ull;
-  cta_ntt_inv16<RM>(A, np, P.logL, itwm, P.pc);
+  if (!ntt_done) cta_ntt_inv16<RM>(A, np, P.logL, itwm, P.pc);
   if (stamps && threadIdx.x == 0) stamps[0] = clock64();
 
   // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
