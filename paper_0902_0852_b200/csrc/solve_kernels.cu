@@ -382,6 +382,9 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   auto ridx = [&](int t) { return dir == 0 ? lidx(n, j, t) : lidx(n, t, j); };
   const int nc = np;  // CTAs of the critical cluster (cluster 0)
   if ((int)blockIdx.x >= nc) {
+    // launched early (programmatic dependent launch): wait for the previous
+    // step's grid before reading x-hat and the accumulators
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (S.debug & 16384) return;
     const int g4 = NW / 4;
     const long long items = (long long)(ntg - 1) * g4;
@@ -421,6 +424,10 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
       reinterpret_cast<uint4*>(twf + rk * L)[i] = reinterpret_cast<const uint4*>(S.twm + rk * L)[i];
       reinterpret_cast<uint4*>(twi + rk * L)[i] = reinterpret_cast<const uint4*>(S.itwm + rk * L)[i];
     }
+  }
+  // the twiddle staging above overlaps the previous step's tail
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (live) {
     const uint4* a = reinterpret_cast<const uint4*>(acch + (long long)t * NW + rk * L);
     const uint4* r = reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW + rk * L);
     const uint4* x = reinterpret_cast<const uint4*>(xhat_in + rk * L);
@@ -759,13 +766,21 @@ cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
     cfg.blockDim = dim3(kSolveNttThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = nc;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    // programmatic dependent launch (HGPU_SOLVE_PDL): the next step's CTAs
+    // are placed while this one drains and wait in griddepcontrol.wait
+    static const int pdl = [] {
+      const char* e = getenv("HGPU_SOLVE_PDL");
+      return e ? atoi(e) : 1;
+    }();
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kc, S, n, Wv, Wa, k2, rhat, xhat_in, xhat_out, acch, j, dir,
                               fin, xbmax, err);
   }
