@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   uint32_t* red = X + Wv + 2;
   const PrimeConsts& c = S.pc[rk];
   uint32_t* Ar = A + rk * L;
+  const int qs = (L + nc - 1) / nc;  // coefficients per CTA after the exchange
   if (live) {
     for (int i = threadIdx.x; i < L / 4; i += blockDim.x) {
       reinterpret_cast<uint4*>(twf + rk * L)[i] = reinterpret_cast<const uint4*>(S.twm + rk * L)[i];
@@ -435,16 +436,45 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
       reinterpret_cast<uint4*>(Ar)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), c);
     __syncthreads();
     cta_ntt_inv16<RM>(Ar, 1, S.logL, twi + rk * L, &c);
-    if (rk != 0) {
-      uint32_t* A0 = cl.map_shared_rank(A, 0) + rk * L;
-      for (int i = threadIdx.x; i < L / 4; i += blockDim.x)
-        reinterpret_cast<uint4*>(A0)[i] = reinterpret_cast<const uint4*>(Ar)[i];
+    // CTA q gets every prime of its coefficient slice [lo_q - (T-1), hi_q)
+    for (int q = 0; q < nc; ++q) {
+      if (q == rk) continue;
+      const int lo = max(0, q * qs - (S.T - 1)), hi = min(L, (q + 1) * qs);
+      uint32_t* Aq = cl.map_shared_rank(A, q) + rk * L;
+      for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) Aq[i] = Ar[i];
+    }
+  }
+  cl.sync();
+  if (live) {
+    // Garner for the slice (plus the T-1 coefficients below it), then the
+    // digit sums of positions [lo, hi) (the last CTA also [L, L+T)) into
+    // CTA 0's S
+    const int lo = rk * qs, hi = min(L, lo + qs), glo = max(0, lo - (S.T - 1));
+    const int gn = hi - glo;
+    uint32_t* Cw = reinterpret_cast<uint32_t*>(Dg);  // np planes of gn words
+    for (int i = glo + threadIdx.x; i < hi; i += blockDim.x) {
+      const unsigned __int128 v = garner_coef(S, A, L, i);
+      for (int u = 0; u < np; ++u) Cw[u * gn + (i - glo)] = (uint32_t)(v >> (32 * u));
+    }
+    __syncthreads();
+    int64_t* S0 = cl.map_shared_rank(Ssum, 0);
+    const int kend = rk == nc - 1 ? M : hi;
+    for (int k = lo + threadIdx.x; k < kend; k += blockDim.x) {
+      int64_t sk = 0;
+      for (int u = 0; u < S.T; ++u) {
+        const int i = k - u;
+        if (i < glo || i >= hi) continue;
+        const uint32_t top = Cw[(np - 1) * gn + (i - glo)];
+        const uint32_t wt = u < np ? Cw[u * gn + (i - glo)] : ((top >> 31) ? 0xFFFFFFFFu : 0u);
+        sk += u == S.T - 1 ? (int64_t)(int32_t)wt : (int64_t)wt;
+      }
+      S0[k] = sk;
     }
   }
   cl.sync();
   if (live && rk == 0) {
     int len = 0;
-    const int sg = reconstruct_int<RM>(S, A, Ssum, Dg, M1, Wa, red, twi, err, &len, nullptr, true);
+    const int sg = reconstruct_int<RM>(S, A, Ssum, Dg, M1, Wa, red, twi, err, &len, nullptr, 2);
     if (sg != 0) {
       if (threadIdx.x == 0) M1[Wa] = 0u;
       __syncthreads();

@@ -80,62 +80,75 @@ __device__ inline void transform_int(const DevPlan& P, const uint32_t* mag, int 
 // Inverse transform of A (np*L residues, bit-reversed, shared memory) back
 // to the exact signed integer it represents: |value| in Lb[0, lcap) (zero
 // padded), *len_out its limb length; returns the sign (+1 / -1), or 0 after
-// flagging kCapCrt (coefficients out of the CRT range).  ntt_done: A already
-// holds the inverse transforms (computed elsewhere).  Scratch: S and Dg
+// flagging kCapCrt (coefficients out of the CRT range).  from = 1: A already
+// holds the inverse transforms; from = 2: S already holds the digit sums
+// (both computed elsewhere, e.g. split over a cluster).  Scratch: S and Dg
 // hold L + T digit sums / digits; red is the scan scratch.  A is clobbered.
+// Garner CRT of coefficient i's np residues (planes `stride` words apart),
+// scaled by 1/L: the signed coefficient as a 128-bit two's complement value.
+__device__ __forceinline__ unsigned __int128 garner_coef(const DevPlan& P, const uint32_t* A,
+                                                         int stride, int i) {
+  const int np = P.np;
+  uint32_t a[kMaxPrimes];
+  for (int j = 0; j < np; ++j) {
+    const uint32_t q = P.pc[j].q;
+    uint32_t v = reduce_2q(A[j * stride + i], q);
+    a[j] = reduce_2q(mul_shoup(v, P.invL[j], P.invLp[j], q), q);
+  }
+  const uint32_t q0 = P.pc[0].q, q1 = P.pc[1].q;
+  const uint32_t x0 = a[0];
+  const uint32_t x0m1 = x0 >= q1 ? x0 - q1 : x0;
+  const uint32_t x1 =
+      reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
+  unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
+  if (np >= 3) {
+    const uint32_t q2 = P.pc[2].q;
+    const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
+    uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
+    u = reduce_2q(u, q2);
+    const uint32_t x2 =
+        reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
+    v += (unsigned __int128)x2 * P.q01;
+    if (np == 4) {
+      // x3 = (a3 - (x0 + x1 q0 + x2 q0 q1)) (q0 q1 q2)^-1  mod q3
+      const uint32_t q3 = P.pc[3].q;
+      const uint32_t x0m3 = x0 >= q3 ? x0 - q3 : x0;
+      const uint32_t x2m3 = x2 >= q3 ? x2 - q3 : x2;
+      uint32_t u3 = x0m3 + reduce_2q(mul_shoup(x1, P.q0m3, P.q0m3p, q3), q3);
+      u3 = reduce_2q(u3, q3);
+      u3 += reduce_2q(mul_shoup(x2m3, P.q01m3, P.q01m3p, q3), q3);
+      u3 = reduce_2q(u3, q3);
+      const uint32_t x3 =
+          reduce_2q(mul_shoup(a[3] + q3 - u3, P.g3, P.g3p, q3), q3);
+      const unsigned __int128 q012 =
+          ((unsigned __int128)P.q012hi << 64) | P.q012lo;
+      v += (unsigned __int128)x3 * q012;
+    }
+  }
+  const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
+  const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
+  if (v >= H) v -= Q;  // wraps to the two's complement of a negative value
+
+  return v;
+}
+
 template <int RM = 16>
 __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
                                       uint64_t* Dg, uint32_t* Lb, int lcap,
                                       uint32_t* red, const uint32_t* itwm,
                                       int* err, int* len_out,
-                                      long long* stamps = nullptr, bool ntt_done = false) {
+                                      long long* stamps = nullptr, int from = 0) {
   const int L = P.L, np = P.np, T = P.T, w = P.w;
   const int M = L + T;
   const uint64_t dmask = (1ull << w) - 1ull;
-  if (!ntt_done) cta_ntt_inv16<RM>(A, np, P.logL, itwm, P.pc);
-  if (stamps && threadIdx.x == 0) stamps[0] = clock64();
-
   // CRT (Garner), scaled by 1/L; signed result in np words, two's complement.
+  if (from == 0) {
+    cta_ntt_inv16<RM>(A, np, P.logL, itwm, P.pc);
+  }
+  if (stamps && threadIdx.x == 0) stamps[0] = clock64();
+  if (from <= 1)
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    uint32_t a[kMaxPrimes];
-    for (int j = 0; j < np; ++j) {
-      const uint32_t q = P.pc[j].q;
-      uint32_t v = reduce_2q(A[j * L + i], q);
-      a[j] = reduce_2q(mul_shoup(v, P.invL[j], P.invLp[j], q), q);
-    }
-    const uint32_t q0 = P.pc[0].q, q1 = P.pc[1].q;
-    const uint32_t x0 = a[0];
-    const uint32_t x0m1 = x0 >= q1 ? x0 - q1 : x0;
-    const uint32_t x1 =
-        reduce_2q(mul_shoup(a[1] + q1 - x0m1, P.g1, P.g1p, q1), q1);
-    unsigned __int128 v = (unsigned __int128)x0 + (unsigned long long)x1 * q0;
-    if (np >= 3) {
-      const uint32_t q2 = P.pc[2].q;
-      const uint32_t x0m2 = x0 >= q2 ? x0 - q2 : x0;
-      uint32_t u = x0m2 + reduce_2q(mul_shoup(x1, P.q0m2, P.q0m2p, q2), q2);
-      u = reduce_2q(u, q2);
-      const uint32_t x2 =
-          reduce_2q(mul_shoup(a[2] + q2 - u, P.g2, P.g2p, q2), q2);
-      v += (unsigned __int128)x2 * P.q01;
-      if (np == 4) {
-        // x3 = (a3 - (x0 + x1 q0 + x2 q0 q1)) (q0 q1 q2)^-1  mod q3
-        const uint32_t q3 = P.pc[3].q;
-        const uint32_t x0m3 = x0 >= q3 ? x0 - q3 : x0;
-        const uint32_t x2m3 = x2 >= q3 ? x2 - q3 : x2;
-        uint32_t u3 = x0m3 + reduce_2q(mul_shoup(x1, P.q0m3, P.q0m3p, q3), q3);
-        u3 = reduce_2q(u3, q3);
-        u3 += reduce_2q(mul_shoup(x2m3, P.q01m3, P.q01m3p, q3), q3);
-        u3 = reduce_2q(u3, q3);
-        const uint32_t x3 =
-            reduce_2q(mul_shoup(a[3] + q3 - u3, P.g3, P.g3p, q3), q3);
-        const unsigned __int128 q012 =
-            ((unsigned __int128)P.q012hi << 64) | P.q012lo;
-        v += (unsigned __int128)x3 * q012;
-      }
-    }
-    const unsigned __int128 Q = ((unsigned __int128)P.Qhi << 64) | P.Qlo;
-    const unsigned __int128 H = ((unsigned __int128)P.Hhi << 64) | P.Hlo;
-    if (v >= H) v -= Q;  // wraps to the two's complement of a negative value
+    const unsigned __int128 v = garner_coef(P, A, L, i);
     for (int t = 0; t < np; ++t) A[t * L + i] = (uint32_t)(v >> (32 * t));
   }
   __syncthreads();
@@ -146,7 +159,9 @@ __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
   // thread owns 8 consecutive positions and decodes each coefficient that
   // reaches them once (8+T-1 decodes instead of 8T).  With w = 32 the pieces
   // are the coefficient's words (sign words above the np-th).
-  if (w == 32) {
+  if (from == 2) {
+    // digit sums supplied by the caller
+  } else if (w == 32) {
     for (int k = threadIdx.x; k < M; k += blockDim.x) {
       int64_t sk = 0;
       for (int t = 0; t < T; ++t) {
