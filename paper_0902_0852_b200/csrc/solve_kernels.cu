@@ -52,7 +52,7 @@ __device__ __forceinline__ long long lidx(int n, int p, int r) {
 // reused as scratch) and its sign; T: Wv + 1, X: Wv + 2 words.
 __device__ void solve_finish_mag(int Wv, int Wa, int k2, uint32_t* M1, bool neg,
                                  const Finish& f, uint32_t* T, uint32_t* X,
-                                 uint32_t* red, int* err) {
+                                 uint32_t* red, int* err, int mlen = -1) {
   const IntBuf& base = f.base;
   const int bi = f.bi;
   const IntBuf& out = f.out;
@@ -61,7 +61,9 @@ __device__ void solve_finish_mag(int Wv, int Wa, int k2, uint32_t* M1, bool neg,
   const int o2i = f.o2i, shift_out = f.shift_out;
   // t = sign * (|acc| >> k2)
   const int st = neg ? -1 : 1;
-  for (int k = threadIdx.x; k <= Wv; k += blockDim.x)
+  // limbs of |acc| >> k2 (all Wv + 1 unless the caller knows |acc|'s length)
+  const int tlen = mlen < 0 ? Wv + 1 : min(Wv + 1, max(0, mlen - (k2 >> 5)) + 1);
+  for (int k = threadIdx.x; k < tlen; k += blockDim.x)
     T[k] = field32(M1, Wa, 32LL * k + k2);
   // X = |base - t|: with base = sb |B| and t = st |T|, base - t =
   // sb (|B| - sb st |T|), whose limb-wise digit sums stay in (-2^32, 2^33):
@@ -73,10 +75,12 @@ __device__ void solve_finish_mag(int Wv, int Wa, int k2, uint32_t* M1, bool neg,
   const int sbt = sb * st;
   const uint32_t* B = base.limbs + (long long)bi * Wv;
   __syncthreads();
-  const int W2 = Wv + 2;
+  // |base - t| < 2^(32 max(nb, tlen) + 1): two spare limbs keep the
+  // capacity check below exact
+  const int W2 = min(Wv + 2, max(nb, tlen) + 2);
   auto inner = [&](int k) -> int64_t {
     const int64_t bv = k < nb ? (int64_t)B[k] : 0;
-    const int64_t tv = k <= Wv ? (int64_t)T[k] : 0;
+    const int64_t tv = k < tlen ? (int64_t)T[k] : 0;
     return sbt > 0 ? bv - tv : bv + tv;
   };
   const bool ineg =
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
   if (threadIdx.x == 0) M1[Wa] = 0u;
   __syncthreads();
   if (stamp) c2 = clock64();
-  solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err);
+  solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err, len);
   __syncthreads();
   if (stamp) c3 = clock64();
   // the finished entry, transformed for the next step
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
     if (sg != 0) {
       if (threadIdx.x == 0) M1[Wa] = 0u;
       __syncthreads();
-      solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err);
+      solve_finish_mag(Wv, Wa, k2, M1, sg < 0 && len > 0, fin, T, X, red, err, len);
     }
     __threadfence();
   }
