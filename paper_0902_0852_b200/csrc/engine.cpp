@@ -499,10 +499,13 @@ void Matrix::release() {
                   (void*)srscr_, (void*)sdscr_, (void*)sys_})
     dfree(p);
   for (void* q : {(void*)rdig_col_, (void*)rdig_row_, (void*)tc_t_, (void*)tc_c_,
-                  (void*)tc_acc_, (void*)tc_ws_, (void*)stw_, (void*)lhat_, (void*)acch_,
+                  (void*)tc_acc_, (void*)tc_ws_, (void*)stw_, (void*)lhat_tab_, (void*)acch_,
                   (void*)sxhat_})
     dfree(q);
-  stw_ = lhat_ = acch_ = sxhat_ = nullptr;
+  for (uint32_t* c : lhat_chunks_) dfree(c);
+  lhat_chunks_.clear();
+  lhat_tab_ = nullptr;
+  stw_ = acch_ = sxhat_ = nullptr;
   sdp_bits_ = sdp_xbits_ = 0;
   lhat_for_ = -1;
   rdig_col_ = rdig_row_ = tc_t_ = tc_ws_ = nullptr;
@@ -1611,10 +1614,13 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         // coefficient bound and keeps two spare digits
         const Plan SP = solve_plan(n, K_, mb + xb);
         dfree(stw_);
-        dfree(lhat_);
+        dfree(lhat_tab_);
+        for (uint32_t* c : lhat_chunks_) dfree(c);
+        lhat_chunks_.clear();
         dfree(acch_);
         dfree(sxhat_);
-        stw_ = lhat_ = acch_ = sxhat_ = nullptr;
+        stw_ = acch_ = sxhat_ = nullptr;
+        lhat_tab_ = nullptr;
         DevPlan S{};
         S.n = n;
         S.K = K_;
@@ -1647,14 +1653,25 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         const size_t need = ((size_t)ne + n + 2) * S.NW * 4;
         if (!ok || need + (1ull << 30) > fr)
           throw Error(HGPU_ERR_CAPACITY, "transform-domain solve does not fit");
-        lhat_ = dalloc<uint32_t>(std::max<size_t>((size_t)ne * S.NW, 1));
+        // chunks of <= 256 MB: a warm pool serves them from the blocks the
+        // factorisation's slot sets returned (one 16 GB block would map
+        // fresh memory, ~0.5 s)
+        lhat_shift_ = 0;
+        while ((2ull << lhat_shift_) * S.NW * 4 <= (256ull << 20)) ++lhat_shift_;
+        const long long per = 1LL << lhat_shift_;
+        const long long nch = (std::max<long long>(ne, 1) + per - 1) / per;
+        for (long long c = 0; c < nch; ++c)
+          lhat_chunks_.push_back(dalloc<uint32_t>((size_t)per * S.NW));
+        lhat_tab_ = dalloc<uint32_t*>(nch);
+        CU(cudaMemcpy(lhat_tab_, lhat_chunks_.data(), nch * sizeof(uint32_t*),
+                      cudaMemcpyHostToDevice));
         acch_ = dalloc<uint32_t>((size_t)n * S.NW);
         sxhat_ = dalloc<uint32_t>(2 * (size_t)S.NW);
         sdp_ = S;
         sdp_bits_ = mb + xb;
         sdp_xbits_ = xb;
       }
-      CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, ne, lhat_, dp_.grid_cap, err_,
+      CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, ne, lhat_store(), dp_.grid_cap, err_,
                            st));
       lhat_for_ = factor_serial_;
     }
@@ -1731,7 +1748,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
     for (int p = 0; p + 1 < n; ++p) {
       const Finish f{vecs, U + p + 1, vecs, Z + p + 1, pairs, 2 * (p + 1) + 1, k2};
       if (ntt) {
-        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_, sxhat_ + (size_t)(p & 1) * SNW,
+        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_store(), sxhat_ + (size_t)(p & 1) * SNW,
                             sxhat_ + (size_t)((p + 1) & 1) * SNW, acch_, p, 0, f, ntt_grid, xbmax,
                             err_, st));
         ++nl;
@@ -1773,7 +1790,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
       const Finish f{vecs, Wq + r - 1, vecs, Y + r - 1, vecs, 0, 0};
       if (ntt) {
         const int par = (n - 1 - r) & 1;
-        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_, sxhat_ + (size_t)par * SNW,
+        CU(launch_solve_ntt(sdp_, n, Wv, Wa, k2, lhat_store(), sxhat_ + (size_t)par * SNW,
                             sxhat_ + (size_t)(par ^ 1) * SNW, acch_, r, 1, f, ntt_grid, xbmax,
                             err_, st));
         ++nl;

@@ -212,7 +212,11 @@ class Matrix {
   int solve_ntt_ = 1;  // 0: off, 1: with fallback to the integer AXPY, 2: strict
   DevPlan sdp_{};
   int sdp_bits_ = 0, sdp_xbits_ = 0;
-  uint32_t *stw_ = nullptr, *lhat_ = nullptr, *acch_ = nullptr, *sxhat_ = nullptr;
+  uint32_t *stw_ = nullptr, *acch_ = nullptr, *sxhat_ = nullptr;
+  std::vector<uint32_t*> lhat_chunks_;  // L-entry transforms, 2^lhat_shift_ per chunk
+  uint32_t** lhat_tab_ = nullptr;       // device copy of the chunk pointers
+  int lhat_shift_ = 0;
+  EntryStore lhat_store() const { return EntryStore{lhat_tab_, lhat_shift_, (long long)sdp_.NW}; }
   long long lhat_for_ = -1;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)

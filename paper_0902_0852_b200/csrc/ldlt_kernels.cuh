@@ -80,6 +80,17 @@ struct DevPlan {
   long long bat_ybuf, bat_scr;
 };
 
+// Fixed-size records (nw words each) kept in chunks of 2^shift records, so
+// a multi-GB store is assembled from pool blocks of a few hundred MB.
+struct EntryStore {
+  uint32_t* const* chunk;
+  int shift;
+  long long nw;
+  __device__ __forceinline__ uint32_t* at(long long e) const {
+    return chunk[e >> shift] + (e & ((1LL << shift) - 1)) * nw;
+  }
+};
+
 struct IntBuf {  // count integers, each hdr (sign*len) + cap limbs
   int* hdr;
   uint32_t* limbs;
@@ -261,11 +272,11 @@ cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf 
 size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa);
 cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* ok);
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
-                              uint32_t* rhat, int grid_cap, int* err, cudaStream_t st);
+                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st);
 cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint32_t* xhat,
                               int xbmax, int* err, cudaStream_t st);
 cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
-                             const uint32_t* rhat, const uint32_t* xhat_in,
+                             EntryStore rhat, const uint32_t* xhat_in,
                              uint32_t* xhat_out, uint32_t* acch, int j, int dir,
                              const Finish& fin, int grid, int xbmax, int* err,
                              cudaStream_t st);

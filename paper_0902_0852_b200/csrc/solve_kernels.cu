@@ -243,7 +243,7 @@ constexpr int kSolveNttThreads = 1024;
 
 // every L entry (packed like L) -> its transform in Montgomery form
 __global__ void __launch_bounds__(256) k_solve_rhat(DevPlan S, int cap, IntBuf L,
-                                                    long long count, uint32_t* rhat,
+                                                    long long count, EntryStore rhat,
                                                     int* err) {
   extern __shared__ uint32_t sm[];
   uint32_t* buf = sm;           // NW
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(256) k_solve_rhat(DevPlan S, int cap, IntBuf L
   for (long long e = blockIdx.x; e < count; e += gridDim.x) {
     int len;
     const int sign = load_int(L, e, cap, mag, &len);
-    transform_int(S, mag, len, 0, sign, buf, rhat + e * (long long)S.NW, true, S.twm, err);
+    transform_int(S, mag, len, 0, sign, buf, rhat.at(e), true, S.twm, err);
   }
 }
 
@@ -283,7 +283,7 @@ __device__ __forceinline__ uint4 pw_madd(uint4 a, uint4 x, uint4 r, const PrimeC
 // pointwise updates of the other targets.
 template <int RM>
 __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n, int Wv, int Wa, int k2,
-                                                   const uint32_t* __restrict__ rhat,
+                                                   EntryStore rhat,
                                                    const uint32_t* __restrict__ xhat_in,
                                                    uint32_t* xhat_out, uint32_t* acch,
                                                    int j, int dir, Finish fin, int xbmax,
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
       const int t = target(kk);
       const PrimeConsts& c = S.pc[(4 * q4) >> S.logL];
       uint4* a = reinterpret_cast<uint4*>(acch + (long long)t * NW) + q4;
-      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW) + q4);
+      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat.at(ridx(t))) + q4);
       const uint4 x = reinterpret_cast<const uint4*>(xhat_in)[q4];
       *a = pw_madd(*a, x, r, c);
     }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
   if (stamp) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
   {
     const uint4* a = reinterpret_cast<const uint4*>(acch + (long long)t * NW);
-    const uint4* r = reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW);
+    const uint4* r = reinterpret_cast<const uint4*>(rhat.at(ridx(t)));
     const uint4* x = reinterpret_cast<const uint4*>(xhat_in);
     for (int q4 = threadIdx.x; q4 < NW / 4; q4 += blockDim.x)
       reinterpret_cast<uint4*>(A)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), S.pc[(4 * q4) >> S.logL]);
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
 // solve plan's digits).
 template <int RM>
 __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
-    DevPlan S, int n, int Wv, int Wa, int k2, const uint32_t* __restrict__ rhat,
+    DevPlan S, int n, int Wv, int Wa, int k2, EntryStore rhat,
     const uint32_t* __restrict__ xhat_in, uint32_t* xhat_out, uint32_t* acch, int j, int dir,
     Finish fin, int xbmax, int* err) {
   namespace cg = cooperative_groups;
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
       const int t = target(kk);
       const PrimeConsts& c = S.pc[(4 * q4) >> S.logL];
       uint4* a = reinterpret_cast<uint4*>(acch + (long long)t * NW) + q4;
-      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW) + q4);
+      const uint4 r = __ldcs(reinterpret_cast<const uint4*>(rhat.at(ridx(t))) + q4);
       const uint4 x = reinterpret_cast<const uint4*>(xhat_in)[q4];
       *a = pw_madd(*a, x, r, c);
     }
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (live) {
     const uint4* a = reinterpret_cast<const uint4*>(acch + (long long)t * NW + rk * L);
-    const uint4* r = reinterpret_cast<const uint4*>(rhat + ridx(t) * (long long)NW + rk * L);
+    const uint4* r = reinterpret_cast<const uint4*>(rhat.at(ridx(t)) + rk * L);
     const uint4* x = reinterpret_cast<const uint4*>(xhat_in + rk * L);
     for (int q4 = threadIdx.x; q4 < L / 4; q4 += blockDim.x)
       reinterpret_cast<uint4*>(Ar)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), c);
@@ -749,7 +749,7 @@ cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* 
 }
 
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
-                              uint32_t* rhat, int grid_cap, int* err, cudaStream_t st) {
+                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;
   // every resident CTA slot (each transform is a latency-bound chain)
   const size_t smem = ((size_t)S.NW + cap) * 4;
@@ -770,7 +770,7 @@ cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint3
 }
 
 cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,
-                             const uint32_t* rhat, const uint32_t* xhat_in,
+                             EntryStore rhat, const uint32_t* xhat_in,
                              uint32_t* xhat_out, uint32_t* acch, int j, int dir,
                              const Finish& fin, int grid, int xbmax, int* err,
                              cudaStream_t st) {
