@@ -771,6 +771,7 @@ void Matrix::panel_broadcast(int owner, int p0, int ns, long long row0,
 }
 
 void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
+  const auto t_run0 = std::chrono::steady_clock::now();
   const Plan& P = plan_;
   const DevPlan& D = dp_;
   cudaStream_t st = stream_;       // trailing updates (bulk)
@@ -1395,10 +1396,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
 
   int herr[kErrWords];
   CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  const auto t_enq = std::chrono::steady_clock::now();
   CU(cudaStreamSynchronize(st));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, ev0_, ev1_));
   res.device_ms = ms;
+  if (std::getenv("HGPU_HOST_TRACE"))
+    std::fprintf(stderr, "factor: host enqueue %.3f ms, device %.3f ms, wall %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t_enq - t_run0).count(), ms,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                           t_run0).count());
   if (tl_path) {
     if (FILE* f = std::fopen(tl_path, "a")) {
       std::fprintf(f, "# factorisation n=%d K=%d device_ms=%.3f\n", n, K_, ms);
@@ -1904,7 +1911,17 @@ FactorResult Matrix::factor(const HostInt& x, unsigned flags) {
   // the PD bound); every rank sees the same flags, so all escalate together
   int min_logL = 0;
   for (int attempt = 0; attempt < 4; ++attempt) {
-    if (!W_ || (min_logL && plan_.logL < min_logL)) build(min_logL);
+    if (!W_ || (min_logL && plan_.logL < min_logL)) {
+      const auto tb = std::chrono::steady_clock::now();
+      build(min_logL);
+      if (std::getenv("HGPU_HOST_TRACE")) {
+        CU(cudaDeviceSynchronize());
+        std::fprintf(stderr, "build: %.3f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               tb)
+                         .count());
+      }
+    }
     try {
       res = FactorResult{};
       res.n = n_;
