@@ -184,6 +184,19 @@ void dev_free(void* p) {
   cudaFreeAsync(p, 0);
 }
 
+// Device memory dalloc can still hand out: free memory plus the blocks the
+// stream-ordered pool keeps after frees (the release threshold is infinite).
+size_t device_available(int device) {
+  size_t fr = 0, tot = 0;
+  CU(cudaMemGetInfo(&fr, &tot));
+  cudaMemPool_t pool;
+  uint64_t resv = 0, used = 0;
+  CU(cudaDeviceGetDefaultMemPool(&pool, device));
+  CU(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &resv));
+  CU(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return fr + (resv > used ? (size_t)(resv - used) : 0);
+}
+
 int block_owner(long block, int world) {
   // reflected round-robin, assignment.hpp:15-23, over column blocks
   const long r = block % (2L * world);
@@ -662,8 +675,7 @@ void Matrix::build(int min_logL) {
     const int nblocks = (n_ + kb - 1) / kb;
     nsets = edf_h_ > 0 ? (size_t)nblocks + 1 : 2 + (size_t)std::max(0, defer_);
     const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
-    size_t free_b = 0, total_b = 0;
-    CU(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = device_available(device_);
     while (nsets > 2 && per_set * nsets > 0.6 * (double)free_b) --nsets;
   }
   nsets_ = (int)nsets;
@@ -1655,8 +1667,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         S.debug = dp_.debug;
         int ok = 0;
         CU(configure_solve_ntt(S, P.cap, Wv, Wa, &ok));
-        size_t fr = 0, tot = 0;
-        CU(cudaMemGetInfo(&fr, &tot));
+        const size_t fr = device_available(device_);
         const size_t need = ((size_t)ne + n + 2) * S.NW * 4;
         if (!ok || need + (1ull << 30) > fr)
           throw Error(HGPU_ERR_CAPACITY, "transform-domain solve does not fit");
