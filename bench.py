@@ -187,6 +187,12 @@ def run_gpu(args) -> None:
     ms_per_step = total_ms / args.steps
     value = mp_macs(n) / (ms_per_step * 1e-3)
 
+    # parity of the benched workload: one more factorisation of the same
+    # matrix at the same shift, its leading block (pivots and every ratio
+    # R_p[r], p < r < n') against the reference's ldlt_det_serial on that
+    # block (tests/golden/leading_blocks.json, generated by oracle/_ref)
+    parity = leading_block_parity(m, x, hgpu)
+
     # end to end through the public API with host buffers: strip upload,
     # transform plan, factorisation, pivots back to the host -- every step
     e2e_ms, h2d, d2h = [], 0, 0
@@ -270,6 +276,7 @@ def run_gpu(args) -> None:
         "imad_probe": probe,
         "clocks": clk,
     }
+    out["parity"] = parity
     if lam:
         out["time_to_lambda_min"] = lam
     traffic = _profiled_traffic()
@@ -285,6 +292,28 @@ def run_gpu(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def leading_block_parity(m, x, hgpu) -> dict:
+    """Leading n' x n' block of this workload's factorisation against the
+    reference's digests (made by tests/golden/make_leading_blocks.py)."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", "leading_blocks.json")
+    want = next((c for c in json.load(open(path))
+                 if c["name"] == "config3" and c["shift"] == "x1"), None)
+    if want is None:
+        return {"checked": False, "why": "no config3/x1 fixture"}
+    nb = want["n_prime"]
+    r = m.ldlt(x, capture_rows=nb, ratio_digest=True)
+    h = hashlib.sha256()
+    for v in r.pivots[:nb]:
+        h.update(hgpu._hex(v).encode() + b"\n")
+    ok_p = h.hexdigest() == want["pivots_sha256"]
+    ok_r = r.ratio_sha256 == want["ratios_sha256"]
+    return {"checked": True, "bit_exact": ok_p and ok_r, "pivots": ok_p, "ratios": ok_r,
+            "block": nb, "n_ratios": want["n_ratios"],
+            "against": "reference ldlt_det_serial + LdltCapture on the leading block "
+                       "(oracle/_ref, tests/golden/leading_blocks.json)"}
 
 
 def _profiled_traffic():

@@ -72,6 +72,14 @@ hgpu_status hgpu_nccl_unique_id(unsigned char out[128]);
 hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
                                  const unsigned char nccl_id[128]);
 
+/* HGPU_CAPTURE keeps only the leading rows x rows block of the ratio
+ * columns (stages p < rows, rows r < rows; 0 = all, the default).  The
+ * leading block of the submatrix-order LDL^T is the factorisation of the
+ * leading block (ldlt.cpp:65-71 touches indices < rows only there), so a
+ * full-size run can be checked against the reference on a leading block
+ * without copying every ratio to the host. */
+hgpu_status hgpu_matrix_set_capture_rows(hgpu_matrix* m, long rows);
+
 /* det(M - xI) by square-root-free LDL^T (ldlt_det_serial / _parallel).
  * x must carry the matrix's frac_bits.  On HGPU_ERR_ZERO_PIVOT the pivot
  * index is available from hgpu_last_zero_pivot(). */

@@ -337,6 +337,19 @@ class RefLib(_TextLib):
             raise RuntimeError(text)
         return int(text)
 
+    def det_sign_parallel_decimal(self, strip: list[int], k: int, decimal: str, workers: int) -> dict:
+        """Sign and bit length of det(M - xI) through ldlt_det_parallel."""
+        text = self._call("oref_det_sign_parallel_decimal",
+                          [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_long],
+                          make_dump(strip, k).encode(), decimal.encode(), workers)
+        if text.startswith("error"):
+            raise RuntimeError(text)
+        out = {}
+        for line in text.splitlines():
+            key, val = line.split()
+            out[key] = float(val) if key == "seconds" else int(val)
+        return out
+
     def interval_sign_decimal(self, n: int, beta_num: int, beta_den: int, kv: int, decimal: str) -> int:
         text = self._call("oref_interval_sign_decimal",
                           [ctypes.c_long, ctypes.c_ulong, ctypes.c_ulong, ctypes.c_long, ctypes.c_char_p],

@@ -135,6 +135,24 @@ char* oref_det_sign_decimal(const char* dump, const char* decimal) {
   });
 }
 
+// Same sign through the reference's multi-worker path (ldlt.cpp:315-341,
+// SharedMemoryChannel): the only practical CPU route at configs 4/5.
+// Output: "sign <s>\nbits <log2|det|>\nseconds <wall>".
+char* oref_det_sign_parallel_decimal(const char* dump, const char* decimal,
+                                     long workers) {
+  return guarded([&] {
+    HankelMatrix m = load(dump);
+    FixedPoint x = decimal_to_fixed_floor(decimal, m.frac_bits());
+    SharedMemoryChannel ch;
+    ParallelDetResult r = ldlt_det_parallel(m, x, workers, ch);
+    std::ostringstream os;
+    os << "sign " << r.determinant.sign() << "\n"
+       << "bits " << mpz_sizeinbase(r.determinant.mantissa().get_mpz_t(), 2) << "\n"
+       << "seconds " << r.timing.total_seconds << "\n";
+    return os.str();
+  });
+}
+
 // Interval-certified sign of det(M - aI) for a decimal probe a at kv bits
 // (hankel_matrix.cpp:33-50, decimal.cpp decimal_to_interval,
 // ldlt.cpp:79-152).  "1", "-1", "0" (straddles) or a ZeroPivot error.

@@ -167,6 +167,13 @@ hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
   });
 }
 
+hgpu_status hgpu_matrix_set_capture_rows(hgpu_matrix* m, long rows) {
+  return guarded([&] {
+    if (!m || rows < 0) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad argument");
+    m->impl->set_capture_rows((int)std::min<long>(rows, 1L << 30));
+  });
+}
+
 hgpu_status hgpu_ldlt_factor(hgpu_matrix* m, int32_t x_size,
                              const uint32_t* x_limbs, long x_frac_bits,
                              unsigned flags, hgpu_factor** out) {
@@ -199,7 +206,7 @@ hgpu_status hgpu_factor_ratio(const hgpu_factor* f, long p, long r,
       throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
     if (!f->res.have_ratios)
       throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "ratios not captured");
-    if (p < 0 || p >= (long)f->res.ratios.size() || r <= p || r >= f->res.n)
+    if (p < 0 || p >= (long)f->res.ratios.size() || r <= p || r >= f->res.capture_rows)
       throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad ratio index");
     const hgpu::HostInt& h = f->res.ratios[p][r - p - 1];
     *size = h.size;

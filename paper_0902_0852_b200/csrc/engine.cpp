@@ -822,9 +822,12 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     llimbs_ = dalloc<uint32_t>(std::max<size_t>(nl, 1) * P.cap);
   }
   const bool profile = flags & HGPU_PROFILE;
+  // capture limit (hgpu_matrix_set_capture_rows): stages and rows < crow
+  const int crow = capture_rows_ > 0 ? std::min(n, capture_rows_) : n;
   if (capture) {
-    res.ratios.assign(n > 0 ? n - 1 : 0, {});
+    res.ratios.assign(crow > 0 ? crow - 1 : 0, {});
     res.have_ratios = true;
+    res.capture_rows = crow;
   }
   std::vector<int> hr_hdr;
   std::vector<uint32_t> hr_limbs;
@@ -1345,7 +1348,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaEventRecord(panel_done[b], sp));
     if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, row0set, sp);
     if (capture) {
-      const int nsr = std::min(ns, n - 1 - p0);
+      const int nsr = std::min(ns, crow - 1 - p0);
       if (nsr > 0) {
         hr_hdr.resize((size_t)nsr * n);
         hr_limbs.resize((size_t)nsr * n * P.cap);
@@ -1357,8 +1360,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         for (int s = 0; s < nsr; ++s) {
           const int p = p0 + s;
           auto& colv = res.ratios[p];
-          colv.resize(n - p - 1);
-          for (int r = p + 1; r < n; ++r) {
+          colv.resize(crow - p - 1);
+          for (int r = p + 1; r < crow; ++r) {
             const size_t idx = (size_t)s * n + r;
             HostInt& h = colv[r - p - 1];
             h.size = hr_hdr[idx];

@@ -54,6 +54,7 @@ struct FactorResult {
   std::vector<std::vector<HostInt>> ratios;  // [p][r-p-1], if captured
   HostInt det;
   bool have_det = false, have_ratios = false;
+  int capture_rows = 0;  // ratios captured for stages and rows < capture_rows
   double device_ms = 0;
   long update_launches = 0;
   double update_ms = 0, update_products = 0;
@@ -89,6 +90,8 @@ class Matrix {
     return plan_;
   }
   int frac_bits() const { return K_; }
+  // HGPU_CAPTURE keeps only the leading rows x rows block (0: all)
+  void set_capture_rows(int rows) { capture_rows_ = rows; }
   int chain_sms() const { return chain_sms_; }
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
@@ -127,6 +130,7 @@ class Matrix {
                     FactorResult& res);
 
   int n_, K_, device_;
+  int capture_rows_ = 0;
   std::vector<HostInt> strip_;
   int strip_bits_ = 0;
   Plan plan_;

@@ -16,6 +16,7 @@ built library, or factoring without a CUDA device, raises.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import os
 from dataclasses import dataclass, field
 
@@ -45,7 +46,7 @@ EXPORTS = (
     "hgpu_smallest_eigenvalue", "hgpu_string_free", "hgpu_inverse_iteration",
     "hgpu_interval_matrix_new", "hgpu_ldlt_interval", "hgpu_factor_pivot_hi",
     "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
-    "hgpu_build_moments", "hgpu_buffer_free",
+    "hgpu_build_moments", "hgpu_buffer_free", "hgpu_matrix_set_capture_rows",
 )
 
 
@@ -91,6 +92,7 @@ def load() -> ctypes.CDLL:
     lib.hgpu_matrix_free.argtypes = [vp]
     lib.hgpu_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.hgpu_matrix_set_comm.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
+    lib.hgpu_matrix_set_capture_rows.argtypes = [vp, i64]
     lib.hgpu_ldlt_factor.argtypes = [vp, i32, u32p, i64, ctypes.c_uint, ctypes.POINTER(vp)]
     lib.hgpu_factor_order.argtypes = [vp]
     lib.hgpu_factor_order.restype = i64
@@ -206,6 +208,21 @@ class LdltResult:
     update_ms: float = 0.0
     update_products: float = 0.0
     launches: int = 0
+    ratio_sha256: str | None = None
+
+
+def _hex(v: int) -> str:
+    return ("-" + format(-v, "x")) if v < 0 else format(v, "x")
+
+
+def ratio_digest(ratios) -> str:
+    """sha256 over the ratios R_p[r] in (p, r) order, one lowercase hex
+    line each (a leading '-' for negatives): the digest
+    ``ldlt(..., ratio_digest=True)`` computes."""
+    h = hashlib.sha256()
+    for v in ratios:
+        h.update(_hex(v).encode() + b"\n")
+    return h.hexdigest()
 
 
 class HankelMatrixGPU:
@@ -250,9 +267,18 @@ class HankelMatrixGPU:
                 "cap_limbs": d.value, "workspace_bytes": wb.value}
 
     def ldlt(self, x: int, capture: bool = False, fold: bool = False, profile: bool = False,
-             x_frac_bits: int | None = None) -> LdltResult:
-        """det(M - xI) via square-root-free LDL^T (ldlt_det_serial)."""
+             x_frac_bits: int | None = None, capture_rows: int = 0,
+             ratio_digest: bool = False) -> LdltResult:
+        """det(M - xI) via square-root-free LDL^T (ldlt_det_serial).
+
+        capture_rows > 0 keeps only the leading capture_rows block of the
+        ratio columns; ratio_digest=True streams them into
+        ``LdltResult.ratio_sha256`` (see :func:`ratio_digest`) instead of the
+        ``ratios`` dict (a full-size capture is ~10^6 big integers)."""
         lib = load()
+        if capture or ratio_digest:
+            _check(lib.hgpu_matrix_set_capture_rows(self._h, capture_rows))
+            capture = True
         xs, xl = int_to_limbs(x)
         flags = (HGPU_CAPTURE if capture else 0) | (HGPU_FOLD if fold else 0) | \
                 (HGPU_PROFILE if profile else 0)
@@ -272,10 +298,18 @@ class HankelMatrixGPU:
                              device_ms=lib.hgpu_factor_device_ms(f),
                              launches=int(lib.hgpu_factor_launches(f)))
             if capture:
-                for p in range(n - 1):
-                    for r in range(p + 1, n):
+                nc = min(n, capture_rows) if capture_rows > 0 else n
+                h = hashlib.sha256() if ratio_digest else None
+                for p in range(nc - 1):
+                    for r in range(p + 1, nc):
                         _check(lib.hgpu_factor_ratio(f, p, r, ctypes.byref(size), ctypes.byref(ptr)))
-                        res.ratios[(p, r)] = limbs_to_int(size.value, ptr)
+                        v = limbs_to_int(size.value, ptr)
+                        if h is None:
+                            res.ratios[(p, r)] = v
+                        else:
+                            h.update(_hex(v).encode() + b"\n")
+                if h is not None:
+                    res.ratio_sha256 = h.hexdigest()
             if fold:
                 _check(lib.hgpu_factor_det(f, ctypes.byref(size), ctypes.byref(ptr)))
                 res.det = limbs_to_int(size.value, ptr)
