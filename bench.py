@@ -406,6 +406,20 @@ def run_reference(args) -> None:
     print(json.dumps(out), flush=True)
 
 
+def _spawn_ranks(n: int) -> None:
+    """--gpus N without a launcher: run this script under torch.distributed.run
+    with N ranks on this node (one process per GPU, NCCL) and exit with its
+    status; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -416,6 +430,11 @@ def main():
     ap.add_argument("--no-lambda", action="store_true",
                     help="skip the time-to-lambda_min measurement")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        _spawn_ranks(args.gpus)
+    if world and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

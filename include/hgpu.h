@@ -72,6 +72,22 @@ hgpu_status hgpu_nccl_unique_id(unsigned char out[128]);
 hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
                                  const unsigned char nccl_id[128]);
 
+/* Multi-GPU in one process (the reference's worker threads, ldlt.cpp:315-341,
+ * with workers -> ranks): `world` column-block-cyclic ranks on
+ * devices[0..world-1], driven by host threads of the calling process.  A
+ * device may repeat (several ranks on one GPU: the multi-rank schedule on a
+ * single device).  The panel owner publishes each finished panel with a CUDA
+ * event; every other rank reads the panel's integers directly from the
+ * owner's memory (NVLink peer loads between GPUs) into its own transforms.
+ * The handle is rank 0: hgpu_ldlt_factor, the eigenvalue drivers and the
+ * accessors use it as a single matrix (bit-identical to world 1). */
+hgpu_status hgpu_matrix_new_group(long n, long frac_bits,
+                                  const int32_t* strip_sizes,
+                                  const uint32_t* strip_limbs, const int* devices,
+                                  int world, hgpu_matrix** out);
+/* Ranks behind the handle (1 unless grouped or joined by set_comm). */
+int hgpu_matrix_world(const hgpu_matrix* m);
+
 /* HGPU_CAPTURE keeps only the leading rows x rows block of the ratio
  * columns (stages p < rows, rows r < rows; 0 = all, the default).  The
  * leading block of the submatrix-order LDL^T is the factorisation of the
@@ -104,6 +120,10 @@ hgpu_status hgpu_factor_det(const hgpu_factor* f, int32_t* size,
 double hgpu_factor_device_ms(const hgpu_factor* f);
 hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
                                      double* ms, double* products);
+/* Multi-rank runs: device time the receiving ranks spent waiting for and
+ * pulling published panels, summed over ranks (the reference's {net},
+ * timing.hpp:7-39).  0 on one rank. */
+double hgpu_factor_net_ms(const hgpu_factor* f);
 /* Number of device kernels the factorisation launched. */
 long long hgpu_factor_launches(const hgpu_factor* f);
 void hgpu_factor_free(hgpu_factor* f);
@@ -172,6 +192,15 @@ hgpu_status hgpu_verify_eigenvalue(hgpu_matrix* m, const char* x_decimal,
                                    int digits, int* status, int* lower_sign,
                                    int* upper_sign, char** probe_low,
                                    char** probe_high);
+
+/* The same, also reporting VerifyOutcome::lower_exact_zero (verify.cpp:26-27):
+ * 1 when the folded det(M - aI) interval is exactly [0, 0], i.e. the probe a
+ * is itself an eigenvalue and bracketing cannot decide at any precision
+ * (driver.cpp:161-170 stops with a diagnosis instead of escalating). */
+hgpu_status hgpu_verify_eigenvalue_ex(hgpu_matrix* m, const char* x_decimal,
+                                      int digits, int* status, int* lower_sign,
+                                      int* upper_sign, int* lower_exact_zero,
+                                      char** probe_low, char** probe_high);
 
 /* Smallest eigenvalue by inverse iteration with Rayleigh-quotient shifts
  * (the north-star's lambda_min step; no reference counterpart -- SURVEY §0

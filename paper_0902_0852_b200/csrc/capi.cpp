@@ -8,6 +8,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/hgpu.h"
 #include "engine.h"
@@ -86,6 +87,25 @@ hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,
     *out = m.release();
   });
 }
+
+hgpu_status hgpu_matrix_new_group(long n, long frac_bits,
+                                  const int32_t* strip_sizes,
+                                  const uint32_t* strip_limbs, const int* devices,
+                                  int world, hgpu_matrix** out) {
+  return guarded([&] {
+    if (!out || !strip_sizes || !devices || world < 1 || world > 64)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad argument");
+    if (n < 1 || n > 100000)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "order out of range");
+    auto m = std::make_unique<hgpu_matrix>();
+    m->impl = std::make_unique<hgpu::Matrix>((int)n, (int)frac_bits, strip_sizes,
+                                             strip_limbs, devices[0]);
+    m->impl->make_group(std::vector<int>(devices, devices + world));
+    *out = m.release();
+  });
+}
+
+int hgpu_matrix_world(const hgpu_matrix* m) { return m ? m->impl->world() : 0; }
 
 void hgpu_matrix_free(hgpu_matrix* m) { delete m; }
 
@@ -239,6 +259,8 @@ hgpu_status hgpu_factor_update_stats(const hgpu_factor* f, long* launches,
     if (products) *products = f->res.update_products;
   });
 }
+
+double hgpu_factor_net_ms(const hgpu_factor* f) { return f ? f->res.net_ms : 0.0; }
 
 long long hgpu_factor_launches(const hgpu_factor* f) {
   return f ? f->res.launches : 0;

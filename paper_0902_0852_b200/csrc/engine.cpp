@@ -12,7 +12,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 
 namespace hgpu {
 
@@ -202,6 +204,48 @@ int block_owner(long block, int world) {
   const long r = block % (2L * world);
   return (int)(r < world ? r : 2L * world - 1 - r);
 }
+
+// ---- in-process rank group ------------------------------------------------
+// The reference's workers (ldlt.cpp:205-311) share one ColumnChannel
+// (channel.hpp:31-56): the owner of a column publishes it, the others await
+// it, and a failing worker poisons the channel so nobody waits forever
+// (ldlt.cpp:181-188).  Here a rank is a Matrix on some device, a "column" is
+// a panel of kb columns, publishing is a CUDA event recorded after the
+// panel on the owner's panel stream, and awaiting is a host wait for that
+// record (never a device-side spin), after which the receiver's stream waits
+// on the event and its k_fwd_ints launches read the owner's integers
+// directly (peer loads over NVLink when the ranks are on different GPUs).
+const std::string kPeerFailed = "a peer rank failed: ";
+
+struct PeerGroup {
+  int world = 1;
+  std::vector<Matrix*> ranks;
+  std::mutex mu;
+  std::condition_variable cv;
+  long long run = 0;  // factorisation in progress (all ranks)
+  bool poisoned = false;
+  std::string why;
+  std::vector<cudaEvent_t> ready_ev;   // [panel]: the owner's event
+  std::vector<long long> ready_run;    // run that recorded it
+  std::vector<cudaEvent_t> pulled_ev;  // [panel * world + rank]
+  std::vector<long long> pulled_run;
+  // end-of-run merge of the error words (min pivot index, OR of flags)
+  long long merge_run = -1;
+  int arrived = 0;
+  int merged[kErrWords];
+
+  template <class Pred>
+  void wait(std::unique_lock<std::mutex>& lk, Pred pred) {
+    cv.wait(lk, [&] { return poisoned || pred(); });
+    if (!pred()) throw Error(HGPU_ERR_COMM, kPeerFailed + why);
+  }
+  void poison(const std::string& w) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!poisoned) why = w;
+    poisoned = true;
+    cv.notify_all();
+  }
+};
 
 Plan choose_plan(int n, int K, int bits, int min_logL) {
   Plan best;
@@ -475,6 +519,9 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : edf_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : pre_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : sn_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : grp_ready_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : grp_pulled_ev_) cudaEventDestroy(e);
+  for (cudaEvent_t e : net_ev_) cudaEventDestroy(e);
   if (stream_next_) cudaStreamDestroy(stream_next_);
   if (stream_pre_) cudaStreamDestroy(stream_pre_);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
@@ -545,6 +592,8 @@ void Matrix::release() {
 void Matrix::set_comm(int rank, int world, const unsigned char* id) {
   if (world < 1 || rank < 0 || rank >= world)
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad rank/world");
+  if (group_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "matrix already belongs to an in-process group");
   CU(cudaSetDevice(device_));
   if (comm_) {
     ncclCommDestroy((ncclComm_t)comm_);
@@ -560,6 +609,214 @@ void Matrix::set_comm(int rank, int world, const unsigned char* id) {
     comm_ = c;
   }
   release();  // ownership changes the workspace layout
+}
+
+void Matrix::make_group(const std::vector<int>& devices) {
+  const int W = (int)devices.size();
+  if (W < 1 || devices[0] != device_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "group devices must start with the matrix's device");
+  if (comm_ || group_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "matrix already belongs to a rank group");
+  if (interval_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "interval matrices run on one rank");
+  if (W == 1) return;
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  for (int d : devices)
+    if (d < 0 || d >= ndev) throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad device index");
+  // receivers load the owner's integers directly: peer access both ways
+  for (int a : devices)
+    for (int b : devices) {
+      if (a == b) continue;
+      int ok = 0;
+      CU(cudaDeviceCanAccessPeer(&ok, a, b));
+      if (!ok)
+        throw Error(HGPU_ERR_COMM, "no peer access from device " + std::to_string(a) +
+                                       " to device " + std::to_string(b));
+      CU(cudaSetDevice(a));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        (void)cudaGetLastError();
+      else
+        CU(e);
+    }
+  CU(cudaSetDevice(device_));
+  std::vector<int32_t> sz;
+  std::vector<uint32_t> lb;
+  for (const HostInt& h : strip_) {
+    sz.push_back(h.size);
+    lb.insert(lb.end(), h.limbs.begin(), h.limbs.end());
+  }
+  auto g = std::make_shared<PeerGroup>();
+  g->world = W;
+  g->ranks.push_back(this);
+  peers_.clear();
+  for (int r = 1; r < W; ++r) {
+    peers_.push_back(std::make_unique<Matrix>(n_, K_, sz.data(), lb.data(), devices[r]));
+    g->ranks.push_back(peers_.back().get());
+  }
+  for (int r = 0; r < W; ++r) {
+    Matrix* m = g->ranks[r];
+    CU(cudaSetDevice(m->device_));
+    m->release();  // ownership changes the workspace layout
+    m->group_ = g;
+    m->rank_ = r;
+    m->world_ = W;
+  }
+  CU(cudaSetDevice(device_));
+}
+
+void Matrix::group_publish(int b, cudaStream_t st) {
+  PeerGroup& g = *group_;
+  CU(cudaEventRecord(grp_ready_ev_[b], st));
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.ready_ev[b] = grp_ready_ev_[b];
+  g.ready_run[b] = grp_run_;
+  g.cv.notify_all();
+}
+
+Matrix* Matrix::group_await(int b, int owner, cudaStream_t st) {
+  PeerGroup& g = *group_;
+  cudaEvent_t e;
+  {
+    std::unique_lock<std::mutex> lk(g.mu);
+    g.wait(lk, [&] { return g.ready_run[b] == grp_run_; });
+    e = g.ready_ev[b];
+  }
+  CU(cudaStreamWaitEvent(st, e, 0));
+  return g.ranks[owner];
+}
+
+void Matrix::group_pulled(int b, cudaStream_t st) {
+  PeerGroup& g = *group_;
+  CU(cudaEventRecord(grp_pulled_ev_[b], st));
+  std::lock_guard<std::mutex> lk(g.mu);
+  g.pulled_ev[(size_t)b * g.world + rank_] = grp_pulled_ev_[b];
+  g.pulled_run[(size_t)b * g.world + rank_] = grp_run_;
+  g.cv.notify_all();
+}
+
+void Matrix::group_wait_pulled(int b, cudaStream_t st) {
+  PeerGroup& g = *group_;
+  for (int r = 0; r < g.world; ++r) {
+    if (r == rank_) continue;
+    const size_t i = (size_t)b * g.world + r;
+    cudaEvent_t e;
+    {
+      std::unique_lock<std::mutex> lk(g.mu);
+      g.wait(lk, [&] { return g.pulled_run[i] == grp_run_; });
+      e = g.pulled_ev[i];
+    }
+    CU(cudaStreamWaitEvent(st, e, 0));
+  }
+}
+
+void Matrix::group_merge_err(int* herr) {
+  PeerGroup& g = *group_;
+  std::unique_lock<std::mutex> lk(g.mu);
+  if (g.merge_run != grp_run_) {
+    g.merge_run = grp_run_;
+    g.arrived = 0;
+    g.merged[0] = INT_MAX;
+    for (int k = 1; k < kErrWords; ++k) g.merged[k] = 0;
+  }
+  g.merged[kErrZeroPivot] = std::min(g.merged[kErrZeroPivot], herr[kErrZeroPivot]);
+  for (int k = 1; k < kErrWords; ++k) g.merged[k] |= herr[k];
+  ++g.arrived;
+  g.cv.notify_all();
+  g.wait(lk, [&] { return g.arrived == g.world; });
+  for (int k = 0; k < kErrWords; ++k) herr[k] = g.merged[k];
+}
+
+// ldlt_det_parallel over the group (ldlt.cpp:315-341): one host thread per
+// rank runs the same panel schedule on its own columns; the plan and the
+// capacity retries are decided for all ranks together.
+FactorResult Matrix::factor_group(const HostInt& x, unsigned flags) {
+  PeerGroup& g = *group_;
+  const int W = g.world;
+  int min_logL = 0;
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    for (Matrix* m : g.ranks) {
+      CU(cudaSetDevice(m->device_));
+      if (!m->W_ || (min_logL && m->plan_.logL < min_logL)) m->build(min_logL);
+    }
+    CU(cudaSetDevice(device_));
+    const int nblocks = (n_ + plan_.kb - 1) / plan_.kb;
+    {
+      std::lock_guard<std::mutex> lk(g.mu);
+      ++g.run;
+      g.poisoned = false;
+      g.why.clear();
+      g.ready_ev.assign(nblocks + 1, nullptr);
+      g.ready_run.assign(nblocks + 1, -1);
+      g.pulled_ev.assign((size_t)(nblocks + 1) * W, nullptr);
+      g.pulled_run.assign((size_t)(nblocks + 1) * W, -1);
+    }
+    std::vector<FactorResult> res(W);
+    std::vector<std::exception_ptr> errs(W);
+    auto body = [&](int r) {
+      Matrix* m = g.ranks[r];
+      try {
+        CU(cudaSetDevice(m->device_));
+        res[r].n = n_;
+        res[r].K = K_;
+        // rank 0 holds every pivot and (for captures / KEEP_L) reads the
+        // other ranks' ratio columns in place
+        const unsigned f = r == 0 ? flags : (flags & HGPU_PROFILE);
+        m->run(x, f, res[r]);
+      } catch (const std::exception& e) {
+        errs[r] = std::current_exception();
+        g.poison(std::string("rank ") + std::to_string(r) + ": " + e.what());
+      }
+    };
+    std::vector<std::thread> th;
+    for (int r = 1; r < W; ++r) th.emplace_back(body, r);
+    body(0);
+    for (std::thread& t : th) t.join();
+    CU(cudaSetDevice(device_));
+    // the first failure that is not a consequence of another rank's
+    std::exception_ptr first;
+    for (int r = 0; r < W && !first; ++r) {
+      if (!errs[r]) continue;
+      try {
+        std::rethrow_exception(errs[r]);
+      } catch (const Error& e) {
+        if (std::string(e.what()).rfind(kPeerFailed, 0) != 0) first = errs[r];
+      } catch (...) {
+        first = errs[r];
+      }
+    }
+    for (int r = 0; r < W && !first; ++r)
+      if (errs[r]) first = errs[r];
+    if (!first) {
+      FactorResult out = std::move(res[0]);
+      for (int r = 1; r < W; ++r) {
+        out.device_ms = std::max(out.device_ms, res[r].device_ms);
+        out.launches += res[r].launches;
+        out.update_launches += res[r].update_launches;
+        out.update_ms += res[r].update_ms;
+        out.update_products += res[r].update_products;
+        out.net_ms += res[r].net_ms;
+      }
+      return out;
+    }
+    try {
+      std::rethrow_exception(first);
+    } catch (const Error& e) {
+      if (e.status != HGPU_ERR_CAPACITY) throw;
+      if (e.cap_flags == kCapAmax && recip_bound_) {
+        for (Matrix* m : g.ranks) m->recip_bound_ = false;
+        continue;
+      }
+      min_logL = plan_.logL + 1;
+      for (Matrix* m : g.ranks) {
+        CU(cudaSetDevice(m->device_));
+        m->release();
+      }
+      CU(cudaSetDevice(device_));
+    }
+  }
+  throw Error(HGPU_ERR_CAPACITY, "values outgrew every transform plan");
 }
 
 void Matrix::build(int min_logL) {
@@ -759,26 +1016,31 @@ void Matrix::ratio_gemm(int which, int p, int r_begin, int r_end, IntBuf vint,
 
 void Matrix::panel_broadcast(int owner, int p0, int ns, long long row0,
                              cudaStream_t st) {
-  if (world_ == 1) return;
+  if (world_ == 1 || !comm_) return;
   ncclComm_t c = (ncclComm_t)comm_;
   const Plan& P = plan_;
-  const size_t slot_rows = (size_t)ns * n_;
-  int* vh = vhdr_ + row0;
-  int* rh = rhdr_ + row0;
-  uint32_t* vl = vlimbs_ + row0 * P.cap;
-  uint32_t* rl = rlimbs_ + row0 * P.cap;
+  // stage p = p0 + s: V_p[r] for r >= p and R_p[r] for r > p (the rows below
+  // p are unused), each at the slot's cap stride -- ns (n - p) rows instead
+  // of the whole slot set.  The error words are not broadcast: every rank
+  // keeps its own flags until the end-of-run reduction (run()).
   NC(ncclGroupStart());
-  NC(ncclBroadcast(vh, vh, slot_rows, ncclInt32, owner, c, st));
-  NC(ncclBroadcast(rh, rh, slot_rows, ncclInt32, owner, c, st));
-  NC(ncclBroadcast(vl, vl, slot_rows * P.cap, ncclUint32, owner, c, st));
-  NC(ncclBroadcast(rl, rl, slot_rows * P.cap, ncclUint32, owner, c, st));
+  for (int s = 0; s < ns; ++s) {
+    const int p = p0 + s;
+    const long long r0 = row0 + (long long)s * n_ + p;
+    const size_t rows = (size_t)(n_ - p);
+    NC(ncclBroadcast(vhdr_ + r0, vhdr_ + r0, rows, ncclInt32, owner, c, st));
+    NC(ncclBroadcast(rhdr_ + r0, rhdr_ + r0, rows, ncclInt32, owner, c, st));
+    NC(ncclBroadcast(vlimbs_ + r0 * P.cap, vlimbs_ + r0 * P.cap, rows * P.cap, ncclUint32,
+                     owner, c, st));
+    NC(ncclBroadcast(rlimbs_ + r0 * P.cap, rlimbs_ + r0 * P.cap, rows * P.cap, ncclUint32,
+                     owner, c, st));
+  }
   NC(ncclBroadcast(phdr_ + p0, phdr_ + p0, ns, ncclInt32, owner, c, st));
   NC(ncclBroadcast(plimbs_ + (size_t)p0 * P.cap, plimbs_ + (size_t)p0 * P.cap,
                    (size_t)ns * P.cap, ncclUint32, owner, c, st));
   for (int k = 0; k < 3; ++k)
     NC(ncclBroadcast(stats_ + (size_t)k * n_ + p0, stats_ + (size_t)k * n_ + p0,
                      ns, ncclInt32, owner, c, st));
-  NC(ncclBroadcast(err_, err_, kErrWords, ncclInt32, owner, c, st));
   NC(ncclGroupEnd());
 }
 
@@ -805,6 +1067,10 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
   CU(cudaMemsetAsync(stats_, 0xff, 3 * (size_t)n * sizeof(int), st));  // -1
   const long long launches0 = kernel_launch_count();
+  if (group_) {
+    std::lock_guard<std::mutex> lk(group_->mu);
+    grp_run_ = group_->run;
+  }
   CU(cudaEventRecord(ev0_, st));
   CU(launch_fwd_ints(D, IntBuf{x_hdr_, x_limbs_}, 0, xhat_, 0, 1, 0, nullptr,
                      err_, st));
@@ -840,6 +1106,20 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   }
   // events: panel_done[b], next_ready[b] (panel b's columns fully updated),
   // trail_done[b] (slot set of panel b released)
+  if (world_ > 1)
+    while ((int)net_ev_.size() < 2 * nblocks + 2) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      net_ev_.push_back(e);
+    }
+  std::vector<int> net_panels;
+  if (group_)
+    for (auto* evs : {&grp_ready_ev_, &grp_pulled_ev_})
+      while ((int)evs->size() < nblocks + 1) {
+        cudaEvent_t e;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs->push_back(e);
+      }
   cudaEvent_t* panel_done = pev_.data();
   cudaEvent_t* next_ready = pev_.data() + nblocks + 1;
   cudaEvent_t* trail_done = pev_.data() + 2 * nblocks + 2;
@@ -1040,6 +1320,15 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       if (b - sdef >= 0) CU(cudaStreamWaitEvent(su1, rest_done[b - sdef], 0));
       for (int bb = std::max(0, b + 1 - sdef); bb <= b - 1; ++bb)
         trailing(bb, p1, std::min(n, p1 + kb), su1, 13);
+    }
+    if (owner == rank_ && group_) {
+      // group: the receivers of the last panel this rank wrote into the same
+      // slot set must have pulled it (read its integers) before it is reused
+      for (int bb = b - nsets; bb >= 0; bb -= nsets)
+        if (block_owner(bb, world_) == rank_) {
+          group_wait_pulled(bb, sp);
+          break;
+        }
     }
     if (owner == rank_) {
       // Per stage p three chains run concurrently:
@@ -1335,27 +1624,57 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         }
       }
     }
-    panel_broadcast(owner, p0, ns, row0set, sp);
+    // the panel's integers on every rank: NCCL broadcast into the local slot
+    // set, or (in-process group) read from the owner's slot set in place
+    IntBuf src_v = vint, src_r = rint;
+    long long src_row0 = row0set;
+    if (world_ > 1 && owner != rank_) {
+      CU(cudaEventRecord(net_ev_[2 * b], sp));
+      net_panels.push_back(b);
+    }
+    if (group_) {
+      if (owner == rank_) {
+        group_publish(b, sp);
+      } else {
+        const Matrix* o = group_await(b, owner, sp);
+        src_v = IntBuf{o->vhdr_, o->vlimbs_};
+        src_r = IntBuf{o->rhdr_, o->rlimbs_};
+        src_row0 = o->slot_row0(b);
+        // the panel's pivots (fold) and stage statistics (k_validate)
+        CU(cudaMemcpyAsync(phdr_ + p0, o->phdr_ + p0, ns * sizeof(int), cudaMemcpyDefault, sp));
+        CU(cudaMemcpyAsync(plimbs_ + (size_t)p0 * P.cap, o->plimbs_ + (size_t)p0 * P.cap,
+                           (size_t)ns * P.cap * 4, cudaMemcpyDefault, sp));
+        for (int k = 0; k < 3; ++k)
+          CU(cudaMemcpyAsync(stats_ + (size_t)k * n + p0, o->stats_ + (size_t)k * n + p0,
+                             ns * sizeof(int), cudaMemcpyDefault, sp));
+      }
+    } else {
+      panel_broadcast(owner, p0, ns, row0set, sp);
+    }
     if (owner != rank_ && p1 < n) {
+      // transforms of the rows this rank's columns need (rows >= p1); in a
+      // group these launches are the transfer: they load the owner's limbs
       for (int s = 0; s < ns; ++s) {
         const long long row0 = row0set + (long long)s * n;
-        CU(launch_fwd_ints(D, vint, row0 + p1, vhat_, row0 + p1, n - p1, 0,
+        const long long srow = src_row0 + (long long)s * n;
+        CU(launch_fwd_ints(D, src_v, srow + p1, vhat_, row0 + p1, n - p1, 0,
                            nullptr, err_, sp));
-        CU(launch_fwd_ints(D, rint, row0 + p1, rhat_, row0 + p1, n - p1, 1,
+        CU(launch_fwd_ints(D, src_r, srow + p1, rhat_, row0 + p1, n - p1, 1,
                            nullptr, err_, sp));
       }
     }
+    if (world_ > 1 && owner != rank_) CU(cudaEventRecord(net_ev_[2 * b + 1], sp));
     CU(cudaEventRecord(panel_done[b], sp));
-    if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, row0set, sp);
+    if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, sp, src_r);
     if (capture) {
       const int nsr = std::min(ns, crow - 1 - p0);
       if (nsr > 0) {
         hr_hdr.resize((size_t)nsr * n);
         hr_limbs.resize((size_t)nsr * n * P.cap);
-        CU(cudaMemcpyAsync(hr_hdr.data(), rhdr_ + row0set, hr_hdr.size() * 4,
-                           cudaMemcpyDeviceToHost, sp));
-        CU(cudaMemcpyAsync(hr_limbs.data(), rlimbs_ + row0set * P.cap,
-                           hr_limbs.size() * 4, cudaMemcpyDeviceToHost, sp));
+        CU(cudaMemcpyAsync(hr_hdr.data(), src_r.hdr + src_row0, hr_hdr.size() * 4,
+                           cudaMemcpyDefault, sp));
+        CU(cudaMemcpyAsync(hr_limbs.data(), src_r.limbs + src_row0 * P.cap,
+                           hr_limbs.size() * 4, cudaMemcpyDefault, sp));
         CU(cudaStreamSynchronize(sp));
         for (int s = 0; s < nsr; ++s) {
           const int p = p0 + s;
@@ -1372,6 +1691,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         }
       }
     }
+    if (group_ && owner != rank_) group_pulled(b, sp);
     // ---- trailing update of panel b on the bulk stream: the next panel's
     // columns first (they gate panel b+1), then everything to their right,
     // which overlaps panel b+1's factorisation
@@ -1409,10 +1729,20 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   CU(cudaEventRecord(ev1_, st));
   res.launches = kernel_launch_count() - launches0;
 
+  if (comm_ && world_ > 1) {
+    // every rank raised its own flags (its transforms, its updates): the
+    // factorisation's status is the first zero pivot and the union of flags
+    ncclComm_t c = (ncclComm_t)comm_;
+    NC(ncclGroupStart());
+    NC(ncclAllReduce(err_, err_, 1, ncclInt32, ncclMin, c, st));
+    NC(ncclAllReduce(err_ + 1, err_ + 1, kErrWords - 1, ncclInt32, ncclMax, c, st));
+    NC(ncclGroupEnd());
+  }
   int herr[kErrWords];
   CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
   const auto t_enq = std::chrono::steady_clock::now();
   CU(cudaStreamSynchronize(st));
+  if (group_) group_merge_err(herr);
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, ev0_, ev1_));
   res.device_ms = ms;
@@ -1432,6 +1762,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       }
       std::fclose(f);
     }
+  }
+  for (int b : net_panels) {
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, net_ev_[2 * b], net_ev_[2 * b + 1]));
+    res.net_ms += t;
   }
   if (profile) {
     for (size_t i = 0; i < uev_used; i += 2) {
@@ -1473,7 +1808,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
 }
 
 // R_p[r] for the panel's stages (rows r > p) into the packed L store.
-void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st) {
+void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st,
+                          IntBuf srcb) {
   const Plan& P = plan_;
   const int n = n_;
   for (int s = 0; s < ns; ++s) {
@@ -1482,10 +1818,9 @@ void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st) {
     const long long src = row0set + (long long)s * n + p + 1;
     const long long dst = (long long)p * (n - 1) - (long long)p * (p - 1) / 2;
     const size_t rows = (size_t)(n - p - 1);
-    CU(cudaMemcpyAsync(lhdr_ + dst, rhdr_ + src, rows * 4,
-                       cudaMemcpyDeviceToDevice, st));
-    CU(cudaMemcpyAsync(llimbs_ + dst * P.cap, rlimbs_ + src * P.cap,
-                       rows * P.cap * 4, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemcpyAsync(lhdr_ + dst, srcb.hdr + src, rows * 4, cudaMemcpyDefault, st));
+    CU(cudaMemcpyAsync(llimbs_ + dst * P.cap, srcb.limbs + src * P.cap,
+                       rows * P.cap * 4, cudaMemcpyDefault, st));
   }
   have_L_ = true;
   ++factor_serial_;
@@ -1521,8 +1856,9 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
   const auto t_start = std::chrono::steady_clock::now();
   if (!have_L_)
     throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve needs a HGPU_KEEP_L factorisation");
-  if (world_ != 1)
-    throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve runs on a single rank");
+  if (world_ != 1 && !(group_ && rank_ == 0))
+    throw Error(HGPU_ERR_INVALID_ARGUMENT,
+                "solve runs on a single rank (or rank 0 of an in-process group)");
   const Plan& P = plan_;
   const int n = n_, k2 = K_ / 2;
   cudaStream_t st = stream_;
@@ -1643,6 +1979,22 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         dfree(sxhat_);
         stw_ = acch_ = sxhat_ = nullptr;
         lhat_tab_ = nullptr;
+        // nothing describes the freed buffers any more; an allocation failure
+        // below leaves the solve unplanned and reports a capacity failure, so
+        // solve() falls back to the schoolbook AXPY
+        sdp_bits_ = sdp_xbits_ = 0;
+        lhat_for_ = -1;
+        auto unplan = [&]() {
+          dfree(stw_);
+          dfree(lhat_tab_);
+          for (uint32_t* c : lhat_chunks_) dfree(c);
+          lhat_chunks_.clear();
+          dfree(acch_);
+          dfree(sxhat_);
+          stw_ = acch_ = sxhat_ = nullptr;
+          lhat_tab_ = nullptr;
+        };
+        try {
         DevPlan S{};
         S.n = n;
         S.K = K_;
@@ -1691,6 +2043,12 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         sdp_ = S;
         sdp_bits_ = mb + xb;
         sdp_xbits_ = xb;
+        } catch (const Error& e) {
+          unplan();
+          if (e.status != HGPU_ERR_CUDA) throw;
+          throw Error(HGPU_ERR_CAPACITY,
+                      std::string("transform-domain solve allocation failed: ") + e.what());
+        }
       }
       CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, ne, lhat_store(), dp_.grid_cap, err_,
                            st));
@@ -1917,6 +2275,11 @@ void Matrix::fold(FactorResult& res) {
 }
 
 FactorResult Matrix::factor(const HostInt& x, unsigned flags) {
+  if (group_) {
+    if (rank_ != 0)
+      throw Error(HGPU_ERR_INVALID_ARGUMENT, "a group is driven by its rank 0");
+    return factor_group(x, flags);
+  }
   CU(cudaSetDevice(device_));
   FactorResult res;
   res.n = n_;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -67,13 +68,29 @@ struct FactorResult {
   std::vector<HostInt> pivots_hi;
   HostInt det_hi;
   int det_sign = 0;
+  bool det_exact_zero = false;  // folded det interval is exactly [0, 0]
+  double net_ms = 0;  // receivers' wait + pull of panels (device time, {net})
 };
+
+// In-process rank group (hgpu_matrix_new_group, engine.cpp): W ranks of
+// one column-block-cyclic factorisation in this process, on one or more
+// devices, driven by host threads and ordered by CUDA events.
+struct PeerGroup;
 
 class Matrix {
  public:
   Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs, int device);
   ~Matrix();
   void set_comm(int rank, int world, const unsigned char* id);
+  // Makes this matrix rank 0 of an in-process group over `devices` (one
+  // rank per entry; a device may repeat, e.g. to run the multi-rank schedule
+  // on one GPU).  The other ranks are owned by this one; factor() drives
+  // them all.  A panel's owner publishes its slot set and every other rank
+  // pulls the panel's integers from the owner's memory (peer reads over
+  // NVLink across GPUs) straight into its own transforms (ldlt.cpp:255-307's
+  // owner / receiver roles; no NCCL, no device-side waiting).
+  void make_group(const std::vector<int>& devices);
+  int world() const { return world_; }
   FactorResult factor(const HostInt& x, unsigned flags);
   // PrecisionMismatch as in ldlt.cpp:36 when x carries other frac bits.
   FactorResult factor_checked(const HostInt& x, long x_frac_bits,
@@ -110,6 +127,15 @@ class Matrix {
                                unsigned flags);
 
  private:
+  FactorResult factor_group(const HostInt& x, unsigned flags);
+  long long slot_row0(int b) const { return (long long)(b % nsets_) * plan_.kb * n_; }
+  // group transport (engine.cpp): owner publishes panel b, receivers wait for
+  // it and pull, owner waits for the pulls before reusing a slot set
+  void group_publish(int b, cudaStream_t st);
+  Matrix* group_await(int b, int owner, cudaStream_t st);
+  void group_pulled(int b, cudaStream_t st);
+  void group_wait_pulled(int b, cudaStream_t st);
+  void group_merge_err(int* herr);
   void build(int min_logL);
   void release();
   void run(const HostInt& x, unsigned flags, FactorResult& res);
@@ -123,7 +149,8 @@ class Matrix {
   void ratio_gemm(int which, int p, int r_begin, int r_end, IntBuf vint,
                   long long row0, const uint32_t* yb, const int* yss,
                   IntBuf rint, int* maxdegR, uint32_t* dscr, cudaStream_t s);
-  void keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st);
+  void keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st,
+                    IntBuf src);
   void build_interval();
   void release_interval();
   void run_interval(const HostInt& xlo, const HostInt& xhi, unsigned flags,
@@ -137,6 +164,11 @@ class Matrix {
   DevPlan dp_{};
   int rank_ = 0, world_ = 1;
   void* comm_ = nullptr;  // ncclComm_t
+  std::shared_ptr<PeerGroup> group_;                // in-process group, or null
+  std::vector<std::unique_ptr<Matrix>> peers_;      // ranks 1.. (rank 0 only)
+  std::vector<cudaEvent_t> grp_ready_ev_, grp_pulled_ev_;
+  std::vector<cudaEvent_t> net_ev_;  // receivers: [2b] before, [2b+1] after a panel's arrival
+  long long grp_run_ = 0;
   std::vector<long long> colbase_h_;
   std::vector<int> owned_blocks_;
   // device buffers

@@ -128,6 +128,29 @@ std::vector<Z> exact_moments(long n, const Rational& b, long k) {
   return lo;
 }
 
+// workers (driver.cpp:102-114: one thread per worker in ldlt_det_parallel)
+// -> column-block-cyclic ranks, one per GPU from HGPU_DEVICE on, at most the
+// devices present.  HGPU_RANK_DEVICES="d0,d1,..." names the rank devices
+// explicitly (a device may repeat: the multi-rank schedule on one GPU).
+std::vector<int> rank_devices(long workers, int base) {
+  std::vector<int> devs;
+  if (const char* e = std::getenv("HGPU_RANK_DEVICES")) {
+    for (const char* c = e; *c;) {
+      char* end = nullptr;
+      const long d = std::strtol(c, &end, 10);
+      if (end == c) break;
+      devs.push_back((int)d);
+      c = *end == ',' ? end + 1 : end;
+    }
+    if (!devs.empty()) return devs;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 1;
+  const long w = std::max(1L, std::min<long>(workers, (long)ndev - base));
+  for (long i = 0; i < w; ++i) devs.push_back(base + (int)i);
+  return devs;
+}
+
 std::unique_ptr<Matrix> upload(const std::vector<Z>& strip, long k, int device) {
   std::vector<int32_t> sizes;
   std::vector<uint32_t> limbs, tmp;
@@ -135,13 +158,14 @@ std::unique_ptr<Matrix> upload(const std::vector<Z>& strip, long k, int device) 
     sizes.push_back(z.to_limbs(tmp));
     limbs.insert(limbs.end(), tmp.begin(), tmp.end());
   }
-  return std::make_unique<Matrix>((int)((strip.size() + 1) / 2), (int)k,
-                                  sizes.data(), limbs.data(), device);
+  auto m = std::make_unique<Matrix>((int)((strip.size() + 1) / 2), (int)k,
+                                    sizes.data(), limbs.data(), device);
+  return m;
 }
 
 // The DetEvaluator: GPU factorisation + GPU fold (ldlt_det_serial semantics).
-DetFn gpu_det(Matrix& m, long k, double* seconds) {
-  return [&m, k, seconds](const Z& x) -> Z {
+DetFn gpu_det(Matrix& m, long k, double* seconds, double* net = nullptr) {
+  return [&m, k, seconds, net](const Z& x) -> Z {
     std::vector<uint32_t> xl;
     HostInt xi;
     xi.size = x.to_limbs(xl);
@@ -149,9 +173,15 @@ DetFn gpu_det(Matrix& m, long k, double* seconds) {
     const auto t0 = std::chrono::steady_clock::now();
     try {
       FactorResult r = m.factor(xi, HGPU_FOLD);
+      // timing.hpp:7-39: {net} is the receivers' wait for and pull of the
+      // published panels (per-rank average, CUDA events); receivers never
+      // divide (every ratio comes from the owner), so {d} stays 0 as with
+      // the reference's unthrottled channel; {c} is the rest
+      const double nets = r.net_ms * 1e-3 / std::max(1, m.world());
+      if (net) *net += nets;
       if (seconds)
         *seconds += std::chrono::duration<double>(
-                        std::chrono::steady_clock::now() - t0).count();
+                        std::chrono::steady_clock::now() - t0).count() - nets;
       return Z::from_limbs(r.det.size, r.det.limbs.data());
     } catch (const Error& e) {
       if (seconds)
@@ -199,12 +229,14 @@ RunResult run(const RunConfig& cfg) {
   std::vector<Z> strip;
   for (;;) {
     strip = exact_moments(cfg.n, cfg.beta, k);
-    std::unique_ptr<Matrix> m = upload(strip, k, device_from_env());
+    const std::vector<int> devs = rank_devices(cfg.workers, device_from_env());
+    std::unique_ptr<Matrix> m = upload(strip, k, devs[0]);
+    if (devs.size() > 1) m->make_group(devs);
     try {
       std::optional<Z> acc;
       if (hint) acc = shl(*hint, (unsigned long)(k - hint_k));
       tr = secant_smallest_eigenvalue(cfg.n, strip[0],
-                                      gpu_det(*m, k, &res.compute_s), k, 15,
+                                      gpu_det(*m, k, &res.compute_s, &res.net_s), k, 15,
                                       acc ? &*acc : nullptr);
       break;
     } catch (const SecantError& e) {
@@ -246,11 +278,11 @@ RunResult run(const RunConfig& cfg) {
       hgpu_status hs = hgpu_interval_matrix_new(
           cfg.n, kv, sizes.data(), limbs.data(), sizes_hi.data(),
           limbs_hi.data(), device_from_env(), &im);
-      int st = 2, ls = 0, us = 0;
+      int st = 2, ls = 0, us = 0, lz = 0;
       char *pa = nullptr, *pb = nullptr;
       if (hs == HGPU_OK)
-        hs = hgpu_verify_eigenvalue(im, res.eigenvalue.c_str(), 15, &st, &ls,
-                                    &us, &pa, &pb);
+        hs = hgpu_verify_eigenvalue_ex(im, res.eigenvalue.c_str(), 15, &st, &ls,
+                                       &us, &lz, &pa, &pb);
       hgpu_matrix_free(im);
       const std::string probe_low = pa ? pa : "";
       hgpu_string_free(pa);
@@ -267,6 +299,14 @@ RunResult run(const RunConfig& cfg) {
         throw Refuted(
             "refuted: interval verification contradicted the converged value at " +
             probe_low);
+      if (lz) {
+        // driver.cpp:161-170: det(M - aI) = [0, 0], the truncated probe is
+        // itself an eigenvalue; bracketing cannot decide at any precision
+        res.verified = false;
+        res.diagnosis = "det(M - aI) is exactly zero: the 15-digit probe " + probe_low +
+                        " is itself an eigenvalue; bracketing verification does not apply";
+        break;
+      }
       kv = escalate(kv, cap);
     }
   }

@@ -107,6 +107,17 @@ extern "C" hgpu_status hgpu_verify_eigenvalue(hgpu_matrix* m,
                                               int* upper_sign,
                                               char** probe_low,
                                               char** probe_high) {
+  return hgpu_verify_eigenvalue_ex(m, x_decimal, digits, status, lower_sign,
+                                   upper_sign, nullptr, probe_low, probe_high);
+}
+
+extern "C" hgpu_status hgpu_verify_eigenvalue_ex(hgpu_matrix* m,
+                                                 const char* x_decimal, int digits,
+                                                 int* status, int* lower_sign,
+                                                 int* upper_sign,
+                                                 int* lower_exact_zero,
+                                                 char** probe_low,
+                                                 char** probe_high) {
   using namespace hgpu;
   try {
     Matrix* mm = matrix_impl(m);
@@ -132,11 +143,14 @@ extern "C" hgpu_status hgpu_verify_eigenvalue(hgpu_matrix* m,
     const std::string a = sci_string(xs);
     const std::string b = bump_last_digit(a);
     int ls = 0, us = 0, st = 2;  // 0 verified, 1 refuted, 2 inconclusive
+    bool lz = false;  // det(M - aI) == [0, 0] (verify.cpp:26-27)
     try {
       Z alo, ahi, blo, bhi;
       decimal_to_interval(a, kv, alo, ahi);
       decimal_to_interval(b, kv, blo, bhi);
-      ls = mm->factor_interval(host_int(alo), host_int(ahi), 0).det_sign;
+      const FactorResult ra = mm->factor_interval(host_int(alo), host_int(ahi), 0);
+      ls = ra.det_sign;
+      lz = ra.det_exact_zero;
       us = mm->factor_interval(host_int(blo), host_int(bhi), 0).det_sign;
       if (ls > 0 && us < 0) st = 0;
       else if (ls < 0 || us > 0) st = 1;
@@ -148,6 +162,7 @@ extern "C" hgpu_status hgpu_verify_eigenvalue(hgpu_matrix* m,
     if (status) *status = st;
     if (lower_sign) *lower_sign = ls;
     if (upper_sign) *upper_sign = us;
+    if (lower_exact_zero) *lower_exact_zero = lz ? 1 : 0;
     if (probe_low) *probe_low = dup_c(a);
     if (probe_high) *probe_high = dup_c(b);
     return HGPU_OK;

@@ -337,6 +337,7 @@ void Matrix::run_interval(const HostInt& xlo, const HostInt& xhi,
     res.det_hi = from_z(hi);
     res.have_det = true;
     res.det_sign = lo.sgn() > 0 ? 1 : (hi.sgn() < 0 ? -1 : 0);
+    res.det_exact_zero = lo.sgn() == 0 && hi.sgn() == 0;
   };
   if (flags & HGPU_FOLD) {
     exact_fold();

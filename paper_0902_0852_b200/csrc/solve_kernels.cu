@@ -408,6 +408,10 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   }
   // every CTA of cluster 0 reaches every cluster barrier (no early return)
   cg::cluster_group cl = cg::this_cluster();
+  // arrive now, wait just before the first store into another CTA's shared
+  // memory: a CTA's distributed shared memory may only be accessed once
+  // every CTA of the cluster has started
+  asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
   const int rk = (int)blockIdx.x;  // prime handled by this CTA
   const bool live = ntg > 0 && !(S.debug & 32768);
   const int t = live ? target(0) : 0;
@@ -440,6 +444,9 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
       reinterpret_cast<uint4*>(Ar)[q4] = pw_madd(a[q4], x[q4], __ldcs(r + q4), c);
     __syncthreads();
     cta_ntt_inv16<RM>(Ar, 1, S.logL, twi + rk * L, &c);
+  }
+  asm volatile("barrier.cluster.wait;" ::: "memory");
+  if (live) {
     // CTA q gets every prime of its coefficient slice [lo_q - (T-1), hi_q)
     for (int q = 0; q < nc; ++q) {
       if (q == rk) continue;

@@ -47,6 +47,8 @@ EXPORTS = (
     "hgpu_interval_matrix_new", "hgpu_ldlt_interval", "hgpu_factor_pivot_hi",
     "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
     "hgpu_build_moments", "hgpu_buffer_free", "hgpu_matrix_set_capture_rows",
+    "hgpu_matrix_new_group", "hgpu_matrix_world", "hgpu_verify_eigenvalue_ex",
+    "hgpu_factor_net_ms",
 )
 
 
@@ -90,6 +92,10 @@ def load() -> ctypes.CDLL:
     lib.hgpu_matrix_new.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int32), u32p, ctypes.c_int,
                                     ctypes.POINTER(vp)]
     lib.hgpu_matrix_free.argtypes = [vp]
+    lib.hgpu_matrix_new_group.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int32), u32p,
+                                          ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.hgpu_matrix_world.argtypes = [vp]
+    lib.hgpu_matrix_world.restype = ctypes.c_int
     lib.hgpu_nccl_unique_id.argtypes = [ctypes.c_char_p]
     lib.hgpu_matrix_set_comm.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.hgpu_matrix_set_capture_rows.argtypes = [vp, i64]
@@ -106,6 +112,8 @@ def load() -> ctypes.CDLL:
     lib.hgpu_factor_device_ms.restype = ctypes.c_double
     lib.hgpu_factor_update_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_factor_net_ms.argtypes = [vp]
+    lib.hgpu_factor_net_ms.restype = ctypes.c_double
     lib.hgpu_factor_launches.argtypes = [vp]
     lib.hgpu_factor_launches.restype = ctypes.c_longlong
     lib.hgpu_factor_free.argtypes = [vp]
@@ -135,6 +143,8 @@ def load() -> ctypes.CDLL:
     lib.hgpu_verify_eigenvalue.argtypes = [vp, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                            ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_void_p)]
+    lib.hgpu_verify_eigenvalue_ex.argtypes = [vp, ctypes.c_char_p, ctypes.c_int] + \
+        [ctypes.POINTER(ctypes.c_int)] * 4 + [ctypes.POINTER(ctypes.c_void_p)] * 2
     pp32 = ctypes.POINTER(ctypes.POINTER(ctypes.c_int32))
     ppu32 = ctypes.POINTER(ctypes.POINTER(ctypes.c_uint32))
     lib.hgpu_build_moments.argtypes = [i64, ctypes.c_ulong, ctypes.c_ulong, i64, ctypes.c_int,
@@ -209,6 +219,7 @@ class LdltResult:
     update_products: float = 0.0
     launches: int = 0
     ratio_sha256: str | None = None
+    net_ms: float = 0.0
 
 
 def _hex(v: int) -> str:
@@ -229,7 +240,11 @@ class HankelMatrixGPU:
     """The anti-diagonal strip of M (HankelMatrix, hankel_matrix.hpp:17-42)
     resident on one B200, ready for repeated det(M - xI) evaluations."""
 
-    def __init__(self, strip: list[int], frac_bits: int, device: int = 0):
+    def __init__(self, strip: list[int], frac_bits: int, device: int = 0,
+                 devices: list[int] | None = None):
+        """devices=[d0, d1, ...]: an in-process column-block-cyclic rank
+        group, one rank per entry (ldlt_det_parallel with workers ->
+        ranks; hgpu_matrix_new_group).  A device may repeat."""
         lib = load()
         if len(strip) % 2 == 0 or not strip:
             raise ValueError("strip must hold 2n-1 anti-diagonals")
@@ -237,9 +252,21 @@ class HankelMatrixGPU:
         self.frac_bits = frac_bits
         sizes, limbs = pack_ints(strip)
         h = ctypes.c_void_p()
-        _check(lib.hgpu_matrix_new(self.n, frac_bits, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                   _u32p(limbs), device, ctypes.byref(h)))
+        if devices and len(devices) > 1:
+            devs = (ctypes.c_int * len(devices))(*devices)
+            _check(lib.hgpu_matrix_new_group(self.n, frac_bits,
+                                             sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                             _u32p(limbs), devs, len(devices), ctypes.byref(h)))
+        else:
+            _check(lib.hgpu_matrix_new(self.n, frac_bits,
+                                       sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       _u32p(limbs), devices[0] if devices else device,
+                                       ctypes.byref(h)))
         self._h = h
+
+    @property
+    def world(self) -> int:
+        return int(load().hgpu_matrix_world(self._h))
 
     def close(self) -> None:
         if getattr(self, "_h", None):
@@ -296,6 +323,7 @@ class HankelMatrixGPU:
                 pivots.append(limbs_to_int(size.value, ptr))
             res = LdltResult(n=n, frac_bits=self.frac_bits, pivots=pivots,
                              device_ms=lib.hgpu_factor_device_ms(f),
+                             net_ms=lib.hgpu_factor_net_ms(f),
                              launches=int(lib.hgpu_factor_launches(f)))
             if capture:
                 nc = min(n, capture_rows) if capture_rows > 0 else n
@@ -403,12 +431,14 @@ class IntervalMatrixGPU(HankelMatrixGPU):
 def verify_eigenvalue(m: IntervalMatrixGPU, x_decimal: str, digits: int = 15) -> dict:
     """verify_eigenvalue (verify.cpp:8-42) on the GPU interval LDL^T."""
     lib = load()
-    st, ls, us = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    st, ls, us, lz = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     a, b = ctypes.c_void_p(), ctypes.c_void_p()
-    _check(lib.hgpu_verify_eigenvalue(m._h, x_decimal.encode(), digits, ctypes.byref(st), ctypes.byref(ls),
-                                      ctypes.byref(us), ctypes.byref(a), ctypes.byref(b)), m.frac_bits)
+    _check(lib.hgpu_verify_eigenvalue_ex(m._h, x_decimal.encode(), digits, ctypes.byref(st),
+                                         ctypes.byref(ls), ctypes.byref(us), ctypes.byref(lz),
+                                         ctypes.byref(a), ctypes.byref(b)), m.frac_bits)
     return {"status": ("verified", "refuted", "inconclusive")[st.value], "lower_sign": ls.value,
-            "upper_sign": us.value, "probe_low": _take_string(a), "probe_high": _take_string(b)}
+            "upper_sign": us.value, "lower_exact_zero": bool(lz.value),
+            "probe_low": _take_string(a), "probe_high": _take_string(b)}
 
 
 def _take_string(ptr: ctypes.c_void_p) -> str:

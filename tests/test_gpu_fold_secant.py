@@ -88,13 +88,14 @@ def test_secant_beta_7_4_against_reference(hg, ref):
     assert got["eigenvalue"] == want["eigenvalue"]
 
 
-def _heig_run(path, n, beta, k=0, verify=False):
+def _heig_run(path, n, beta, k=0, verify=False, workers=1):
     lib = ctypes.CDLL(path)
     lib.heig_config_new.restype = ctypes.c_void_p
     lib.heig_config_set_n.argtypes = [ctypes.c_void_p, ctypes.c_long]
     lib.heig_config_set_beta.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
     lib.heig_config_set_precision_bits.argtypes = [ctypes.c_void_p, ctypes.c_long]
     lib.heig_config_set_verify.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.heig_config_set_workers.argtypes = [ctypes.c_void_p, ctypes.c_long]
     lib.heig_run.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
     lib.heig_result_to_json.argtypes = [ctypes.c_void_p]
     lib.heig_result_to_json.restype = ctypes.c_void_p
@@ -105,7 +106,8 @@ def _heig_run(path, n, beta, k=0, verify=False):
     cfg = lib.heig_config_new()
     for st in (lib.heig_config_set_n(cfg, n), lib.heig_config_set_beta(cfg, beta.encode()),
                lib.heig_config_set_precision_bits(cfg, k),
-               lib.heig_config_set_verify(cfg, int(verify))):
+               lib.heig_config_set_verify(cfg, int(verify)),
+               lib.heig_config_set_workers(cfg, workers)):
         if st != 0:
             lib.heig_config_free(cfg)
             return st, lib.heig_last_error().decode()
