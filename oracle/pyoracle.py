@@ -398,9 +398,10 @@ class RefLib(_TextLib):
                           n, beta_num, beta_den, kv, x_decimal.encode())
         if text.startswith("error"):
             raise RuntimeError(text)
-        st, lo, hi, a, b = text.split()
+        st, lo, hi, a, b, lz = text.split()
         return {"status": ("verified", "refuted", "inconclusive")[int(st)],
-                "lower_sign": int(lo), "upper_sign": int(hi), "probe_low": a, "probe_high": b}
+                "lower_sign": int(lo), "upper_sign": int(hi), "lower_exact_zero": bool(int(lz)),
+                "probe_low": a, "probe_high": b}
 
     def truncate_sig_digits(self, x: int, frac_bits: int, digits: int) -> str:
         return self._call("oref_truncate_sig_digits", [ctypes.c_char_p, ctypes.c_long, ctypes.c_int],

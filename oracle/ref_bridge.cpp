@@ -199,7 +199,7 @@ char* oref_decimal_to_interval(const char* s, long frac_bits) {
 }
 
 // verify_eigenvalue (verify.cpp:8-42) on build_interval_matrix(n, beta, kv):
-// "<status> <lower_sign> <upper_sign> <probe_low> <probe_high>" with status
+// "<status> <lower_sign> <upper_sign> <probe_low> <probe_high> <lower_exact_zero>" with status
 // 0 verified, 1 refuted, 2 inconclusive and signs 1/-1/0 (0: indeterminate).
 char* oref_verify(long n, unsigned long bnum, unsigned long bden, long kv,
                   const char* x_decimal) {
@@ -214,7 +214,7 @@ char* oref_verify(long n, unsigned long bnum, unsigned long bden, long kv,
     os << (o.status == VerifyStatus::Verified ? 0
            : o.status == VerifyStatus::Refuted ? 1 : 2)
        << " " << sg(o.lower_sign) << " " << sg(o.upper_sign) << " "
-       << o.probe_low << " " << o.probe_high;
+       << o.probe_low << " " << o.probe_high << " " << (o.lower_exact_zero ? 1 : 0);
     return os.str();
   });
 }

@@ -873,7 +873,15 @@ void Matrix::build(int min_logL) {
     int per_sm = 2;
     if (const char* g = std::getenv("HGPU_GRID")) per_sm = std::max(1, std::atoi(g));
     D.grid_cap = per_sm * nsm;
+    D.recip_fast = 1;  // HGPU_RECIP_FAST=0: the original reciprocal (same Y)
+    if (const char* rf = std::getenv("HGPU_RECIP_FAST")) D.recip_fast = std::atoi(rf);
     if (const char* dbg = std::getenv("HGPU_DEBUG")) D.debug = std::atoi(dbg);
+#ifndef HGPU_TIMING_EXPERIMENTS
+    // bits that skip work (512: the deferred update, 16384 / 32768: the
+    // solve's pointwise / critical work) exist for timing experiments only
+    // and give wrong results: a production build ignores them
+    D.debug &= ~(512 | 16384 | 32768);
+#endif
   }
 
   CU(configure_kernels(D, &div_smem_, &div_global_, &recip_global_));
@@ -1397,6 +1405,10 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             PivotDiv pd{};
             pd.recip_words = std::min<long long>(
                 (long long)recip_scratch_words(D), recip_words_bound(D, dmax_bits_, pivot_segs_));
+            if (D.recip_fast)
+              pd.recip_words = std::min<long long>(
+                  (long long)recip_scratch_words(D),
+                  std::max(pd.recip_words, recip_fast_words_bound(D, dmax_bits_)));
             if (p > p0) {
               pd.on = 1;
               pd.vrow0 = row0 - n;  // stage p-1 of this panel's slot set

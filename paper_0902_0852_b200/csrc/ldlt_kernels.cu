@@ -418,10 +418,20 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
   }
 }
 
+}  // namespace hgpu
+#include "recip_fast.cuh"
+namespace hgpu {
+
 __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long prow,
                         const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
                         uint32_t* Ybuf, int* ys, uint32_t* gscratch,
                         int use_gscratch, int* err) {
+  extern __shared__ uint32_t sm_dyn[];
+  if (P.recip_fast && !use_gscratch && gridDim.y == 1) {
+    if (stage_aborted(err)) return;
+    recip_fast_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn, err);
+    return;
+  }
   recip_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, gscratch,
              use_gscratch, err, blockIdx.y);
 }
@@ -713,9 +723,16 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
                maxdegV, err, 0, nullptr, 0, 0, 1);
   __syncthreads();
   if (ph) t[3] = clock64();
-  if (p < P.n - 1)
-    recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
-               gscratch, use_gscratch, err, 0, pd.recip_words);
+  if (p < P.n - 1) {
+    if (P.recip_fast && !use_gscratch) {
+      extern __shared__ uint32_t sm_dyn[];
+      recip_fast_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn,
+                      err);
+    } else {
+      recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
+                 gscratch, use_gscratch, err, 0, pd.recip_words);
+    }
+  }
   if (ph) {
     t[4] = clock64();
     printf("k_pivot p=%d div %lld col %lld extract %lld recip %lld cycles\n", p,
@@ -1238,6 +1255,12 @@ long long recip_words_bound(const DevPlan& P, int dmax_bits, int segs) {
   const long long e = (long long)(dmax_bits - P.k2) / 2 + P.k2 + 6;
   const long long Lm = (e + 32 + 32 + 31) / 32 + 2;
   return 10 * Lm + 71 + (long long)segs * (3 * Lm + 2) + 8;
+}
+
+long long recip_fast_words_bound(const DevPlan& P, int dmax_bits) {
+  const long long e = (long long)(dmax_bits - P.k2) / 2 + P.k2 + 6;
+  const long long Lm = (e + 32 + 32 + 31) / 32 + 2;
+  return rf_scratch_words((int)Lm);
 }
 
 size_t recip_scratch_words(const DevPlan& P) {

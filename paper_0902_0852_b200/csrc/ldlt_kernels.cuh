@@ -73,6 +73,7 @@ struct DevPlan {
   int tw_smem;          // 1: kernels stage the Montgomery tables in SMEM
   int grid_cap;         // CTAs for grid-stride row kernels
   int debug;            // HGPU_DEBUG bits (bisection aid), 0 in production
+  int recip_fast;       // 1: recip_fast_body (recip_fast.cuh) on shared scratch
   // batched division (the triangular solve's diagonal): instance b =
   // blockIdx.y offsets its rows, reciprocal and scratch by b * these strides
   // (all 0 in the LDL^T, where gridDim.y == 1)
@@ -157,6 +158,8 @@ struct PivotDiv {
 // reciprocal scratch words for diagonal entries of at most dmax_bits bits
 // (PD bound on the stage's precision, as k_recip computes it) and `segs`
 // product segments
+// shared-memory words of recip_fast_body at that bound
+long long recip_fast_words_bound(const DevPlan& P, int dmax_bits);
 long long recip_words_bound(const DevPlan& P, int dmax_bits, int segs);
 // stage p's pivot chain in one CTA: (pd) the previous stage's ratio of row p,
 // the pivot-entry update with the panel's first nslots stages, its

@@ -67,7 +67,15 @@ int hgpu_probe_imad(int kind, double* ops_per_s, double* sm_mhz,
   int dev = 0, nsm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 1;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int threads = 512, blocks = nsm * 4;
+  // one wave: as many 512-thread CTAs per SM as are resident at once (the
+  // register file limits it), so the kernel time is one CTA's cycle count
+  const int threads = 512;
+  int per_sm = 0;
+  if (kind == 0)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, imad32_kernel, threads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, imadwide_kernel, threads, 0);
+  const int blocks = nsm * (per_sm > 0 ? per_sm : 1);
   void* out = nullptr;
   unsigned long long* cyc = nullptr;
   if (cudaMalloc(&out, (size_t)threads * blocks * 8) != cudaSuccess) return 2;
@@ -95,8 +103,8 @@ int hgpu_probe_imad(int kind, double* ops_per_s, double* sm_mhz,
   }
   const double ops = (double)threads * blocks * kIters * kChains;
   *ops_per_s = ops / (best_ms * 1e-3);
-  // every CTA is resident at once (4 x 512 threads per SM), so the kernel
-  // time is the per-CTA cycle count at the SM clock
+  // every CTA is resident at once (one wave), so the kernel time is the
+  // per-CTA cycle count at the SM clock
   *sm_mhz = (double)best_cyc / (best_ms * 1e-3) / 1e6;
   *ops_per_clk_sm = ops / ((double)best_cyc * nsm);
   cudaFree(out);

@@ -113,7 +113,7 @@ def test_group_repeated_and_shifted(hg, ref):
     m = hg.HankelMatrixGPU(strip, k, devices=[0, 0])
     for x in (0, -(1 << (k - 16)), 0):
         got = m.ldlt(x, fold=True)
-        want = po.OracleLib().ldlt(strip, x, k, capture=False)
+        want = po.OracleLib().ldlt(strip, x, k, capture=True)
         assert got.pivots == want.pivots
         assert got.det == want.det
 
