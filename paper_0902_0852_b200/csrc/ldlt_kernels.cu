@@ -429,8 +429,9 @@ __global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long
   extern __shared__ uint32_t sm_dyn[];
   if (P.recip_fast && !use_gscratch && gridDim.y == 1) {
     if (stage_aborted(err)) return;
-    recip_fast_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn, err);
-    return;
+    if (recip_fast_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn,
+                        rf::dyn_smem_words(), err))
+      return;
   }
   recip_body(P, vint, prow, maxbitsV, p, piv, dmax_bits, Ybuf, ys, gscratch,
              use_gscratch, err, blockIdx.y);
@@ -724,11 +725,10 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
   __syncthreads();
   if (ph) t[3] = clock64();
   if (p < P.n - 1) {
-    if (P.recip_fast && !use_gscratch) {
-      extern __shared__ uint32_t sm_dyn[];
-      recip_fast_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn,
-                      err);
-    } else {
+    extern __shared__ uint32_t sm_dyn[];
+    if (!(P.recip_fast && !use_gscratch &&
+          recip_fast_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys, sm_dyn,
+                          rf::dyn_smem_words(), err))) {
       recip_body(P, vint, vrow0 + p, maxbitsV, p, piv, dmax_bits, Ybuf, ys,
                  gscratch, use_gscratch, err, 0, pd.recip_words);
     }
@@ -1266,8 +1266,9 @@ long long recip_fast_words_bound(const DevPlan& P, int dmax_bits) {
 size_t recip_scratch_words(const DevPlan& P) {
   // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
   const size_t Lm = (size_t)P.ycap + 4;
-  return (Lm + 2) + Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
-         6 * (3 * Lm + 2) + 64;
+  const size_t old_words = (Lm + 2) + Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
+                           6 * (3 * Lm + 2) + 64;
+  return std::max(old_words, (size_t)rf_scratch_words((int)Lm));
 }
 
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,

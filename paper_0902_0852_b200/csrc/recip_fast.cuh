@@ -27,6 +27,13 @@ namespace rf {
 
 constexpr int kSegMax = 6;  // i-range segments per column block (planes)
 
+// 32-bit words of the launch's dynamic shared memory
+__device__ __forceinline__ long long dyn_smem_words() {
+  uint32_t b;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(b));
+  return b / 4;
+}
+
 // Block-wide resolution of sum_{k<M} v_k 2^{32k} into 32-bit digits mod
 // 2^{32M}, for v_k + bias in [0, 3 2^32) with bias = 0 or 2^32 - 1 (biased:
 // v_k in [-2^32 + 1, 2^33]; the biases sum to 2^{32M} - 1, so a carry of 1
@@ -224,13 +231,16 @@ __host__ __device__ inline long long rf_scratch_words(int Lm) {
          2LL * (3 * Lm + 4) + 3LL * rf::kSegMax * (Lm + 4) + 64;
 }
 
-__device__ void recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
+// Returns false (having done nothing) when the stage's precision needs more
+// than avail_words of scratch; the caller then runs recip_body.
+__device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
                                 const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
-                                uint32_t* Ybuf, int* ys, uint32_t* sm, int* err) {
+                                uint32_t* Ybuf, int* ys, uint32_t* sm, long long avail_words,
+                                int* err) {
   __shared__ uint32_t red[64];
   const int h = vint.hdr[prow];
   const int nD = h < 0 ? -h : h;
-  if (nD == 0) return;  // flagged as ZeroPivot by k_extract
+  if (nD == 0) return true;  // flagged as ZeroPivot by k_extract
   const uint32_t* Dg = vint.limbs + prow * (long long)P.cap;
   const int n = limbs_bits(Dg, nD);
   int amax;
@@ -250,8 +260,9 @@ __device__ void recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
   const int nYf = (Pt + 2 + 31) / 32 + 1;
   if (nYf > P.ycap) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
-    return;
+    return true;
   }
+  if (rf_scratch_words(Lm) > avail_words) return false;
   const int dbase = max(0, nD - (Lm + 2));
   const int nDs = nD - dbase;
   // Y, Pr and E are product operands b: kGuard zero words on either side
@@ -395,6 +406,7 @@ __device__ void recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
     ys[1] = nY;
     ys[2] = amax;
   }
+  return true;
 }
 
 }  // namespace hgpu
