@@ -481,6 +481,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_UPDATE_TC")) update_tc_ = std::atoi(e) != 0;
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -885,6 +886,7 @@ void Matrix::build(int min_logL) {
   }
 
   CU(configure_kernels(D, &div_smem_, &div_global_, &recip_global_));
+  if (update_tc_) CU(configure_update_tc());
 
   const size_t NW = (size_t)D.NW;
   const int kb = P.kb;
@@ -1204,7 +1206,12 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       CU(cudaEventRecord(uev_[uev_used], us));
     }
     const long long r0 = set_row0(b);
+    const bool tc = update_tc_ && c_end - c_begin <= 32 && nslots <= 256 && D.NW % 4 == 0 &&
+                    D.L % 4 == 0;
     TL(kind, b, us, [&] {
+      if (tc)
+        return launch_update_tc(D, W_, colbase_, vhat_ + r0 * NW, rhat_ + r0 * NW, slot_stride,
+                                nslots, c_begin, c_end, err_, us);
       return launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW,
                            rhat_ + r0 * NW, slot_stride, nslots, c_begin, c_end,
                            err_, us);

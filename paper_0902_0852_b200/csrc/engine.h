@@ -258,6 +258,9 @@ class Matrix {
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
   // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)
   bool pre_entry_ = true;
+  // trailing update on the tensor cores (tc_update.cu, HGPU_UPDATE_TC=1);
+  // bit-identical, measured slower than k_update_tiled: off by default
+  bool update_tc_ = false;
   // the chain's next row on its own stream (HGPU_NEXT_ROW)
   bool next_row_ = false;
   cudaStream_t stream_next_ = nullptr;

@@ -1186,6 +1186,7 @@ __global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
 
 static thread_local long long g_launches = 0;
 long long kernel_launch_count() { return g_launches; }
+long long kernel_launch_count_add(long long k) { return g_launches += k; }
 
 // HGPU_SYNC_DEBUG=1: synchronise after every launch so a fault is reported
 // by the launch that caused it (debug aid; off by default).

@@ -221,6 +221,13 @@ cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
 cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
+// tensor-core trailing update of one band (tc_update.cu)
+cudaError_t launch_update_tc(const DevPlan& P, uint32_t* W, const long long* colbase,
+                             const uint32_t* Vhat, const uint32_t* Rhat,
+                             long long row_stride_slot, int nslots, int c_begin, int c_end,
+                             const int* err, cudaStream_t st);
+cudaError_t configure_update_tc();
+long long kernel_launch_count_add(long long k);
 long long kernel_launch_count();
 // iv_kernels.cu (interval LDL^T)
 // nonpos (optional): set to 1 when some class is not +1

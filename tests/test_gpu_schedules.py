@@ -3,7 +3,8 @@
 The factorisation's results may not depend on how the panel work is spread
 over streams (near/far rows, far lanes, deferred trailing update, SM split)
 nor on how the stage's ratios are formed (k_divide or the int8 tensor-core
-ratio GEMM): every variant must equal the reference's ldlt_det_serial
+ratio GEMM), how the trailing update multiplies (IMAD or the tcgen05 int8
+update, HGPU_UPDATE_TC) or which reciprocal body runs: every variant must equal the reference's ldlt_det_serial
 (ldlt.cpp:31-77) bit for bit.  The knobs are environment variables read when
 a matrix is created (engine.cpp).  N is chosen so that the matrix has far
 rows (N > 64) and several panels (kb = 32).
@@ -32,6 +33,9 @@ VARIANTS = [
     {"HGPU_NEXT_ROW": "1"},
     {"HGPU_NEXT_ROW": "1", "HGPU_PRE_ENTRY": "0", "HGPU_FAR_SUB": "0"},
     {"HGPU_NEXT_ROW": "1", "HGPU_NEAR": "100", "HGPU_EDF": "0"},
+    {"HGPU_UPDATE_TC": "1"},
+    {"HGPU_UPDATE_TC": "1", "HGPU_EDF": "0", "HGPU_FAR_SUB": "0"},
+    {"HGPU_RECIP_FAST": "0"},
 ]
 
 
