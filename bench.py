@@ -247,6 +247,12 @@ def run_gpu(args) -> None:
                       "(hgpu_verify_eigenvalue), strip upload included"}
         del im
 
+    # BASELINE configs 4 and 5 (after everything config 3 measures, so the
+    # device pool they grow does not shape the config-3 numbers)
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        secondary = secondary_configs(hgpu, args)
+
     # roofline of the dominant kernel (trailing update): modular products per
     # launch / average launch time, against the measured IMAD.WIDE rate
     probe = probe_imad()
@@ -277,6 +283,8 @@ def run_gpu(args) -> None:
         "clocks": clk,
     }
     out["parity"] = parity
+    if secondary:
+        out["secondary_configs"] = secondary
     if lam:
         out["time_to_lambda_min"] = lam
     traffic = _profiled_traffic()
@@ -292,6 +300,46 @@ def run_gpu(args) -> None:
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+SECONDARY = [
+    # (config, N, beta_num, beta_den, P)
+    (4, 1500, 1, 2, 65536),
+    (5, 2000, 3, 2, 32768),
+]
+
+
+def secondary_configs(hgpu, args) -> list:
+    """BASELINE configs 4 and 5 at full size on one GPU: one warm-up and
+    one timed factorisation of M - x1 I each (device time, CUDA events), with
+    the trailing update's share (HGPU_PROFILE) beside the panel side.  The
+    config-5 moments come from the repo's threaded build_matrix (bit-identical
+    to the reference's, tests/test_moments.py); its time is reported apart."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    out = []
+    for cfg, n, bn, bd, k in SECONDARY:
+        t0 = time.perf_counter()
+        if (bn, bd) == (1, 2):
+            strip = [2 * math.factorial(2 * (1 + s) - 1) << k for s in range(2 * n - 1)]
+        else:
+            strip = hgpu.build_moments(n, bn, bd, k)
+        t_strip = time.perf_counter() - t0
+        x = x1_shift(strip, k)
+        mm = hgpu.HankelMatrixGPU(strip, k)
+        mm.ldlt(x)
+        r = mm.ldlt(x, profile=True)
+        plan = mm.plan()
+        mm.close()
+        del mm
+        out.append({"config": cfg, "n": n, "beta": f"{bn}/{bd}", "precision_bits": k,
+                    "shift": "x1 (secant.cpp:7-16)", "ms_per_factorisation": r.device_ms,
+                    "mp_macs_per_s": mp_macs(n) / (r.device_ms * 1e-3),
+                    "update_ms": r.update_ms, "update_share": r.update_ms / r.device_ms,
+                    "gpu_launches": r.launches, "plan": plan,
+                    "moments_seconds": round(t_strip, 2),
+                    "moments": "exact factorials" if (bn, bd) == (1, 2)
+                    else "hgpu_build_moments (host threads)"})
+    return out
 
 
 def leading_block_parity(m, x, hgpu) -> dict:
@@ -427,6 +475,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the config 4 / 5 factorisation timings")
     ap.add_argument("--no-lambda", action="store_true",
                     help="skip the time-to-lambda_min measurement")
     args = ap.parse_args()

@@ -739,6 +739,7 @@ FactorResult Matrix::factor_group(const HostInt& x, unsigned flags) {
   for (int attempt = 0; attempt < 4; ++attempt) {
     for (Matrix* m : g.ranks) {
       CU(cudaSetDevice(m->device_));
+      if (m->ws_released_) m->reclaim_workspace();
       if (!m->W_ || (min_logL && m->plan_.logL < min_logL)) m->build(min_logL);
     }
     CU(cudaSetDevice(device_));
@@ -818,6 +819,66 @@ FactorResult Matrix::factor_group(const HostInt& x, unsigned flags) {
     }
   }
   throw Error(HGPU_ERR_CAPACITY, "values outgrew every transform plan");
+}
+
+// Panel slot sets (V/R integers and transforms): two for the lookahead (the
+// interval path: one), 2 + deferral depth (HGPU_DEFER), or one per panel for
+// the EDF schedule, fewer when the device memory would not hold them beside
+// the workspace.
+void Matrix::alloc_slots() {
+  const Plan& P = plan_;
+  const size_t NW = (size_t)dp_.NW;
+  const int kb = P.kb;
+  size_t nsets = 1;
+  if (!interval_) {
+    const int nblocks = (n_ + kb - 1) / kb;
+    nsets = edf_h_ > 0 ? (size_t)nblocks + 1 : 2 + (size_t)std::max(0, defer_);
+    const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
+    const size_t free_b = device_available(device_);
+    while (nsets > 2 && per_set * nsets > 0.6 * (double)free_b) --nsets;
+  }
+  nsets_ = (int)nsets;
+  vhdr_ = dalloc<int>(nsets * kb * n_);
+  rhdr_ = dalloc<int>(nsets * kb * n_);
+  vlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
+  rlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
+  vhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
+  rhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
+  ws_released_ = false;
+}
+
+// The transform-domain solve needs the L-entry transforms of the whole factor
+// (ne x NW words); at configs 4/5 they do not fit beside the factorisation's
+// workspace.  The solves never touch W or the slot sets, so they are handed
+// back to the pool for the solves and taken again by the next factorisation
+// (whose L-entry transforms are recomputed anyway).
+void Matrix::release_workspace() {
+  for (void* q : {(void*)W_, (void*)vhdr_, (void*)rhdr_, (void*)vlimbs_, (void*)rlimbs_,
+                  (void*)vhat_, (void*)rhat_})
+    dfree(q);
+  W_ = vlimbs_ = rlimbs_ = vhat_ = rhat_ = nullptr;
+  vhdr_ = rhdr_ = nullptr;
+  ws_released_ = true;
+}
+
+void Matrix::reclaim_workspace() {
+  release_solve_transforms();
+  W_ = dalloc<uint32_t>((size_t)std::max<long long>(plan_.entries, 1) * dp_.NW);
+  alloc_slots();
+  ws_released_ = false;
+}
+
+void Matrix::release_solve_transforms() {
+  dfree(stw_);
+  dfree(lhat_tab_);
+  for (uint32_t* c : lhat_chunks_) dfree(c);
+  lhat_chunks_.clear();
+  dfree(acch_);
+  dfree(sxhat_);
+  stw_ = acch_ = sxhat_ = nullptr;
+  lhat_tab_ = nullptr;
+  sdp_bits_ = sdp_xbits_ = 0;
+  lhat_for_ = -1;
 }
 
 void Matrix::build(int min_logL) {
@@ -930,28 +991,7 @@ void Matrix::build(int min_logL) {
   if (herr[kErrCapacity])
     throw Error(HGPU_ERR_CAPACITY, "strip does not fit the transform plan");
 
-  // two slot sets: panel b uses set b%2 (lookahead needs b+1 while the
-  // trailing update of b still reads b)
-  // (the interval path has no lookahead: one slot set)
-  // slot sets: 2 + deferral depth (HGPU_DEFER, default 4), fewer when the
-  // device memory would not hold them beside the workspace
-  size_t nsets = 1;
-  if (!interval_) {
-    // EDF schedule (edf_h_ > 0): every panel's sets are kept until all of
-    // its updates ran, memory permitting (else the oldest are flushed)
-    const int nblocks = (n_ + kb - 1) / kb;
-    nsets = edf_h_ > 0 ? (size_t)nblocks + 1 : 2 + (size_t)std::max(0, defer_);
-    const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
-    const size_t free_b = device_available(device_);
-    while (nsets > 2 && per_set * nsets > 0.6 * (double)free_b) --nsets;
-  }
-  nsets_ = (int)nsets;
-  vhdr_ = dalloc<int>(nsets * kb * n_);
-  rhdr_ = dalloc<int>(nsets * kb * n_);
-  vlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
-  rlimbs_ = dalloc<uint32_t>(nsets * kb * n_ * P.cap);
-  vhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
-  rhat_ = dalloc<uint32_t>(nsets * kb * n_ * NW);
+  alloc_slots();
   phdr_ = dalloc<int>(n_);
   plimbs_ = dalloc<uint32_t>((size_t)n_ * P.cap);
   // reciprocals in a ring of kYRing stage sets: the far-row divisions of
@@ -2003,16 +2043,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         // solve() falls back to the schoolbook AXPY
         sdp_bits_ = sdp_xbits_ = 0;
         lhat_for_ = -1;
-        auto unplan = [&]() {
-          dfree(stw_);
-          dfree(lhat_tab_);
-          for (uint32_t* c : lhat_chunks_) dfree(c);
-          lhat_chunks_.clear();
-          dfree(acch_);
-          dfree(sxhat_);
-          stw_ = acch_ = sxhat_ = nullptr;
-          lhat_tab_ = nullptr;
-        };
+        auto unplan = [&]() { release_solve_transforms(); };
         try {
         DevPlan S{};
         S.n = n;
@@ -2041,8 +2072,14 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
         S.debug = dp_.debug;
         int ok = 0;
         CU(configure_solve_ntt(S, P.cap, Wv, Wa, &ok));
-        const size_t fr = device_available(device_);
+        size_t fr = device_available(device_);
         const size_t need = ((size_t)ne + n + 2) * S.NW * 4;
+        if (ok && need + (1ull << 30) > fr && W_ && !interval_) {
+          // the factorisation's workspace is idle during the solves
+          CU(cudaStreamSynchronize(st));
+          release_workspace();
+          fr = device_available(device_);
+        }
         if (!ok || need + (1ull << 30) > fr)
           throw Error(HGPU_ERR_CAPACITY, "transform-domain solve does not fit");
         // chunks of <= 256 MB: a warm pool serves them from the blocks the
@@ -2300,6 +2337,7 @@ FactorResult Matrix::factor(const HostInt& x, unsigned flags) {
     return factor_group(x, flags);
   }
   CU(cudaSetDevice(device_));
+  if (ws_released_) reclaim_workspace();
   FactorResult res;
   res.n = n_;
   res.K = K_;

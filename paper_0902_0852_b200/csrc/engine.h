@@ -103,7 +103,7 @@ class Matrix {
     return factor(x, flags);
   }
   const Plan& plan_or_build() {
-    if (!W_) build(0);
+    if (!W_ && !ws_released_) build(0);
     return plan_;
   }
   int frac_bits() const { return K_; }
@@ -137,6 +137,10 @@ class Matrix {
   void group_wait_pulled(int b, cudaStream_t st);
   void group_merge_err(int* herr);
   void build(int min_logL);
+  void alloc_slots();
+  void release_workspace();   // W and slot sets back to the pool (solves)
+  void reclaim_workspace();   // ... and taken again by the next factorisation
+  void release_solve_transforms();
   void release();
   void run(const HostInt& x, unsigned flags, FactorResult& res);
   void panel_broadcast(int owner, int p0, int ns, long long row0,
@@ -261,6 +265,7 @@ class Matrix {
   // trailing update on the tensor cores (tc_update.cu, HGPU_UPDATE_TC=1);
   // bit-identical, measured slower than k_update_tiled: off by default
   bool update_tc_ = false;
+  bool ws_released_ = false;  // W / slot sets handed to the solves' transforms
   // the chain's next row on its own stream (HGPU_NEXT_ROW)
   bool next_row_ = false;
   cudaStream_t stream_next_ = nullptr;
