@@ -139,30 +139,64 @@ def _dist_env():
 
 
 def run_gpu(args) -> None:
+    """N GPUs: by default one process drives all N as an in-process rank
+    group (hgpu_matrix_new_group: panels published with CUDA events, pulled
+    over NVLink peer memory) while the other torchrun ranks wait for it;
+    --transport nccl runs one rank per process with the NCCL panel
+    broadcast instead."""
     import torch
-    world, rank, local = _dist_env()
-    if world > 1:
+    world_env, rank, local = _dist_env()
+    if world_env > 1 and args.transport == "group":
+        import torch.distributed as dist
+        dist.init_process_group("gloo")  # rendezvous only; no device traffic
+        try:
+            if rank == 0:
+                _run_gpu_body(args, hgpu_devices=list(range(world_env)), nccl=False, rank=0, local=0)
+        finally:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    if world_env <= 1 and os.environ.get("BENCH_RANK_DEVICES"):
+        # the rank-group path on explicit devices (a device may repeat: the
+        # multi-rank schedule on a one-GPU lease)
+        devs = [int(d) for d in os.environ["BENCH_RANK_DEVICES"].split(",")]
+        _run_gpu_body(args, hgpu_devices=devs, nccl=False, rank=0, local=devs[0])
+        return
+    if world_env > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _run_gpu_body(args, hgpu_devices=[local], nccl=world_env > 1, rank=rank, local=local)
+
+
+def _run_gpu_body(args, hgpu_devices, nccl, rank, local) -> None:
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1")) if nccl else 1
+    ndev = world if nccl else len(hgpu_devices)
     torch.cuda.set_device(local)
     from paper_0902_0852_b200 import hgpu
     n, k = CONFIG["n"], CONFIG["precision_bits"]
     strip = config_strip(n, k)
     x = x1_shift(strip, k)
 
-    m = hgpu.HankelMatrixGPU(strip, k, device=local)
-    if world > 1:
-        import torch.distributed as dist
-        obj = [hgpu.HankelMatrixGPU.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        m.set_comm(rank, world, obj[0])
+    def new_matrix():
+        mm = hgpu.HankelMatrixGPU(strip, k, device=local,
+                                  devices=hgpu_devices if len(hgpu_devices) > 1 else None)
+        if nccl:
+            import torch.distributed as dist
+            obj = [hgpu.HankelMatrixGPU.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            mm.set_comm(rank, world, obj[0])
+        return mm
+
+    m = new_matrix()
     plan = m.plan()
 
     def barrier():
-        if world > 1:
+        if nccl:
             import torch.distributed as dist
             dist.barrier()
-        torch.cuda.synchronize()
+        for d in sorted(set(hgpu_devices)):
+            torch.cuda.synchronize(d)
 
     for _ in range(args.warmup):
         m.ldlt(x)
@@ -179,7 +213,7 @@ def run_gpu(args) -> None:
     barrier()
     clk = clocks.stop()
     total_ms = sum(dev_ms)
-    if world > 1:
+    if nccl:
         import torch.distributed as dist
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -203,12 +237,7 @@ def run_gpu(args) -> None:
     for _ in range(max(1, min(args.steps, 3))):
         barrier()
         t0 = time.perf_counter()
-        mm = hgpu.HankelMatrixGPU(strip, k, device=local)
-        if world > 1:
-            import torch.distributed as dist
-            obj = [hgpu.HankelMatrixGPU.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            mm.set_comm(rank, world, obj[0])
+        mm = new_matrix()
         rr = mm.ldlt(x)
         barrier()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
@@ -220,10 +249,10 @@ def run_gpu(args) -> None:
     # refactorisation from the seed-0 start vector, x = 0, to the 2^-(P/2)
     # rule, through the public API (single rank: the solve is not sharded)
     lam = None
-    if world == 1 and not args.no_lambda:
+    if not nccl and not args.no_lambda:
         barrier()
         t0 = time.perf_counter()
-        mm = hgpu.HankelMatrixGPU(strip, k, device=local)
+        mm = new_matrix()
         rq = hgpu.inverse_iteration(mm, hgpu.seeded_start_vector(n, k), 0, 40, digits=40)
         barrier()
         lam = {"seconds": time.perf_counter() - t0, "iterations": rq["iterations"],
@@ -250,7 +279,7 @@ def run_gpu(args) -> None:
     # BASELINE configs 4 and 5 (after everything config 3 measures, so the
     # device pool they grow does not shape the config-3 numbers)
     secondary = None
-    if world == 1 and not args.no_secondary:
+    if ndev == 1 and not args.no_secondary:
         secondary = secondary_configs(hgpu, args)
 
     # roofline of the dominant kernel (trailing update): modular products per
@@ -263,11 +292,14 @@ def run_gpu(args) -> None:
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": ndev, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32 (exact mod-q residues, 32-bit limbs)",
         "data": "synthetic: exact factorial moments (the reference's beta=1 strip)",
-        "config": dict(CONFIG, parallelism=f"column-block-cyclic x{world}",
+        "config": dict(CONFIG, parallelism=f"column-block-cyclic x{ndev}",
+                       transport=("nccl broadcast, one process per GPU" if nccl else
+                                  "in-process rank group, NVLink peer reads" if ndev > 1
+                                  else "single rank"),
                        plan=plan),
         "limb_products_per_s": schoolbook_limb_products(n, k) / (ms_per_step * 1e-3),
         "e2e": {"value": mp_macs(n) / (e2e_step * 1e-3), "unit": UNIT,
@@ -293,11 +325,11 @@ def run_gpu(args) -> None:
         out["roofline"]["traffic_source"] = traffic["source"]
         # the same kernel profiled alone: IMAD.WIDE (FMA-heavy) pipe busy %
         out["roofline"]["ncu_imad_pipe_frac_alone"] = (traffic["pipe_pct"] or 0) / 100 or None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ndev == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if nccl:
         import torch.distributed as dist
         dist.destroy_process_group()
 
@@ -475,6 +507,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="group", choices=["group", "nccl"],
+                    help="N > 1: one process drives every GPU (group) or one NCCL rank per process")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the config 4 / 5 factorisation timings")
     ap.add_argument("--no-lambda", action="store_true",
