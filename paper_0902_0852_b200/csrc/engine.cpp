@@ -439,6 +439,8 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
     }
     const GreenSplit& g = green_split(device_, want);
     if (g.ok) {
+      split_ga_ = (void*)g.ga;
+      split_gb_ = (void*)g.gb;
       // bulk stream on the large group, pivot chain on the reserved SMs;
       // the panel stream where HGPU_SM_SPLIT places it
       stream_ = green_stream(g.gb, 0);
@@ -461,13 +463,22 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&stream_upd1_, cudaStreamNonBlocking, hi));
+    // with an SM split every other stream lives on the large group, so the
+    // reserved SMs run the pivot chain alone (primary-context streams would
+    // still reach them)
+    const bool excl = split_gb_ != nullptr;
+    if (excl)
+      stream_upd1_ = green_stream((CUgreenCtx)split_gb_, hi);
+    else
+      CU(cudaStreamCreateWithPriority(&stream_upd1_, cudaStreamNonBlocking, hi));
     // HGPU_UPD_SMS=k: the deferred update runs on k SMs only (green context)
     int upd_sms = 0;
     if (const char* e = std::getenv("HGPU_UPD_SMS")) upd_sms = std::atoi(e);
     const GreenSplit& gu = green_split(device_, upd_sms);
     if (gu.ok)
       stream_upd2_ = green_stream(gu.ga, lo);
+    else if (excl)
+      stream_upd2_ = green_stream((CUgreenCtx)split_gb_, lo);
     else
       CU(cudaStreamCreateWithPriority(&stream_upd2_, cudaStreamNonBlocking, lo));
   }
@@ -485,8 +496,14 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CU(cudaStreamCreateWithPriority(&stream_pre_, cudaStreamNonBlocking, hi));
-    CU(cudaStreamCreateWithPriority(&stream_next_, cudaStreamNonBlocking, hi));
+    if (split_gb_) {
+      // the pivot entry's early stages gate k_pivot: on the chain's SMs
+      stream_pre_ = green_stream((CUgreenCtx)split_ga_, hi);
+      stream_next_ = green_stream((CUgreenCtx)split_gb_, hi);
+    } else {
+      CU(cudaStreamCreateWithPriority(&stream_pre_, cudaStreamNonBlocking, hi));
+      CU(cudaStreamCreateWithPriority(&stream_next_, cudaStreamNonBlocking, hi));
+    }
   }
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
@@ -495,8 +512,12 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     far_streams_[0] = stream_far_;
-    for (int l = 1; l < kMaxFarLanes; ++l)
-      CU(cudaStreamCreateWithPriority(&far_streams_[l], cudaStreamNonBlocking, hi));
+    for (int l = 1; l < kMaxFarLanes; ++l) {
+      if (split_gb_)
+        far_streams_[l] = green_stream((CUgreenCtx)split_gb_, hi);
+      else
+        CU(cudaStreamCreateWithPriority(&far_streams_[l], cudaStreamNonBlocking, hi));
+    }
     for (int l = 0; l < kMaxFarLanes; ++l)
       CU(cudaEventCreateWithFlags(&far_ev_[l], cudaEventDisableTiming));
   }

@@ -226,6 +226,9 @@ class Matrix {
   int pivot_segs_ = 6;       // k_pivot's reciprocal product segments (HGPU_PIVOT_SEGS)
   int nsets_ = 2;   // V/R slot sets (2 + deferral, memory permitting)
   int chain_sms_ = 0;  // SMs reserved for the pivot chain (green context), 0 = none
+  // HGPU_SM_SPLIT partition (CUgreenCtx of the chain's and the other SMs)
+  void* split_ga_ = nullptr;
+  void* split_gb_ = nullptr;
   std::vector<cudaEvent_t> pev_, sev_;
   bool recip_bound_ = true;  // reciprocal precision from the PD bound
   // whole L factor (HGPU_KEEP_L): R_p[r], p < r, packed strictly lower

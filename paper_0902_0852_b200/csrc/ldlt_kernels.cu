@@ -681,12 +681,11 @@ __global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
 // fused to save two launches per stage): column p's pivot entry receives the
 // panel's stages [0, s) (as k_update_col), is extracted (k_extract, row p:
 // pivot, V_p[p], ZeroPivot) and the stage's reciprocal is formed (k_recip).
-__global__ void __launch_bounds__(512)
-k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
-        const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
-        IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
-        int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
-        int use_gscratch, int* err, PivotDiv pd) {
+__device__ __forceinline__ void pivot_body(
+    DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+    const uint32_t* Rhat, long long row_stride_slot, int nslots, int p, IntBuf vint,
+    long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat, int* maxdegV, int dmax_bits,
+    uint32_t* Ybuf, int* ys, uint32_t* gscratch, int use_gscratch, int* err, PivotDiv pd) {
   if (stage_aborted(err)) return;
   // HGPU_DEBUG & 4096: phase clocks of sampled stages (timing aid)
   const bool ph = (P.debug & 4096) && p % 100 == 50 && threadIdx.x == 0;
@@ -738,6 +737,30 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
     printf("k_pivot p=%d div %lld col %lld extract %lld recip %lld cycles\n", p,
            t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3]);
   }
+}
+
+__global__ void __launch_bounds__(512)
+k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+        const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
+        IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
+        int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+        int use_gscratch, int* err, PivotDiv pd) {
+  pivot_body(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, p, vint, vrow0, piv, maxbitsV,
+             vhat, maxdegV, dmax_bits, Ybuf, ys, gscratch, use_gscratch, err, pd);
+}
+
+// The same chain step in a footprint that fits beside two k_update_tiled
+// CTAs on one SM (256 threads, <= 80 registers: 20K of the 64K registers;
+// the 512-thread kernel needs a whole SM's register file, so in the step it
+// waits for an SM to drain completely).
+__global__ void __launch_bounds__(256, 3)
+k_pivot_lean(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+             const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
+             IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
+             int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
+             int use_gscratch, int* err, PivotDiv pd) {
+  pivot_body(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, p, vint, vrow0, piv, maxbitsV,
+             vhat, maxdegV, dmax_bits, Ybuf, ys, gscratch, use_gscratch, err, pd);
 }
 
 // ------------------------------------------- ratios on the tensor cores ---
@@ -1303,9 +1326,14 @@ cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase
     const int v = e ? atoi(e) : 512;
     return (v >= 128 && v <= 512 && v % 32 == 0) ? v : 512;
   }();
-  k_pivot<<<1, threads, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
-                                p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
-                                dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
+  if (threads == 256)
+    k_pivot_lean<<<1, 256, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
+                                       p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
+                                       dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
+  else
+    k_pivot<<<1, threads, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
+                                  p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
+                                  dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
   return post_launch(st);
 }
 
@@ -1488,6 +1516,9 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
     const size_t dv = divide_smem_words(P) * 4;
     if ((int)dv <= maxopt) piv_smem = std::max(piv_smem, dv);
     if ((e = cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)piv_smem)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(k_pivot_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)piv_smem)) != cudaSuccess)
       return e;
   }
