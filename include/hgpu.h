@@ -230,6 +230,11 @@ hgpu_status hgpu_matrix_plan(const hgpu_matrix* m, int* nprimes, int* length,
  * to blocks of `block` columns). */
 int hgpu_block_owner(long block_index, int world);
 
+/* Returns every idle block of the device's stream-ordered memory pool to the
+ * driver (the engine keeps freed blocks for reuse, so repeated matrices skip
+ * cudaMalloc): lets a caller measure a cold start in a warm process. */
+hgpu_status hgpu_trim_pool(int device);
+
 long hgpu_last_zero_pivot(void);
 const char* hgpu_last_error(void);
 const char* hgpu_version(void);

@@ -2,6 +2,7 @@
 // it: every status-returning entry point maps hgpu::Error (and anything else)
 // to a status and a thread-local message, like the reference's C ABI does
 // (/root/reference/proj/src/capi.cpp:24-35, :118-139).
+#include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <cstring>
@@ -71,6 +72,15 @@ long hgpu_last_zero_pivot(void) { return g_last_pivot; }
 
 int hgpu_block_owner(long block_index, int world) {
   return world < 1 ? 0 : hgpu::block_owner(block_index, world);
+}
+
+hgpu_status hgpu_trim_pool(int device) {
+  return guarded([&] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(pool, 0) != cudaSuccess)
+      throw hgpu::Error(HGPU_ERR_CUDA, "cannot trim the device memory pool");
+  });
 }
 
 hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,

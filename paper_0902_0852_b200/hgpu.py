@@ -48,7 +48,7 @@ EXPORTS = (
     "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
     "hgpu_build_moments", "hgpu_buffer_free", "hgpu_matrix_set_capture_rows",
     "hgpu_matrix_new_group", "hgpu_matrix_world", "hgpu_verify_eigenvalue_ex",
-    "hgpu_factor_net_ms",
+    "hgpu_factor_net_ms", "hgpu_trim_pool",
 )
 
 
@@ -112,6 +112,7 @@ def load() -> ctypes.CDLL:
     lib.hgpu_factor_device_ms.restype = ctypes.c_double
     lib.hgpu_factor_update_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(ctypes.c_double)]
+    lib.hgpu_trim_pool.argtypes = [ctypes.c_int]
     lib.hgpu_factor_net_ms.argtypes = [vp]
     lib.hgpu_factor_net_ms.restype = ctypes.c_double
     lib.hgpu_factor_launches.argtypes = [vp]
@@ -495,6 +496,11 @@ def inverse_iteration(m: "HankelMatrixGPU", u: list[int], sigma: int = 0, max_it
     eig = _take_string(ev)
     rhos = [int(l, 16) for l in _take_string(tr).split("\n") if l.strip()]
     return {"eigenvalue": eig, "rho": rhos, "iterations": it.value, "seconds": secs.value}
+
+
+def trim_pool(device: int = 0) -> None:
+    """Hands the engine's idle pool blocks back to the driver (cold start)."""
+    _check(load().hgpu_trim_pool(device))
 
 
 def block_owner(block: int, world: int) -> int:
