@@ -493,6 +493,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_UPDATE_TC")) update_tc_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_COL_EXTRACT")) col_extract_ = std::atoi(e);
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1571,15 +1572,23 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
           }
           // near rows of column p on the panel stream (rows > p)
           const int rb = nr ? p + 2 : p + 1;
-          TL(3, p, sp, [&] {
-            return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
-                                     p, rb, rn, err_, sp);
-          });
-          TL(4, p, sp, [&] {
-            return launch_extract(D, W_, colbase_, p, rb, rn, vint, row0,
-                                  piv, maxbitsV, vhat_, maxdegV, err_, sp, 0,
-                                  rg_near ? vdig_ : nullptr, rg_kd_);
-          });
+          if (col_extract_ & 1) {
+            TL(4, p, sp, [&] {
+              return launch_col_extract(D, W_, colbase_, vh, rh, slot_stride, s, p, rb, rn,
+                                        vint, row0, piv, maxbitsV, vhat_, maxdegV, err_, sp,
+                                        rg_near ? vdig_ : nullptr, rg_kd_);
+            });
+          } else {
+            TL(3, p, sp, [&] {
+              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+                                       p, rb, rn, err_, sp);
+            });
+            TL(4, p, sp, [&] {
+              return launch_extract(D, W_, colbase_, p, rb, rn, vint, row0,
+                                    piv, maxbitsV, vhat_, maxdegV, err_, sp, 0,
+                                    rg_near ? vdig_ : nullptr, rg_kd_);
+            });
+          }
           CU(cudaEventRecord(sev_[4 * p], sp));
           // R_p[p+1] on the chain (it only needs V_p[p+1] besides the pivot):
           // inside the next stage's k_pivot, except at the panel's last stage
@@ -1628,16 +1637,26 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               // column p receives the stages of its own sub-panel [ps, p);
               // earlier sub-panels arrived by the rank-fsub updates below
               const int ps = fsub > 0 ? p0 + (s / fsub) * fsub : p0;
-              TL(10, p, fs, [&] {
-                return launch_update_col(D, W_, colbase_, vh + (ps - p0) * slot_stride,
-                                         rh + (ps - p0) * slot_stride, slot_stride,
-                                         p - ps, p, lo, hi, err_, fs);
-              });
-              TL(11, p, fs, [&] {
-                return launch_extract(D, W_, colbase_, p, lo, hi, vint, row0,
-                                      piv, maxbitsV, vhat_, maxdegV, err_, fs, 0,
-                                      rg_far ? vdig_ : nullptr, rg_kd_);
-              });
+              if (col_extract_ & 2) {
+                TL(11, p, fs, [&] {
+                  return launch_col_extract(D, W_, colbase_, vh + (ps - p0) * slot_stride,
+                                            rh + (ps - p0) * slot_stride, slot_stride, p - ps,
+                                            p, lo, hi, vint, row0, piv, maxbitsV, vhat_,
+                                            maxdegV, err_, fs, rg_far ? vdig_ : nullptr,
+                                            rg_kd_);
+                });
+              } else {
+                TL(10, p, fs, [&] {
+                  return launch_update_col(D, W_, colbase_, vh + (ps - p0) * slot_stride,
+                                           rh + (ps - p0) * slot_stride, slot_stride,
+                                           p - ps, p, lo, hi, err_, fs);
+                });
+                TL(11, p, fs, [&] {
+                  return launch_extract(D, W_, colbase_, p, lo, hi, vint, row0,
+                                        piv, maxbitsV, vhat_, maxdegV, err_, fs, 0,
+                                        rg_far ? vdig_ : nullptr, rg_kd_);
+                });
+              }
               CU(cudaStreamWaitEvent(fs, sev_[4 * p + 1], 0));
               if (rg_far) {
                 TL(12, p, fs, [&] {

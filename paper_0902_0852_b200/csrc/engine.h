@@ -268,6 +268,9 @@ class Matrix {
   // trailing update on the tensor cores (tc_update.cu, HGPU_UPDATE_TC=1);
   // bit-identical, measured slower than k_update_tiled: off by default
   bool update_tc_ = false;
+  // near (bit 1) / far (bit 2) rows' column update fused with the extraction
+  // (k_col_extract, HGPU_COL_EXTRACT)
+  int col_extract_ = 0;
   bool ws_released_ = false;  // W / slot sets handed to the solves' transforms
   // the chain's next row on its own stream (HGPU_NEXT_ROW)
   bool next_row_ = false;

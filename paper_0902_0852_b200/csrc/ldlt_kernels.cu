@@ -197,6 +197,50 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
   }
 }
 
+// Near / far rows of stage p in one launch: each CTA takes a row, applies the
+// panel's pending stages to its entry W[r][p] (k_update_col's arithmetic, as
+// k_pivot does for the pivot entry) and extracts it (extract_body).  One
+// launch instead of two per stage on the panel's latency path, and no wait
+// for the column update's grid to drain.
+__global__ void __launch_bounds__(256)
+k_col_extract(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+              const uint32_t* Rhat, long long row_stride_slot, int nslots, int p, int r_begin,
+              int r_end, IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
+              int* maxdegV, int* err, uint8_t* vdig, int kd) {
+  if (stage_aborted(err)) return;
+  const long long NW = P.NW;
+  for (int r = r_begin + blockIdx.x; r < r_end; r += gridDim.x) {
+    if (nslots > 0) {
+      uint32_t* dst = W + (colbase[p] + (r - p)) * NW;
+      const uint32_t* vp = Vhat + (long long)p * NW;
+      const uint32_t* rp = Rhat + (long long)r * NW;
+      for (int wd = threadIdx.x; wd < P.NW; wd += blockDim.x) {
+        uint64_t acc = 0;
+        int s = 0;
+        for (; s + 1 < nslots; s += 2) {
+          const long long o0 = s * row_stride_slot + wd, o1 = o0 + row_stride_slot;
+          const uint32_t v0 = __ldg(vp + o0), r0 = __ldg(rp + o0);
+          const uint32_t v1 = __ldg(vp + o1), r1 = __ldg(rp + o1);
+          acc += (uint64_t)v0 * r0;
+          acc += (uint64_t)v1 * r1;
+        }
+        if (s < nslots) {
+          const long long o0 = s * row_stride_slot + wd;
+          acc += (uint64_t)__ldg(vp + o0) * __ldg(rp + o0);
+        }
+        const PrimeConsts& pc = P.pc[wd / P.L];
+        const uint32_t t32 = reduce_sum64(acc, pc);
+        const uint32_t old = dst[wd];
+        dst[wd] = old >= t32 ? old - t32 : old + pc.q - t32;
+      }
+      __syncthreads();
+    }
+    extract_body(P, W, colbase, p, r, r + 1, vint, vrow0, piv, maxbitsV, vhat, maxdegV, err, 0,
+                 vdig, kd, 0, 1);
+    __syncthreads();
+  }
+}
+
 __global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, int r_begin, int r_end, IntBuf vint,
                           long long vrow0, IntBuf piv, int* maxbitsV,
@@ -1469,6 +1513,21 @@ cudaError_t launch_update_rect(const DevPlan& P, uint32_t* W,
   return post_launch(st);
 }
 
+cudaError_t launch_col_extract(const DevPlan& P, uint32_t* W, const long long* colbase,
+                               const uint32_t* Vhat, const uint32_t* Rhat,
+                               long long row_stride_slot, int nslots, int p, int r_begin,
+                               int r_end, IntBuf vint, long long vrow0, IntBuf piv,
+                               int* maxbitsV, uint32_t* vhat, int* maxdegV, int* err,
+                               cudaStream_t st, uint8_t* vdig, int kd) {
+  const int rows = r_end - r_begin;
+  if (rows <= 0) return cudaSuccess;
+  ++g_launches;
+  k_col_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
+      P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, p, r_begin, r_end, vint, vrow0, piv,
+      maxbitsV, vhat, maxdegV, err, vdig, kd);
+  return post_launch(st);
+}
+
 cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
                               const long long* colbase, const uint32_t* Vhat,
                               const uint32_t* Rhat, long long row_stride_slot,
@@ -1503,6 +1562,14 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
   if ((int)ext > maxopt || (int)fwd > maxopt) return cudaErrorInvalidValue;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k_extract,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ext)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_fwd_ints,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fwd)) != cudaSuccess)
+    return e;
+    if ((e = cudaFuncSetAttribute(k_col_extract,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ext)) != cudaSuccess)
     return e;

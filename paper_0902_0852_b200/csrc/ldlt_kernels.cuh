@@ -222,6 +222,14 @@ cudaError_t launch_validate(const DevPlan& P, const int* maxdegV,
                             const int* maxdegR, int nstages, int* err,
                             cudaStream_t st);
 // tensor-core trailing update of one band (tc_update.cu)
+// column update of rows [r_begin, r_end) with the panel's nslots pending
+// stages fused with their extraction (one CTA per row)
+cudaError_t launch_col_extract(const DevPlan& P, uint32_t* W, const long long* colbase,
+                               const uint32_t* Vhat, const uint32_t* Rhat,
+                               long long row_stride_slot, int nslots, int p, int r_begin,
+                               int r_end, IntBuf vint, long long vrow0, IntBuf piv,
+                               int* maxbitsV, uint32_t* vhat, int* maxdegV, int* err,
+                               cudaStream_t st, uint8_t* vdig, int kd);
 cudaError_t launch_update_tc(const DevPlan& P, uint32_t* W, const long long* colbase,
                              const uint32_t* Vhat, const uint32_t* Rhat,
                              long long row_stride_slot, int nslots, int c_begin, int c_end,

@@ -1,0 +1,4 @@
+for i in 1 2 3; do for v in "HGPU_COL_EXTRACT=0" "HGPU_COL_EXTRACT=1"; do
+  env $v python bench.py --steps 5 --warmup 3 --no-lambda --no-cpu-baseline --no-secondary > gpurun_out/sw.json 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/sw.json').read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step'],1), d['parity']['bit_exact'])"
+done; done

@@ -36,6 +36,9 @@ VARIANTS = [
     {"HGPU_UPDATE_TC": "1"},
     {"HGPU_UPDATE_TC": "1", "HGPU_EDF": "0", "HGPU_FAR_SUB": "0"},
     {"HGPU_RECIP_FAST": "0"},
+    {"HGPU_COL_EXTRACT": "3"},
+    {"HGPU_PIVOT_THREADS": "256", "HGPU_COL_EXTRACT": "1"},
+    {"HGPU_SM_SPLIT": "4:b", "HGPU_COL_EXTRACT": "1"},
 ]
 
 
