@@ -710,7 +710,21 @@ __device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int 
   }
 }
 
-__global__ void k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+__global__ void __launch_bounds__(256, 3) k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+                         int r_begin, int r_end,
+                         const uint32_t* Ybuf, const int* ys, IntBuf rint,
+                         long long rrow0, uint32_t* rhat, int* maxdegR,
+                         uint32_t* gscratch, int use_gscratch, int* err,
+                         IvDiv iv) {
+  divide_body(P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat,
+              maxdegR, gscratch, use_gscratch, err, iv, blockIdx.x, gridDim.x,
+              blockIdx.y);
+}
+
+// A single row (the pivot chain's next row) with 512 threads; the multi-row
+// kernel above is held to 80 registers so that a CTA fits beside two
+// trailing-update CTAs on an SM instead of waiting for one to leave.
+__global__ void __launch_bounds__(512) k_divide1(DevPlan P, IntBuf vint, long long vrow0, int p,
                          int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
@@ -1425,9 +1439,14 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
                                    : divide_smem_words(P) * 4;
   ++g_launches;
-  k_divide<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, smem, st>>>(
-      P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
-      gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
+  if (rows == 1)
+    k_divide1<<<1, 512, smem, st>>>(P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0,
+                                    rhat, maxdegR, gscratch, use_gscratch, err,
+                                    iv ? *iv : IvDiv{});
+  else
+    k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
+        P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
+        gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
   return post_launch(st);
 }
 
@@ -1611,12 +1630,20 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   tab)) != cudaSuccess)
       return e;
+    if ((e = cudaFuncSetAttribute(k_divide1,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  tab)) != cudaSuccess)
+      return e;
     if ((e = cudaFuncSetAttribute(k_ratio_finish,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   tab)) != cudaSuccess)
       return e;
   } else {
     if ((e = cudaFuncSetAttribute(k_divide,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)div)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(k_divide1,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)div)) != cudaSuccess)
       return e;
