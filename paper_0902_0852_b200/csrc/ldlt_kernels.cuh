@@ -74,6 +74,8 @@ struct DevPlan {
   int grid_cap;         // CTAs for grid-stride row kernels
   int debug;            // HGPU_DEBUG bits (bisection aid), 0 in production
   int recip_fast;       // 1: recip_fast_body (recip_fast.cuh) on shared scratch
+  int tw_global;        // solve plans: 1 = NTT twiddles read from global (L1/L2)
+                        // instead of staged in shared memory (large NW)
   // batched division (the triangular solve's diagonal): instance b =
   // blockIdx.y offsets its rows, reciprocal and scratch by b * these strides
   // (all 0 in the LDL^T, where gridDim.y == 1)
@@ -288,7 +290,7 @@ cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf 
 // transform-domain AXPY of the triangular solves (solve_kernels.cu, opt-in):
 // plan S, per-factorisation transforms of L, per-step launch
 size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa);
-cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* ok);
+cudaError_t configure_solve_ntt(DevPlan& S, int cap, int Wv, int Wa, int* ok);
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
                               EntryStore rhat, int grid_cap, int* err, cudaStream_t st);
 cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint32_t* xhat,

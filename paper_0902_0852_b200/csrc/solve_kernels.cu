@@ -237,7 +237,7 @@ __global__ void k_int_bits(IntBuf v, int idx0, int step, int stride, int count,
 // red 64
 __host__ __device__ inline long long solve_ntt_words(const DevPlan& S, int Wv, int Wa) {
   const long long M = S.L + S.T;
-  return 3LL * S.NW + 4 * M + (Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
+  return (S.tw_global ? 1LL : 3LL) * S.NW + 4 * M + (Wa + 1) + (Wv + 1) + (Wv + 2) + 64;
 }
 constexpr int kSolveNttThreads = 1024;
 
@@ -316,18 +316,23 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
   const int t = target(0);
   const int M = S.L + S.T;
   uint32_t* A = sm;
-  uint32_t* twf = A + NW;
-  uint32_t* twi = twf + NW;
-  int64_t* Ssum = reinterpret_cast<int64_t*>(twi + NW);
+  // twiddles staged in shared memory, or (tw_global: plans whose 3 NW words
+  // do not fit) read from global memory through L1
+  uint32_t* twf_s = A + NW;
+  uint32_t* twi_s = twf_s + NW;
+  const uint32_t* twf = S.tw_global ? S.twm : twf_s;
+  const uint32_t* twi = S.tw_global ? S.itwm : twi_s;
+  int64_t* Ssum = reinterpret_cast<int64_t*>(S.tw_global ? A + NW : twi_s + NW);
   uint64_t* Dg = reinterpret_cast<uint64_t*>(Ssum + M);
   uint32_t* M1 = reinterpret_cast<uint32_t*>(Dg + M);
   uint32_t* T = M1 + Wa + 1;
   uint32_t* X = T + Wv + 1;
   uint32_t* red = X + Wv + 2;
-  for (int i = threadIdx.x; i < NW / 4; i += blockDim.x) {
-    reinterpret_cast<uint4*>(twf)[i] = reinterpret_cast<const uint4*>(S.twm)[i];
-    reinterpret_cast<uint4*>(twi)[i] = reinterpret_cast<const uint4*>(S.itwm)[i];
-  }
+  if (!S.tw_global)
+    for (int i = threadIdx.x; i < NW / 4; i += blockDim.x) {
+      reinterpret_cast<uint4*>(twf_s)[i] = reinterpret_cast<const uint4*>(S.twm)[i];
+      reinterpret_cast<uint4*>(twi_s)[i] = reinterpret_cast<const uint4*>(S.itwm)[i];
+    }
   const bool stamp = (S.debug & 8192) && (j == 500 || j == 501) && threadIdx.x == 0;
   long long c0 = stamp ? clock64() : 0, c1 = 0, c2 = 0, c3 = 0;
   unsigned long long g0 = 0;
@@ -417,9 +422,11 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   const int t = live ? target(0) : 0;
   const int M = L + S.T;
   uint32_t* A = sm;
-  uint32_t* twf = A + NW;
-  uint32_t* twi = twf + NW;
-  int64_t* Ssum = reinterpret_cast<int64_t*>(twi + NW);
+  uint32_t* twf_s = A + NW;
+  uint32_t* twi_s = twf_s + NW;
+  const uint32_t* twf = S.tw_global ? S.twm : twf_s;
+  const uint32_t* twi = S.tw_global ? S.itwm : twi_s;
+  int64_t* Ssum = reinterpret_cast<int64_t*>(S.tw_global ? A + NW : twi_s + NW);
   uint64_t* Dg = reinterpret_cast<uint64_t*>(Ssum + M);
   uint32_t* M1 = reinterpret_cast<uint32_t*>(Dg + M);
   uint32_t* T = M1 + Wa + 1;
@@ -428,10 +435,10 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
   const PrimeConsts& c = S.pc[rk];
   uint32_t* Ar = A + rk * L;
   const int qs = (L + nc - 1) / nc;  // coefficients per CTA after the exchange
-  if (live) {
+  if (live && !S.tw_global) {
     for (int i = threadIdx.x; i < L / 4; i += blockDim.x) {
-      reinterpret_cast<uint4*>(twf + rk * L)[i] = reinterpret_cast<const uint4*>(S.twm + rk * L)[i];
-      reinterpret_cast<uint4*>(twi + rk * L)[i] = reinterpret_cast<const uint4*>(S.itwm + rk * L)[i];
+      reinterpret_cast<uint4*>(twf_s + rk * L)[i] = reinterpret_cast<const uint4*>(S.twm + rk * L)[i];
+      reinterpret_cast<uint4*>(twi_s + rk * L)[i] = reinterpret_cast<const uint4*>(S.itwm + rk * L)[i];
     }
   }
   // the twiddle staging above overlaps the previous step's tail
@@ -734,10 +741,15 @@ size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa) {
   return (size_t)solve_ntt_words(S, Wv, Wa);
 }
 
-cudaError_t configure_solve_ntt(const DevPlan& S, int cap, int Wv, int Wa, int* ok) {
+cudaError_t configure_solve_ntt(DevPlan& S, int cap, int Wv, int Wa, int* ok) {
   int dev = 0, maxopt = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  // twiddles from global memory when staging them would not fit (or when
+  // HGPU_SOLVE_TW_GLOBAL=1 asks for it)
+  const char* twg = getenv("HGPU_SOLVE_TW_GLOBAL");
+  S.tw_global = twg && atoi(twg) ? 1 : 0;
+  if (!S.tw_global && solve_ntt_words(S, Wv, Wa) * 4 > (size_t)maxopt) S.tw_global = 1;
   const size_t step = solve_ntt_words(S, Wv, Wa) * 4;
   const size_t rh = ((size_t)S.NW + cap) * 4, xh = ((size_t)S.NW + Wv) * 4;
   *ok = step <= (size_t)maxopt && rh <= (size_t)maxopt && xh <= (size_t)maxopt;
