@@ -30,6 +30,7 @@ OUT = os.path.join(HERE, "leading_blocks.json")
 
 # (name, N, beta_num, beta_den, K, n')
 CASES = [
+    ("config2", 300, 7, 4, 4096, 300),   # the whole matrix
     ("config3", 1000, 1, 1, 24576, 270),
     ("config4", 1500, 1, 2, 65536, 200),
     ("config5", 2000, 3, 2, 32768, 200),
@@ -65,12 +66,18 @@ def one(args):
 
 
 def main():
+    only = set(sys.argv[1:])  # e.g. config2: regenerate some cases only
     jobs = []
     for name, n, bn, bd, k, nb in CASES:
         shifts = ["x1"] if name == "config3" else ["x0", "x1"]
+        if only and name not in only:
+            continue
         jobs += [(name, n, bn, bd, k, nb, w) for w in shifts]
     with ProcessPoolExecutor(len(jobs)) as ex:
         out = list(ex.map(one, jobs))
+    if only and os.path.exists(OUT):
+        keep = [c for c in json.load(open(OUT)) if c["name"] not in only]
+        out = sorted(keep + out, key=lambda c: (c["name"], c["shift"]))
     with open(OUT, "w") as f:
         json.dump(out, f, indent=1)
     for o in out:
