@@ -194,7 +194,7 @@ class Matrix {
   static constexpr int kYRing = 64;
   // rows [p0, p0 + near_rows_) of a panel run in step with the pivot chain,
   // the rest on the far stream (HGPU_NEAR, default two panels)
-  int near_rows_ = 64;
+  int near_rows_ = 34;
   // ratio GEMM (HGPU_RATIO_GEMM bits: 1 far rows, 2 near rows; 0 = k_divide,
   // the default: the int8 path is exact but measured slower end to end)
   int ratio_gemm_ = 0;

@@ -1,0 +1,5 @@
+# A/B of two environment settings on one box: ab_env.sh "ENV_A" "ENV_B"
+for i in 1 2 3; do for v in "$1" "$2"; do
+  env $v python bench.py --steps 5 --warmup 3 --no-lambda --no-cpu-baseline --no-secondary > gpurun_out/sw.json 2>&1
+  python -c "import json,sys; d=json.loads(open('gpurun_out/sw.json').read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step'],1), d['parity']['bit_exact'])" || tail -3 gpurun_out/sw.json
+done; done
