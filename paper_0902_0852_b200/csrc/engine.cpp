@@ -494,6 +494,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_UPDATE_TC")) update_tc_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_COL_EXTRACT")) col_extract_ = std::atoi(e);
+  if (const char* e = std::getenv("HGPU_LOOKAHEAD")) lookahead_ = std::atoi(e);
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1257,7 +1258,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     tl_.push_back({kind, p, a, b});
   };
   auto timed_update = [&](int b, int nslots, int c_begin, int c_end,
-                          cudaStream_t us, int kind) {
+                          cudaStream_t us, int kind, int s0 = 0) {
     if (c_begin >= c_end || nslots <= 0) return;
     if (profile) {
       while (uev_.size() < uev_used + 2) {
@@ -1267,7 +1268,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       }
       CU(cudaEventRecord(uev_[uev_used], us));
     }
-    const long long r0 = set_row0(b);
+    const long long r0 = set_row0(b) + (long long)s0 * n;  // stage s0 of the panel
     const bool tc = update_tc_ && c_end - c_begin <= 32 && nslots <= 256 && D.NW % 4 == 0 &&
                     D.L % 4 == 0;
     TL(kind, b, us, [&] {
@@ -1288,12 +1289,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     }
   };
   // trailing update of panel b restricted to owned columns in [lo, hi)
-  auto trailing = [&](int b, int lo, int hi, cudaStream_t us, int kind) {
-    const int p0 = b * kb, nsl = std::min(kb, n - 1 - p0);
+  // (stages [s0, s0 + ns) of the panel; ns < 0: all from s0)
+  auto trailing = [&](int b, int lo, int hi, cudaStream_t us, int kind, int s0 = 0,
+                      int ns = -1) {
+    const int p0 = b * kb;
+    const int nsl = ns >= 0 ? ns : std::min(kb, n - 1 - p0) - s0;
+    if (nsl <= 0) return;
     int run_begin = -1, run_end = -1;
     auto flush = [&]() {
       if (run_begin >= 0 && run_begin < run_end)
-        timed_update(b, nsl, run_begin, run_end, us, kind);
+        timed_update(b, nsl, run_begin, run_end, us, kind, s0);
       run_begin = run_end = -1;
     };
     for (int ob : owned_blocks_) {
@@ -1378,6 +1383,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
     const long long row0set = set_row0(b);
+    // stages of this panel already applied to band b+1 (sub-panel lookahead)
+    int la_done = 0;
     // ---- panel b on the high-priority streams
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
     // slot set reuse: su1's last use of panel b - nsets precedes next_ready[b]
@@ -1687,6 +1694,32 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
               }
             }
           }
+          if (lookahead_ && edf && far && !nr && fsub > 0 && (s + 1) % fsub == 0 &&
+              p + 1 < p1 && p1 < n) {
+            // sub-panel lookahead: stages [p+1-fsub, p] of this panel onto band
+            // b+1 now, on su1 (idle during the panel), so the panel boundary
+            // only waits for the last sub-panel's share of U(b, b+1).  Band
+            // b+1's rows are near rows (near divide of stage p) or far rows
+            // (each lane's launches up to stage p); su2 last touched the band
+            // at the end of panel b-1 (band_ev)
+            // (lookahead_ 2: on su2 at the lowest priority, after the band's
+            // pending deadline-ordered work, instead of su1)
+            cudaStream_t lu = lookahead_ == 2 ? su2 : su1;
+            CU(cudaStreamWaitEvent(lu, sev_[4 * p + 2], 0));
+            for (int l = 0; l < nlanes; ++l) {
+              CU(cudaEventRecord(far_ev_[l], far_streams_[l]));
+              CU(cudaStreamWaitEvent(lu, far_ev_[l], 0));
+            }
+            if (lu == su1 && la_done == 0 && band_ev[b + 1])
+              CU(cudaStreamWaitEvent(su1, band_ev[b + 1], 0));
+            trailing(b, p1, std::min(n, p1 + kb), lu, 15, la_done, fsub);
+            la_done += fsub;
+            if (lu == su2) {
+              cudaEvent_t e = edf_event();
+              CU(cudaEventRecord(e, su2));
+              band_ev[b + 1] = e;  // su1's share at the panel end waits for it
+            }
+          }
           if (p + 1 == p1 || p + 1 == n - 1) {
             // join: the next step on sp needs R_p[p+1] as well
             CU(cudaStreamWaitEvent(sp, sev_[4 * p + 3], 0));
@@ -1800,7 +1833,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       if (p1 < n) {
         const int p2 = std::min(n, p1 + kb);
         if (band_ev[b + 1]) CU(cudaStreamWaitEvent(su1, band_ev[b + 1], 0));
-        trailing(b, p1, p2, su1, 8);
+        trailing(b, p1, p2, su1, 8, la_done);  // what the lookahead left
       }
       CU(cudaEventRecord(next_ready[b + 1], su1));
       edf_next[b] = b + 2;

@@ -271,6 +271,9 @@ class Matrix {
   // near (bit 1) / far (bit 2) rows' column update fused with the extraction
   // (k_col_extract, HGPU_COL_EXTRACT)
   int col_extract_ = 0;
+  // band b+1 receives panel b's stages sub-panel by sub-panel during the
+  // panel instead of all at its end (HGPU_LOOKAHEAD)
+  int lookahead_ = 0;  // 1: on su1, 2: on su2 (lowest priority)
   bool ws_released_ = false;  // W / slot sets handed to the solves' transforms
   // the chain's next row on its own stream (HGPU_NEXT_ROW)
   bool next_row_ = false;

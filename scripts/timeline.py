@@ -6,7 +6,8 @@ import sys
 KIND = {0: "col(pivot)", 1: "extract(pivot)", 2: "recip", 3: "col(rest)", 4: "extract(rest)",
         5: "divide", 6: "col(all)", 7: "extract(all)", 8: "update(next)", 9: "update(rest)",
         10: "col(far)", 11: "extract(far)", 12: "divide(far)",
-        13: "update(catch-up)", 14: "update(far sub-panel)", 16: "pivot entry (early stages)", 17: "next row (sn)"}
+        13: "update(catch-up)", 14: "update(far sub-panel)", 15: "update(next band, lookahead)",
+        16: "pivot entry (early stages)", 17: "next row (sn)"}
 blocks, cur = [], None
 for line in open(sys.argv[1]):
     if line.startswith("#"):

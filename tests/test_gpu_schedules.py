@@ -39,6 +39,9 @@ VARIANTS = [
     {"HGPU_COL_EXTRACT": "3"},
     {"HGPU_PIVOT_THREADS": "256", "HGPU_COL_EXTRACT": "1"},
     {"HGPU_SM_SPLIT": "4:b", "HGPU_COL_EXTRACT": "1"},
+    {"HGPU_LOOKAHEAD": "0"},
+    {"HGPU_LOOKAHEAD": "1", "HGPU_FAR_SUB": "4", "HGPU_FAR_LANES": "3"},
+    {"HGPU_LOOKAHEAD": "1", "HGPU_NEAR": "64"},
 ]
 
 
