@@ -88,6 +88,13 @@ hgpu_status hgpu_matrix_new_group(long n, long frac_bits,
 /* Ranks behind the handle (1 unless grouped or joined by set_comm). */
 int hgpu_matrix_world(const hgpu_matrix* m);
 
+/* New moments for the same order and frac_bits (the strip of another beta,
+ * or the same one re-sent): the next hgpu_ldlt_factor copies and transforms
+ * them; the transform plan, workspace and streams are kept when the new
+ * strip fits the plan (otherwise they are rebuilt there).  Inputs copied. */
+hgpu_status hgpu_matrix_set_strip(hgpu_matrix* m, const int32_t* strip_sizes,
+                                  const uint32_t* strip_limbs);
+
 /* HGPU_CAPTURE keeps only the leading rows x rows block of the ratio
  * columns (stages p < rows, rows r < rows; 0 = all, the default).  The
  * leading block of the submatrix-order LDL^T is the factorisation of the

@@ -197,6 +197,14 @@ hgpu_status hgpu_matrix_set_comm(hgpu_matrix* m, int rank, int world,
   });
 }
 
+hgpu_status hgpu_matrix_set_strip(hgpu_matrix* m, const int32_t* strip_sizes,
+                                  const uint32_t* strip_limbs) {
+  return guarded([&] {
+    if (!m || !strip_sizes) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    m->impl->set_strip(strip_sizes, strip_limbs);
+  });
+}
+
 hgpu_status hgpu_matrix_set_capture_rows(hgpu_matrix* m, long rows) {
   return guarded([&] {
     if (!m || rows < 0) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "bad argument");

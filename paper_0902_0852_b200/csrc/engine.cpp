@@ -400,15 +400,11 @@ Plan solve_plan(int n, int K, int bits) {
   return P;
 }
 
-Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
-               int device)
-    : n_(n), K_(K), device_(device) {
-  if (n < 1) throw Error(HGPU_ERR_INVALID_ARGUMENT, "order must be >= 1");
-  if (K < 2 || K % 2 != 0)
-    throw Error(HGPU_ERR_INVALID_ARGUMENT, "frac_bits must be even and >= 2");
-  strip_.resize(2 * n - 1);
+void Matrix::parse_strip(const int32_t* sizes, const uint32_t* limbs) {
+  strip_.assign(2 * n_ - 1, HostInt{});
+  strip_bits_ = 0;
   const uint32_t* src = limbs;
-  for (int s = 0; s < 2 * n - 1; ++s) {
+  for (int s = 0; s < 2 * n_ - 1; ++s) {
     HostInt& h = strip_[s];
     h.size = sizes[s];
     const int len = std::abs(sizes[s]);
@@ -422,6 +418,34 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
                             (32 - __builtin_clz(h.limbs.back()));
     strip_bits_ = std::max(strip_bits_, b);
   }
+}
+
+// A new strip of the same order and precision (e.g. the next matrix of a
+// sweep, or the same moments re-sent): when it fits the current transform
+// plan, only the strip's integers are re-sent and re-transformed by the next
+// factorisation; otherwise the matrix is rebuilt there.
+void Matrix::set_strip(const int32_t* sizes, const uint32_t* limbs) {
+  if (interval_) throw Error(HGPU_ERR_INVALID_ARGUMENT, "interval matrices keep their bounds");
+  CU(cudaSetDevice(device_));
+  parse_strip(sizes, limbs);
+  const bool keep = (W_ || ws_released_) && [&] {
+    const Plan q = choose_plan(n_, K_, strip_bits_ + 64, 0);
+    return q.np == plan_.np && q.L == plan_.L && q.w == plan_.w && q.cap <= plan_.cap;
+  }();
+  if (keep)
+    strip_dirty_ = true;
+  else
+    release();
+  for (auto& pm : peers_) pm->set_strip(sizes, limbs);
+}
+
+Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
+               int device)
+    : n_(n), K_(K), device_(device) {
+  if (n < 1) throw Error(HGPU_ERR_INVALID_ARGUMENT, "order must be >= 1");
+  if (K < 2 || K % 2 != 0)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "frac_bits must be even and >= 2");
+  parse_strip(sizes, limbs);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error(HGPU_ERR_CUDA, "no CUDA device available");
@@ -534,6 +558,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
 Matrix::~Matrix() {
   cudaSetDevice(device_);
   release();
+  if (strip_stage_) cudaFreeHost(strip_stage_);
   if (comm_) ncclCommDestroy((ncclComm_t)comm_);
   for (cudaEvent_t e : uev_) cudaEventDestroy(e);
   if (ev0_) cudaEventDestroy(ev0_);
@@ -1138,6 +1163,35 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   }
   int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
   CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+  if (strip_dirty_) {
+    // set_strip: the new moments into the plan's strip buffers and their
+    // transforms (a capacity overflow raises the flag checked below)
+    const int ns = 2 * n_ - 1;
+    // pinned staging (kept): hdr words, then cap-strided limbs
+    const size_t words = (size_t)ns + (size_t)ns * P.cap;
+    if (strip_stage_words_ < words) {
+      if (strip_stage_) cudaFreeHost(strip_stage_);
+      strip_stage_ = nullptr;
+      CU(cudaHostAlloc((void**)&strip_stage_, words * 4, cudaHostAllocDefault));
+      strip_stage_words_ = words;
+    }
+    int* hdr = reinterpret_cast<int*>(strip_stage_);
+    uint32_t* lim = strip_stage_ + ns;
+    for (int s2 = 0; s2 < ns; ++s2) {
+      if ((int)strip_[s2].limbs.size() > P.cap)
+        throw Error(HGPU_ERR_CAPACITY, "strip entry exceeds limb capacity");
+      hdr[s2] = strip_[s2].size;
+      uint32_t* dst = lim + (size_t)s2 * P.cap;
+      const size_t len = strip_[s2].limbs.size();
+      std::memcpy(dst, strip_[s2].limbs.data(), len * 4);
+      std::memset(dst + len, 0, (P.cap - len) * 4);
+    }
+    CU(cudaMemcpyAsync(strip_hdr_, hdr, ns * sizeof(int), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(strip_limbs_, lim, (size_t)ns * P.cap * 4, cudaMemcpyHostToDevice, st));
+    CU(launch_fwd_ints(D, IntBuf{strip_hdr_, strip_limbs_}, 0, that_, 0, ns, 0, nullptr, err_,
+                       st));
+    strip_dirty_ = false;
+  }
   CU(cudaMemsetAsync(stats_, 0xff, 3 * (size_t)n * sizeof(int), st));  // -1
   const long long launches0 = kernel_launch_count();
   if (group_) {

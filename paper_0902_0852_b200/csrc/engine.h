@@ -109,6 +109,8 @@ class Matrix {
   int frac_bits() const { return K_; }
   // HGPU_CAPTURE keeps only the leading rows x rows block (0: all)
   void set_capture_rows(int rows) { capture_rows_ = rows; }
+  // new moments of the same order and precision (hgpu_matrix_set_strip)
+  void set_strip(const int32_t* sizes, const uint32_t* limbs);
   int chain_sms() const { return chain_sms_; }
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
@@ -136,6 +138,7 @@ class Matrix {
   void group_pulled(int b, cudaStream_t st);
   void group_wait_pulled(int b, cudaStream_t st);
   void group_merge_err(int* herr);
+  void parse_strip(const int32_t* sizes, const uint32_t* limbs);
   void build(int min_logL);
   void alloc_slots();
   void release_workspace();   // W and slot sets back to the pool (solves)
@@ -274,7 +277,10 @@ class Matrix {
   // band b+1 receives panel b's stages sub-panel by sub-panel during the
   // panel instead of all at its end (HGPU_LOOKAHEAD)
   int lookahead_ = 0;  // 1: on su1, 2: on su2 (lowest priority)
-  bool ws_released_ = false;  // W / slot sets handed to the solves' transforms
+  bool ws_released_ = false;
+  bool strip_dirty_ = false;          // set_strip: re-send and re-transform
+  uint32_t* strip_stage_ = nullptr;    // pinned host staging of the strip
+  size_t strip_stage_words_ = 0;  // W / slot sets handed to the solves' transforms
   // the chain's next row on its own stream (HGPU_NEXT_ROW)
   bool next_row_ = false;
   cudaStream_t stream_next_ = nullptr;

@@ -48,7 +48,7 @@ EXPORTS = (
     "hgpu_factor_det_hi", "hgpu_factor_det_sign", "hgpu_verify_eigenvalue",
     "hgpu_build_moments", "hgpu_buffer_free", "hgpu_matrix_set_capture_rows",
     "hgpu_matrix_new_group", "hgpu_matrix_world", "hgpu_verify_eigenvalue_ex",
-    "hgpu_factor_net_ms", "hgpu_trim_pool",
+    "hgpu_factor_net_ms", "hgpu_trim_pool", "hgpu_matrix_set_strip",
 )
 
 
@@ -113,6 +113,7 @@ def load() -> ctypes.CDLL:
     lib.hgpu_factor_update_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(ctypes.c_double),
                                              ctypes.POINTER(ctypes.c_double)]
     lib.hgpu_trim_pool.argtypes = [ctypes.c_int]
+    lib.hgpu_matrix_set_strip.argtypes = [vp, ctypes.POINTER(ctypes.c_int32), u32p]
     lib.hgpu_factor_net_ms.argtypes = [vp]
     lib.hgpu_factor_net_ms.restype = ctypes.c_double
     lib.hgpu_factor_launches.argtypes = [vp]
@@ -264,6 +265,22 @@ class HankelMatrixGPU:
                                        _u32p(limbs), devices[0] if devices else device,
                                        ctypes.byref(h)))
         self._h = h
+
+    def set_strip(self, strip) -> None:
+        """New moments of the same order and precision for the next ldlt()
+        (hgpu_matrix_set_strip): the handle, plan and workspace are kept.
+        `strip`: 2n-1 Python ints, or the (sizes, limbs) arrays of
+        :func:`pack_ints` (host buffers, as a C caller passes them)."""
+        if isinstance(strip, tuple):
+            sizes, limbs = strip
+        else:
+            if len(strip) != 2 * self.n - 1:
+                raise ValueError("strip must hold 2n-1 anti-diagonals")
+            sizes, limbs = pack_ints(strip)
+        if len(sizes) != 2 * self.n - 1:
+            raise ValueError("strip must hold 2n-1 anti-diagonals")
+        _check(load().hgpu_matrix_set_strip(self._h, sizes.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                            _u32p(limbs)))
 
     @property
     def world(self) -> int:

@@ -113,3 +113,19 @@ def test_config1_shifted_against_reference(hg):
             assert ei.value.pivot_index == e.pivot_index
             continue
         assert_same(m.ldlt(xx, capture=True), want)
+
+
+def test_set_strip_reuses_the_handle(hg, ref):
+    # hgpu_matrix_set_strip: new moments of the same order and precision give
+    # the factorisation of a fresh matrix, with the plan kept (fits) or
+    # rebuilt (larger moments)
+    k = 256
+    a = random_pd_hankel(201, 40, k)
+    b = random_pd_hankel(202, 40, k)
+    big = [v << 200 for v in b]
+    m = hg.HankelMatrixGPU(a, k)
+    x = 1 << (k // 3)
+    assert_same(m.ldlt(x, capture=True), ref.ldlt(a, x, k))
+    for strip in (b, big, a):
+        m.set_strip(strip)
+        assert_same(m.ldlt(x, capture=True), ref.ldlt(strip, x, k))
