@@ -24,10 +24,12 @@ __device__ __forceinline__ bool stage_aborted(const int* err) {
 
 // Stages the Montgomery twiddle tables in shared memory (when the plan says
 // they fit) and returns the pointers the transforms should use.
+// A CTA that transforms a single integer reads the tables from global
+// memory (L1) instead: staging them costs more than it saves (`stage`).
 __device__ inline void stage_tables(const DevPlan& P, uint32_t* sm_fwd,
                                     uint32_t* sm_inv, const uint32_t** fwd,
-                                    const uint32_t** inv) {
-  if (P.tw_smem) {
+                                    const uint32_t** inv, bool stage = true) {
+  if (P.tw_smem && stage) {
     for (int i = threadIdx.x; i < P.NW; i += blockDim.x) {
       if (sm_fwd) sm_fwd[i] = P.twm[i];
       if (sm_inv) sm_inv[i] = P.itwm[i];
@@ -112,18 +114,28 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
   uint64_t* Dg = reinterpret_cast<uint64_t*>(S + M);  // M digits
   uint32_t* Lb = reinterpret_cast<uint32_t*>(Dg + M); // cap limbs of |W|
   uint32_t* red = Lb + P.cap;                         // scan scratch
+  // HGPU_DEBUG & 1024: phase clocks of sampled pivot-row extractions
+  long long xs[12];
+  const bool xph = (P.debug & 1024) && p % 100 == 50 && r_begin == p && threadIdx.x == 0;
+  if (xph) xs[0] = clock64();
   const uint32_t* twm;
   const uint32_t* itwm;
-  stage_tables(P, tabf, tabi, &twm, &itwm);
+  // rows this CTA extracts: with one, the tables are read from global memory
+  const bool multi = r_begin + bx + gx < r_end;
+  stage_tables(P, tabf, tabi, &twm, &itwm, multi);
   const uint64_t dmask = (1ull << w) - 1ull;
 
   for (int r = r_begin + bx; r < r_end; r += gx) {
+    if (xph) xs[1] = clock64();
     const uint32_t* src = W + (colbase[p] + (r - p)) * (long long)P.NW;
     for (int i = threadIdx.x; i < P.NW / 4; i += blockDim.x)
       reinterpret_cast<uint4*>(A)[i] = reinterpret_cast<const uint4*>(src)[i];
     __syncthreads();
+    if (xph) xs[2] = clock64();
     int len = 0;
-    const int sg = reconstruct_int(P, A, S, Dg, Lb, P.cap, red, itwm, err, &len);
+    const int sg = reconstruct_int(P, A, S, Dg, Lb, P.cap, red, itwm, err, &len,
+                                   xph ? xs + 3 : nullptr);
+    if (xph) xs[7] = clock64();
     if (sg == 0) return;
     const int wsign = len == 0 ? 0 : sg;
 
@@ -189,11 +201,19 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
         if (vbits > 0) atomicMax(&maxdegV[p], (vbits - 1) / w);
       }
     }
+    if (xph) xs[8] = clock64();
     // transform of V_p[r] for the trailing update (rows r > p)
     if (r > p)
       transform_int(P, Vb, vlen, 0, vsign, A, vhat + vidx * (long long)P.NW,
                     false, twm, err);
     __syncthreads();
+    if (xph) {
+      xs[9] = clock64();
+      printf("extract p=%d tables %lld load %lld iNTT %lld garner %lld digitsums %lld "
+             "resolve+pack %lld V+len %lld fwdNTT %lld cycles\n", p, xs[1] - xs[0],
+             xs[2] - xs[1], xs[3] - xs[2], xs[4] - xs[3], xs[5] - xs[4], xs[7] - xs[5],
+             xs[8] - xs[7], xs[9] - xs[8]);
+    }
   }
 }
 
@@ -624,7 +644,7 @@ __device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int 
   uint32_t* sm = use_gscratch ? gscratch + (long long)bx * cta_words
                               : sm_dyn + (P.tw_smem ? P.NW : 0);
   const uint32_t* twm;
-  stage_tables(P, tab, nullptr, &twm, nullptr);
+  stage_tables(P, tab, nullptr, &twm, nullptr, r_begin + bx + gx < r_end);
   const int CY = (cap + ycap + 2 + 3) & ~3;  // 16-byte aligned regions
   uint32_t* Vt = sm;                 // cap      } later: Qt (cap + ycap)
   uint32_t* Y = Vt + cap;            // ycap     }
