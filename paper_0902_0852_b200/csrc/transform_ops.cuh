@@ -174,27 +174,22 @@ __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
       S[k] = sk;
     }
   } else
-  for (int k0 = threadIdx.x * 8; k0 < M; k0 += blockDim.x * 8) {
-    int64_t acc8[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc8[u] = 0;
-    const int ilo = max(0, k0 - T + 1), ihi = min(L - 1, k0 + 7);
-    for (int i = ilo; i <= ihi; ++i) {
+  // one position per thread: piece t of coefficient k - t for t < T (T
+  // decodes per position, every thread busy; the old 8-positions-per-thread
+  // loop spent most of its time on out-of-range piece tests)
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    int64_t sk = 0;
+    for (int t = 0; t < T; ++t) {
+      const int i = k - t;
+      if (i < 0 || i >= L) continue;
       unsigned __int128 cu = 0;
       for (int u = np - 1; u >= 0; --u) cu = (cu << 32) | A[u * L + i];
       cu <<= (128 - 32 * np);
       const __int128 c = ((__int128)cu) >> (128 - 32 * np);  // sign-extend
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int t = k0 + u - i;  // piece index landing on position k0+u
-        if (t < 0 || t >= T) continue;
-        const __int128 sh = c >> (w * t);
-        acc8[u] += (t == T - 1) ? (int64_t)sh : (int64_t)((uint64_t)sh & dmask);
-      }
+      const __int128 sh = c >> (w * t);
+      sk += (t == T - 1) ? (int64_t)sh : (int64_t)((uint64_t)sh & dmask);
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (k0 + u < M) S[k0 + u] = acc8[u];
+    S[k] = sk;
   }
   __syncthreads();
   if (stamps && threadIdx.x == 0) stamps[2] = clock64();
