@@ -155,10 +155,9 @@ __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
   if (stamps && threadIdx.x == 0) stamps[1] = clock64();
 
   // Digit sums: s_k = sum_t piece_t(c_{k-t}); pieces are w-bit fields of the
-  // two's complement coefficient, the top piece carries the sign.  Each
-  // thread owns 8 consecutive positions and decodes each coefficient that
-  // reaches them once (8+T-1 decodes instead of 8T).  With w = 32 the pieces
-  // are the coefficient's words (sign words above the np-th).
+  // two's complement coefficient, the top piece carries the sign.  With
+  // w = 32 the pieces are the coefficient's words (sign words above the
+  // np-th).
   if (from == 2) {
     // digit sums supplied by the caller
   } else if (w == 32) {
@@ -194,22 +193,37 @@ __device__ inline int reconstruct_int(const DevPlan& P, uint32_t* A, int64_t* S,
   __syncthreads();
   if (stamps && threadIdx.x == 0) stamps[2] = clock64();
 
+  // One resolution of V = sum_k S_k 2^(wk) in two's complement: final carry
+  // 0 -> V = D >= 0; -1 -> V = D - 2^(wM) < 0 and |V| = 2^(wM) - D, formed
+  // digit-wise from the lowest nonzero digit k0 (zeros below it, 2^w - D_k0
+  // at it, complemented digits above) instead of a second resolution.
+  const int carry = cta_resolve(
+      M, w,
+      [&](int k) -> int64_t {
+        int64_t vv = S[k] & (int64_t)dmask;
+        if (k > 0) vv += S[k - 1] >> w;
+        return vv;
+      },
+      [&](int k, uint64_t d) { Dg[k] = d; }, red);
   int sg = 1;
-  int carry = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    carry = cta_resolve(
-        M, w,
-        [&](int k) -> int64_t {
-          const int64_t cur = (int64_t)sg * S[k];
-          int64_t vv = cur & (int64_t)dmask;
-          if (k > 0) vv += ((int64_t)sg * S[k - 1]) >> w;
-          return vv;
-        },
-        [&](int k, uint64_t d) { Dg[k] = d; }, red);
-    if (carry >= 0) break;
-    sg = -1;  // negative: resolve the magnitude instead
+  bool bad = carry != 0 && carry != -1;
+  if (carry == -1) {
+    sg = -1;
+    if (threadIdx.x == 0) red[0] = (uint32_t)M;
+    __syncthreads();
+    for (int k = threadIdx.x; k < M; k += blockDim.x)
+      if (Dg[k]) {
+        atomicMin(red, (uint32_t)k);
+        break;
+      }
+    __syncthreads();
+    const int k0 = (int)red[0];
+    bad = k0 >= M;  // V = -2^(wM): magnitude does not fit M digits
+    for (int k = threadIdx.x; k < M; k += blockDim.x)
+      Dg[k] = k < k0 ? 0ull : (k == k0 ? ((dmask - Dg[k]) + 1ull) : (dmask - Dg[k]));
+    __syncthreads();
   }
-  if (carry != 0) {
+  if (bad) {
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapCrt);
     return 0;
   }
