@@ -1365,20 +1365,31 @@ long long recip_fast_words_bound(const DevPlan& P, int dmax_bits) {
   return rf_scratch_words((int)Lm);
 }
 
-size_t recip_scratch_words(const DevPlan& P) {
-  // Lm bounded by the reciprocal capacity ycap (+ guard limbs)
+// recip_body's scratch at the reciprocal capacity ycap (+ guard limbs)
+static size_t recip_body_words(const DevPlan& P) {
   const size_t Lm = (size_t)P.ycap + 4;
-  const size_t old_words = (Lm + 2) + Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) +
-                           6 * (3 * Lm + 2) + 64;
-  return std::max(old_words, (size_t)rf_scratch_words((int)Lm));
+  return (Lm + 2) + Lm + Lm + (2 * Lm + 1) + (2 * Lm + 2) + (3 * Lm + 2) + 6 * (3 * Lm + 2) + 64;
 }
+
+// Global scratch for either body at ycap.  The fast body needs ~35 words per
+// limb of the stage's actual precision (Lm, usually far below ycap): in
+// shared memory it runs whenever the launch's dynamic shared memory holds
+// that, and otherwise the stage uses recip_body (recip_fast_body checks).
+size_t recip_scratch_words(const DevPlan& P) {
+  return std::max(recip_body_words(P), (size_t)rf_scratch_words(P.ycap + 4));
+}
+
+// the dynamic shared memory k_pivot / k_recip may take: the opt-in limit per
+// block less their static shared memory (set by configure_kernels)
+static size_t g_pivot_dyn = 0, g_recip_dyn = 0;
 
 cudaError_t launch_recip(const DevPlan& P, IntBuf vint, long long prow,
                          const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
                          uint32_t* Ybuf, int* ys, uint32_t* scratch,
                          int use_gscratch, int* err, cudaStream_t st) {
   ++g_launches;
-  const size_t smem = use_gscratch ? 0 : recip_scratch_words(P) * 4;
+  const size_t smem =
+      use_gscratch ? 0 : std::min(recip_scratch_words(P) * 4, std::max(g_recip_dyn, recip_body_words(P) * 4));
   k_recip<<<1, recip_threads(), smem, st>>>(P, vint, prow, maxbitsV, p, piv,
                                             dmax_bits, Ybuf, ys, scratch,
                                             use_gscratch, err);
@@ -1404,14 +1415,23 @@ cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase
     const int v = e ? atoi(e) : 512;
     return (v >= 128 && v <= 512 && v % 32 == 0) ? v : 512;
   }();
+  // k_pivot fills a whole SM's register file, so it always runs alone on its
+  // SM: give it all the shared memory the SM has, so the fast reciprocal
+  // runs at any precision that fits (the bound from dmax is far too loose
+  // for the small pivots of these matrices).
+  PivotDiv q = pd;
+  if (threads != 256 && !use_gscratch && g_pivot_dyn > smem) {
+    smem = g_pivot_dyn;
+    q.recip_words = std::min<long long>((long long)recip_scratch_words(P), (long long)(smem / 4));
+  }
   if (threads == 256)
     k_pivot_lean<<<1, 256, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
                                        p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
-                                       dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
+                                       dmax_bits, Ybuf, ys, scratch, use_gscratch, err, q);
   else
     k_pivot<<<1, threads, smem, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots,
                                   p, vint, vrow0, piv, maxbitsV, vhat, maxdegV,
-                                  dmax_bits, Ybuf, ys, scratch, use_gscratch, err, pd);
+                                  dmax_bits, Ybuf, ys, scratch, use_gscratch, err, q);
   return post_launch(st);
 }
 
@@ -1616,16 +1636,20 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)fwd)) != cudaSuccess)
     return e;
-  const size_t rec = recip_scratch_words(P) * 4;
+  auto dyn_cap = [&](const void* f) -> size_t {
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 0;
+    return (size_t)maxopt > fa.sharedSizeBytes ? (size_t)maxopt - fa.sharedSizeBytes : 0;
+  };
+  g_pivot_dyn = std::min(dyn_cap((const void*)k_pivot), dyn_cap((const void*)k_pivot_lean));
+  g_recip_dyn = dyn_cap((const void*)k_recip);
+  const size_t rec = recip_body_words(P) * 4;
   {
-    size_t piv_smem = std::max(ext, (int)rec > maxopt ? (size_t)0 : rec);
-    const size_t dv = divide_smem_words(P) * 4;
-    if ((int)dv <= maxopt) piv_smem = std::max(piv_smem, dv);
     if ((e = cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)piv_smem)) != cudaSuccess)
+                                  (int)g_pivot_dyn)) != cudaSuccess)
       return e;
     if ((e = cudaFuncSetAttribute(k_pivot_lean, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)piv_smem)) != cudaSuccess)
+                                  (int)g_pivot_dyn)) != cudaSuccess)
       return e;
   }
   // the reciprocal CTA runs beside the bulk kernels; shared-memory scratch
@@ -1634,11 +1658,11 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
   // keeps the scratch in global memory (L1/L2-resident) instead.
   const char* rg = getenv("HGPU_RECIP_SMEM");
   const bool want_smem = rg ? *rg == '1' : true;
-  *recip_global = (int)rec > maxopt || !want_smem;
+  *recip_global = rec > std::min(g_recip_dyn, g_pivot_dyn) || !want_smem;
   if (!*recip_global) {
     if ((e = cudaFuncSetAttribute(k_recip,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)rec)) != cudaSuccess)
+                                  (int)g_recip_dyn)) != cudaSuccess)
       return e;
   }
   const size_t div = divide_smem_words(P) * 4;

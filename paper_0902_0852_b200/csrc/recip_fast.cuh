@@ -262,7 +262,12 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
     if (threadIdx.x == 0) atomicOr(&err[kErrCapacity], kCapLimbs);
     return true;
   }
-  if (rf_scratch_words(Lm) > avail_words) return false;
+  if (rf_scratch_words(Lm) > avail_words) {
+    if ((P.debug & 4096) && p % 100 == 50 && threadIdx.x == 0)
+      printf("recip_fast p=%d falls back: Lm %d needs %lld words, %lld available (n %d amax %d)\n", p,
+             Lm, rf_scratch_words(Lm), avail_words, n, amax);
+    return false;
+  }
   const int dbase = max(0, nD - (Lm + 2));
   const int nDs = nD - dbase;
   // Y, Pr and E are product operands b: kGuard zero words on either side
