@@ -61,7 +61,7 @@ __global__ void k_iv_classify(IntBuf lo, IntBuf hi, long long row0, int r_begin,
 // transform words; each thread one word of a 4x4 (r, c) tile.
 constexpr int kIvT = 4;
 __global__ void __launch_bounds__(128)
-k_update_iv(DevPlan P, uint32_t* Wlo, uint32_t* Whi, const long long* colbase,
+k_update_iv(const __grid_constant__ DevPlan P, uint32_t* Wlo, uint32_t* Whi, const long long* colbase,
             const uint32_t* Vlo, const uint32_t* Vhi, const uint32_t* Rlo,
             const uint32_t* Rhi, const int8_t* clsV, const int8_t* clsR,
             int s_begin, int s_end, int c_begin, int c_end, int r_min,

@@ -48,7 +48,7 @@ __device__ inline void stage_tables(const DevPlan& P, uint32_t* sm_fwd,
 // out + (out_base + i)*NW.  Records deg = floor((bits-1)/w) via atomicMax.
 // Used for the strip moments and the shift at setup, and by ranks that
 // receive a panel over NCCL.  Grid-stride over items.
-__global__ void k_fwd_ints(DevPlan P, IntBuf src, long long in_base,
+__global__ void k_fwd_ints(const __grid_constant__ DevPlan P, IntBuf src, long long in_base,
                            uint32_t* out, long long out_base, int count,
                            int mont, int* maxdeg, int* err) {
   extern __shared__ uint32_t sm[];
@@ -72,7 +72,7 @@ __global__ void k_fwd_ints(DevPlan P, IntBuf src, long long in_base,
 // ldlt.cpp:38-44: cols[c][r-c] = strip[r+c], cols[c][0] -= x.  By linearity
 // the transform of strip[2c]-x is that[2c] - xhat.  grid.x: word blocks,
 // grid.y: column c (all rows r >= c of an owned column).
-__global__ void k_init_w(DevPlan P, const uint32_t* that, const uint32_t* xhat,
+__global__ void k_init_w(const __grid_constant__ DevPlan P, const uint32_t* that, const uint32_t* xhat,
                          const long long* colbase, uint32_t* W) {
   const int c = blockIdx.y;
   const long long base = colbase[c];
@@ -223,7 +223,7 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
 // launch instead of two per stage on the panel's latency path, and no wait
 // for the column update's grid to drain.
 __global__ void __launch_bounds__(256)
-k_col_extract(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+k_col_extract(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
               const uint32_t* Rhat, long long row_stride_slot, int nslots, int p, int r_begin,
               int r_end, IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
               int* maxdegV, int* err, uint8_t* vdig, int kd) {
@@ -261,7 +261,7 @@ k_col_extract(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* 
   }
 }
 
-__global__ void k_extract(DevPlan P, const uint32_t* W, const long long* colbase,
+__global__ void k_extract(const __grid_constant__ DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, int r_begin, int r_end, IntBuf vint,
                           long long vrow0, IntBuf piv, int* maxbitsV,
                           uint32_t* vhat, int* maxdegV, int* err, int round,
@@ -486,7 +486,7 @@ __device__ void recip_body(const DevPlan& P, IntBuf vint, long long prow,
 #include "recip_fast.cuh"
 namespace hgpu {
 
-__global__ void __launch_bounds__(512) k_recip(DevPlan P, IntBuf vint, long long prow,
+__global__ void __launch_bounds__(512) k_recip(const __grid_constant__ DevPlan P, IntBuf vint, long long prow,
                         const int* maxbitsV, int p, IntBuf piv, int dmax_bits,
                         uint32_t* Ybuf, int* ys, uint32_t* gscratch,
                         int use_gscratch, int* err) {
@@ -730,7 +730,7 @@ __device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int 
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_divide(DevPlan P, IntBuf vint, long long vrow0, int p,
+__global__ void __launch_bounds__(256, 3) k_divide(const __grid_constant__ DevPlan P, IntBuf vint, long long vrow0, int p,
                          int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(256, 3) k_divide(DevPlan P, IntBuf vint, long 
 // A single row (the pivot chain's next row) with 512 threads; the multi-row
 // kernel above is held to 80 registers so that a CTA fits beside two
 // trailing-update CTAs on an SM instead of waiting for one to leave.
-__global__ void __launch_bounds__(512) k_divide1(DevPlan P, IntBuf vint, long long vrow0, int p,
+__global__ void __launch_bounds__(512) k_divide1(const __grid_constant__ DevPlan P, IntBuf vint, long long vrow0, int p,
                          int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(512) k_divide1(DevPlan P, IntBuf vint, long lo
 // panel's stages [0, s) (as k_update_col), is extracted (k_extract, row p:
 // pivot, V_p[p], ZeroPivot) and the stage's reciprocal is formed (k_recip).
 __device__ __forceinline__ void pivot_body(
-    DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+    const DevPlan& P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
     const uint32_t* Rhat, long long row_stride_slot, int nslots, int p, IntBuf vint,
     long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat, int* maxdegV, int dmax_bits,
     uint32_t* Ybuf, int* ys, uint32_t* gscratch, int use_gscratch, int* err, PivotDiv pd) {
@@ -818,7 +818,7 @@ __device__ __forceinline__ void pivot_body(
 }
 
 __global__ void __launch_bounds__(512)
-k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+k_pivot(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
         const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
         IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
         int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
@@ -832,7 +832,7 @@ k_pivot(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
 // the 512-thread kernel needs a whole SM's register file, so in the step it
 // waits for an SM to drain completely).
 __global__ void __launch_bounds__(256, 3)
-k_pivot_lean(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+k_pivot_lean(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
              const uint32_t* Rhat, long long row_stride_slot, int nslots, int p,
              IntBuf vint, long long vrow0, IntBuf piv, int* maxbitsV, uint32_t* vhat,
              int* maxdegV, int dmax_bits, uint32_t* Ybuf, int* ys, uint32_t* gscratch,
@@ -891,7 +891,7 @@ __global__ void k_toeplitz(const uint32_t* Ybuf, const int* ys, int k2, int kd,
 
 // Rows r in [r_begin, r_end) of stage p from the GEMM's columns
 // C[(r - r_begin) * ncols + k'] (see above); same outputs as k_divide.
-__global__ void k_ratio_finish(DevPlan P, IntBuf vint, long long vrow0, int p,
+__global__ void k_ratio_finish(const __grid_constant__ DevPlan P, IntBuf vint, long long vrow0, int p,
                                int r_begin, int r_end, const uint32_t* Ybuf,
                                const int* ys, const int32_t* C, int ncols,
                                IntBuf rint, long long rrow0, uint32_t* rhat,
@@ -1003,7 +1003,7 @@ __global__ void k_ratio_finish(DevPlan P, IntBuf vint, long long vrow0, int p,
 // whole panel (products < 2^56, <= 256 stages), one Montgomery reduction.
 template <int TILE>
 __global__ void __launch_bounds__(128)
-k_update(DevPlan P, uint32_t* W, const long long* colbase,
+k_update(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase,
          const uint32_t* Vhat, const uint32_t* Rhat, long long row_stride_slot,
          int nslots, int c_begin, int c_end, int nct, int nrt, const int* err) {
   if (stage_aborted(err)) return;
@@ -1103,7 +1103,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }  // namespace
 
 __global__ void __launch_bounds__(128, 2)
-k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
+k_update_tiled(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase,
                const uint32_t* Vhat, const uint32_t* Rhat,
                long long row_stride_slot, int nslots, int c_begin, int c_end,
                int nct, int nrt, const int* err, int r_lo, int r_hi, int rect) {
@@ -1222,7 +1222,7 @@ k_update_tiled(DevPlan P, uint32_t* W, const long long* colbase,
 // of once per stage.  Thread: one word x TR rows.
 template <int TR>
 __global__ void __launch_bounds__(128)
-k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
+k_update_col(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase,
              const uint32_t* Vhat, const uint32_t* Rhat,
              long long row_stride_slot, int nslots, int c, int r_begin,
              int r_end, const int* err) {
@@ -1266,7 +1266,7 @@ k_update_col(DevPlan P, uint32_t* W, const long long* colbase,
 // Checks the transform capacity after the factorisation: for every stage
 // deg V + deg R < L (no cyclic wrap) and the accumulated coefficient bound
 // sum_p (min(degV,degR)+1)(2^w-1)^2 + 2^(w+1) < Q/2 (exact CRT).
-__global__ void k_validate(DevPlan P, const int* maxdegV, const int* maxdegR,
+__global__ void k_validate(const __grid_constant__ DevPlan P, const int* maxdegV, const int* maxdegR,
                            int nstages, int* err) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const long double dig = (long double)((1ull << P.w) - 1ull);

@@ -242,7 +242,7 @@ __host__ __device__ inline long long solve_ntt_words(const DevPlan& S, int Wv, i
 constexpr int kSolveNttThreads = 1024;
 
 // every L entry (packed like L) -> its transform in Montgomery form
-__global__ void __launch_bounds__(256) k_solve_rhat(DevPlan S, int cap, IntBuf L,
+__global__ void __launch_bounds__(256) k_solve_rhat(const __grid_constant__ DevPlan S, int cap, IntBuf L,
                                                     long long count, EntryStore rhat,
                                                     int* err) {
   extern __shared__ uint32_t sm[];
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) k_solve_rhat(DevPlan S, int cap, IntBuf L
 }
 
 // transform of the signed limb integer xv[xi] (stride Wv) -> xhat
-__global__ void __launch_bounds__(512) k_solve_xhat(DevPlan S, IntBuf xv, int xi, int Wv,
+__global__ void __launch_bounds__(512) k_solve_xhat(const __grid_constant__ DevPlan S, IntBuf xv, int xi, int Wv,
                                                     uint32_t* xhat, int xbmax, int* err) {
   extern __shared__ uint32_t sm[];
   uint32_t* buf = sm;
@@ -282,7 +282,7 @@ __device__ __forceinline__ uint4 pw_madd(uint4 a, uint4 x, uint4 r, const PrimeC
 // target (t = j+1 resp. j-1) and writes xhat_out; blocks >= 1 stream the
 // pointwise updates of the other targets.
 template <int RM>
-__global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n, int Wv, int Wa, int k2,
+__global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(const __grid_constant__ DevPlan S, int n, int Wv, int Wa, int k2,
                                                    EntryStore rhat,
                                                    const uint32_t* __restrict__ xhat_in,
                                                    uint32_t* xhat_out, uint32_t* acch,
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt(DevPlan S, int n
 // solve plan's digits).
 template <int RM>
 __global__ void __launch_bounds__(kSolveNttThreads) k_solve_ntt_cl(
-    DevPlan S, int n, int Wv, int Wa, int k2, EntryStore rhat,
+    const __grid_constant__ DevPlan S, int n, int Wv, int Wa, int k2, EntryStore rhat,
     const uint32_t* __restrict__ xhat_in, uint32_t* xhat_out, uint32_t* acch, int j, int dir,
     Finish fin, int xbmax, int* err) {
   namespace cg = cooperative_groups;

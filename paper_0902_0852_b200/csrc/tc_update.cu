@@ -83,7 +83,7 @@ __device__ __forceinline__ uint32_t plane4(uint32_t w0, uint32_t w1, uint32_t w2
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1)
-k_update_tc(DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
+k_update_tc(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase, const uint32_t* Vhat,
             const uint32_t* Rhat, long long row_stride_slot, int nslots, int c_begin,
             int c_end, int nchalf, const int* err) {
   extern __shared__ __align__(1024) uint8_t smem[];
