@@ -107,9 +107,13 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
   if (stage_aborted(err)) return;
   const int L = P.L, np = P.np, T = P.T, w = P.w;
   const int M = L + T;
+  // rows this CTA extracts: with one, the tables are read from global memory
+  // (and take no shared memory: the launch may size it without them)
+  const bool multi = r_begin + bx + gx < r_end;
+  const int tw_words = (P.tw_smem && multi) ? P.NW : 0;
   uint32_t* tabf = sm;
-  uint32_t* tabi = sm + (P.tw_smem ? P.NW : 0);
-  uint32_t* A = tabi + (P.tw_smem ? P.NW : 0);  // np*L residues -> CRT words
+  uint32_t* tabi = sm + tw_words;
+  uint32_t* A = tabi + tw_words;  // np*L residues -> CRT words
   int64_t* S = reinterpret_cast<int64_t*>(A + P.NW);  // M digit sums
   uint64_t* Dg = reinterpret_cast<uint64_t*>(S + M);  // M digits
   uint32_t* Lb = reinterpret_cast<uint32_t*>(Dg + M); // cap limbs of |W|
@@ -120,8 +124,6 @@ __device__ void extract_body(const DevPlan& P, const uint32_t* W, const long lon
   if (xph) xs[0] = clock64();
   const uint32_t* twm;
   const uint32_t* itwm;
-  // rows this CTA extracts: with one, the tables are read from global memory
-  const bool multi = r_begin + bx + gx < r_end;
   stage_tables(P, tabf, tabi, &twm, &itwm, multi);
   const uint64_t dmask = (1ull << w) - 1ull;
 
@@ -640,11 +642,13 @@ __device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int 
     ys += b * P.bat_ys;
     gscratch += (long long)b * gx * cta_words;
   }
+  // one row per CTA: twiddles from global memory, no table region
+  const bool multi = r_begin + bx + gx < r_end;
   uint32_t* tab = sm_dyn;
   uint32_t* sm = use_gscratch ? gscratch + (long long)bx * cta_words
-                              : sm_dyn + (P.tw_smem ? P.NW : 0);
+                              : sm_dyn + ((P.tw_smem && multi) ? P.NW : 0);
   const uint32_t* twm;
-  stage_tables(P, tab, nullptr, &twm, nullptr, r_begin + bx + gx < r_end);
+  stage_tables(P, tab, nullptr, &twm, nullptr, multi);
   const int CY = (cap + ycap + 2 + 3) & ~3;  // 16-byte aligned regions
   uint32_t* Vt = sm;                 // cap      } later: Qt (cap + ycap)
   uint32_t* Y = Vt + cap;            // ycap     }
@@ -1322,9 +1326,9 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
   return post_launch(st);
 }
 
-size_t extract_smem_bytes(const DevPlan& P) {
+size_t extract_smem_bytes(const DevPlan& P, bool staged) {
   const int M = P.L + P.T;
-  return (size_t)((P.tw_smem ? 2 * P.NW : 0) + P.NW + 4 * M + P.cap + 64) * 4;
+  return (size_t)((P.tw_smem && staged ? 2 * P.NW : 0) + P.NW + 4 * M + P.cap + 64) * 4;
 }
 
 cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
@@ -1336,8 +1340,10 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
-  // a single row is on the pivot chain: give it more threads
-  k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256, extract_smem_bytes(P), st>>>(
+  // a single row is on the pivot chain: give it more threads; one row per
+  // CTA needs no twiddle tables in shared memory
+  k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256,
+              extract_smem_bytes(P, rows > P.grid_cap), st>>>(
       P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
       maxdegV, err, round, vdig, kd);
   return post_launch(st);
@@ -1405,7 +1411,7 @@ cudaError_t launch_pivot(const DevPlan& P, uint32_t* W, const long long* colbase
                          int use_gscratch, int* err, cudaStream_t st,
                          const PivotDiv& pd) {
   ++g_launches;
-  size_t smem = std::max(extract_smem_bytes(P),
+  size_t smem = std::max(extract_smem_bytes(P, true),
                          use_gscratch ? (size_t)0 : (size_t)pd.recip_words * 4);
   if (pd.on)
     smem = std::max(smem, pd.use_dscr ? (size_t)(P.tw_smem ? P.NW : 0) * 4
@@ -1476,8 +1482,10 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
   r_end = min(r_end, P.n);
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
-  const size_t smem = use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
-                                   : divide_smem_words(P) * 4;
+  // one row per CTA: no twiddle table in shared memory
+  const size_t tw = rows <= P.grid_cap && P.tw_smem ? (size_t)P.NW * 4 : 0;
+  const size_t smem = (use_gscratch ? (size_t)(P.tw_smem ? P.NW : 0) * 4
+                                    : divide_smem_words(P) * 4) - tw;
   ++g_launches;
   if (rows == 1)
     k_divide1<<<1, 512, smem, st>>>(P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0,
@@ -1519,6 +1527,18 @@ cudaError_t launch_ratio_finish(const DevPlan& P, IntBuf vint, long long vrow0,
   return post_launch(st);
 }
 
+// HGPU_UPD_PAD (bytes): dynamic shared memory requested per k_update_tiled
+// CTA (at least its 32 KB tile); ~76 KB holds the update to two CTAs per SM,
+// leaving every SM a slot for the panel's single-row kernels (experiment)
+static size_t upd_smem() {
+  static const size_t v = [] {
+    const char* e = getenv("HGPU_UPD_PAD");
+    const size_t base = (size_t)kUT * kUT * kUWords * 4;
+    return e ? std::max(base, (size_t)atol(e)) : base;
+  }();
+  return v;
+}
+
 cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
@@ -1532,7 +1552,7 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
     for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
     dim3 grid((unsigned)tiles, P.NW / kUWords);
     ++g_launches;
-    k_update_tiled<<<grid, 128, kUT * kUT * kUWords * 4, st>>>(P, W, colbase, Vhat, Rhat,
+    k_update_tiled<<<grid, 128, upd_smem(), st>>>(P, W, colbase, Vhat, Rhat,
                                          row_stride_slot, nslots, c_begin,
                                          c_end, nct, nrt, err, c_begin, P.n, 0);
     return cudaGetLastError();
@@ -1566,7 +1586,7 @@ cudaError_t launch_update_rect(const DevPlan& P, uint32_t* W,
   const int nrt = (r_hi - r_lo + kUT - 1) / kUT;
   dim3 grid((unsigned)(nct * nrt), P.NW / kUWords);
   ++g_launches;
-  k_update_tiled<<<grid, 128, kUT * kUT * kUWords * 4, st>>>(
+  k_update_tiled<<<grid, 128, upd_smem(), st>>>(
       P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c_begin, c_end, nct, nrt,
       err, r_lo, r_hi, 1);
   return post_launch(st);
@@ -1581,7 +1601,7 @@ cudaError_t launch_col_extract(const DevPlan& P, uint32_t* W, const long long* c
   const int rows = r_end - r_begin;
   if (rows <= 0) return cudaSuccess;
   ++g_launches;
-  k_col_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P), st>>>(
+  k_col_extract<<<min(rows, P.grid_cap), 256, extract_smem_bytes(P, false), st>>>(
       P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, p, r_begin, r_end, vint, vrow0, piv,
       maxbitsV, vhat, maxdegV, err, vdig, kd);
   return post_launch(st);
@@ -1616,7 +1636,7 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
   cudaGetDevice(&dev);
   int maxopt = 0;
   cudaDeviceGetAttribute(&maxopt, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t ext = extract_smem_bytes(P);
+  const size_t ext = extract_smem_bytes(P, true);
   const size_t fwd = (size_t)((P.tw_smem ? P.NW : 0) + P.NW + P.cap) * 4;
   if ((int)ext > maxopt || (int)fwd > maxopt) return cudaErrorInvalidValue;
   cudaError_t e;
@@ -1641,6 +1661,10 @@ cudaError_t configure_kernels(const DevPlan& P, size_t* div_smem,
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 0;
     return (size_t)maxopt > fa.sharedSizeBytes ? (size_t)maxopt - fa.sharedSizeBytes : 0;
   };
+  if ((e = cudaFuncSetAttribute(k_update_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::min(upd_smem(), dyn_cap((const void*)k_update_tiled)))) !=
+      cudaSuccess)
+    return e;
   g_pivot_dyn = std::min(dyn_cap((const void*)k_pivot), dyn_cap((const void*)k_pivot_lean));
   g_recip_dyn = dyn_cap((const void*)k_recip);
   const size_t rec = recip_body_words(P) * 4;
