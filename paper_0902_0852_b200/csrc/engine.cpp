@@ -514,6 +514,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_SOLVE_NTT")) solve_ntt_ = std::atoi(e);
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_EDF_RUN")) edf_run_ = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_UPDATE_TC")) update_tc_ = std::atoi(e) != 0;
@@ -601,7 +602,33 @@ void Matrix::release() {
                   (void*)stats_, (void*)err_})
     dfree(p);
   release_interval();
-  // inverse-iteration state (sized by the plan's capacity)
+  // inverse-iteration state (sized by the plan's capacity); a resident
+  // start vector survives a re-plan through a host copy
+  if (start_resident_ && svhdr_) {
+    try {
+      const int n = n_, Wv = sWv_;
+      std::vector<int> hdr((size_t)n);
+      std::vector<uint32_t> lim((size_t)n * Wv);
+      CU(cudaMemcpy(hdr.data(), svhdr_, hdr.size() * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(lim.data(), svlimbs_, lim.size() * 4, cudaMemcpyDeviceToHost));
+      saved_start_.assign(n, HostInt{});
+      for (int i = 0; i < n; ++i) {
+        saved_start_[i].size = hdr[i];
+        saved_start_[i].limbs.assign(lim.begin() + (size_t)i * Wv,
+                                     lim.begin() + (size_t)i * Wv + std::abs(hdr[i]));
+      }
+    } catch (const Error&) {
+      saved_start_.clear();
+    }
+  }
+  start_resident_ = have_y_ = false;
+  for (void* p : {(void*)rq_prod_, (void*)rq_out_, (void*)rq_scr_, (void*)rq_colsum_,
+                  (void*)rq_sign_})
+    dfree(p);
+  rq_prod_ = rq_out_ = rq_scr_ = nullptr;
+  rq_colsum_ = nullptr;
+  rq_sign_ = nullptr;
+  rq_maxlen_ = rq_grid_ = 0;
   for (void* p : {(void*)lhdr_, (void*)llimbs_, (void*)svhdr_, (void*)svlimbs_,
                   (void*)sacc_, (void*)sgscr_, (void*)spair_hdr_,
                   (void*)spair_limbs_, (void*)sbits_, (void*)sybuf_,
@@ -1392,7 +1419,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         continue;
       }
       int m = 1;
-      while (m < 8 && bp + m <= bmax && edf_next[bp + m] == j &&
+      while (m < edf_run_ && bp + m <= bmax && edf_next[bp + m] == j &&
              (bp % nsets) + m < nsets)
         ++m;
       edf_enqueue(bp, m, j);
@@ -2014,11 +2041,28 @@ void Matrix::keep_panel_L(int p0, int ns, long long row0set, cudaStream_t st,
 
 std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
                                    long long* launches) {
+  set_start(u);
+  return solve_resident(launches, true);
+}
+
+// Solves with the right-hand side already in the solve buffer's u rows
+// (set_start, or rescale_start after an earlier solve); y stays on the
+// device (rows 3n..4n) and is copied back only on request.
+std::vector<HostInt> Matrix::solve_resident(long long* launches, bool download) {
+  if (!start_resident_ && !saved_start_.empty()) {
+    // a re-plan released the solve buffers: the start vector comes back
+    const std::vector<HostInt> u = std::move(saved_start_);
+    saved_start_.clear();
+    set_start(u);
+  }
+  if (!start_resident_)
+    throw Error(HGPU_ERR_INVALID_ARGUMENT, "solve_resident needs a start vector (set_start)");
   // tensor-core AXPY (HGPU_SOLVE_TC=1) once an earlier solve has recorded
   // the operand widths; any capacity flag reruns the solve on the integer path
+  // (the u rows are never written by a solve, so a rerun reads the same u)
   if (solve_ntt_) {
     try {
-      return solve_impl(u, launches, 2);
+      return solve_impl(launches, 2, download);
     } catch (const Error& e) {
       if (e.status != HGPU_ERR_CAPACITY || solve_ntt_ == 2) throw;
       sdp_bits_ = 0;  // re-plan from the widths the integer path records
@@ -2027,17 +2071,156 @@ std::vector<HostInt> Matrix::solve(const std::vector<HostInt>& u,
   }
   if (solve_tc_ && solve_xlimbs_ > 0) {
     try {
-      return solve_impl(u, launches, 1);
+      return solve_impl(launches, 1, download);
     } catch (const Error& e) {
       if (e.status != HGPU_ERR_CAPACITY) throw;
       solve_xlimbs_ = 0;
     }
   }
-  return solve_impl(u, launches, 0);
+  return solve_impl(launches, 0, download);
 }
 
-std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
-                                        long long* launches, int mode) {
+void Matrix::ensure_solve_buffers() {
+  if (svhdr_) return;
+  const Plan& P = plan_or_build();
+  const int n = n_;
+  CU(cudaSetDevice(device_));
+  sWv_ = 2 * P.cap + 8;
+  sWa_ = P.cap + sWv_ + 2;
+  svhdr_ = dalloc<int>(4 * (size_t)n);
+  svlimbs_ = dalloc<uint32_t>(4 * (size_t)n * sWv_);
+  sacc_ = dalloc<uint32_t>((size_t)n * sWa_);
+  spair_hdr_ = dalloc<int>(2 * (size_t)n);
+  spair_limbs_ = dalloc<uint32_t>(2 * (size_t)n * sWv_);
+  bool axpy_global = false;
+  CU(configure_solve_kernels(P.cap, sWv_, sWa_, &axpy_global));
+  if (axpy_global)
+    sgscr_ = dalloc<uint32_t>((size_t)dp_.grid_cap *
+                              solve_axpy_smem_words(sWv_, P.cap, sWv_, sWa_));
+}
+
+// The right-hand side u (n signed limb vectors) into the solve buffer.
+void Matrix::set_start(const std::vector<HostInt>& u) {
+  if (world_ != 1 && !(group_ && rank_ == 0))
+    throw Error(HGPU_ERR_INVALID_ARGUMENT,
+                "solve runs on a single rank (or rank 0 of an in-process group)");
+  if ((int)u.size() != n_) throw Error(HGPU_ERR_INVALID_ARGUMENT, "start vector length");
+  ensure_solve_buffers();
+  const int n = n_, Wv = sWv_;
+  cudaStream_t st = stream_;
+  CU(cudaSetDevice(device_));
+  std::vector<int> hdr((size_t)n, 0);
+  std::vector<uint32_t> lim((size_t)n * Wv, 0);
+  for (int i = 0; i < n; ++i) {
+    if ((int)u[i].limbs.size() > Wv)
+      throw Error(HGPU_ERR_CAPACITY, "start vector entry too large");
+    hdr[i] = u[i].size;
+    std::copy(u[i].limbs.begin(), u[i].limbs.end(), lim.begin() + (size_t)i * Wv);
+  }
+  CU(cudaMemcpyAsync(svhdr_, hdr.data(), hdr.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(svlimbs_, lim.data(), lim.size() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  start_resident_ = true;
+  have_y_ = false;
+  saved_start_.clear();
+}
+
+namespace {
+// M + 2 two's-complement limbs -> sign and magnitude
+HostInt from_twos(const uint32_t* w, int words) {
+  HostInt h;
+  const bool neg = (w[words - 1] & 0x80000000u) != 0;
+  h.limbs.assign(w, w + words);
+  if (neg) {
+    uint64_t c = 1;
+    for (uint32_t& x : h.limbs) {
+      c += (uint64_t)(uint32_t)~x;
+      x = (uint32_t)c;
+      c >>= 32;
+    }
+  }
+  while (!h.limbs.empty() && h.limbs.back() == 0) h.limbs.pop_back();
+  h.size = neg ? -(int)h.limbs.size() : (int)h.limbs.size();
+  return h;
+}
+}  // namespace
+
+// num = y.u and den = y.y of the last solve, exact, on the device
+// (rq_kernels.cu); ybits = max_i bits(|y_i|), which fixes the next scaling.
+void Matrix::rayleigh(HostInt& num, HostInt& den, long& ybits, long long* launches) {
+  if (!have_y_) throw Error(HGPU_ERR_INVALID_ARGUMENT, "rayleigh needs a solve");
+  const int n = n_, Wv = sWv_;
+  cudaStream_t st = stream_;
+  CU(cudaSetDevice(device_));
+  const int maxlen = std::max(1, std::max(last_ulimbs_, last_ylimbs_));
+  const int M = 2 * maxlen;
+  if (maxlen > rq_maxlen_) {
+    dfree(rq_prod_);
+    dfree(rq_colsum_);
+    dfree(rq_out_);
+    dfree(rq_scr_);
+    rq_scr_ = nullptr;
+    const int cap = maxlen + maxlen / 8 + 8;  // room for the iterates to grow
+    if (!rq_sign_) rq_sign_ = dalloc<int>(2 * (size_t)n);
+    rq_prod_ = dalloc<uint32_t>(2 * (size_t)n * 2 * cap);
+    rq_colsum_ = dalloc<long long>(2 * (size_t)2 * cap);
+    rq_out_ = dalloc<uint32_t>(2 * ((size_t)2 * cap + 2));
+    bool global = false;
+    CU(configure_rq_kernels(cap, &global));
+    rq_grid_ = n;
+    if (global) {
+      rq_grid_ = std::min(n, 2 * 148);
+      rq_scr_ = dalloc<uint32_t>((size_t)rq_grid_ * rq_products_words(cap));
+    }
+    rq_maxlen_ = cap;
+  }
+  // the shared-memory layout follows the operands actually met (maxlen), the
+  // global scratch the allocation (rq_maxlen_)
+  const int lay = rq_scr_ ? rq_maxlen_ : maxlen;
+  const int Ml = 2 * lay;
+  (void)M;
+  IntBuf vecs{svhdr_, svlimbs_};
+  int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
+  CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+  CU(launch_rq_products(vecs, 3 * n, 0, n, Wv, lay, rq_prod_, rq_sign_, rq_scr_, rq_grid_,
+                        err_, st));
+  CU(launch_rq_reduce(rq_prod_, rq_sign_, n, Ml, rq_colsum_, rq_out_, st));
+  CU(launch_int_bits_batch(vecs, 3 * n, 1, Wv, n, sbits_, st));
+  if (launches) *launches += 4;
+  std::vector<uint32_t> out(2 * ((size_t)Ml + 2));
+  std::vector<int> bits((size_t)n);
+  int herr[kErrWords];
+  CU(cudaMemcpyAsync(out.data(), rq_out_, out.size() * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(bits.data(), sbits_, bits.size() * 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr[kErrCapacity])
+    throw Error(HGPU_ERR_INTERNAL, "Rayleigh-quotient layout smaller than its operands");
+  num = from_twos(out.data(), Ml + 2);
+  den = from_twos(out.data() + Ml + 2, Ml + 2);
+  ybits = 0;
+  for (int i = 0; i < n; ++i) ybits = std::max<long>(ybits, bits[i]);
+}
+
+// u <- y 2^-sh (tdiv_2exp for sh > 0): the next start vector, on the device.
+void Matrix::rescale_start(long sh, long long* launches) {
+  if (!have_y_) throw Error(HGPU_ERR_INVALID_ARGUMENT, "rescale_start needs a solve");
+  const int n = n_, Wv = sWv_;
+  cudaStream_t st = stream_;
+  CU(cudaSetDevice(device_));
+  IntBuf vecs{svhdr_, svlimbs_};
+  int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
+  CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
+  CU(launch_rq_rescale(vecs, 3 * n, 0, n, Wv, (int)sh, err_, st));
+  if (launches) *launches += 1;
+  int herr[kErrWords];
+  CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (herr[kErrCapacity]) throw Error(HGPU_ERR_CAPACITY, "rescaled start vector too large");
+  have_y_ = false;
+}
+
+std::vector<HostInt> Matrix::solve_impl(long long* launches, int mode, bool download) {
   const bool tc = mode == 1, ntt = mode == 2;
   const auto t_start = std::chrono::steady_clock::now();
   if (!have_L_)
@@ -2049,20 +2232,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
   const int n = n_, k2 = K_ / 2;
   cudaStream_t st = stream_;
   CU(cudaSetDevice(device_));
-  if (!svhdr_) {
-    sWv_ = 2 * P.cap + 8;
-    sWa_ = P.cap + sWv_ + 2;
-    svhdr_ = dalloc<int>(4 * (size_t)n);
-    svlimbs_ = dalloc<uint32_t>(4 * (size_t)n * sWv_);
-    sacc_ = dalloc<uint32_t>((size_t)n * sWa_);
-    spair_hdr_ = dalloc<int>(2 * (size_t)n);
-    spair_limbs_ = dalloc<uint32_t>(2 * (size_t)n * sWv_);
-    bool axpy_global = false;
-    CU(configure_solve_kernels(P.cap, sWv_, sWa_, &axpy_global));
-    if (axpy_global)
-      sgscr_ = dalloc<uint32_t>((size_t)dp_.grid_cap *
-                                solve_axpy_smem_words(sWv_, P.cap, sWv_, sWa_));
-  }
+  ensure_solve_buffers();
   // division plan: the LDL^T plan with integer capacity Wv (k_recip/k_divide
   // over pairs (piv_p, z_p 2^k2), scratch in global memory, no transform),
   // batched over all n pairs on gridDim.y
@@ -2254,22 +2424,8 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
   IntBuf pairs{spair_hdr_, spair_limbs_};
   IntBuf L{lhdr_, llimbs_};
   const int U = 0, Z = n, Wq = 2 * n, Y = 3 * n;
-  {
-    std::vector<int> hdr(4 * (size_t)n, 0);
-    std::vector<uint32_t> lim((size_t)n * Wv, 0);
-    for (int i = 0; i < n; ++i) {
-      if ((int)u[i].limbs.size() > Wv)
-        throw Error(HGPU_ERR_CAPACITY, "start vector entry too large");
-      hdr[i] = u[i].size;
-      std::copy(u[i].limbs.begin(), u[i].limbs.end(),
-                lim.begin() + (size_t)i * Wv);
-    }
-    CU(cudaMemcpyAsync(svhdr_, hdr.data(), hdr.size() * 4,
-                       cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(svlimbs_, lim.data(), lim.size() * 4,
-                       cudaMemcpyHostToDevice, st));
-    CU(cudaStreamSynchronize(st));
-  }
+  // (the z | w | y headers are rewritten by the solve's own kernels)
+  CU(cudaMemsetAsync(svhdr_ + n, 0, 3 * (size_t)n * sizeof(int), st));
   // the AXPY's shared-memory layout at full operand capacities (measured:
   // layouts sized to the operands actually met let the block scheduler pack
   // more CTAs per SM and ran slower on this grid)
@@ -2278,7 +2434,7 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
   long long nl = 0;
   int herr[kErrWords];
   std::vector<int> vh(4 * (size_t)n);
-  std::vector<uint32_t> yl((size_t)n * Wv);
+  std::vector<uint32_t> yl(download ? (size_t)n * Wv : 0);
   {
     int herr0[kErrWords] = {INT_MAX, 0, 0, 0};
     CU(cudaMemcpyAsync(err_, herr0, sizeof(herr0), cudaMemcpyHostToDevice, st));
@@ -2372,8 +2528,9 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
     }
     CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(vh.data(), svhdr_, vh.size() * 4, cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(yl.data(), svlimbs_ + (size_t)Y * Wv, yl.size() * 4,
-                       cudaMemcpyDeviceToHost, st));
+    if (download)
+      CU(cudaMemcpyAsync(yl.data(), svlimbs_ + (size_t)Y * Wv, yl.size() * 4,
+                         cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
   }
   if (launches) *launches += nl;
@@ -2400,6 +2557,13 @@ std::vector<HostInt> Matrix::solve_impl(const std::vector<HostInt>& u,
       mx = std::max(mx, std::max(std::abs(vh[(size_t)Z + i]), std::abs(vh[(size_t)Y + i])));
     solve_xlimbs_ = std::max(solve_xlimbs_, mx);
   }
+  last_ulimbs_ = last_ylimbs_ = 0;
+  for (int i = 0; i < n; ++i) {
+    last_ulimbs_ = std::max(last_ulimbs_, std::abs(vh[(size_t)U + i]));
+    last_ylimbs_ = std::max(last_ylimbs_, std::abs(vh[(size_t)Y + i]));
+  }
+  have_y_ = true;
+  if (!download) return {};
   std::vector<int> yh(vh.begin() + Y, vh.begin() + Y + n);
   std::vector<HostInt> y(n);
   for (int i = 0; i < n; ++i) {

@@ -115,9 +115,16 @@ class Matrix {
   // Solves (M - sI) y = u with the factors of the last HGPU_KEEP_L
   // factorisation (solve_kernels.cu); u, y at F fractional bits.
   std::vector<HostInt> solve(const std::vector<HostInt>& u, long long* launches);
+  // Device-resident inverse iteration (host/rqi.cpp): the start vector stays
+  // in the solve buffer, y.u and y.y are formed by rq_kernels.cu, and the next
+  // start vector is y rescaled in place; only num, den and bits(y) come back.
+  void set_start(const std::vector<HostInt>& u);
+  std::vector<HostInt> solve_resident(long long* launches, bool download);
+  void rayleigh(HostInt& num, HostInt& den, long& ybits, long long* launches);
+  void rescale_start(long sh, long long* launches);
   // mode 0: integer AXPY, 1: tensor-core AXPY, 2: transform-domain AXPY
-  std::vector<HostInt> solve_impl(const std::vector<HostInt>& u, long long* launches,
-                                  int mode);
+  std::vector<HostInt> solve_impl(long long* launches, int mode, bool download);
+  void ensure_solve_buffers();
   int order() const { return n_; }
   const HostInt& strip_entry(int s) const { return strip_[s]; }
   // Interval mode (iv_engine.cpp): the constructor's strip holds the lower
@@ -247,6 +254,14 @@ class Matrix {
   int* spair_hdr_ = nullptr;    // (piv_p, z_p 2^k2) pairs, 2n rows
   uint32_t* spair_limbs_ = nullptr;
   int* sbits_ = nullptr;
+  // Rayleigh quotient on the device (rq_kernels.cu)
+  bool start_resident_ = false, have_y_ = false;
+  std::vector<HostInt> saved_start_;  // the start vector across a re-plan
+  int last_ulimbs_ = 0, last_ylimbs_ = 0;  // widest u / y entry of the last solve
+  int rq_maxlen_ = 0, rq_grid_ = 0;
+  uint32_t *rq_prod_ = nullptr, *rq_out_ = nullptr, *rq_scr_ = nullptr;
+  long long* rq_colsum_ = nullptr;
+  int* rq_sign_ = nullptr;
   uint32_t *sybuf_ = nullptr, *srscr_ = nullptr, *sdscr_ = nullptr;
   int* sys_ = nullptr;
   int dmax_bits_ = 0;
@@ -266,6 +281,7 @@ class Matrix {
   long long lhat_for_ = -1;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
+  int edf_run_ = 8;  // panels accumulated by one EDF update launch (HGPU_EDF_RUN, 1-8)
   // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)
   bool pre_entry_ = true;
   // trailing update on the tensor cores (tc_update.cu, HGPU_UPDATE_TC=1);

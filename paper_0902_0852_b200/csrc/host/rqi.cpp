@@ -9,6 +9,8 @@
 // plain steps) phase 2 (Rayleigh-quotient iteration) refactors at s = rho;
 // once it is below 2^-max(64, K/16) phase 3 keeps those factors again (each
 // solve then gains ~K/8 bits for the price of a solve, not a factorisation):
+// Every O(n) multiprecision step runs on the GPU and the iterate never
+// leaves it: the host keeps only sigma, rho and the stopping rule.
 //   factor   M - s_k I = L D L^T          (GPU LDL^T, HGPU_KEEP_L)
 //   solve    (M - s_k I) y = u_k          (GPU triangular solves, exact with
 //                                          one truncation per entry)
@@ -27,7 +29,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "../../../include/hgpu.h"
@@ -44,12 +45,6 @@ char* dup_c(const std::string& s) {
   char* o = static_cast<char*>(std::malloc(s.size() + 1));
   if (o) std::memcpy(o, s.c_str(), s.size() + 1);
   return o;
-}
-
-HostInt to_host(const Z& z) {
-  HostInt h;
-  h.size = z.to_limbs(h.limbs);
-  return h;
 }
 
 Z from_host(const HostInt& h) { return Z::from_limbs(h.size, h.limbs.data()); }
@@ -75,14 +70,18 @@ extern "C" hgpu_status hgpu_inverse_iteration(
       throw Error(HGPU_ERR_INVALID_ARGUMENT, "bad argument");
     const long n = mm->order(), k = mm->frac_bits(), k2 = k / 2;
     const auto t0 = std::chrono::steady_clock::now();
-    std::vector<Z> u(n);
+    // the start vector goes to the device once; every later iterate stays
+    // there (solve -> Rayleigh quotient -> rescale, engine.cpp / rq_kernels.cu)
     {
+      std::vector<HostInt> uh(n);
       const uint32_t* src = u_limbs;
       for (long i = 0; i < n; ++i) {
         const int len = std::abs(u_sizes[i]);
-        u[i] = Z::from_limbs(u_sizes[i], src);
+        uh[i].size = u_sizes[i];
+        uh[i].limbs.assign(src, src + len);
         src += len;
       }
+      mm->set_start(uh);
     }
     Z sigma = Z::from_limbs(sigma_size, sigma_limbs);
     Z rho_prev, d_min, rho;
@@ -116,33 +115,17 @@ extern "C" hgpu_status hgpu_inverse_iteration(
         factored = true;
       }
       auto tb = std::chrono::steady_clock::now();
-      std::vector<HostInt> uh(n);
-      for (long i = 0; i < n; ++i) uh[i] = to_host(u[i]);
       long long nl = 0;
-      const std::vector<HostInt> yh = mm->solve(uh, &nl);
-      std::vector<Z> y(n);
+      mm->solve_resident(&nl, false);
+      // y.u, y.y: 2n products of ~K-bit integers and their exact sums on the
+      // device; the host receives the two sums and max bits(y_i)
+      long ybits = 0;
       Z num, den;
       {
-        // u.y and y.y: n products of ~K-bit integers each, split over host
-        // threads (GMP objects are per thread; the partial sums are exact)
-        const long nth = std::max(1L, std::min<long>(
-                                          16, std::min<long>((long)std::thread::hardware_concurrency(),
-                                                             n / 32 + 1)));
-        std::vector<Z> pn(nth), pd(nth);
-        std::vector<std::thread> pool;
-        for (long t = 0; t < nth; ++t)
-          pool.emplace_back([&, t] {
-            for (long i = t; i < n; i += nth) {
-              y[i] = from_host(yh[i]);
-              pn[t] = pn[t] + y[i] * u[i];
-              pd[t] = pd[t] + y[i] * y[i];
-            }
-          });
-        for (std::thread& th : pool) th.join();
-        for (long t = 0; t < nth; ++t) {
-          num = num + pn[t];
-          den = den + pd[t];
-        }
+        HostInt hn, hd;
+        mm->rayleigh(hn, hd, ybits, &nl);
+        num = from_host(hn);
+        den = from_host(hd);
       }
       if (den.sgn() == 0) throw Error(HGPU_ERR_INTERNAL, "solve returned zero");
       rho = sigma + tdiv(shl(num, (unsigned long)k), den);
@@ -185,12 +168,8 @@ extern "C" hgpu_status hgpu_inverse_iteration(
       have_prev = true;
       if (phase == 1) ++plain;
       // next start vector: y scaled so that max |u_i| lies in [1/2, 1)
-      long mb = 0;
-      for (long i = 0; i < n; ++i) mb = std::max(mb, y[i].bits());
-      const long sh = mb - k;
-      for (long i = 0; i < n; ++i)
-        u[i] = sh > 0 ? tdiv_2exp(y[i], (unsigned long)sh)
-                      : shl(y[i], (unsigned long)(-sh));
+      // (tdiv_2exp(y_i, sh) for sh > 0, else y_i 2^-sh), in place on the device
+      mm->rescale_start(ybits - k, &nl);
       if (phase == 2) {
         sigma = rho;
         factored = false;

@@ -304,6 +304,20 @@ cudaError_t configure_solve_tc(int Wv, int Wa, int mc, int* ok);
 cudaError_t launch_int_bits_batch(IntBuf v, int idx0, int step, int stride,
                                   int count, int* out, cudaStream_t st);
 cudaError_t configure_solve_kernels(int cap, int Wv, int Wa, bool* axpy_global);
+// rq_kernels.cu (the Rayleigh quotient of inverse iteration on the device):
+// products |y_i u_i|, y_i^2 of the solve buffer's rows yi0 + i, ui0 + i
+// (M = 2 maxlen columns each, sign apart), their exact signed sums as M + 2
+// two's-complement limbs (out[0..M+2): num, out[M+2..2M+4): den), and the
+// next start vector u_i = y_i scaled by 2^-sh (truncated toward zero).
+size_t rq_products_words(int maxlen);
+cudaError_t configure_rq_kernels(int maxlen, bool* use_global);
+cudaError_t launch_rq_products(IntBuf v, int yi0, int ui0, int n, int Wv, int maxlen,
+                               uint32_t* prod, int* psign, uint32_t* gscratch, int grid,
+                               int* err, cudaStream_t st);
+cudaError_t launch_rq_reduce(const uint32_t* prod, const int* psign, int n, int M,
+                             long long* colsum, uint32_t* out, cudaStream_t st);
+cudaError_t launch_rq_rescale(IntBuf v, int yi0, int ui0, int n, int Wv, int sh, int* err,
+                              cudaStream_t st);
 // fold_kernels.cu
 long long fold_pivots_device(const uint32_t* plimbs, const int* plen, int n,
                              int pcap, int K, uint32_t* X0, uint32_t* X1,
