@@ -1010,7 +1010,9 @@ void Matrix::build(int min_logL) {
     int per_sm = 2;
     if (const char* g = std::getenv("HGPU_GRID")) per_sm = std::max(1, std::atoi(g));
     D.grid_cap = per_sm * nsm;
-    D.recip_fast = 1;  // HGPU_RECIP_FAST=0: the original reciprocal (same Y)
+    // HGPU_RECIP_FAST=0: the original reciprocal; 1: the latency-lean body (same
+    // Y bit for bit); 3 (default): its first levels on the register ladder
+    D.recip_fast = 3;
     if (const char* rf = std::getenv("HGPU_RECIP_FAST")) D.recip_fast = std::atoi(rf);
     if (const char* dbg = std::getenv("HGPU_DEBUG")) D.debug = std::atoi(dbg);
 #ifndef HGPU_TIMING_EXPERIMENTS

@@ -219,6 +219,93 @@ __device__ inline void serial_mul(const uint32_t* a, int na, const uint32_t* b, 
   }
 }
 
+
+// ---- register ladder -------------------------------------------------------
+// The first Newton levels (precision <= kRegBits) on warp 0 in registers: a
+// 512-bit fixed-point reciprocal of the divisor's top 512 bits, one 32-bit
+// limb per lane, operands exchanged by shuffles, so no level of it touches
+// shared memory or a barrier (the shared-memory levels cost 12-19k cycles
+// each for a few limbs of work).
+constexpr int kRegBits = 400;
+
+// Digits of sum_k v_k 2^(32 k) + cin mod 2^1024, lane k holding v_k < 3 2^32:
+// after the carries c_k = v_k >> 32 move one lane up the remaining carries
+// are binary, and the ballot identity of fast_resolve gives every lane's.
+__device__ __forceinline__ uint32_t warp_digits(unsigned long long v, uint32_t cin) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t d = (uint32_t)v, c = (uint32_t)(v >> 32);
+  uint32_t cprev = __shfl_up_sync(0xffffffffu, c, 1);
+  if (lane == 0) cprev = cin;
+  const unsigned long long sv = (unsigned long long)d + cprev;
+  const bool g = (sv >> 32) != 0;
+  const bool pr = !g && (uint32_t)sv == 0xFFFFFFFFu;
+  const uint32_t G = __ballot_sync(0xffffffffu, g), P = __ballot_sync(0xffffffffu, pr);
+  const unsigned long long x = (unsigned long long)(G | P), y = G;
+  const unsigned long long t = x + y;
+  return (uint32_t)sv + (uint32_t)(((t ^ x ^ y) >> lane) & 1u);
+}
+
+// limb `lane` of a * b (a, b: 16 limbs, lane l < 16 holds limb l, 0 above)
+__device__ __forceinline__ uint32_t warp_mul16(uint32_t a, uint32_t b) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long lo = 0;
+  uint32_t hi = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t ai = __shfl_sync(0xffffffffu, a, i);
+    const int j = lane - i;
+    uint32_t bj = __shfl_sync(0xffffffffu, b, j & 31);
+    if (j < 0 || j > 15) bj = 0u;
+    const unsigned long long p = (unsigned long long)ai * bj;
+    lo += p;
+    hi += lo < p ? 1u : 0u;
+  }
+  unsigned long long v = (uint32_t)lo;
+  const uint32_t w1 = __shfl_up_sync(0xffffffffu, (uint32_t)(lo >> 32), 1);
+  const uint32_t w2 = __shfl_up_sync(0xffffffffu, hi, 2);
+  if (lane >= 1) v += w1;
+  if (lane >= 2) v += w2;
+  return warp_digits(v, 0u);
+}
+
+// Warp 0: lane l < 16 holds limb l of d in [2^511, 2^512); returns limb l of
+// y = floor(2^(pa + 512) / d) within one unit (pa <= kRegBits).  x ~ 2^1022 / d
+// (x / 2^510 ~ 1 / (d / 2^512) in (1, 2]) by four full-width Newton steps
+// x <- x (2 - d x) from the FP64 seed (relative error 2^-51 -> 2^-102 ->
+// 2^-204 -> 2^-408 -> the truncation floor of a few 2^-510), then
+// y = x >> (510 - pa): the error of x is far below one unit of y.
+__device__ inline uint32_t reg_reciprocal(uint32_t d, int pa) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t d15 = __shfl_sync(0xffffffffu, d, 15), d14 = __shfl_sync(0xffffffffu, d, 14);
+  const double dd = ldexp((double)d15, 32) + (double)d14;                      // [2^63, 2^64]
+  const unsigned long long x63 = (unsigned long long)(ldexp(1.0, 126) / dd);   // x / 2^448
+  uint32_t x = lane == 14 ? (uint32_t)x63 : lane == 15 ? (uint32_t)(x63 >> 32) : 0u;
+#pragma unroll 1
+  for (int it = 0; it < 4; ++it) {
+    // T = floor(d x / 2^512) ~ 2^510;  E2 = 2^511 - T (2 - d x in units of 2^-510)
+    const uint32_t pr = warp_mul16(d, x);
+    const uint32_t t = __shfl_down_sync(0xffffffffu, pr, 16);  // lanes < 16: limb 16 + lane
+    const unsigned long long m = lane == 15 ? 0x80000000ull : 0ull;
+    // lanes >= 16 hold the bias alone: their digits resolve to zero
+    const unsigned long long v = lane < 16 ? m + 0xFFFFFFFFull - t : 0xFFFFFFFFull;
+    uint32_t e2 = warp_digits(v, 1u);
+    if (lane >= 16) e2 = 0u;
+    // x' = floor(x E2 / 2^510): bit 510 = limb 15, bit 30
+    const uint32_t q = warp_mul16(x, e2);
+    const uint32_t q15 = __shfl_down_sync(0xffffffffu, q, 15);
+    const uint32_t q16 = __shfl_down_sync(0xffffffffu, q, 16);
+    x = lane < 16 ? (q15 >> 30) | (q16 << 2) : 0u;
+  }
+  const int sh = 510 - pa;  // >= 110
+  const int ws = sh >> 5, bs = sh & 31;
+  const int src = lane + ws;
+  uint32_t lo = __shfl_sync(0xffffffffu, x, src & 31);
+  uint32_t hi = __shfl_sync(0xffffffffu, x, (src + 1) & 31);
+  if (src > 15) lo = 0u;
+  if (src + 1 > 15) hi = 0u;
+  return bs ? (lo >> bs) | (hi << (32 - bs)) : lo;
+}
+
 }  // namespace rf
 
 // The reciprocal of stage p's pivot value V_p[p] = vint[prow]; arguments and
@@ -238,6 +325,7 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
                                 uint32_t* Ybuf, int* ys, uint32_t* sm, long long avail_words,
                                 int* err) {
   __shared__ uint32_t red[64];
+  const long long t_entry = (P.debug & 256) ? clock64() : 0;
   const int h = vint.hdr[prow];
   const int nD = h < 0 ? -h : h;
   if (nD == 0) return true;  // flagged as ZeroPivot by k_extract
@@ -307,7 +395,29 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
   // before the first with nDt > 128 or nY > 128
   bool warp_class = true;
   const bool prof = (P.debug & 256) && p == 50 && threadIdx.x == 0;
-  for (int i = 0; i + 1 < nl; ++i) {
+  // register ladder: levels [0, i0) replaced by one 512-bit reciprocal on
+  // thread 0: Y_{i0} = floor(2^(n + lv[i0]) / D) within a unit (the ladder's
+  // own levels keep a few units; every later level tolerates < 16)
+  int i0 = 0;
+  if (P.recip_fast & 2)
+    while (i0 + 1 < nl && lv[i0 + 1] <= rf::kRegBits) ++i0;
+  if (i0 > 0) {
+    const long long t_reg = prof ? clock64() : 0;
+    const int pa = lv[i0];
+    const int nYr = min(Lm, (pa + 2 + 31) / 32 + 1);
+    if (threadIdx.x < 32) {
+      const int l = (int)threadIdx.x;
+      uint32_t dl = 0u;
+      if (l < 16) dl = field32(Ds, nDs, (long long)n - 512 + 32LL * l - 32LL * dbase);
+      const uint32_t yl = rf::reg_reciprocal(dl, pa);
+      if (l < nYr && l < 16) Y[l] = yl;
+    }
+    __syncthreads();
+    nY = nYr;
+    if (prof) printf("recip_fast register ladder to level %d (pa=%d): %lld cycles (entry + %lld)\n", i0, pa,
+                     clock64() - t_reg, t_reg - t_entry);
+  }
+  for (int i = i0; i + 1 < nl; ++i) {
     long long tph[6];
     if (prof) tph[0] = clock64();
     const int pa = lv[i], pb = lv[i + 1], dlt = pb - pa;
@@ -359,6 +469,9 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
         for (int k = 0; k < nYn; ++k) Y[k] = Dt[k];
       }
       __syncthreads();
+      if (prof)
+        printf("recip_fast lvl %d (thread 0) pa=%d pb=%d nDt=%d nY=%d: %lld cycles (entry + %lld)\n", i,
+               pa, pb, nDt, nY, clock64() - tph[0], tph[0] - t_entry);
       nY = nYn;
       continue;
     }
@@ -405,7 +518,9 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
     }
     nY = nYn;
   }
+  const long long t_lv = prof ? clock64() : 0;
   for (int k = threadIdx.x; k < P.ycap; k += blockDim.x) Ybuf[k] = k < nY ? Y[k] : 0u;
+  if (prof) printf("recip_fast store %lld cycles, total %lld\n", clock64() - t_lv, clock64() - t_entry);
   if (threadIdx.x == 0) {
     ys[0] = S;
     ys[1] = nY;
