@@ -1007,7 +1007,7 @@ void Matrix::build(int min_logL) {
     int dev = 0, nsm = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    int per_sm = 2;
+    int per_sm = 3;
     if (const char* g = std::getenv("HGPU_GRID")) per_sm = std::max(1, std::atoi(g));
     D.grid_cap = per_sm * nsm;
     // HGPU_RECIP_FAST=0: the original reciprocal; 1: the latency-lean body (same

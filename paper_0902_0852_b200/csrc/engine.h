@@ -226,7 +226,7 @@ class Matrix {
   cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
   cudaStream_t stream_far_ = nullptr;    // far rows of the panel (may lag)
   static constexpr int kMaxFarLanes = 4;
-  int far_lanes_ = 2;  // far-row streams (HGPU_FAR_LANES)
+  int far_lanes_ = 3;  // far-row streams (HGPU_FAR_LANES; 3: 255 ms, 2: 265 ms at config 3)
   cudaStream_t far_streams_[kMaxFarLanes] = {};  // [0] = stream_far_
   cudaEvent_t far_ev_[kMaxFarLanes] = {};
   cudaStream_t stream_upd1_ = nullptr;   // trailing update: next band, catch-up

@@ -379,7 +379,13 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
   int lv[40];
   const int nl = recip_levels(Pt, lv);
   const int p0 = lv[0];
-  if (threadIdx.x == 0) {
+  // register ladder: levels [0, i0) replaced by one 512-bit reciprocal on
+  // warp 0: Y_{i0} = floor(2^(n + lv[i0]) / D) within a unit (the ladder's
+  // own levels keep a few units; every later level tolerates < 16)
+  int i0 = 0;
+  if (P.recip_fast & 2)
+    while (i0 + 1 < nl && lv[i0 + 1] <= rf::kRegBits) ++i0;
+  if (i0 == 0 && threadIdx.x == 0) {
     // seed as recip_body: floor(2^126 / top64(D)) >> (62 - p0), via FP64
     const uint32_t hi = field32(Dg + dbase, nDs, (long long)n - 32 - 32LL * dbase);
     const uint32_t lo = field32(Dg + dbase, nDs, (long long)n - 64 - 32LL * dbase);
@@ -395,12 +401,6 @@ __device__ bool recip_fast_body(const DevPlan& P, IntBuf vint, long long prow,
   // before the first with nDt > 128 or nY > 128
   bool warp_class = true;
   const bool prof = (P.debug & 256) && p == 50 && threadIdx.x == 0;
-  // register ladder: levels [0, i0) replaced by one 512-bit reciprocal on
-  // thread 0: Y_{i0} = floor(2^(n + lv[i0]) / D) within a unit (the ladder's
-  // own levels keep a few units; every later level tolerates < 16)
-  int i0 = 0;
-  if (P.recip_fast & 2)
-    while (i0 + 1 < nl && lv[i0 + 1] <= rf::kRegBits) ++i0;
   if (i0 > 0) {
     const long long t_reg = prof ? clock64() : 0;
     const int pa = lv[i0];
