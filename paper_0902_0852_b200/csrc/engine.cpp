@@ -481,7 +481,12 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       CU(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
       CU(cudaStreamCreateWithPriority(&stream_panel_, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&stream_helper_, cudaStreamNonBlocking, hi));
-      CU(cudaStreamCreateWithPriority(&stream_far_, cudaStreamNonBlocking, hi));
+      // far rows one priority level below the chain and the near rows
+      // (HGPU_FAR_PRIO levels below): a freed SM slot goes to a near-row CTA first
+      int fo = 0;  // measured equal at 0, 1, 2 (profiles/r02/sweep_prio_r02.txt)
+      if (const char* e = std::getenv("HGPU_FAR_PRIO")) fo = std::max(0, std::atoi(e));
+      far_prio_ = std::min(lo, hi + fo);
+      CU(cudaStreamCreateWithPriority(&stream_far_, cudaStreamNonBlocking, far_prio_));
     }
   }
   {
@@ -531,7 +536,14 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       CU(cudaStreamCreateWithPriority(&stream_pre_, cudaStreamNonBlocking, hi));
       CU(cudaStreamCreateWithPriority(&stream_next_, cudaStreamNonBlocking, hi));
     }
+    // the near rows' early stages: beside the panel stream (with an SM split
+    // on the large group, where the panel's near rows run)
+    if (split_gb_)
+      stream_pre2_ = green_stream((CUgreenCtx)split_gb_, hi);
+    else
+      CU(cudaStreamCreateWithPriority(&stream_pre2_, cudaStreamNonBlocking, hi));
   }
+  if (const char* e = std::getenv("HGPU_PRE_NEAR")) pre_near_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -543,7 +555,7 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       if (split_gb_)
         far_streams_[l] = green_stream((CUgreenCtx)split_gb_, hi);
       else
-        CU(cudaStreamCreateWithPriority(&far_streams_[l], cudaStreamNonBlocking, hi));
+        CU(cudaStreamCreateWithPriority(&far_streams_[l], cudaStreamNonBlocking, far_prio_));
     }
     for (int l = 0; l < kMaxFarLanes; ++l)
       CU(cudaEventCreateWithFlags(&far_ev_[l], cudaEventDisableTiming));
@@ -574,6 +586,8 @@ Matrix::~Matrix() {
   for (cudaEvent_t e : net_ev_) cudaEventDestroy(e);
   if (stream_next_) cudaStreamDestroy(stream_next_);
   if (stream_pre_) cudaStreamDestroy(stream_pre_);
+  if (stream_pre2_) cudaStreamDestroy(stream_pre2_);
+  for (cudaEvent_t e : pre2_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
     if (h) cublasDestroy((cublasHandle_t)h);
@@ -1445,6 +1459,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pre_ev_.push_back(e);
   }
+  while ((int)pre2_ev_.size() < n) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pre2_ev_.push_back(e);
+  }
   {
     // bits bound of any diagonal Schur complement W_rr (PD: <= M_rr - x)
     int db = 0;
@@ -1527,6 +1546,9 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       // far rows' in-panel update in sub-panels of fsub stages (0: plain
       // left-looking); needs the far rows below the panel's columns
       const int fsub = (far_sub_ > 0 && near_end >= p1 && D.NW % 32 == 0) ? far_sub_ : 0;
+      // near rows' early stages on the pre stream (plain near path only)
+      const bool pre_near_on = pre_near_ && !nr && !(col_extract_ & 1) && fused_pivot_ &&
+                               recip_bound_;
       if (far) {
         CU(cudaEventRecord(sev_[4 * n + 1], sp));
         for (int l = 0; l < nlanes; ++l)
@@ -1669,8 +1691,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                                         rg_near ? vdig_ : nullptr, rg_kd_);
             });
           } else {
+            // stages [p0, p-2] arrived ahead of time on the pre stream (below,
+            // enqueued at stage p-2): only stage p-1 is left
+            int s0 = 0;
+            if (pre_near_on && s >= 2 && rb < rn) {
+              CU(cudaStreamWaitEvent(sp, pre2_ev_[p], 0));
+              s0 = s - 1;
+            }
             TL(3, p, sp, [&] {
-              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s,
+              return launch_update_col(D, W_, colbase_, vh + s0 * slot_stride,
+                                       rh + s0 * slot_stride, slot_stride, s - s0,
                                        p, rb, rn, err_, sp);
             });
             TL(4, p, sp, [&] {
@@ -1711,6 +1741,19 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             });
           }
           CU(cudaEventRecord(sev_[4 * p + 2], sp));
+          if (pre_near_on && p + 2 < p1 && p + 3 < rn) {
+            // column c = p + 2: every stage up to p is now complete for the
+            // near rows (R^_p from the division just enqueued, V^_p[c] from
+            // the extraction before it); it takes them on the pre stream
+            // while the panel stream works on column p + 1
+            const int c = p + 2;
+            CU(cudaStreamWaitEvent(stream_pre2_, sev_[4 * p + 2], 0));
+            TL(18, c, stream_pre2_, [&] {
+              return launch_update_col(D, W_, colbase_, vh, rh, slot_stride, s + 1, c, c + 1,
+                                       rn, err_, stream_pre2_);
+            });
+            CU(cudaEventRecord(pre2_ev_[c], stream_pre2_));
+          }
           if (far) {
             // far rows: column p receives stages [p0, p) (V^_s[p] of the
             // near rows, extract(near p-1) done; their own R^_s on the lane's

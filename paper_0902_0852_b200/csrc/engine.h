@@ -226,6 +226,7 @@ class Matrix {
   cudaStream_t stream_helper_ = nullptr; // pivot -> reciprocal chain
   cudaStream_t stream_far_ = nullptr;    // far rows of the panel (may lag)
   static constexpr int kMaxFarLanes = 4;
+  int far_prio_ = 0;  // stream priority of the far lanes (HGPU_FAR_PRIO levels below the chain)
   int far_lanes_ = 3;  // far-row streams (HGPU_FAR_LANES; 3: 255 ms, 2: 265 ms at config 3)
   cudaStream_t far_streams_[kMaxFarLanes] = {};  // [0] = stream_far_
   cudaEvent_t far_ev_[kMaxFarLanes] = {};
@@ -303,6 +304,12 @@ class Matrix {
   std::vector<cudaEvent_t> sn_ev_;
   cudaStream_t stream_pre_ = nullptr;
   std::vector<cudaEvent_t> pre_ev_;
+  // near rows' column update ahead of the panel stream (HGPU_PRE_NEAR): column
+  // c receives the panel's stages up to c-2 on its own stream as soon as the
+  // ratios of stage c-2 exist, so the panel stream applies only stage c-1
+  bool pre_near_ = false;  // bit-exact, measured equal (255.0 vs 254.7 ms): off
+  cudaStream_t stream_pre2_ = nullptr;
+  std::vector<cudaEvent_t> pre2_ev_;
   std::vector<cudaEvent_t> edf_ev_;
   int solve_xlimbs_ = 0;          // widest z / y entry of the solves so far
   long long factor_serial_ = 0;   // KEEP_L factorisations so far

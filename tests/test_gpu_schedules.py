@@ -42,6 +42,11 @@ VARIANTS = [
     {"HGPU_LOOKAHEAD": "0"},
     {"HGPU_LOOKAHEAD": "1", "HGPU_FAR_SUB": "4", "HGPU_FAR_LANES": "3"},
     {"HGPU_LOOKAHEAD": "1", "HGPU_NEAR": "64"},
+    {"HGPU_RECIP_FAST": "1"},
+    {"HGPU_PRE_NEAR": "1"},
+    {"HGPU_PRE_NEAR": "1", "HGPU_FAR_LANES": "2", "HGPU_GRID": "2", "HGPU_FAR_PRIO": "1"},
+    {"HGPU_PRE_NEAR": "1", "HGPU_NEAR": "100", "HGPU_EDF_RUN": "2"},
+    {"HGPU_EDF_RUN": "3", "HGPU_FAR_PRIO": "2"},
 ]
 
 
