@@ -544,6 +544,12 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       CU(cudaStreamCreateWithPriority(&stream_pre2_, cudaStreamNonBlocking, hi));
   }
   if (const char* e = std::getenv("HGPU_PRE_NEAR")) pre_near_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_LAG_FAR")) lag_far_ = std::atoi(e) != 0;
+  if (!split_gb_) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream_join_, cudaStreamNonBlocking, hi));
+  }
   if (const char* e = std::getenv("HGPU_PIVOT_SEGS")) pivot_segs_ = std::max(1, std::min(6, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_FAR_LANES"))
     far_lanes_ = std::max(1, std::min(kMaxFarLanes, std::atoi(e)));
@@ -587,6 +593,8 @@ Matrix::~Matrix() {
   if (stream_next_) cudaStreamDestroy(stream_next_);
   if (stream_pre_) cudaStreamDestroy(stream_pre_);
   if (stream_pre2_) cudaStreamDestroy(stream_pre2_);
+  if (stream_join_) cudaStreamDestroy(stream_join_);
+  for (cudaEvent_t e : lag_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : pre2_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
   for (void* h : blas_)
@@ -1354,9 +1362,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaEventRecord(b, s));
     tl_.push_back({kind, p, a, b});
   };
+  // rows: the whole lower part (r_lo < 0), rows below r_hi only (r_lo < 0,
+  // r_hi >= 0), or the rectangle [r_lo, r_hi) (r_lo >= c_end)
   auto timed_update = [&](int b, int nslots, int c_begin, int c_end,
-                          cudaStream_t us, int kind, int s0 = 0) {
+                          cudaStream_t us, int kind, int s0 = 0, int r_lo = -1,
+                          int r_hi = -1) {
     if (c_begin >= c_end || nslots <= 0) return;
+    if (r_lo >= 0 && r_lo >= r_hi) return;
     if (profile) {
       while (uev_.size() < uev_used + 2) {
         cudaEvent_t e;
@@ -1367,20 +1379,24 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     }
     const long long r0 = set_row0(b) + (long long)s0 * n;  // stage s0 of the panel
     const bool tc = update_tc_ && c_end - c_begin <= 32 && nslots <= 256 && D.NW % 4 == 0 &&
-                    D.L % 4 == 0;
+                    D.L % 4 == 0 && r_lo < 0 && r_hi < 0;
     TL(kind, b, us, [&] {
       if (tc)
         return launch_update_tc(D, W_, colbase_, vhat_ + r0 * NW, rhat_ + r0 * NW, slot_stride,
                                 nslots, c_begin, c_end, err_, us);
+      if (r_lo >= 0)
+        return launch_update_rect(D, W_, colbase_, vhat_ + r0 * NW, rhat_ + r0 * NW,
+                                  slot_stride, nslots, c_begin, c_end, r_lo, r_hi, err_, us);
       return launch_update(D, P.tile, W_, colbase_, vhat_ + r0 * NW,
                            rhat_ + r0 * NW, slot_stride, nslots, c_begin, c_end,
-                           err_, us);
+                           err_, us, r_hi);
     });
     if (profile) {
       CU(cudaEventRecord(uev_[uev_used + 1], us));
       uev_used += 2;
       double pairs = 0;
-      for (int c = c_begin; c < c_end; ++c) pairs += n - c;
+      const int rb_ = r_lo >= 0 ? r_lo : 0, re_ = r_hi >= 0 ? std::min(n, r_hi) : n;
+      for (int c = c_begin; c < c_end; ++c) pairs += std::max(0, re_ - std::max(c, rb_));
       res.update_products += pairs * nslots * (double)NW;
       ++res.update_launches;
     }
@@ -1459,6 +1475,11 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pre_ev_.push_back(e);
   }
+  while ((int)lag_ev_.size() < 2 * nblocks + 4) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    lag_ev_.push_back(e);
+  }
   while ((int)pre2_ev_.size() < n) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1481,9 +1502,15 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   CU(cudaEventRecord(next_ready[0], st));  // init done
   CU(cudaStreamWaitEvent(su1, next_ready[0], 0));
   CU(cudaStreamWaitEvent(su2, next_ready[0], 0));
+  // lagged far rows (see engine.h): single rank, EDF order, plain near path
+  const bool lag_ok = lag_far_ && edf && world_ == 1 && !group_ && !capture && !lookahead_ &&
+                      stream_join_ && near_rows_ >= kb && P.tile == 16 && D.NW % 32 == 0 &&
+                      !update_tc_;
+  bool prev_lag = false;  // panel b-1 left band b's far rows to lag_ev_[2b+1]
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
+    bool lag = false;       // this panel ends without its lanes >= 1
     const long long row0set = set_row0(b);
     // stages of this panel already applied to band b+1 (sub-panel lookahead)
     int la_done = 0;
@@ -1549,10 +1576,18 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       // near rows' early stages on the pre stream (plain near path only)
       const bool pre_near_on = pre_near_ && !nr && !(col_extract_ & 1) && fused_pivot_ &&
                                recip_bound_;
+      // rows of lane 0 when the other lanes lag: the next panel's near rows
+      const int mid = std::min(n, p1 + near_rows_);
+      lag = lag_ok && far && nlanes >= 2 && !div_global_ && !rg_far && p1 < n && near_end < mid;
       if (far) {
         CU(cudaEventRecord(sev_[4 * n + 1], sp));
-        for (int l = 0; l < nlanes; ++l)
+        for (int l = 0; l < nlanes; ++l) {
           CU(cudaStreamWaitEvent(far_streams_[l], sev_[4 * n + 1], 0));
+          // band b's far rows took panel b-1 after the chain moved on
+          if (prev_lag) CU(cudaStreamWaitEvent(far_streams_[l], lag_ev_[2 * b + 1], 0));
+        }
+      } else if (prev_lag) {
+        CU(cudaStreamWaitEvent(sp, lag_ev_[2 * b + 1], 0));
       }
       for (int p = p0; p < p1; ++p) {
         const int s = p - p0;
@@ -1762,8 +1797,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             // so that one lane's division overlaps another's extraction.
             for (int l = 0; l < nlanes; ++l) {
               cudaStream_t fs = far_streams_[l];
-              const int lo = near_end + (int)((long long)(n - near_end) * l / nlanes);
-              const int hi = near_end + (int)((long long)(n - near_end) * (l + 1) / nlanes);
+              int lo = near_end + (int)((long long)(n - near_end) * l / nlanes);
+              int hi = near_end + (int)((long long)(n - near_end) * (l + 1) / nlanes);
+              if (lag) {
+                // lane 0: [near_end, mid); lanes 1..: [mid, n) in equal parts
+                lo = l == 0 ? near_end : mid + (int)((long long)(n - mid) * (l - 1) / (nlanes - 1));
+                hi = l == 0 ? mid : mid + (int)((long long)(n - mid) * l / (nlanes - 1));
+              }
               if (lo >= hi) continue;
               if (p > p0) CU(cudaStreamWaitEvent(fs, sev_[4 * (p - 1)], 0));
               if (nr && p > p0) CU(cudaStreamWaitEvent(fs, sn_ev_[p - 1], 0));
@@ -1853,7 +1893,8 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
             if (far)
               for (int l = 0; l < nlanes; ++l) {
                 CU(cudaEventRecord(far_ev_[l], far_streams_[l]));
-                CU(cudaStreamWaitEvent(sp, far_ev_[l], 0));
+                // (lagging lanes join on the join stream after the panel)
+                if (!lag || l == 0) CU(cudaStreamWaitEvent(sp, far_ev_[l], 0));
               }
           }
         } else {
@@ -1922,8 +1963,18 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       }
     }
     if (world_ > 1 && owner != rank_) CU(cudaEventRecord(net_ev_[2 * b + 1], sp));
-    CU(cudaEventRecord(panel_done[b], sp));
-    if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, sp, src_r);
+    if (lag) {
+      // early: chain, near rows and lane 0; done: every lane (join stream)
+      CU(cudaEventRecord(lag_ev_[2 * b], sp));
+      CU(cudaStreamWaitEvent(stream_join_, lag_ev_[2 * b], 0));
+      for (int l = 1; l < kMaxFarLanes; ++l)
+        CU(cudaStreamWaitEvent(stream_join_, far_ev_[l], 0));
+      CU(cudaEventRecord(panel_done[b], stream_join_));
+      if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, stream_join_, src_r);
+    } else {
+      CU(cudaEventRecord(panel_done[b], sp));
+      if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, sp, src_r);
+    }
     if (capture) {
       const int nsr = std::min(ns, crow - 1 - p0);
       if (nsr > 0) {
@@ -1953,15 +2004,30 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     // ---- trailing update of panel b on the bulk stream: the next panel's
     // columns first (they gate panel b+1), then everything to their right,
     // which overlaps panel b+1's factorisation
-    CU(cudaStreamWaitEvent(su1, panel_done[b], 0));
+    if (!lag) CU(cudaStreamWaitEvent(su1, panel_done[b], 0));
     CU(cudaStreamWaitEvent(su2, panel_done[b], 0));
     if (edf) {
+      if (lag) {
+        // band b+1: the next panel's near rows now (they gate panel b+1), the
+        // rows below once the lagging lanes are done (they gate panel b+1's
+        // far lanes, lag_ev_[2(b+1)+1])
+        const int p2 = std::min(n, p1 + kb), mid = std::min(n, p1 + near_rows_);
+        const int nsl = std::min(kb, n - 1 - p0);
+        CU(cudaStreamWaitEvent(su1, lag_ev_[2 * b], 0));
+        if (band_ev[b + 1]) CU(cudaStreamWaitEvent(su1, band_ev[b + 1], 0));
+        timed_update(b, nsl, p1, p2, su1, 8, 0, -1, mid);
+        CU(cudaEventRecord(next_ready[b + 1], su1));
+        CU(cudaStreamWaitEvent(su1, panel_done[b], 0));
+        timed_update(b, nsl, p1, p2, su1, 8, 0, mid, n);
+        CU(cudaEventRecord(lag_ev_[2 * (b + 1) + 1], su1));
+      } else {
       if (p1 < n) {
         const int p2 = std::min(n, p1 + kb);
         if (band_ev[b + 1]) CU(cudaStreamWaitEvent(su1, band_ev[b + 1], 0));
         trailing(b, p1, p2, su1, 8, la_done);  // what the lookahead left
       }
       CU(cudaEventRecord(next_ready[b + 1], su1));
+      }
       edf_next[b] = b + 2;
       const int jmax = std::min(nblocks - 1, b + edf_h_ + 1);
       for (int j = b + 2; j <= jmax; ++j) edf_band(j, b);
@@ -1975,10 +2041,15 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       CU(cudaEventRecord(next_ready[b + 1], su1));
     }
     if (!edf) CU(cudaEventRecord(rest_done[b], su2));
+    prev_lag = lag;
   }
   // join the panel and update streams back into the bulk stream
   CU(cudaEventRecord(panel_done[nblocks], sp));
   CU(cudaStreamWaitEvent(st, panel_done[nblocks], 0));
+  if (stream_join_) {
+    CU(cudaEventRecord(lag_ev_[2 * nblocks + 2], stream_join_));
+    CU(cudaStreamWaitEvent(st, lag_ev_[2 * nblocks + 2], 0));
+  }
   CU(cudaEventRecord(trail_done[0], su1));
   CU(cudaStreamWaitEvent(st, trail_done[0], 0));
   CU(cudaEventRecord(trail_done[1], su2));

@@ -307,6 +307,13 @@ class Matrix {
   // near rows' column update ahead of the panel stream (HGPU_PRE_NEAR): column
   // c receives the panel's stages up to c-2 on its own stream as soon as the
   // ratios of stage c-2 exist, so the panel stream applies only stage c-1
+  // far rows beyond the next panel's near window lag the chain by up to one
+  // panel (HGPU_LAG_FAR): the panel ends when the chain, the near rows and
+  // lane 0 (the next panel's near rows) are done; band b+1 is updated for
+  // those rows at once and for the rest when the other lanes finish
+  bool lag_far_ = false;  // bit-exact; 254.0 ms with four lanes against 254.6: off
+  cudaStream_t stream_join_ = nullptr;
+  std::vector<cudaEvent_t> lag_ev_;  // [2b]: panel b early, [2b+1]: band b far rows updated
   bool pre_near_ = false;  // bit-exact, measured equal (255.0 vs 254.7 ms): off
   cudaStream_t stream_pre2_ = nullptr;
   std::vector<cudaEvent_t> pre2_ev_;

@@ -1543,18 +1543,22 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
                           int nslots, int c_begin, int c_end, const int* err,
-                          cudaStream_t st) {
+                          cudaStream_t st, int r_hi) {
   if (c_begin >= c_end || nslots <= 0) return cudaSuccess;
+  if (r_hi >= 0 && !(tile == 16 && P.NW % kUWords == 0)) return cudaErrorInvalidValue;
   if (tile == 16 && P.NW % kUWords == 0) {
+    const int rows_end = r_hi >= 0 ? min(r_hi, P.n) : P.n;
+    if (rows_end <= c_begin) return cudaSuccess;
     const int nct = (c_end - c_begin + kUT - 1) / kUT;
-    const int nrt = (P.n - c_begin + kUT - 1) / kUT;
+    const int nrt = (rows_end - c_begin + kUT - 1) / kUT;
     long long tiles = 0;
+    if (nrt < nct) return cudaErrorInvalidValue;  // (the kernel's tile walk)
     for (int ct = 0; ct < nct; ++ct) tiles += nrt - ct;
     dim3 grid((unsigned)tiles, P.NW / kUWords);
     ++g_launches;
     k_update_tiled<<<grid, 128, upd_smem(), st>>>(P, W, colbase, Vhat, Rhat,
                                          row_stride_slot, nslots, c_begin,
-                                         c_end, nct, nrt, err, c_begin, P.n, 0);
+                                         c_end, nct, nrt, err, c_begin, rows_end, 0);
     return cudaGetLastError();
   }
   if (tile == 16) tile = 8;

@@ -208,7 +208,7 @@ cudaError_t launch_update(const DevPlan& P, int tile, uint32_t* W,
                           const long long* colbase, const uint32_t* Vhat,
                           const uint32_t* Rhat, long long row_stride_slot,
                           int nslots, int c_begin, int c_end, const int* err,
-                          cudaStream_t st);
+                          cudaStream_t st, int r_hi = -1);  // rows below r_hi only (tiled kernel)
 // rectangle rows [r_lo, r_hi) x columns [c_begin, c_end), r_lo >= c_end
 cudaError_t launch_update_rect(const DevPlan& P, uint32_t* W,
                                const long long* colbase, const uint32_t* Vhat,
