@@ -214,7 +214,8 @@ hgpu_status hgpu_verify_eigenvalue_ex(hgpu_matrix* m, const char* x_decimal,
  * D1 -- and pinned against oracle/pyoracle.py:inverse_iteration_py).  Each
  * step solves (M - s I) y = u_k with the GPU L, D factors of M - s I
  * (HGPU_KEEP_L; forward and back triangular solves, exact with one
- * truncation per entry) and sets rho_k = s + (y.u_k)/(y.y).  Phase 1 keeps
+ * truncation per entry) and sets rho_k = s + (y.u_k)/(y.y); the iterate stays
+ * on the device (dot products and rescaling by rq_kernels.cu).  Phase 1 keeps
  * s = sigma until rho's relative change is < 2^-32, phase 2 refactors at
  * s = rho_k each step until it is < 2^-max(64, frac_bits/16), phase 3 keeps
  * those factors; stop when the change is below 2^-(frac_bits/2) or stalls.  u: n signed

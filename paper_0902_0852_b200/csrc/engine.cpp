@@ -1970,10 +1970,16 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       for (int l = 1; l < kMaxFarLanes; ++l)
         CU(cudaStreamWaitEvent(stream_join_, far_ev_[l], 0));
       CU(cudaEventRecord(panel_done[b], stream_join_));
-      if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, stream_join_, src_r);
     } else {
       CU(cudaEventRecord(panel_done[b], sp));
-      if (flags & HGPU_KEEP_L) keep_panel_L(p0, ns, src_row0, sp, src_r);
+    }
+    if (flags & HGPU_KEEP_L) {
+      // the panel's ratio columns into the packed L store: off the panel
+      // stream (2 ns copies per panel) when there is a join stream and the
+      // slot set is not reused before the end (every panel has its own)
+      cudaStream_t ks = (stream_join_ && nsets > nblocks && !group_) ? stream_join_ : sp;
+      if ((ks != sp) != lag) CU(cudaStreamWaitEvent(ks, panel_done[b], 0));
+      keep_panel_L(p0, ns, src_row0, ks, src_r);
     }
     if (capture) {
       const int nsr = std::min(ns, crow - 1 - p0);
