@@ -545,6 +545,13 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   }
   if (const char* e = std::getenv("HGPU_PRE_NEAR")) pre_near_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_LAG_FAR")) lag_far_ = std::atoi(e) != 0;
+  if (const char* e = std::getenv("HGPU_PRE_LHAT")) pre_lhat_ = std::atoi(e) != 0;
+  if (!split_gb_) {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CU(cudaStreamCreateWithPriority(&stream_lhat_, cudaStreamNonBlocking, lo));
+    CU(cudaEventCreateWithFlags(&lhat_ev_, cudaEventDisableTiming));
+  }
   if (!split_gb_) {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -594,6 +601,8 @@ Matrix::~Matrix() {
   if (stream_pre_) cudaStreamDestroy(stream_pre_);
   if (stream_pre2_) cudaStreamDestroy(stream_pre2_);
   if (stream_join_) cudaStreamDestroy(stream_join_);
+  if (stream_lhat_) cudaStreamDestroy(stream_lhat_);
+  if (lhat_ev_) cudaEventDestroy(lhat_ev_);
   for (cudaEvent_t e : lag_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : pre2_ev_) cudaEventDestroy(e);
   for (cudaEvent_t e : tl_pool_) cudaEventDestroy(e);
@@ -644,6 +653,9 @@ void Matrix::release() {
     }
   }
   start_resident_ = have_y_ = false;
+  dfree(lhat_err_);
+  lhat_err_ = nullptr;
+  lhat_pre_for_ = -1;
   for (void* p : {(void*)rq_prod_, (void*)rq_out_, (void*)rq_scr_, (void*)rq_colsum_,
                   (void*)rq_sign_})
     dfree(p);
@@ -1507,6 +1519,19 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                       stream_join_ && near_rows_ >= kb && P.tile == 16 && D.NW % 32 == 0 &&
                       !update_tc_;
   bool prev_lag = false;  // panel b-1 left band b's far rows to lag_ev_[2b+1]
+  // L-entry transforms during the factorisation: a solve plan with its own
+  // chunk store exists (not borrowing the workspace), single rank
+  const bool pre_lhat_on = pre_lhat_ && (flags & HGPU_KEEP_L) && solve_ntt_ && sdp_bits_ > 0 &&
+                           !lhat_chunks_.empty() && lhat_tab_ && stream_lhat_ && world_ == 1 &&
+                           !group_ && !interval_;
+  if (pre_lhat_on) {
+    if (!lhat_err_) lhat_err_ = dalloc<int>(kErrWords);
+    const int z[kErrWords] = {INT_MAX, 0, 0, 0};
+    CU(cudaMemcpyAsync(lhat_err_, z, sizeof(z), cudaMemcpyHostToDevice, st));
+    CU(cudaEventRecord(lhat_ev_, st));
+    CU(cudaStreamWaitEvent(stream_lhat_, lhat_ev_, 0));
+  }
+  lhat_pre_for_ = -1;
   for (int b = 0; b < nblocks; ++b) {
     const int p0 = b * kb, p1 = std::min(n, p0 + kb), ns = p1 - p0;
     const int owner = block_owner(b, world_);
@@ -1980,6 +2005,19 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       cudaStream_t ks = (stream_join_ && nsets > nblocks && !group_) ? stream_join_ : sp;
       if ((ks != sp) != lag) CU(cudaStreamWaitEvent(ks, panel_done[b], 0));
       keep_panel_L(p0, ns, src_row0, ks, src_r);
+      if (pre_lhat_on) {
+        // this panel's entries of the packed L store (contiguous: stages
+        // p0 .. p1-1), transformed in the solve plan while the factorisation
+        // goes on
+        const long long e0 = (long long)p0 * (n - 1) - (long long)p0 * (p0 - 1) / 2;
+        const int pe = std::min(p1, n - 1);
+        const long long e1 = (long long)pe * (n - 1) - (long long)pe * (pe - 1) / 2;
+        CU(cudaEventRecord(lhat_ev_, ks));
+        CU(cudaStreamWaitEvent(stream_lhat_, lhat_ev_, 0));
+        CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, e1 - e0, lhat_store(),
+                             dp_.grid_cap, lhat_err_, stream_lhat_, e0));
+        kernel_launch_count_add(1);
+      }
     }
     if (capture) {
       const int nsr = std::min(ns, crow - 1 - p0);
@@ -2075,8 +2113,17 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   }
   int herr[kErrWords];
   CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  int lherr[kErrWords] = {INT_MAX, 0, 0, 0};
+  if (pre_lhat_on) {
+    // (after ev1_: the tail of the L-entry transforms is not factorisation time)
+    CU(cudaEventRecord(lhat_ev_, stream_lhat_));
+    CU(cudaStreamWaitEvent(st, lhat_ev_, 0));
+    CU(cudaMemcpyAsync(lherr, lhat_err_, sizeof(lherr), cudaMemcpyDeviceToHost, st));
+  }
   const auto t_enq = std::chrono::steady_clock::now();
   CU(cudaStreamSynchronize(st));
+  if (pre_lhat_on && have_L_ && !lherr[kErrCapacity] && !lherr[kErrInternal])
+    lhat_pre_for_ = factor_serial_;
   if (group_) group_merge_err(herr);
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, ev0_, ev1_));
@@ -2445,7 +2492,15 @@ std::vector<HostInt> Matrix::solve_impl(long long* launches, int mode, bool down
       int mb = 1;
       for (long long i = 0; i < ne; ++i) mb = std::max(mb, bits[i]);
       const int xb = 32 * std::max(P.cap, solve_xlimbs_ + 16);
-      if (mb + xb != sdp_bits_) {
+      // a plan made for wider operands stays exact; re-plan when the operands
+      // outgrow it (or shrink by enough to matter)
+      const bool fits = sdp_bits_ > 0 && xb <= sdp_xbits_ && mb + sdp_xbits_ <= sdp_bits_ &&
+                        mb + sdp_xbits_ + 4096 > sdp_bits_;
+      if (fits && lhat_pre_for_ == factor_serial_) {
+        // transformed during the factorisation in this very plan
+        lhat_for_ = factor_serial_;
+      } else {
+      if (!fits) {
         // bits of one product; choose_plan adds the column count n to the
         // coefficient bound and keeps two spare digits
         const Plan SP = solve_plan(n, K_, mb + xb);
@@ -2528,6 +2583,7 @@ std::vector<HostInt> Matrix::solve_impl(long long* launches, int mode, bool down
       CU(launch_solve_rhat(sdp_, P.cap, IntBuf{lhdr_, llimbs_}, ne, lhat_store(), dp_.grid_cap, err_,
                            st));
       lhat_for_ = factor_serial_;
+      }
     }
     xbmax = sdp_xbits_;
   }

@@ -280,6 +280,15 @@ class Matrix {
   int lhat_shift_ = 0;
   EntryStore lhat_store() const { return EntryStore{lhat_tab_, lhat_shift_, (long long)sdp_.NW}; }
   long long lhat_for_ = -1;
+  // L-entry transforms during the factorisation (HGPU_PRE_LHAT): once a solve
+  // plan exists, every panel's ratio columns are transformed right after they
+  // are copied to the L store, on a lowest-priority stream; the next solve
+  // keeps them if the plan still fits and no entry was flagged
+  bool pre_lhat_ = true;
+  cudaStream_t stream_lhat_ = nullptr;
+  cudaEvent_t lhat_ev_ = nullptr;
+  int* lhat_err_ = nullptr;
+  long long lhat_pre_for_ = -1;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
   int edf_run_ = 8;  // panels accumulated by one EDF update launch (HGPU_EDF_RUN, 1-8)

@@ -292,7 +292,8 @@ cudaError_t launch_solve_acc_tc(int n, int Wv, int Wa, int k2, IntBuf L, IntBuf 
 size_t solve_ntt_smem_words(const DevPlan& S, int Wv, int Wa);
 cudaError_t configure_solve_ntt(DevPlan& S, int cap, int Wv, int Wa, int* ok);
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
-                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st);
+                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st,
+                              long long e_begin = 0);  // entries [e_begin, e_begin + count)
 cudaError_t launch_solve_xhat(const DevPlan& S, IntBuf xv, int xi, int Wv, uint32_t* xhat,
                               int xbmax, int* err, cudaStream_t st);
 cudaError_t launch_solve_ntt(const DevPlan& S, int n, int Wv, int Wa, int k2,

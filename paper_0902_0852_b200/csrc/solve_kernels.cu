@@ -243,12 +243,12 @@ constexpr int kSolveNttThreads = 1024;
 
 // every L entry (packed like L) -> its transform in Montgomery form
 __global__ void __launch_bounds__(256) k_solve_rhat(const __grid_constant__ DevPlan S, int cap, IntBuf L,
-                                                    long long count, EntryStore rhat,
-                                                    int* err) {
+                                                    long long e_begin, long long count,
+                                                    EntryStore rhat, int* err) {
   extern __shared__ uint32_t sm[];
   uint32_t* buf = sm;           // NW
   uint32_t* mag = buf + S.NW;   // cap
-  for (long long e = blockIdx.x; e < count; e += gridDim.x) {
+  for (long long e = e_begin + blockIdx.x; e < e_begin + count; e += gridDim.x) {
     int len;
     const int sign = load_int(L, e, cap, mag, &len);
     transform_int(S, mag, len, 0, sign, buf, rhat.at(e), true, S.twm, err);
@@ -768,7 +768,8 @@ cudaError_t configure_solve_ntt(DevPlan& S, int cap, int Wv, int Wa, int* ok) {
 }
 
 cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long count,
-                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st) {
+                              EntryStore rhat, int grid_cap, int* err, cudaStream_t st,
+                              long long e_begin) {
   if (count <= 0) return cudaSuccess;
   // every resident CTA slot (each transform is a latency-bound chain)
   const size_t smem = ((size_t)S.NW + cap) * 4;
@@ -777,8 +778,8 @@ cudaError_t launch_solve_rhat(const DevPlan& S, int cap, IntBuf L, long long cou
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_rhat, 256, smem);
   const long long grid = std::max<long long>(grid_cap, (long long)nsm * std::max(1, per_sm));
-  k_solve_rhat<<<(int)std::min<long long>(count, grid), 256, smem, st>>>(S, cap, L, count,
-                                                                        rhat, err);
+  k_solve_rhat<<<(int)std::min<long long>(count, grid), 256, smem, st>>>(S, cap, L, e_begin,
+                                                                        count, rhat, err);
   return cudaGetLastError();
 }
 

@@ -153,6 +153,22 @@ def test_transform_domain_solve_bit_exact(hg, seed, n, k, monkeypatch):
     assert got["iterations"] == len(want)
 
 
+@pytest.mark.parametrize("pre", ["0", "1"])
+def test_l_entry_transforms_during_or_after_the_factorisation(hg, pre, monkeypatch):
+    """HGPU_PRE_LHAT: from the second factorisation of a run on, the L-entry
+    transforms are formed panel by panel during the factorisation (1) or all
+    at once by the first solve after it (0): the same Rayleigh quotients."""
+    monkeypatch.setenv("HGPU_SOLVE_NTT", "2")
+    monkeypatch.setenv("HGPU_PRE_LHAT", pre)
+    seed, n, k = 121, 90, 1536
+    strip = random_pd_hankel(seed, n, k)
+    u = hg.seeded_start_vector(n, k)
+    want = po.inverse_iteration_py(strip, k, u, 0, 40)
+    got = hg.inverse_iteration(hg.HankelMatrixGPU(strip, k), u, 0, 40)
+    assert got["rho"] == want
+    assert got["iterations"] == len(want)
+
+
 def test_transform_domain_solve_config2(hg, monkeypatch):
     """Config 2 at full size through the transform-domain solve: the final
     Rayleigh quotient and the certified 40 digits of the golden fixture."""
