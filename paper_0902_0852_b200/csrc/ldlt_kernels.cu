@@ -1117,7 +1117,10 @@ k_update(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbas
 // from L2 feeds 16 products (0.5 B/product).
 namespace {
 constexpr int kUT = 16;        // CTA tile edge
-constexpr int kUStages = 4;    // cp.async pipeline depth
+#ifndef HGPU_USTAGES
+#define HGPU_USTAGES 4
+#endif
+constexpr int kUStages = HGPU_USTAGES;    // cp.async pipeline depth
 constexpr int kUWords = 32;    // words per CTA
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -1184,6 +1187,7 @@ k_update_tiled(const __grid_constant__ DevPlan P, uint32_t* W, const long long* 
   };
   // W tile prefetch: 256 pairs x 8 chunks of 16 B, 16 per thread, committed
   // with the first operand stage
+#ifndef HGPU_UPD_NOPREFETCH
 #pragma unroll 4
   for (int h = 0; h < (kUT * kUT * 8) / 128; ++h) {
     const int chunk = tid + 128 * h;
@@ -1193,6 +1197,7 @@ k_update_tiled(const __grid_constant__ DevPlan P, uint32_t* W, const long long* 
       cp_async16(&sW[pair * kUWords + part * 4],
                  W + (colbase[c] + (r - c)) * NW + w0 + part * 4);
   }
+#endif
 #pragma unroll
   for (int s = 0; s < kUStages - 1; ++s) {
     if (s < nslots) issue(s);
@@ -1239,7 +1244,11 @@ k_update_tiled(const __grid_constant__ DevPlan P, uint32_t* W, const long long* 
       const int r = r0 + rm + i;
       if (r < c || r >= r_hi) continue;
       const uint32_t t32 = reduce_sum64(acc[i][j], pc);
+#ifndef HGPU_UPD_NOPREFETCH
       const uint32_t old = sW[((rm + i) * kUT + cm + j) * kUWords + lane];
+#else
+      const uint32_t old = W[(base + (r - c)) * NW + wd];
+#endif
       W[(base + (r - c)) * NW + wd] = old >= t32 ? old - t32 : old + pc.q - t32;
     }
   }
@@ -1565,7 +1574,11 @@ cudaError_t launch_ratio_finish(const DevPlan& P, IntBuf vint, long long vrow0,
 static size_t upd_smem() {
   static const size_t v = [] {
     const char* e = getenv("HGPU_UPD_PAD");
+#ifndef HGPU_UPD_NOPREFETCH
     const size_t base = (size_t)kUT * kUT * kUWords * 4;
+#else
+    const size_t base = 0;
+#endif
     return e ? std::max(base, (size_t)atol(e)) : base;
   }();
   return v;
