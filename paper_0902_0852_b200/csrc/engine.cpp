@@ -2112,6 +2112,9 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     NC(ncclGroupEnd());
   }
   int herr[kErrWords];
+  // (the copy into pageable memory below returns when it is done, i.e. at
+  // the end of the device work: the enqueue time is taken before it)
+  const auto t_enq = std::chrono::steady_clock::now();
   CU(cudaMemcpyAsync(herr, err_, sizeof(herr), cudaMemcpyDeviceToHost, st));
   int lherr[kErrWords] = {INT_MAX, 0, 0, 0};
   if (pre_lhat_on) {
@@ -2120,7 +2123,6 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     CU(cudaStreamWaitEvent(st, lhat_ev_, 0));
     CU(cudaMemcpyAsync(lherr, lhat_err_, sizeof(lherr), cudaMemcpyDeviceToHost, st));
   }
-  const auto t_enq = std::chrono::steady_clock::now();
   CU(cudaStreamSynchronize(st));
   if (pre_lhat_on && have_L_ && !lherr[kErrCapacity] && !lherr[kErrInternal])
     lhat_pre_for_ = factor_serial_;
