@@ -996,6 +996,11 @@ void Matrix::build(int min_logL) {
   // bounded by the largest diagonal moment (plus the shift); 64 bits margin.
   plan_ = choose_plan(n_, K_, strip_bits_ + 64, min_logL);
   Plan& P = plan_;
+  // panel width (experiment knob: 16, 32 or 64 columns; 32 measured best)
+  if (const char* e = std::getenv("HGPU_KB")) {
+    const int v = std::atoi(e);
+    if (v == 16 || v == 32 || v == 64) P.kb = v;
+  }
   // ownership: column blocks of kb columns, reflected round-robin
   const int nblocks = (n_ + P.kb - 1) / P.kb;
   owned_blocks_.clear();
@@ -1463,7 +1468,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
         continue;
       }
       int m = 1;
-      while (m < edf_run_ && bp + m <= bmax && edf_next[bp + m] == j &&
+      while (m < std::min(edf_run_, 256 / kb) && bp + m <= bmax && edf_next[bp + m] == j &&
              (bp % nsets) + m < nsets)
         ++m;
       edf_enqueue(bp, m, j);
@@ -1580,7 +1585,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
       // trailing update of the panel.  near_end = p0 + near_rows_.
       // Events (per stage): sev_[4p] extract(near p) done, sev_[4p+1]
       // recip(p) done, sev_[4p+2] near divide(p) done, sev_[4p+3] chain done.
-      const int near_end = std::min(n, p0 + near_rows_);
+      const int near_end = std::min(n, p0 + std::max(near_rows_, kb + 2));
       const bool far = near_end < n && recip_bound_;
       // ratio GEMM for this run's operand bounds (else k_divide)
       const bool rg_ok = ratio_gemm_ && rg_kd_ > 0 &&

@@ -201,7 +201,7 @@ class Matrix {
   uint32_t* plimbs_ = nullptr;
   uint32_t *ybuf_ = nullptr, *rscratch_ = nullptr, *dscratch_ = nullptr,
            *dscratch2_ = nullptr, *dscratch3_ = nullptr;
-  static constexpr int kYRing = 64;
+  static constexpr int kYRing = 128;
   // rows [p0, p0 + near_rows_) of a panel run in step with the pivot chain,
   // the rest on the far stream (HGPU_NEAR, default two panels)
   int near_rows_ = 34;

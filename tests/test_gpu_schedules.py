@@ -47,6 +47,8 @@ VARIANTS = [
     {"HGPU_PRE_NEAR": "1", "HGPU_FAR_LANES": "2", "HGPU_GRID": "2", "HGPU_FAR_PRIO": "1"},
     {"HGPU_PRE_NEAR": "1", "HGPU_NEAR": "100", "HGPU_EDF_RUN": "2"},
     {"HGPU_EDF_RUN": "3", "HGPU_FAR_PRIO": "2"},
+    {"HGPU_KB": "16"},
+    {"HGPU_KB": "64", "HGPU_FAR_SUB": "16"},
     {"HGPU_LAG_FAR": "1"},
     {"HGPU_LAG_FAR": "1", "HGPU_FAR_LANES": "4", "HGPU_PRE_NEAR": "1"},
     {"HGPU_LAG_FAR": "1", "HGPU_FAR_LANES": "2", "HGPU_NEAR": "40", "HGPU_FAR_SUB": "0"},
