@@ -337,8 +337,17 @@ def _run_gpu_body(args, hgpu_devices, nccl, rank, local) -> None:
     if traffic:
         out["roofline"]["traffic"] = traffic["dram_bytes_per_launch"]
         out["roofline"]["traffic_source"] = traffic["source"]
-        # the same kernel profiled alone: IMAD.WIDE (FMA-heavy) pipe busy %
-        out["roofline"]["ncu_imad_pipe_frac_alone"] = (traffic["pipe_pct"] or 0) / 100 or None
+        # the same kernel profiled alone: IMAD.WIDE (FMA-heavy) pipe busy %,
+        # time-weighted over every launch of a factorisation, and on a full
+        # band run; its HBM rate alone (GB/s)
+        out["roofline"]["ncu_imad_pipe_frac_alone"] = (traffic.get("pipe_pct") or 0) / 100 or None
+        if traffic.get("pipe_pct_full_band_run"):
+            out["roofline"]["ncu_imad_pipe_frac_full_band_run"] = traffic["pipe_pct_full_band_run"] / 100
+        if traffic.get("hbm_gbs_alone"):
+            out["roofline"]["ncu_hbm_gbs_alone"] = traffic["hbm_gbs_alone"]
+        if upd_n and traffic.get("dram_bytes_per_launch"):
+            # profiled bytes per launch over the launch's time in the step
+            out["roofline"]["hbm_gbs_in_step"] = traffic["dram_bytes_per_launch"] / (upd_avg_ms * 1e-3) / 1e9
     if rank == 0 and ndev == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
     if rank == 0:
@@ -411,17 +420,30 @@ def leading_block_parity(m, x, hgpu) -> dict:
 
 
 def _profiled_traffic():
-    """dram bytes per k_update_tiled launch from the committed ncu --set full
-    summary (profiles/*/k_update_full.json), if present."""
+    """DRAM bytes per k_update_tiled launch (average over every launch of one
+    factorisation) and the kernel's IMAD.WIDE pipe utilisation alone, from the
+    committed ncu summaries (profiles/*/k_update_all_launches.json, and the
+    full band run of k_update_full.json), if present."""
     import glob
+    out = {}
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "k_update_all_launches.json")))
+    if files:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        out = {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"),
+               "pipe_pct": d.get("sm_pipe_fmaheavy_pct_time_weighted"),
+               "hbm_gbs_alone": d.get("hbm_gbs_alone"),
+               "source": os.path.relpath(files[-1], ROOT)}
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "k_update_full.json")))
-    if not files:
-        return None
-    with open(files[-1]) as f:
-        d = json.load(f)
-    return {"dram_bytes_per_launch": d.get("dram_bytes_per_launch"),
-            "pipe_pct": d.get("sm_pipe_fmaheavy_pct_of_peak_elapsed"),
-            "source": os.path.relpath(files[-1], ROOT)}
+    if files:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        out["pipe_pct_full_band_run"] = d.get("sm_pipe_fmaheavy_pct_of_peak_elapsed")
+        if "dram_bytes_per_launch" not in out:
+            out.update(dram_bytes_per_launch=d.get("dram_bytes_per_launch"),
+                       pipe_pct=d.get("sm_pipe_fmaheavy_pct_of_peak_elapsed"),
+                       source=os.path.relpath(files[-1], ROOT))
+    return out or None
 
 
 def probe_imad() -> dict:
