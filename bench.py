@@ -346,7 +346,8 @@ def _run_gpu_body(args, hgpu_devices, nccl, rank, local) -> None:
         if traffic.get("hbm_gbs_alone"):
             out["roofline"]["ncu_hbm_gbs_alone"] = traffic["hbm_gbs_alone"]
         if upd_n and traffic.get("dram_bytes_per_launch"):
-            # profiled bytes per launch over the launch's time in the step
+            # profiled bytes per launch (the same su1 + su2 launches the engine
+            # times) over the launch's average time in the step
             out["roofline"]["hbm_gbs_in_step"] = traffic["dram_bytes_per_launch"] / (upd_avg_ms * 1e-3) / 1e9
     if rank == 0 and ndev == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args)
