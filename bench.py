@@ -261,6 +261,16 @@ def _run_gpu_body(args, hgpu_devices, nccl, rank, local) -> None:
                "method": "shifted inverse iteration + RQI on the GPU LDL^T (hgpu_inverse_iteration)",
                "includes": "strip upload, every factorisation and triangular solve",
                "pool": "warm (the engine's device memory pool kept from the timed steps)"}
+        # the same again on the same handle: solve buffers, the solve plan and
+        # the L store are in place (the steady state of a sweep over matrices
+        # of one shape); the strip is handed over again
+        barrier()
+        t0 = time.perf_counter()
+        mm.set_strip((sizes, limbs))
+        r2 = hgpu.inverse_iteration(mm, hgpu.seeded_start_vector(n, k), 0, 40, digits=40)
+        barrier()
+        lam["seconds_steady_state"] = time.perf_counter() - t0
+        lam["steady_state_same_digits"] = r2["eigenvalue"] == rq["eigenvalue"]
         del mm
         # the same with the pool handed back to the driver first: the cold
         # start a fresh process pays (workspace and slot-set allocations)
