@@ -1279,8 +1279,13 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
   have_L_ = false;
   if ((flags & HGPU_KEEP_L) && !lhdr_) {
     const size_t nl = (size_t)n * (n - 1) / 2;
+    const auto ta = std::chrono::steady_clock::now();
     lhdr_ = dalloc<int>(std::max<size_t>(nl, 1));
     llimbs_ = dalloc<uint32_t>(std::max<size_t>(nl, 1) * P.cap);
+    if (std::getenv("HGPU_HOST_TRACE"))
+      std::fprintf(stderr, "L store: %.1f MB allocated in %.3f ms\n", nl * (double)P.cap * 4 / 1e6,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta)
+                       .count());
   }
   const bool profile = flags & HGPU_PROFILE;
   // capture limit (hgpu_matrix_set_capture_rows): stages and rows < crow
