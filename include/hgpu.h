@@ -64,6 +64,19 @@ hgpu_status hgpu_matrix_new(long n, long frac_bits, const int32_t* strip_sizes,
                             hgpu_matrix** out);
 void hgpu_matrix_free(hgpu_matrix* m);
 
+/* The reference's on-disk interchange of a matrix (hankel_matrix.cpp:52-87):
+ * one line per anti-diagonal, "s=<index> hex=<mantissa, base 16> fracbits=<K>".
+ * hgpu_matrix_new_from_dump reads such a file the way load_matrix_dump does
+ * (lines in order of s, empty lines skipped, 2n-1 anti-diagonals; anything
+ * else is the reference's MalformedInput -> HGPU_ERR_INVALID_ARGUMENT with
+ * its message) and uploads the strip; n and frac_bits (the last line's, as in
+ * the reference) are reported.  hgpu_matrix_dump writes the matrix's strip in
+ * the same format (dump_matrix, :52-57), so a strip can go from either side
+ * to the other unchanged. */
+hgpu_status hgpu_matrix_new_from_dump(const char* path, int device, hgpu_matrix** out,
+                                      long* n, long* frac_bits);
+hgpu_status hgpu_matrix_dump(const hgpu_matrix* m, const char* path);
+
 /* Multi-GPU: join a column-block-cyclic factorisation as `rank` of `world`
  * (one process per GPU).  `nccl_id` is the 128-byte ncclUniqueId produced by
  * hgpu_nccl_unique_id on rank 0 and shared by the caller.  Must be called

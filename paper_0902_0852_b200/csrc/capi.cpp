@@ -6,13 +6,16 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <new>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "../../include/hgpu.h"
 #include "engine.h"
+#include "host/bigz.h"
 
 struct hgpu_matrix {
   std::unique_ptr<hgpu::Matrix> impl;
@@ -112,6 +115,72 @@ hgpu_status hgpu_matrix_new_group(long n, long frac_bits,
                                              strip_limbs, devices[0]);
     m->impl->make_group(std::vector<int>(devices, devices + world));
     *out = m.release();
+  });
+}
+
+hgpu_status hgpu_matrix_new_from_dump(const char* path, int device, hgpu_matrix** out,
+                                      long* n_out, long* frac_bits_out) {
+  return guarded([&] {
+    if (!path || !out) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    std::ifstream is(path);
+    if (!is) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, std::string("cannot open dump file: ") + path);
+    // load_matrix_dump (hankel_matrix.cpp:65-87)
+    std::vector<int32_t> sizes;
+    std::vector<uint32_t> limbs, one;
+    long frac_bits = 0;
+    std::string line;
+    while (std::getline(is, line)) {
+      if (line.empty()) continue;
+      std::istringstream ls(line);
+      std::string s_tok, hex_tok, fb_tok;
+      ls >> s_tok >> hex_tok >> fb_tok;
+      if (s_tok.rfind("s=", 0) != 0 || hex_tok.rfind("hex=", 0) != 0 ||
+          fb_tok.rfind("fracbits=", 0) != 0)
+        throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "matrix dump line: " + line);
+      long s = 0;
+      try {
+        s = std::stol(s_tok.substr(2));
+        frac_bits = std::stol(fb_tok.substr(9));
+      } catch (const std::exception&) {
+        throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "matrix dump line: " + line);
+      }
+      if (s != (long)sizes.size())
+        throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT,
+                          "matrix dump out of order at s=" + std::to_string(s));
+      hgpu::Z z;
+      if (__gmpz_set_str(z.p(), hex_tok.c_str() + 4, 16) != 0)
+        throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "matrix dump line: " + line);
+      sizes.push_back(z.to_limbs(one));
+      limbs.insert(limbs.end(), one.begin(), one.end());
+    }
+    if (sizes.empty() || sizes.size() % 2 == 0)
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "matrix dump must hold 2n-1 anti-diagonals");
+    const long n = (long)(sizes.size() + 1) / 2;
+    if (n > 100000 || frac_bits < 2 || frac_bits > (1L << 24))
+      throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "matrix dump: order or fracbits out of range");
+    if (n_out) *n_out = n;
+    if (frac_bits_out) *frac_bits_out = frac_bits;
+    if (limbs.empty()) limbs.push_back(0u);
+    auto m = std::make_unique<hgpu_matrix>();
+    m->impl = std::make_unique<hgpu::Matrix>((int)n, (int)frac_bits, sizes.data(), limbs.data(),
+                                             device);
+    *out = m.release();
+  });
+}
+
+hgpu_status hgpu_matrix_dump(const hgpu_matrix* m, const char* path) {
+  return guarded([&] {
+    if (!m || !path) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, "null argument");
+    std::ofstream os(path);
+    if (!os) throw hgpu::Error(HGPU_ERR_INVALID_ARGUMENT, std::string("cannot open dump file: ") + path);
+    // dump_matrix (hankel_matrix.cpp:52-57)
+    const int n = m->impl->order();
+    for (int s = 0; s < 2 * n - 1; ++s) {
+      const hgpu::HostInt& h = m->impl->strip_entry(s);
+      os << "s=" << s << " hex=" << hgpu::Z::from_limbs(h.size, h.limbs.data()).hex()
+         << " fracbits=" << m->impl->frac_bits() << "\n";
+    }
+    if (!os) throw hgpu::Error(HGPU_ERR_INTERNAL, std::string("write failed: ") + path);
   });
 }
 

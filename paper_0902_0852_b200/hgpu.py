@@ -49,6 +49,7 @@ EXPORTS = (
     "hgpu_build_moments", "hgpu_buffer_free", "hgpu_matrix_set_capture_rows",
     "hgpu_matrix_new_group", "hgpu_matrix_world", "hgpu_verify_eigenvalue_ex",
     "hgpu_factor_net_ms", "hgpu_trim_pool", "hgpu_matrix_set_strip",
+    "hgpu_matrix_new_from_dump", "hgpu_matrix_dump",
 )
 
 
@@ -94,6 +95,9 @@ def load() -> ctypes.CDLL:
     lib.hgpu_matrix_free.argtypes = [vp]
     lib.hgpu_matrix_new_group.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int32), u32p,
                                           ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(vp)]
+    lib.hgpu_matrix_new_from_dump.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(vp),
+                                              ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long)]
+    lib.hgpu_matrix_dump.argtypes = [vp, ctypes.c_char_p]
     lib.hgpu_matrix_world.argtypes = [vp]
     lib.hgpu_matrix_world.restype = ctypes.c_int
     lib.hgpu_nccl_unique_id.argtypes = [ctypes.c_char_p]
@@ -265,6 +269,24 @@ class HankelMatrixGPU:
                                        _u32p(limbs), devices[0] if devices else device,
                                        ctypes.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_dump(cls, path: str, device: int = 0) -> "HankelMatrixGPU":
+        """load_matrix_dump (hankel_matrix.cpp:65-87): the reference's
+        "s=.. hex=.. fracbits=.." file straight onto the device."""
+        lib = load()
+        h = ctypes.c_void_p()
+        n, k = ctypes.c_long(), ctypes.c_long()
+        _check(lib.hgpu_matrix_new_from_dump(os.fsencode(path), device, ctypes.byref(h),
+                                             ctypes.byref(n), ctypes.byref(k)))
+        self = cls.__new__(cls)
+        self.n, self.frac_bits, self._h = int(n.value), int(k.value), h
+        return self
+
+    def dump(self, path: str) -> None:
+        """dump_matrix (hankel_matrix.cpp:52-57): the strip in the reference's
+        interchange format."""
+        _check(load().hgpu_matrix_dump(self._h, os.fsencode(path)))
 
     def set_strip(self, strip) -> None:
         """New moments of the same order and precision for the next ldlt()

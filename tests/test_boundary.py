@@ -53,17 +53,13 @@ def test_block_owner_is_reference_assignment():
 def test_version_and_errors_without_device():
     lib = hgpu.load()
     assert b"sm_100a" in lib.hgpu_version()
+    # no CPU fallback: without a device, creating a matrix fails loudly
     try:
-        import torch
-        has_gpu = torch.cuda.is_available()
-    except Exception:
-        has_gpu = False
-    if has_gpu:
-        pytest.skip("a GPU is present")
-    # no CPU fallback: creating a device matrix fails loudly
-    with pytest.raises(hgpu.HgpuError) as e:
         hgpu.HankelMatrixGPU([1 << 32], 32)
-    assert e.value.status == 4
+    except hgpu.HgpuError as e:
+        assert e.status == 4  # HGPU_ERR_CUDA
+    else:
+        pytest.skip("a GPU is present")
 
 
 def test_int_limb_roundtrip():
@@ -71,3 +67,30 @@ def test_int_limb_roundtrip():
         s, limbs = hgpu.int_to_limbs(v)
         ptr = limbs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
         assert hgpu.limbs_to_int(s, ptr) == v
+
+
+MALFORMED = [
+    ("s=0 hex=ff fracbits=32\ns=2 hex=1 fracbits=32\n", "matrix dump out of order at s=2"),
+    ("s=0 hex=ff fracbits=32\ns=1 hex=1 fracbits=32\n", "matrix dump must hold 2n-1 anti-diagonals"),
+    ("", "matrix dump must hold 2n-1 anti-diagonals"),
+    ("s=0 mantissa=ff fracbits=32\n", "matrix dump line: s=0 mantissa=ff fracbits=32"),
+    ("s=0 hex=xyz fracbits=32\n", "matrix dump line: s=0 hex=xyz fracbits=32"),
+]
+
+
+@pytest.mark.parametrize("text,message", MALFORMED)
+def test_dump_loader_rejects_what_the_reference_rejects(tmp_path, text, message):
+    """load_matrix_dump (hankel_matrix.cpp:65-87): MalformedInput cases, same
+    messages, checked before any device work (so this runs without a GPU)."""
+    path = tmp_path / "m.dump"
+    path.write_text(text)
+    with pytest.raises(hgpu.HgpuError) as e:
+        hgpu.HankelMatrixGPU.from_dump(str(path))
+    assert e.value.status == 1  # HGPU_ERR_INVALID_ARGUMENT
+    assert message in str(e.value)
+
+
+def test_dump_loader_missing_file(tmp_path):
+    with pytest.raises(hgpu.HgpuError) as e:
+        hgpu.HankelMatrixGPU.from_dump(str(tmp_path / "absent.dump"))
+    assert e.value.status == 1 and "cannot open dump file" in str(e.value)

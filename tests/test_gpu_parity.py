@@ -5,6 +5,8 @@ the reference's ldlt_det_serial (ldlt.cpp:31-77) on the same strip and shift.
 """
 import math
 
+import ctypes
+
 import pytest
 
 from helpers import random_pd_hankel, strip_from_ints
@@ -129,3 +131,35 @@ def test_set_strip_reuses_the_handle(hg, ref):
     for strip in (b, big, a):
         m.set_strip(strip)
         assert_same(m.ldlt(x, capture=True), ref.ldlt(strip, x, k))
+
+
+def test_dump_interchange_round_trip(hg, tmp_path):
+    """The reference's on-disk matrix format (hankel_matrix.cpp:52-87): a dump
+    written by the reference itself loads onto the device and factorises like
+    the strip passed through the ABI, and hgpu_matrix_dump writes the
+    reference's text back byte for byte (negative and zero mantissas too)."""
+    ref = po.RefLib()
+    n, k = 24, 768
+    text = ref._call("oref_build_strip", [ctypes.c_long, ctypes.c_ulong, ctypes.c_ulong, ctypes.c_long],
+                     n, 7, 4, k)
+    strip, kk = po.parse_dump(text)
+    assert kk == k
+    src = tmp_path / "ref.dump"
+    src.write_text(text)
+    m = hg.HankelMatrixGPU.from_dump(str(src))
+    assert (m.n, m.frac_bits) == (n, k)
+    x = -(1 << (k - 16))
+    got = m.ldlt(x, capture=True)
+    want = po.OracleLib().ldlt(strip, x, k, capture=True)
+    assert got.pivots == want.pivots and got.ratios == want.ratios
+    out = tmp_path / "gpu.dump"
+    m.dump(str(out))
+    assert out.read_text() == text
+    # signed and zero entries survive the trip
+    odd = [5, -(1 << 70) - 3, 0, 1 << 40, -1]
+    a = hg.HankelMatrixGPU(odd, 64)
+    a.dump(str(out))
+    assert out.read_text() == po.make_dump(odd, 64)
+    b = hg.HankelMatrixGPU.from_dump(str(out))
+    b.dump(str(src))
+    assert src.read_text() == po.make_dump(odd, 64)
