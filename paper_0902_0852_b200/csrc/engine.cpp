@@ -520,6 +520,8 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
   if (const char* e = std::getenv("HGPU_FAR_SUB")) far_sub_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF")) edf_h_ = std::max(0, std::atoi(e));
   if (const char* e = std::getenv("HGPU_EDF_RUN")) edf_run_ = std::max(1, std::min(8, std::atoi(e)));
+  if (const char* e = std::getenv("HGPU_FLUSH_AHEAD")) flush_ahead_ = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("HGPU_FLUSH_BATCH")) flush_batch_ = std::max(1, std::min(8, std::atoi(e)));
   if (const char* e = std::getenv("HGPU_PRE_ENTRY")) pre_entry_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_NEXT_ROW")) next_row_ = std::atoi(e) != 0;
   if (const char* e = std::getenv("HGPU_UPDATE_TC")) update_tc_ = std::atoi(e) != 0;
@@ -944,7 +946,14 @@ void Matrix::alloc_slots() {
     nsets = edf_h_ > 0 ? (size_t)nblocks + 1 : 2 + (size_t)std::max(0, defer_);
     const double per_set = (double)kb * n_ * (2.0 * NW + 2.0 * P.cap + 2.0) * 4.0;
     const size_t free_b = device_available(device_);
-    while (nsets > 2 && per_set * nsets > 0.6 * (double)free_b) --nsets;
+    // share of the free memory the slot sets may take (the rest is for the L
+    // store and the solve buffers of an inverse iteration); HGPU_SLOT_SETS
+    // forces a count (tests of the reuse path on small matrices)
+    double frac = 0.6;
+    if (const char* e = std::getenv("HGPU_SLOT_FRAC")) frac = std::min(0.9, std::max(0.1, std::atof(e)));
+    while (nsets > 2 && per_set * nsets > frac * (double)free_b) --nsets;
+    if (const char* e = std::getenv("HGPU_SLOT_SETS"))
+      nsets = std::min(nsets, (size_t)std::max(2, std::atoi(e)));
   }
   nsets_ = (int)nsets;
   vhdr_ = dalloc<int>(nsets * kb * n_);
@@ -1529,6 +1538,7 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
                       stream_join_ && near_rows_ >= kb && P.tile == 16 && D.NW % 32 == 0 &&
                       !update_tc_;
   bool prev_lag = false;  // panel b-1 left band b's far rows to lag_ev_[2b+1]
+  int edf_flushed = 0;    // panels [0, edf_flushed) have had all their bands enqueued
   // L-entry transforms during the factorisation: a solve plan with its own
   // chunk store exists (not borrowing the workspace), single rank
   const bool pre_lhat_on = pre_lhat_ && (flags & HGPU_KEEP_L) && solve_ntt_ && sdp_bits_ > 0 &&
@@ -1552,13 +1562,33 @@ void Matrix::run(const HostInt& x, unsigned flags, FactorResult& res) {
     // ---- panel b on the high-priority streams
     CU(cudaStreamWaitEvent(sp, next_ready[b], 0));
     // slot set reuse: su1's last use of panel b - nsets precedes next_ready[b]
-    if (edf && b >= nsets) {
-      // EDF: the panel whose set is reused gets its remaining bands now
-      const int bo = b - nsets;
-      for (int j = edf_next[bo]; j < nblocks; ++j) edf_enqueue(bo, 1, j);
-      edf_next[bo] = INT_MAX;
-      CU(cudaEventRecord(rest_done[bo], su2));
-      CU(cudaStreamWaitEvent(sp, rest_done[bo], 0));
+    if (edf && nsets <= nblocks) {
+      // EDF with reused slot sets: a panel whose set comes up for reuse gets
+      // all its remaining bands (it is "flushed").  Flushing at the reuse
+      // stalls the chain for the whole flush; instead the oldest pending
+      // panels are flushed flush_ahead_ panels early, several per launch
+      // (adjacent slot sets, one pass over W per band), and the panel stream
+      // only waits for the event of the set it actually reuses.
+      const int fa = std::min(flush_ahead_, std::max(0, nsets - 3));
+      const int need = std::min(b, b - nsets + 1 + fa);  // panels < need are flushed
+      if (need > edf_flushed) {
+        const int upto = std::max(need, std::min(b - 2, edf_flushed + flush_batch_));
+        int bp = edf_flushed;
+        while (bp < upto) {
+          int m = 1;
+          while (m < std::min(edf_run_, 256 / kb) && bp + m < upto &&
+                 edf_next[bp + m] == edf_next[bp] && (bp % nsets) + m < nsets)
+            ++m;
+          for (int j = edf_next[bp]; j < nblocks; ++j) edf_enqueue(bp, m, j);
+          for (int k2 = 0; k2 < m; ++k2) {
+            edf_next[bp + k2] = INT_MAX;
+            CU(cudaEventRecord(rest_done[bp + k2], su2));
+          }
+          bp += m;
+        }
+        edf_flushed = upto;
+      }
+      if (b >= nsets) CU(cudaStreamWaitEvent(sp, rest_done[b - nsets], 0));
     } else if (!edf && b >= nsets) {
       CU(cudaStreamWaitEvent(sp, rest_done[b - nsets], 0));
     }

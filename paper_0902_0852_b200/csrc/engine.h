@@ -291,6 +291,11 @@ class Matrix {
   long long lhat_pre_for_ = -1;
   int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
+  // slot sets are reused when memory is short (configs 4, 5): the panels whose
+  // sets come up for reuse are flushed (all their remaining bands) this many
+  // panels ahead of the reuse, in batches of up to flush_batch_ panels per
+  // launch (HGPU_FLUSH_AHEAD / HGPU_FLUSH_BATCH; 0 / 1: at the reuse, one by one)
+  int flush_ahead_ = 2, flush_batch_ = 4;
   int edf_run_ = 8;  // panels accumulated by one EDF update launch (HGPU_EDF_RUN, 1-8)
   // pivot entry's earlier stages ahead of k_pivot (HGPU_PRE_ENTRY)
   bool pre_entry_ = true;

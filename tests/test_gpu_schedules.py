@@ -48,6 +48,9 @@ VARIANTS = [
     {"HGPU_PRE_NEAR": "1", "HGPU_NEAR": "100", "HGPU_EDF_RUN": "2"},
     {"HGPU_EDF_RUN": "3", "HGPU_FAR_PRIO": "2"},
     {"HGPU_KB": "16"},
+    {"HGPU_SLOT_SETS": "3"},
+    {"HGPU_SLOT_SETS": "4", "HGPU_FLUSH_AHEAD": "0", "HGPU_FLUSH_BATCH": "1"},
+    {"HGPU_SLOT_SETS": "4", "HGPU_FLUSH_AHEAD": "3", "HGPU_FLUSH_BATCH": "8"},
     {"HGPU_KB": "64", "HGPU_FAR_SUB": "16"},
     {"HGPU_LAG_FAR": "1"},
     {"HGPU_LAG_FAR": "1", "HGPU_FAR_LANES": "4", "HGPU_PRE_NEAR": "1"},
