@@ -508,8 +508,13 @@ Matrix::Matrix(int n, int K, const int32_t* sizes, const uint32_t* limbs,
       stream_upd2_ = green_stream(gu.ga, lo);
     else if (excl)
       stream_upd2_ = green_stream((CUgreenCtx)split_gb_, lo);
-    else
-      CU(cudaStreamCreateWithPriority(&stream_upd2_, cudaStreamNonBlocking, lo));
+    else {
+      // HGPU_UPD_PRIO=k: the deferred update k levels above the lowest
+      // priority (experiment: 0, the lowest, measured best)
+      int up = 0;
+      if (const char* e = std::getenv("HGPU_UPD_PRIO")) up = std::max(0, std::atoi(e));
+      CU(cudaStreamCreateWithPriority(&stream_upd2_, cudaStreamNonBlocking, std::max(hi, lo - up)));
+    }
   }
   CU(cudaEventCreate(&ev0_));
   CU(cudaEventCreate(&ev1_));
