@@ -756,6 +756,17 @@ void Matrix::make_group(const std::vector<int>& devices) {
         (void)cudaGetLastError();
       else
         CU(e);
+      // the buffers come from device b's stream-ordered pool (dev_alloc):
+      // pool memory is mapped on a peer only through cudaMemPoolSetAccess
+      // (cudaDeviceEnablePeerAccess covers cudaMalloc memory alone); the
+      // access applies to the pool's existing and future allocations
+      cudaMemPool_t pool;
+      CU(cudaDeviceGetDefaultMemPool(&pool, b));
+      cudaMemAccessDesc desc{};
+      desc.location.type = cudaMemLocationTypeDevice;
+      desc.location.id = a;
+      desc.flags = cudaMemAccessFlagsProtReadWrite;
+      CU(cudaMemPoolSetAccess(pool, &desc, 1));
     }
   CU(cudaSetDevice(device_));
   std::vector<int32_t> sz;
