@@ -290,7 +290,12 @@ k_col_extract(const __grid_constant__ DevPlan P, uint32_t* W, const long long* c
   }
 }
 
-__global__ void k_extract(const __grid_constant__ DevPlan P, const uint32_t* W, const long long* colbase,
+#ifdef HGPU_EXTRACT_MINB  // experiment: cap k_extract's registers (512 threads x MINB CTAs per SM)
+__global__ void __launch_bounds__(512, HGPU_EXTRACT_MINB)
+#else
+__global__ void
+#endif
+k_extract(const __grid_constant__ DevPlan P, const uint32_t* W, const long long* colbase,
                           int p, int r_begin, int r_end, IntBuf vint,
                           long long vrow0, IntBuf piv, int* maxbitsV,
                           uint32_t* vhat, int* maxdegV, int* err, int round,
