@@ -289,7 +289,7 @@ class Matrix {
   cudaEvent_t lhat_ev_ = nullptr;
   int* lhat_err_ = nullptr;
   long long lhat_pre_for_ = -1;
-  int far_sub_ = 8;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off)
+  int far_sub_ = 16;  // far rows' in-panel sub-panel width (HGPU_FAR_SUB, 0 = off; 16 with the 4-row column update: 241.7 ms, 8: 246.3 ms)
   int edf_h_ = 1;    // EDF trailing-update horizon in panels (HGPU_EDF, 0 = off)
   // slot sets are reused when memory is short (configs 4, 5): the panels whose
   // sets come up for reuse are flushed (all their remaining bands) this many

@@ -1277,9 +1277,10 @@ k_update_col(const __grid_constant__ DevPlan P, uint32_t* W, const long long* co
   const int r0 = r_begin + blockIdx.x * TR;
   const PrimeConsts pc = P.pc[wd / P.L];
   const long long NW = P.NW;
-  const uint32_t* rp[TR];
-#pragma unroll
-  for (int i = 0; i < TR; ++i) rp[i] = Rhat + (long long)min(r0 + i, r_end - 1) * NW + wd;
+  // rows r0 .. r0 + TR - 1 (consecutive: one base pointer; rows past r_end
+  // read the last valid row and are not written)
+  const int nv = min(TR, r_end - r0);
+  const uint32_t* rp = Rhat + (long long)r0 * NW + wd;
   const uint32_t* vp = Vhat + (long long)c * NW + wd;
   uint64_t acc[TR];
 #pragma unroll
@@ -1289,21 +1290,19 @@ k_update_col(const __grid_constant__ DevPlan P, uint32_t* W, const long long* co
     const uint32_t b = __ldg(vp + off);
     uint32_t a[TR];
 #pragma unroll
-    for (int i = 0; i < TR; ++i) a[i] = __ldg(rp[i] + off);
+    for (int i = 0; i < TR; ++i) a[i] = __ldg(rp + off + (long long)min(i, nv - 1) * NW);
 #pragma unroll
     for (int i = 0; i < TR; ++i) acc[i] += (uint64_t)a[i] * b;
   }
-  const long long base = colbase[c];
+  uint32_t* wp = W + (colbase[c] + (r0 - c)) * NW + wd;
   uint32_t old[TR];
 #pragma unroll
-  for (int i = 0; i < TR; ++i)
-    old[i] = r0 + i < r_end ? W[(base + (r0 + i - c)) * NW + wd] : 0u;
+  for (int i = 0; i < TR; ++i) old[i] = i < nv ? wp[(long long)i * NW] : 0u;
 #pragma unroll
   for (int i = 0; i < TR; ++i) {
-    if (r0 + i >= r_end) continue;
+    if (i >= nv) continue;
     const uint32_t t32 = reduce_sum64(acc[i], pc);
-    W[(base + (r0 + i - c)) * NW + wd] =
-        old[i] >= t32 ? old[i] - t32 : old[i] + pc.q - t32;
+    wp[(long long)i * NW] = old[i] >= t32 ? old[i] - t32 : old[i] + pc.q - t32;
   }
 }
 
@@ -1667,12 +1666,28 @@ cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
                               int nslots, int c, int r_begin, int r_end,
                               const int* err, cudaStream_t st) {
   if (nslots <= 0 || r_begin >= r_end) return cudaSuccess;
-  constexpr int TR = 16;
-  dim3 grid((r_end - r_begin + TR - 1) / TR, (P.NW + 127) / 128);
+  // rows per thread (HGPU_COL_TR: 2, 4, 8 or 16).  4 (40 registers: many
+  // small CTAs that fit beside the trailing update's) measured best in the
+  // step: 241.7 ms against 249.4 / 246.8 for 8 / 16 at config 3
+  static const int tr = [] {
+    const char* e = getenv("HGPU_COL_TR");
+    const int v = e ? atoi(e) : 4;
+    return (v == 2 || v == 8 || v == 16) ? v : 4;
+  }();
+  dim3 grid((r_end - r_begin + tr - 1) / tr, (P.NW + 127) / 128);
   ++g_launches;
-  k_update_col<TR><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat,
-                                         row_stride_slot, nslots, c, r_begin,
-                                         r_end, err);
+  if (tr == 2)
+    k_update_col<2><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
+                                          r_begin, r_end, err);
+  else if (tr == 4)
+    k_update_col<4><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
+                                          r_begin, r_end, err);
+  else if (tr == 8)
+    k_update_col<8><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
+                                          r_begin, r_end, err);
+  else
+    k_update_col<16><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
+                                           r_begin, r_end, err);
   return post_launch(st);
 }
 
