@@ -1371,6 +1371,17 @@ cudaError_t launch_init_w(const DevPlan& P, const uint32_t* that,
   return post_launch(st);
 }
 
+// threads of a multi-row extraction / division CTA (HGPU_ROW_THREADS: 128 or
+// 256; experiment)
+static int row_threads() {
+  static const int v = [] {
+    const char* e = getenv("HGPU_ROW_THREADS");
+    const int t = e ? atoi(e) : 256;
+    return t == 128 ? 128 : 256;
+  }();
+  return v;
+}
+
 size_t extract_smem_bytes(const DevPlan& P, bool staged) {
   const int M = P.L + P.T;
   return (size_t)((P.tw_smem && staged ? 2 * P.NW : 0) + P.NW + 4 * M + P.cap + 64) * 4;
@@ -1387,7 +1398,7 @@ cudaError_t launch_extract(const DevPlan& P, const uint32_t* W,
   ++g_launches;
   // a single row is on the pivot chain: give it more threads; one row per
   // CTA needs no twiddle tables in shared memory
-  k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : 256,
+  k_extract<<<min(rows, P.grid_cap), rows == 1 ? 512 : row_threads(),
               extract_smem_bytes(P, rows > P.grid_cap), st>>>(
       P, W, colbase, p, r_begin, r_end, vint, vrow0, piv, maxbitsV, vhat,
       maxdegV, err, round, vdig, kd);
@@ -1537,7 +1548,7 @@ cudaError_t launch_divide(const DevPlan& P, IntBuf vint, long long vrow0,
                                     rhat, maxdegR, gscratch, use_gscratch, err,
                                     iv ? *iv : IvDiv{});
   else
-    k_divide<<<min(rows, P.grid_cap), 256, smem, st>>>(
+    k_divide<<<min(rows, P.grid_cap), row_threads(), smem, st>>>(
         P, vint, vrow0, p, r_begin, r_end, Ybuf, ys, rint, rrow0, rhat, maxdegR,
         gscratch, use_gscratch, err, iv ? *iv : IvDiv{});
   return post_launch(st);
