@@ -766,7 +766,10 @@ __device__ void divide_body(const DevPlan& P, IntBuf vint, long long vrow0, int 
   }
 }
 
-__global__ void __launch_bounds__(256, 3) k_divide(const __grid_constant__ DevPlan P, IntBuf vint, long long vrow0, int p,
+#ifndef HGPU_DIVIDE_MINB
+#define HGPU_DIVIDE_MINB 3  // 80 registers; 4: 64 registers (experiment)
+#endif
+__global__ void __launch_bounds__(256, HGPU_DIVIDE_MINB) k_divide(const __grid_constant__ DevPlan P, IntBuf vint, long long vrow0, int p,
                          int r_begin, int r_end,
                          const uint32_t* Ybuf, const int* ys, IntBuf rint,
                          long long rrow0, uint32_t* rhat, int* maxdegR,
