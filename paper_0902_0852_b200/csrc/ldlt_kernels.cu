@@ -1288,6 +1288,15 @@ k_update_col(const __grid_constant__ DevPlan P, uint32_t* W, const long long* co
   uint64_t acc[TR];
 #pragma unroll
   for (int i = 0; i < TR; ++i) acc[i] = 0;
+  // the stage loop is unrolled so that the loads of several stages are in
+  // flight together: the kernel is bound by L2 latency (one dependent round
+  // trip per stage otherwise), and in the step that latency is several times
+  // what it is alone
+#ifndef HGPU_COL_UNROLL
+#define HGPU_COL_UNROLL 4
+#endif
+  constexpr int kColUnroll = HGPU_COL_UNROLL;
+#pragma unroll kColUnroll
   for (int s = 0; s < nslots; ++s) {
     const long long off = s * row_stride_slot;
     const uint32_t b = __ldg(vp + off);
