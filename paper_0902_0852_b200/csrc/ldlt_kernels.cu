@@ -1144,7 +1144,11 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 }  // namespace
 
+#ifdef HGPU_UPD_MAXREG  // experiment: leave register headroom beside three update CTAs
+__global__ void __maxnreg__(HGPU_UPD_MAXREG)
+#else
 __global__ void __launch_bounds__(128, 2)
+#endif
 k_update_tiled(const __grid_constant__ DevPlan P, uint32_t* W, const long long* colbase,
                const uint32_t* Vhat, const uint32_t* Rhat,
                long long row_stride_slot, int nslots, int c_begin, int c_end,
@@ -1697,8 +1701,18 @@ cudaError_t launch_update_col(const DevPlan& P, uint32_t* W,
     const int v = e ? atoi(e) : 4;
     return (v == 2 || v == 8 || v == 16) ? v : 4;
   }();
-  dim3 grid((r_end - r_begin + tr - 1) / tr, (P.NW + 127) / 128);
+  // threads per CTA (HGPU_COL_THREADS: 64 or 128)
+  static const int ct = [] {
+    const char* e = getenv("HGPU_COL_THREADS");
+    return (e && atoi(e) == 64) ? 64 : 128;
+  }();
+  dim3 grid((r_end - r_begin + tr - 1) / tr, (P.NW + ct - 1) / ct);
   ++g_launches;
+  if (ct == 64 && tr == 4) {
+    k_update_col<4><<<grid, 64, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
+                                         r_begin, r_end, err);
+    return post_launch(st);
+  }
   if (tr == 2)
     k_update_col<2><<<grid, 128, 0, st>>>(P, W, colbase, Vhat, Rhat, row_stride_slot, nslots, c,
                                           r_begin, r_end, err);
