@@ -47,6 +47,9 @@ VARIANTS = [
     {"HGPU_PRE_NEAR": "1", "HGPU_FAR_LANES": "2", "HGPU_GRID": "2", "HGPU_FAR_PRIO": "1"},
     {"HGPU_PRE_NEAR": "1", "HGPU_NEAR": "100", "HGPU_EDF_RUN": "2"},
     {"HGPU_EDF_RUN": "3", "HGPU_FAR_PRIO": "2"},
+    {"HGPU_COL_TR": "16", "HGPU_FAR_SUB": "8"},
+    {"HGPU_COL_TR": "8", "HGPU_ROW_THREADS": "128"},
+    {"HGPU_COL_TR": "2", "HGPU_COL_THREADS": "64"},
     {"HGPU_KB": "16"},
     {"HGPU_SLOT_SETS": "3"},
     {"HGPU_SLOT_SETS": "4", "HGPU_FLUSH_AHEAD": "0", "HGPU_FLUSH_BATCH": "1"},
